@@ -1,0 +1,172 @@
+/* nlfem_gpu.h -- C-ABI of the B200 nonlocal stiffness assembler.
+ *
+ * Drop-in for the reference's hot path
+ *
+ *   LinearSystem nlfem::assemble(const ElementTable& et, const DofMap& dofs,
+ *                                const Kernel& kernel, const ScalarFn& f,
+ *                                const ScalarFn& g, const AssemblyConfig& cfg,
+ *                                AssemblyStats* stats);
+ *     (reference proj/include/nlfem/assembly.hpp:71-73, proj/src/assembly.cpp:617-843)
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Inputs are borrowed for the duration of a call.  Output arrays are owned by
+ * the library and released with nlfem_gpu_free_csr().  Every entry point
+ * returns 0 on success or an nlfem_gpu_status code, with a message in `err`.
+ * There is no CPU fallback: without a usable sm_100 device the calls fail
+ * with NLFEM_GPU_ENODEVICE.
+ */
+#ifndef NLFEM_GPU_H
+#define NLFEM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes.  1..8 mirror nlfem::ErrorCode (reference core.hpp:18-27) in
+ * declaration order + 1, so callers can rethrow nlfem::Error(code - 1, msg). */
+enum nlfem_gpu_status {
+  NLFEM_GPU_OK = 0,
+  NLFEM_GPU_BAD_INDEX = 1,
+  NLFEM_GPU_DANGLING_VERTEX = 2,
+  NLFEM_GPU_NON_MANIFOLD = 3,
+  NLFEM_GPU_SEED_MISMATCH = 4,
+  NLFEM_GPU_BALL_EXITS_MESH = 5, /* reference assembly.cpp:710-719 */
+  NLFEM_GPU_DEGENERATE_HULL = 6,
+  NLFEM_GPU_BAD_MESH_FILE = 7,
+  NLFEM_GPU_BAD_CONFIG = 8,      /* reference assembly.cpp:620-622 */
+  NLFEM_GPU_ENODEVICE = 100,     /* no sm_100 device / CUDA error */
+  NLFEM_GPU_ENOMEM = 101,
+  NLFEM_GPU_EUNSUPPORTED = 102   /* strategy outside {barycenter,nocaps,fullcaps} */
+};
+
+/* Strategy ids follow nlfem::Strategy (reference ball_approx.hpp:17-24). */
+enum nlfem_gpu_strategy {
+  NLFEM_STRATEGY_INSIDE = 0,
+  NLFEM_STRATEGY_OVERLAP = 1,
+  NLFEM_STRATEGY_BARYCENTER = 2,
+  NLFEM_STRATEGY_NOCAPS = 3,
+  NLFEM_STRATEGY_APPROXCAPS = 4,
+  NLFEM_STRATEGY_FULLCAPS = 5
+};
+
+/* Monte Carlo sample stream for fullcaps.
+ * PHILOX: Philox4x32-10, key = (seed lo32, seed hi32), counter =
+ * (outer elem, inner elem, quad pt, block); sample s of an item uses uniforms
+ * 3s..3s+2.  Regions and estimator are the reference's
+ * (assembly.cpp:383-399, ball_approx.cpp:257-298). */
+enum nlfem_gpu_sampler { NLFEM_SAMPLER_PHILOX = 0 };
+
+/* ElementTable (reference ball_approx.hpp:38-58) as flat host arrays.
+ * Simplex vertices are node_xyz[verts[4t+i]] (ball_approx.cpp:56). */
+typedef struct {
+  int32_t node_count;
+  int32_t elem_count;
+  const double* node_xyz;   /* [node_count*3]  ElementTable::node            */
+  const int32_t* verts;     /* [elem_count*4]  ElementTable::verts           */
+  const int32_t* neighbor;  /* [elem_count*4]  ElementTable::neighbor, -1    */
+  const double* center;     /* [elem_count*3]  ElementTable::center          */
+  const double* radius;     /* [elem_count]    ElementTable::radius          */
+  const double* volume;     /* [elem_count]    ElementTable::volume          */
+  const double* diam;       /* [elem_count]    ElementTable::diam            */
+  const uint8_t* region;    /* [elem_count]    ElementTable::region (0/1)    */
+  const double* inv_edges;  /* [elem_count*9]  ElementTable::inv_edges       */
+} nlfem_gpu_mesh;
+
+/* DofMap (reference assembly.hpp:19-26): dof_of_node[v] = -1 when constrained. */
+typedef struct {
+  int32_t node_count;
+  int32_t unknowns;
+  const int32_t* dof_of_node;
+} nlfem_gpu_dofs;
+
+/* Kernel (reference polynomial.hpp:36-46): C * 1[|x-y| < delta], 3D only. */
+typedef struct {
+  double C;
+  double delta;
+} nlfem_gpu_kernel;
+
+/* Polynomial f or g (reference polynomial.hpp:13-25): terms in Polynomial
+ * sort order; evaluated exactly as Polynomial::eval (polynomial.cpp:28-37). */
+typedef struct {
+  int32_t nterms;
+  const double* coef;   /* [nterms]   */
+  const int32_t* exps;  /* [nterms*3] */
+} nlfem_gpu_poly;
+
+/* AssemblyConfig (reference assembly.hpp:50-55). */
+typedef struct {
+  int32_t strategy;     /* nlfem_gpu_strategy                                  */
+  int32_t mc_samples;   /* per Monte Carlo sub-simplex, as the reference       */
+  uint64_t seed;
+  int32_t sampler;      /* nlfem_gpu_sampler                                   */
+  int32_t device;       /* CUDA device ordinal (-1: current)                    */
+} nlfem_gpu_config;
+
+/* LinearSystem (reference assembly.hpp:36-42): CSR with sorted columns. */
+typedef struct {
+  int32_t rows;
+  int64_t nnz;
+  int32_t* row_ptr;     /* [rows+1] (library-owned) */
+  int32_t* col_idx;     /* [nnz]                    */
+  double* values;       /* [nnz]                    */
+  double* rhs;          /* [rows]                   */
+} nlfem_gpu_csr;
+
+/* AssemblyStats (reference assembly.hpp:57-63) plus GPU counters. */
+typedef struct {
+  double seconds;          /* wall time of the whole call                     */
+  int32_t threads;         /* 1 (one host thread drives the device)           */
+  int32_t blocks;          /* ceil(interior/32), the reference's block count  */
+  uint64_t mc_samples;     /* draws, per MC sub-simplex semantics             */
+  uint64_t mc_hits;
+  int64_t element_pairs;   /* (T,T') with a piece for some quad point of T     */
+  int64_t items;           /* (T,q,T') with pieces                            */
+  int64_t nnz_ext;         /* node-pattern size incl. constrained columns     */
+  double device_ms;        /* device pipeline time (CUDA events)              */
+  double phase_ms[8];      /* prep, pairs, pattern, integrate, finalize, ...  */
+} nlfem_gpu_stats;
+
+/* One-shot drop-in: host arrays in, host CSR out (upload + device pipeline +
+ * download inside the call).  The analogue of nlfem::assemble. */
+int nlfem_gpu_assemble(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
+                       const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
+                       const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
+                       nlfem_gpu_csr* out, nlfem_gpu_stats* stats, char* err,
+                       size_t errlen);
+
+void nlfem_gpu_free_csr(nlfem_gpu_csr* csr);
+
+/* Device-resident session: the mesh is uploaded once; run() executes the
+ * device pipeline with inputs already in HBM and leaves the CSR on the device;
+ * download() copies it out.  Not reentrant per session. */
+typedef struct nlfem_gpu_session nlfem_gpu_session;
+
+int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
+                             const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
+                             const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
+                             nlfem_gpu_session** out, char* err, size_t errlen);
+/* stream: a cudaStream_t (NULL = the legacy default stream). */
+int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* stats,
+                          char* err, size_t errlen);
+int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* err,
+                               size_t errlen);
+/* Element-pair list of the last run, for set parity: for each interior outer
+ * element (in ascending id order) its partner ids and per-quad-point class
+ * codes (5 bits per point).  Arrays sized by *npairs after a
+ * call with NULL buffers. */
+int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* outer_offsets,
+                            int32_t* partner, uint32_t* info, char* err, size_t errlen);
+/* Kernel launches of the last run (for the bench's gpu_launches key). */
+int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s);
+void nlfem_gpu_session_destroy(nlfem_gpu_session* s);
+
+/* Build / version string (e.g. "nlfem_gpu sm_100a ..."). */
+const char* nlfem_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NLFEM_GPU_H */

@@ -1,0 +1,453 @@
+"""B200-native nonlocal stiffness assembly (hot path of arXiv 2302.07499).
+
+Python mirror of the reference's public interface for this path
+(reference proj/python/nlfem_module.cpp:148-227, proj/python/nlfem/__init__.py):
+
+    generate_mesh(n, res, delta)            -> {"coords", "cells", "region"}
+    assemble_system(coords, cells, region, delta, strategy="nocaps",
+                    normalization="mass", problem_terms=None, threads=0,
+                    seed=0x5eed, mc_samples=200)
+                                            -> {"row_ptr", "col_idx", "values", "rhs",
+                                                "node_of_dof", "constrained",
+                                                "assembly_s", "threads", ...}
+    strategy_names()
+
+Same argument meaning and error behaviour (ValueError for malformed arrays,
+NlfemError for reference error codes).  Everything below the ctypes boundary
+is the in-tree libnlfem_gpu.so: host setup in C++ and the assembly in sm_100a
+CUDA.  There is no CPU fallback: without the library or a B200 the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnlfem_gpu.so")
+
+STRATEGIES = ["inside", "overlap", "barycenter", "nocaps", "approxcaps", "fullcaps"]
+GPU_STRATEGIES = ("barycenter", "nocaps", "fullcaps")
+ERROR_NAMES = {1: "BadIndex", 2: "DanglingVertex", 3: "NonManifold", 4: "SeedMismatch",
+               5: "BallExitsMesh", 6: "DegenerateHull", 7: "BadMeshFile", 8: "BadConfig",
+               100: "NoDevice", 101: "OutOfMemory", 102: "Unsupported"}
+
+
+class NlfemError(RuntimeError):
+    """Error raised by the assembler; `code` follows include/nlfem_gpu.h."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+        self.name = ERROR_NAMES.get(code, "Unknown")
+
+
+# --------------------------------------------------------------------------- ctypes
+
+class _Mesh(C.Structure):
+    _fields_ = [("node_count", C.c_int32), ("elem_count", C.c_int32),
+                ("node_xyz", C.c_void_p), ("verts", C.c_void_p), ("neighbor", C.c_void_p),
+                ("center", C.c_void_p), ("radius", C.c_void_p), ("volume", C.c_void_p),
+                ("diam", C.c_void_p), ("region", C.c_void_p), ("inv_edges", C.c_void_p)]
+
+
+class _Dofs(C.Structure):
+    _fields_ = [("node_count", C.c_int32), ("unknowns", C.c_int32),
+                ("dof_of_node", C.c_void_p)]
+
+
+class _Kernel(C.Structure):
+    _fields_ = [("C", C.c_double), ("delta", C.c_double)]
+
+
+class _Poly(C.Structure):
+    _fields_ = [("nterms", C.c_int32), ("coef", C.c_void_p), ("exps", C.c_void_p)]
+
+
+class _Config(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("mc_samples", C.c_int32), ("seed", C.c_uint64),
+                ("sampler", C.c_int32), ("device", C.c_int32)]
+
+
+class _Csr(C.Structure):
+    _fields_ = [("rows", C.c_int32), ("nnz", C.c_int64), ("row_ptr", C.POINTER(C.c_int32)),
+                ("col_idx", C.POINTER(C.c_int32)), ("values", C.POINTER(C.c_double)),
+                ("rhs", C.POINTER(C.c_double))]
+
+
+class Stats(C.Structure):
+    """nlfem_gpu_stats (include/nlfem_gpu.h); mirrors nlfem::AssemblyStats."""
+    _fields_ = [("seconds", C.c_double), ("threads", C.c_int32), ("blocks", C.c_int32),
+                ("mc_samples", C.c_uint64), ("mc_hits", C.c_uint64),
+                ("element_pairs", C.c_int64), ("items", C.c_int64), ("nnz_ext", C.c_int64),
+                ("device_ms", C.c_double), ("phase_ms", C.c_double * 8)]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}
+        d["phase_ms"] = list(self.phase_ms)[:5]
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Load libnlfem_gpu.so (raises if it was not built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; "
+                          "g.build()'` (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.nlfem_gpu_version.restype = C.c_char_p
+    L.nlfem_gpu_assemble.restype = C.c_int
+    L.nlfem_gpu_assemble.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
+                                     P(_Config), P(_Csr), P(Stats), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_free_csr.argtypes = [P(_Csr)]
+    L.nlfem_gpu_session_create.restype = C.c_int
+    L.nlfem_gpu_session_create.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
+                                           P(_Config), P(vp), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_run.restype = C.c_int
+    L.nlfem_gpu_session_run.argtypes = [vp, vp, P(Stats), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_download.restype = C.c_int
+    L.nlfem_gpu_session_download.argtypes = [vp, P(_Csr), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_pairs.restype = C.c_int
+    L.nlfem_gpu_session_pairs.argtypes = [vp, P(i64), vp, vp, vp, C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_launches.restype = i64
+    L.nlfem_gpu_session_launches.argtypes = [vp]
+    L.nlfem_gpu_session_destroy.argtypes = [vp]
+    L.nlfem_host_lattice_mesh.restype = C.c_int
+    L.nlfem_host_lattice_mesh.argtypes = [i32, dbl, i64, P(i64), P(i64), vp, vp, vp]
+    L.nlfem_host_element_table.restype = C.c_int
+    L.nlfem_host_element_table.argtypes = [vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp,
+                                           C.c_char_p, C.c_size_t]
+    L.nlfem_host_dofmap.restype = i32
+    L.nlfem_host_dofmap.argtypes = [vp, vp, i64, i64, vp, vp]
+    L.nlfem_host_kernel_constant.restype = dbl
+    L.nlfem_host_kernel_constant.argtypes = [dbl, i32]
+    L.nlfem_host_forcing.restype = i32
+    L.nlfem_host_forcing.argtypes = [dbl, i32, vp, i32, vp, i32]
+    L.nlfem_host_normalize_poly.restype = i32
+    L.nlfem_host_normalize_poly.argtypes = [vp, i32, vp, i32]
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = [
+    "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
+    "nlfem_gpu_session_run", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
+    "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
+    "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
+    "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
+]
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(rc: int, err) -> None:
+    if rc:
+        msg = err.value.decode(errors="replace") if err is not None else ""
+        raise NlfemError(rc, msg or ERROR_NAMES.get(rc, f"error {rc}"))
+
+
+# --------------------------------------------------------------------------- host setup
+
+def strategy_names() -> list[str]:
+    return list(STRATEGIES)
+
+
+def generate_mesh(n: int, res: int, delta: float, jitter_seed: int | None = None) -> dict:
+    """Structured mesh of the reference's generate_mesh (mesh.cpp:115-121), 3D only.
+
+    jitter_seed adds the config-3 interior-vertex jitter."""
+    if n != 3:
+        raise ValueError("the GPU assembler is 3D only (n must be 3)")
+    L = lib()
+    nn, nc = C.c_int64(), C.c_int64()
+    js = -1 if jitter_seed is None else int(jitter_seed)
+    rc = L.nlfem_host_lattice_mesh(res, delta, js, C.byref(nn), C.byref(nc), None, None, None)
+    _check(rc, None)
+    coords = np.empty((nn.value, 3))
+    cells = np.empty((nc.value, 4), np.int32)
+    region = np.empty(nc.value, np.uint8)
+    _check(L.nlfem_host_lattice_mesh(res, delta, js, C.byref(nn), C.byref(nc), _p(coords),
+                                     _p(cells), _p(region)), None)
+    return {"coords": coords, "cells": cells, "region": region}
+
+
+def _mesh_arrays(coords, cells, region):
+    coords = np.asarray(coords)
+    cells = np.asarray(cells)
+    region = np.asarray(region)
+    if coords.ndim != 2 or coords.shape[1] != 3:
+        raise ValueError("coords must have shape (nodes, 3)")
+    if cells.ndim != 2 or cells.shape[1] != 4:
+        raise ValueError("cells must have shape (count, 4)")
+    if region.ndim != 1 or region.shape[0] != cells.shape[0]:
+        raise ValueError("region must have shape (cell count,)")
+    if cells.size and (cells.min() < 0 or cells.max() >= coords.shape[0]):
+        raise ValueError("cell vertex index out of range")
+    if region.size and not np.isin(region, (0, 1)).all():
+        raise ValueError("region must be 0 or 1")
+    return (np.ascontiguousarray(coords, np.float64), np.ascontiguousarray(cells, np.int32),
+            np.ascontiguousarray(region, np.uint8))
+
+
+class ElementTable:
+    """build_cmap + build_element_table + build_dofmap, restated on the host."""
+
+    def __init__(self, coords, cells, region):
+        coords, cells, region = _mesh_arrays(coords, cells, region)
+        L = lib()
+        K, V = cells.shape[0], coords.shape[0]
+        self.coords, self.cells, self.region = coords, cells, region
+        self.verts = np.empty((K, 4), np.int32)
+        self.neighbor = np.empty((K, 4), np.int32)
+        self.center = np.empty((K, 3))
+        self.radius = np.empty(K)
+        self.volume = np.empty(K)
+        self.diam = np.empty(K)
+        self.inv_edges = np.empty((K, 9))
+        err = C.create_string_buffer(512)
+        _check(L.nlfem_host_element_table(
+            _p(coords), V, _p(cells), _p(region), K, _p(self.verts), _p(self.neighbor),
+            _p(self.center), _p(self.radius), _p(self.volume), _p(self.diam),
+            _p(self.inv_edges), err, 512), err)
+        self.dof_of_node = np.empty(V, np.int32)
+        self.constrained = np.empty(V, np.uint8)
+        self.unknowns = int(L.nlfem_host_dofmap(_p(self.verts), _p(region), K, V,
+                                                _p(self.dof_of_node), _p(self.constrained)))
+        self.node_of_dof = np.nonzero(self.dof_of_node >= 0)[0].astype(np.int32)
+
+    @property
+    def elem_count(self) -> int:
+        return self.cells.shape[0]
+
+    @property
+    def node_count(self) -> int:
+        return self.coords.shape[0]
+
+    def _structs(self):
+        m = _Mesh(self.node_count, self.elem_count, _p(self.coords), _p(self.verts),
+                  _p(self.neighbor), _p(self.center), _p(self.radius), _p(self.volume),
+                  _p(self.diam), _p(self.region), _p(self.inv_edges))
+        d = _Dofs(self.node_count, self.unknowns, _p(self.dof_of_node))
+        return m, d
+
+    def nbytes(self) -> int:
+        """Host->device bytes of one upload of this table."""
+        return sum(a.nbytes for a in (self.coords, self.verts, self.neighbor, self.center,
+                                      self.radius, self.volume, self.diam, self.region,
+                                      self.inv_edges, self.dof_of_node))
+
+
+def kernel_constant(delta: float, normalization: str = "mass") -> float:
+    return float(lib().nlfem_host_kernel_constant(delta, _norm_flag(normalization)))
+
+
+def _norm_flag(normalization: str) -> int:
+    if normalization == "mass":
+        return 0
+    if normalization == "moment2":
+        return 1
+    raise ValueError("normalization must be mass or moment2")
+
+
+def normalize_terms(terms) -> np.ndarray:
+    t = np.ascontiguousarray(terms, np.float64).reshape(-1, 4)
+    out = np.empty((max(len(t), 1) * 2 + 8, 4))
+    n = lib().nlfem_host_normalize_poly(_p(t), len(t), _p(out), len(out))
+    return out[:n].copy()
+
+
+def default_problem_terms() -> np.ndarray:
+    """u = x(1-x) y(1-y) z(1-z) (reference problem.cpp:20-26)."""
+    terms = []
+    for ex in (1, 2):
+        for ey in (1, 2):
+            for ez in (1, 2):
+                c = (-1.0) ** ((ex == 2) + (ey == 2) + (ez == 2))
+                terms.append([c, ex, ey, ez])
+    return normalize_terms(np.array(terms))
+
+
+def _check_terms(problem_terms) -> np.ndarray:
+    arr = np.asarray(problem_terms, np.float64)
+    if arr.ndim != 2 or arr.shape[1] != 4:
+        raise ValueError("problem_terms must have shape (terms, 4): c, e0, e1, e2")
+    e = arr[:, 1:]
+    if (e != np.floor(e)).any() or (e < 0).any():
+        raise ValueError("exponents must be nonnegative integers")
+    out = normalize_terms(arr)
+    if len(out) == 0:
+        raise ValueError("problem_terms is empty")
+    return out
+
+
+def forcing_terms(delta: float, uterms, normalization: str = "mass") -> np.ndarray:
+    """f = -L u (reference problem.cpp:5-11)."""
+    ut = np.ascontiguousarray(uterms, np.float64)
+    out = np.empty((64, 4))
+    n = lib().nlfem_host_forcing(delta, _norm_flag(normalization), _p(ut), len(ut), _p(out), 64)
+    return out[:n].copy()
+
+
+def _poly_struct(terms: np.ndarray):
+    coef = np.ascontiguousarray(terms[:, 0], np.float64)
+    exps = np.ascontiguousarray(terms[:, 1:], np.int32)
+    return _Poly(len(terms), _p(coef), _p(exps)), (coef, exps)
+
+
+# --------------------------------------------------------------------------- assembly
+
+class Session:
+    """Device-resident assembly session (nlfem_gpu_session_*).
+
+    The element table is uploaded once; run() executes the whole device
+    pipeline with inputs in HBM; download() returns the CSR system."""
+
+    def __init__(self, table: ElementTable, delta: float, strategy: str = "nocaps",
+                 normalization: str = "mass", problem_terms=None, seed: int = 0x5EED,
+                 mc_samples: int = 200, device: int = -1):
+        if strategy not in STRATEGIES:
+            raise NlfemError(8, f"BadConfig: unknown strategy '{strategy}' (expected inside, "
+                                "overlap, barycenter, nocaps, approxcaps, or fullcaps)")
+        L = lib()
+        self.table = table
+        self.delta = float(delta)
+        self.strategy = strategy
+        self.C = kernel_constant(delta, normalization)
+        u = default_problem_terms() if problem_terms is None else _check_terms(problem_terms)
+        self.uterms = u
+        self.fterms = forcing_terms(delta, u, normalization)
+        if not (delta > 0):
+            raise NlfemError(8, "BadConfig: delta must be positive")
+        m, d = table._structs()
+        k = _Kernel(self.C, self.delta)
+        fp, self._fkeep = _poly_struct(self.fterms)
+        gp, self._gkeep = _poly_struct(u)
+        cfg = _Config(STRATEGIES.index(strategy), int(mc_samples), int(seed) & (2**64 - 1), 0,
+                      int(device))
+        self._h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _check(L.nlfem_gpu_session_create(C.byref(m), C.byref(d), C.byref(k), C.byref(fp),
+                                          C.byref(gp), C.byref(cfg), C.byref(self._h), err,
+                                          1024), err)
+        self.stats = Stats()
+
+    def run(self, stream: int | None = None) -> Stats:
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_run(self._h, C.c_void_p(stream or 0),
+                                           C.byref(self.stats), err, 1024), err)
+        return self.stats
+
+    def download(self) -> dict:
+        csr = _Csr()
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_download(self._h, C.byref(csr), err, 1024), err)
+        try:
+            n, nnz = csr.rows, csr.nnz
+            out = {
+                "row_ptr": np.ctypeslib.as_array(csr.row_ptr, (n + 1,)).copy(),
+                "col_idx": np.ctypeslib.as_array(csr.col_idx, (max(nnz, 1),))[:nnz].copy(),
+                "values": np.ctypeslib.as_array(csr.values, (max(nnz, 1),))[:nnz].copy(),
+                "rhs": np.ctypeslib.as_array(csr.rhs, (max(n, 1),))[:n].copy(),
+            }
+        finally:
+            lib().nlfem_gpu_free_csr(C.byref(csr))
+        return out
+
+    def pairs(self) -> dict:
+        """Element-pair list of the last run (set parity): offsets per interior
+        outer element, partner ids and 5-bit-per-quad-point class codes."""
+        L = lib()
+        n = C.c_int64()
+        err = C.create_string_buffer(512)
+        _check(L.nlfem_gpu_session_pairs(self._h, C.byref(n), None, None, None, err, 512), err)
+        ki = int((self.table.region == 0).sum())
+        off = np.empty(ki + 1, np.int64)
+        partner = np.empty(max(n.value, 1), np.int32)
+        info = np.empty(max(n.value, 1), np.uint32)
+        _check(L.nlfem_gpu_session_pairs(self._h, C.byref(n), _p(off), _p(partner), _p(info),
+                                         err, 512), err)
+        return {"offsets": off, "partner": partner[:n.value], "info": info[:n.value],
+                "interior": np.nonzero(self.table.region == 0)[0].astype(np.int32)}
+
+    def launches(self) -> int:
+        return int(lib().nlfem_gpu_session_launches(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nlfem_gpu_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
+             normalization: str = "mass", problem_terms=None, seed: int = 0x5EED,
+             mc_samples: int = 200, device: int = -1) -> tuple[dict, dict]:
+    """One call through nlfem_gpu_assemble (host arrays in, host CSR out)."""
+    if strategy not in STRATEGIES:
+        raise NlfemError(8, f"BadConfig: unknown strategy '{strategy}'")
+    L = lib()
+    Cn = kernel_constant(delta, normalization)
+    u = default_problem_terms() if problem_terms is None else _check_terms(problem_terms)
+    f = forcing_terms(delta, u, normalization)
+    m, d = table._structs()
+    fp, fk = _poly_struct(f)
+    gp, gk = _poly_struct(u)
+    cfg = _Config(STRATEGIES.index(strategy), int(mc_samples), int(seed) & (2**64 - 1), 0,
+                  int(device))
+    csr, st = _Csr(), Stats()
+    err = C.create_string_buffer(1024)
+    rc = L.nlfem_gpu_assemble(C.byref(m), C.byref(d), C.byref(_Kernel(Cn, float(delta))),
+                              C.byref(fp), C.byref(gp), C.byref(cfg), C.byref(csr), C.byref(st),
+                              err, 1024)
+    _check(rc, err)
+    try:
+        n, nnz = csr.rows, csr.nnz
+        out = {
+            "row_ptr": np.ctypeslib.as_array(csr.row_ptr, (n + 1,)).copy(),
+            "col_idx": np.ctypeslib.as_array(csr.col_idx, (max(nnz, 1),))[:nnz].copy(),
+            "values": np.ctypeslib.as_array(csr.values, (max(nnz, 1),))[:nnz].copy(),
+            "rhs": np.ctypeslib.as_array(csr.rhs, (max(n, 1),))[:n].copy(),
+        }
+    finally:
+        L.nlfem_gpu_free_csr(C.byref(csr))
+    return out, st.as_dict()
+
+
+def assemble_system(coords, cells, region, delta, strategy="nocaps", normalization="mass",
+                    problem_terms=None, threads=0, seed=0x5EED, mc_samples=200) -> dict:
+    """Mirror of the reference's nlfem.assemble_system (nlfem_module.cpp:202-227).
+
+    `threads` is accepted for signature compatibility; one host thread drives
+    the GPU."""
+    t0 = time.perf_counter()
+    table = ElementTable(coords, cells, region)
+    out, st = assemble(table, delta, strategy, normalization, problem_terms, seed, mc_samples)
+    out["node_of_dof"] = table.node_of_dof
+    out["constrained"] = table.constrained
+    out["assembly_s"] = st["seconds"]
+    out["threads"] = 1
+    out["stats"] = st
+    out["wall_s"] = time.perf_counter() - t0
+    return out
+
+
+__all__ = ["NlfemError", "assemble_system", "assemble", "generate_mesh", "ElementTable",
+           "Session", "Stats", "strategy_names", "kernel_constant", "forcing_terms",
+           "default_problem_terms", "lib", "LIB_PATH"]

@@ -1,0 +1,222 @@
+// geom.cuh -- device restatement of the reference's simplex/ball geometry.
+//
+// Every function keeps the reference's operation order; the translation unit
+// is compiled with -fmad=false so nvcc cannot contract a*b+c into DFMA.  With
+// IEEE +,-,*,/,sqrt on both sides the results are bit-identical to the
+// reference's (x86-64, FMA-free) binary, which is what makes the element-pair
+// sets, the straddle sub-simplices and hence the sparsity pattern bit-exact.
+#pragma once
+#include <cstdint>
+
+struct Vd {
+  double x, y, z;
+};
+
+__device__ __forceinline__ Vd vsub(Vd a, Vd b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ Vd vadd(Vd a, Vd b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ Vd vscale(double s, Vd a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ double vdot(Vd a, Vd b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ Vd vcross(Vd a, Vd b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double vnorm2(Vd a) { return vdot(a, a); }
+__device__ __forceinline__ double vdist(Vd a, Vd b) { return sqrt(vnorm2(vsub(a, b))); }
+
+// Outer/inner degree-2 tetrahedral rule (reference quadrature.cpp:22-29).
+#define NLFEM_QA 0.5854101966249685
+#define NLFEM_QB 0.1381966011250105
+__device__ __forceinline__ double qbary(int k, int i) { return k == i ? NLFEM_QA : NLFEM_QB; }
+
+// Quadrature point: p = b0*v0; p = p + b_i*v_i (reference assembly.cpp:689-694).
+__device__ __forceinline__ Vd quad_point(const Vd v[4], int k) {
+  Vd p = vscale(qbary(k, 0), v[0]);
+  for (int i = 1; i < 4; ++i) p = vadd(p, vscale(qbary(k, i), v[i]));
+  return p;
+}
+
+// simplex_volume (reference geometry.cpp:59-62); tet_volume (ball_approx.cpp:144-146).
+__device__ __forceinline__ double tet_volume(Vd a, Vd b, Vd c, Vd d) {
+  return fabs(vdot(vcross(vsub(b, a), vsub(c, a)), vsub(d, a))) / 6.0;
+}
+
+// classify_simplex inside flags (reference geometry.cpp:8-24): bit i set iff
+// |v_i - c|^2 < (r - 1e-10 r)^2.
+__device__ __forceinline__ int inside_mask(const Vd v[4], Vd c, double r) {
+  const double r_in = r - 1e-10 * r;
+  const double r2 = r_in * r_in;
+  int m = 0;
+  for (int i = 0; i < 4; ++i)
+    if (vnorm2(vsub(v[i], c)) < r2) m |= 1 << i;
+  return m;
+}
+
+// edge_sphere_crossing (reference geometry.cpp:26-37).
+__device__ __forceinline__ double edge_crossing(Vd a, Vd b, Vd c, double r) {
+  const Vd d = vsub(b, a);
+  const Vd u = vsub(a, c);
+  const double A = vnorm2(d);
+  const double B = vdot(u, d);
+  const double C = vnorm2(u) - r * r;
+  double disc = B * B - A * C;
+  if (disc < 0) disc = 0;
+  const double sq = sqrt(disc);
+  double t = (B <= 0) ? (-B + sq) / A : -C / (B + sq);
+  return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+}
+
+// crossing_points (reference geometry.cpp:39-50): inside slots ascending, then
+// outside slots ascending; at most 4 for a tetrahedron.
+__device__ __forceinline__ int crossing_points(const Vd v[4], int mask, Vd c, double r, Vd q[4]) {
+  int n = 0;
+  for (int i = 0; i < 4; ++i) {
+    if (!(mask >> i & 1)) continue;
+    for (int o = 0; o < 4; ++o) {
+      if (mask >> o & 1) continue;
+      const double t = edge_crossing(v[i], v[o], c, r);
+      q[n++] = vadd(v[i], vscale(t, vsub(v[o], v[i])));
+    }
+  }
+  return n;
+}
+
+struct Tet {
+  Vd v[4];
+};
+
+// push_piece (reference ball_approx.cpp:135-142): keep iff volume > tau.
+__device__ __forceinline__ void push_piece(Tet* out, int& n, Vd a, Vd b, Vd c, Vd d, double tau) {
+  if (tet_volume(a, b, c, d) > tau) {
+    out[n].v[0] = a;
+    out[n].v[1] = b;
+    out[n].v[2] = c;
+    out[n].v[3] = d;
+    ++n;
+  }
+}
+
+// split_prism / split_warped_prism (reference ball_approx.cpp:150-175).
+__device__ __forceinline__ void split_prism(Tet* out, int& n, const Vd A[3], const Vd B[3],
+                                            double tau) {
+  push_piece(out, n, A[0], A[1], A[2], B[0], tau);
+  push_piece(out, n, A[1], A[2], B[0], B[1], tau);
+  push_piece(out, n, A[2], B[0], B[1], B[2], tau);
+}
+
+__device__ __forceinline__ void split_warped_prism(Tet* out, int& n, const Vd A[3],
+                                                   const Vd B[3], double tau) {
+  const double va = tet_volume(A[0], A[1], A[2], B[0]) + tet_volume(A[1], A[2], B[0], B[1]) +
+                    tet_volume(A[2], B[0], B[1], B[2]);
+  const double vb = tet_volume(A[0], A[2], A[1], B[0]) + tet_volume(A[2], A[1], B[0], B[2]) +
+                    tet_volume(A[1], B[0], B[2], B[1]);
+  if (vb > va) {
+    const Vd A2[3] = {A[0], A[2], A[1]};
+    const Vd B2[3] = {B[0], B[2], B[1]};
+    split_prism(out, n, A2, B2, tau);
+  } else {
+    split_prism(out, n, A, B, tau);
+  }
+}
+
+// detail::straddle_inner without sphere points (reference ball_approx.cpp:195-255).
+__device__ __forceinline__ int straddle_inner(const Vd v[4], int mask, Vd c, double r,
+                                              double tau, Tet out[3]) {
+  Vd q[4];
+  crossing_points(v, mask, c, r, q);
+  int in_slot[4], m = 0;
+  for (int i = 0; i < 4; ++i)
+    if (mask >> i & 1) in_slot[m++] = i;
+  int n = 0;
+  if (m == 1) {
+    push_piece(out, n, v[in_slot[0]], q[0], q[1], q[2], tau);
+  } else if (m == 2) {
+    const Vd A[3] = {v[in_slot[0]], q[0], q[1]};
+    const Vd B[3] = {v[in_slot[1]], q[2], q[3]};
+    split_warped_prism(out, n, A, B, tau);
+  } else {
+    const Vd A[3] = {v[in_slot[0]], v[in_slot[1]], v[in_slot[2]]};
+    const Vd B[3] = {q[0], q[1], q[2]};
+    split_prism(out, n, A, B, tau);
+  }
+  return n;
+}
+
+// detail::straddle_outer (reference ball_approx.cpp:257-298).
+__device__ __forceinline__ int straddle_outer(const Vd v[4], int mask, Vd c, double r,
+                                              double tau, Tet out[3]) {
+  Vd q[4];
+  crossing_points(v, mask, c, r, q);
+  int out_slot[4], m = 0, mo = 0;
+  for (int i = 0; i < 4; ++i) {
+    if (mask >> i & 1) ++m;
+    else out_slot[mo++] = i;
+  }
+  int n = 0;
+  if (m == 1) {
+    const Vd A[3] = {q[0], q[1], q[2]};
+    const Vd B[3] = {v[out_slot[0]], v[out_slot[1]], v[out_slot[2]]};
+    split_prism(out, n, A, B, tau);
+  } else if (m == 2) {
+    const Vd A[3] = {v[out_slot[0]], q[0], q[2]};
+    const Vd B[3] = {v[out_slot[1]], q[1], q[3]};
+    split_warped_prism(out, n, A, B, tau);
+  } else {
+    push_piece(out, n, v[out_slot[0]], q[0], q[1], q[2], tau);
+  }
+  return n;
+}
+
+// point_triangle_distance, Ericson's region walk (reference geometry.cpp:98-127).
+__device__ __forceinline__ double point_triangle_distance(Vd p, Vd a, Vd b, Vd c) {
+  const Vd ab = vsub(b, a), ac = vsub(c, a), ap = vsub(p, a);
+  const double d1 = vdot(ab, ap), d2 = vdot(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return vdist(p, a);
+  const Vd bp = vsub(p, b);
+  const double d3 = vdot(ab, bp), d4 = vdot(ac, bp);
+  if (d3 >= 0 && d4 <= d3) return vdist(p, b);
+  const double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) {
+    const double t = d1 / (d1 - d3);
+    return vdist(p, vadd(a, vscale(t, ab)));
+  }
+  const Vd cp = vsub(p, c);
+  const double d5 = vdot(ab, cp), d6 = vdot(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return vdist(p, c);
+  const double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) {
+    const double t = d2 / (d2 - d6);
+    return vdist(p, vadd(a, vscale(t, ac)));
+  }
+  const double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) {
+    const double t = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    return vdist(p, vadd(b, vscale(t, vsub(c, b))));
+  }
+  const double denom = 1.0 / (va + vb + vc);
+  const double vv = vb * denom, w = vc * denom;
+  return vdist(p, vadd(vadd(a, vscale(vv, ab)), vscale(w, ac)));
+}
+
+// distance_point_simplex (reference geometry.cpp:64-82, 129-144).
+__device__ __forceinline__ double distance_point_simplex(Vd p, const Vd v[4]) {
+  const Vd e1 = vsub(v[1], v[0]), e2 = vsub(v[2], v[0]), e3 = vsub(v[3], v[0]);
+  const Vd b = vsub(p, v[0]);
+  const double det = vdot(e1, vcross(e2, e3));
+  const double l1 = vdot(b, vcross(e2, e3)) / det;
+  const double l2 = vdot(e1, vcross(b, e3)) / det;
+  const double l3 = vdot(e1, vcross(e2, b)) / det;
+  const double l0 = 1.0 - l1 - l2 - l3;
+  if (!(l0 < 0) && !(l1 < 0) && !(l2 < 0) && !(l3 < 0)) return 0.0;
+  double d = point_triangle_distance(p, v[1], v[2], v[3]);
+  d = fmin(d, point_triangle_distance(p, v[0], v[2], v[3]));
+  d = fmin(d, point_triangle_distance(p, v[0], v[1], v[3]));
+  return fmin(d, point_triangle_distance(p, v[0], v[1], v[2]));
+}
+
+// detail::facet_distance (reference ball_approx.cpp:122-131).
+__device__ __forceinline__ double facet_distance(const Vd v[4], int slot, Vd p) {
+  Vd f[3];
+  int k = 0;
+  for (int i = 0; i < 4; ++i)
+    if (i != slot) f[k++] = v[i];
+  return point_triangle_distance(p, f[0], f[1], f[2]);
+}

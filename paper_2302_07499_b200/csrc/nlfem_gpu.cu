@@ -1,0 +1,1735 @@
+// nlfem_gpu.cu -- B200 (sm_100a) nonlocal stiffness assembly behind the C-ABI
+// declared in include/nlfem_gpu.h.  Drop-in for nlfem::assemble
+// (reference proj/src/assembly.cpp:617-843) for the barycenter, nocaps and
+// fullcaps strategies.
+//
+// Pipeline (one CUDA stream, DESIGN.md has the roofline of each stage):
+//   prep      element records (128 B/elem), uniform grid over element centers,
+//             node->element incidence, per-row fixed-point scales
+//   K1 pairs  warp per outer element T: grid candidates, the reference's exact
+//             per-(T,q,T') predicates -> element-pair list with 5-bit class
+//             codes per quadrature point (two passes: count, fill)
+//   K5 pattern node rows R(i) = nodes of partners of T ∋ i, S = R ∪ R^T,
+//             mirror slots, element edge slots, unknown-only output CSR
+//   K3/K4     CTA per outer element: closed-form whole elements, Gauss on
+//             straddle sub-simplices (thread per pair), Philox Monte Carlo caps
+//             (warp per cap item) -> 4x4 element-pair blocks, scattered as
+//             exact int64 fixed point into the node pattern
+//   K6        fixed point -> FP64, mirror, constraint folding into the rhs
+//
+// Determinism: every value that reaches the matrix is a deterministic FP64
+// number converted to int64 with a power-of-two per-row scale; integer adds
+// are associative, so the result is bitwise identical for any launch order,
+// block count or GPU count.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "geom.cuh"
+#include "nlfem_gpu.h"
+#include "nlfem_mc_stream.h"
+
+#define FULLMASK 0xffffffffu
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      throw Fail{NLFEM_GPU_ENODEVICE, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+void put_err(char* err, size_t len, const std::string& m) {
+  if (!err || len == 0) return;
+  std::strncpy(err, m.c_str(), len - 1);
+  err[len - 1] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// device parameter block
+
+constexpr int kMaxTerms = 32;
+
+struct Poly {
+  int n;
+  double c[kMaxTerms];
+  int e[kMaxTerms][3];
+};
+
+__device__ __forceinline__ double poly_eval(const Poly& P, Vd p) {
+  // Polynomial::eval (reference polynomial.cpp:28-37)
+  double acc = 0;
+  for (int t = 0; t < P.n; ++t) {
+    double v = P.c[t];
+    for (int i = 0; i < P.e[t][0]; ++i) v *= p.x;
+    for (int i = 0; i < P.e[t][1]; ++i) v *= p.y;
+    for (int i = 0; i < P.e[t][2]; ++i) v *= p.z;
+    acc += v;
+  }
+  return acc;
+}
+
+struct Dev {
+  int K, J, KI, unknowns;
+  int strategy, mc;
+  unsigned long long seed;
+  double C, delta, slack, inside_cut, dd;
+  // element data
+  const double4* erec;  // [4K]: (c, r), (v0, v1.x), (v1.yz, v2.xy), (v2.z, v3)
+  const int4* verts;
+  const int4* nbr;
+  const double* vol;
+  const double* tau;
+  const double* inv;  // [9K]
+  const uint8_t* region;
+  const int* interior;  // [KI]
+  const int* dof;       // [J]
+  const double* node;   // [3J]
+  // grid
+  double gox, goy, goz, ginv, hg, rmax;
+  int gx, gy, gz;
+  const int* cell_start;
+  const int* cell_elems;
+  // node incidence (interior elements) sorted by element id
+  const int* ni_off;
+  const int* ni_el;
+  // fixed point
+  const double* scale;
+  const double* iscale;
+  Poly f, g;
+};
+
+__constant__ Dev cD;
+
+__device__ __forceinline__ void load_elem(int t, Vd& c, double& r, Vd v[4]) {
+  const double4 a = cD.erec[4 * t], b = cD.erec[4 * t + 1], e = cD.erec[4 * t + 2],
+                d = cD.erec[4 * t + 3];
+  c = {a.x, a.y, a.z};
+  r = a.w;
+  v[0] = {b.x, b.y, b.z};
+  v[1] = {b.w, e.x, e.y};
+  v[2] = {e.z, e.w, d.x};
+  v[3] = {d.y, d.z, d.w};
+}
+
+__device__ __forceinline__ void load_verts(int t, Vd v[4]) {
+  const double4 b = cD.erec[4 * t + 1], e = cD.erec[4 * t + 2], d = cD.erec[4 * t + 3];
+  v[0] = {b.x, b.y, b.z};
+  v[1] = {b.w, e.x, e.y};
+  v[2] = {e.z, e.w, d.x};
+  v[3] = {d.y, d.z, d.w};
+}
+
+// ---------------------------------------------------------------------------
+// generic helpers: exclusive scan of int64 counts (3-phase, deterministic)
+
+constexpr int kScanBlock = 1024;
+
+template <class Tin>
+__global__ void k_scan_block(const Tin* in, long long* out, long long* sums, long long n) {
+  __shared__ long long s[kScanBlock];
+  const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
+  s[threadIdx.x] = i < n ? (long long)in[i] : 0;
+  __syncthreads();
+  for (int off = 1; off < kScanBlock; off <<= 1) {
+    long long v = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  if (i < n) out[i] = s[threadIdx.x] - (i < n ? (long long)in[i] : 0);
+  if (threadIdx.x == kScanBlock - 1) sums[blockIdx.x] = s[threadIdx.x];
+}
+
+__global__ void k_scan_add(long long* out, const long long* offs, long long n) {
+  const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
+  if (i < n) out[i] += offs[blockIdx.x];
+}
+
+// ---------------------------------------------------------------------------
+// prep kernels
+
+__global__ void k_erec(int K, const double* node, const int4* verts, const double* center,
+                       const double* radius, double4* erec) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  const int4 w = verts[t];
+  const double* a = node + 3 * (long long)w.x;
+  const double* b = node + 3 * (long long)w.y;
+  const double* c = node + 3 * (long long)w.z;
+  const double* d = node + 3 * (long long)w.w;
+  erec[4 * t] = make_double4(center[3 * t], center[3 * t + 1], center[3 * t + 2], radius[t]);
+  erec[4 * t + 1] = make_double4(a[0], a[1], a[2], b[0]);
+  erec[4 * t + 2] = make_double4(b[1], b[2], c[0], c[1]);
+  erec[4 * t + 3] = make_double4(c[2], d[0], d[1], d[2]);
+}
+
+__device__ __forceinline__ int cell_of(double c, double o, double inv, int n) {
+  int k = (int)floor((c - o) * inv);
+  return k < 0 ? 0 : (k >= n ? n - 1 : k);
+}
+
+__global__ void k_cell_count(int K, int* key, int* cnt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  const double4 a = cD.erec[4 * t];
+  const int cx = cell_of(a.x, cD.gox, cD.ginv, cD.gx);
+  const int cy = cell_of(a.y, cD.goy, cD.ginv, cD.gy);
+  const int cz = cell_of(a.z, cD.goz, cD.ginv, cD.gz);
+  const int k = (cz * cD.gy + cy) * cD.gx + cx;
+  key[t] = k;
+  atomicAdd(cnt + k, 1);
+}
+
+__global__ void k_fill_by_key(int n, const int* key, const long long* off, int* cursor, int* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int k = key[t];
+  const int pos = atomicAdd(cursor + k, 1);
+  out[off[k] + pos] = t;
+}
+
+// Sort each short segment ascending (insertion sort, one thread per segment);
+// makes the atomic fills deterministic.
+__global__ void k_sort_segments(int nseg, const long long* off, int* data) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const long long a = off[s], b = off[s + 1];
+  for (long long i = a + 1; i < b; ++i) {
+    const int x = data[i];
+    long long j = i - 1;
+    while (j >= a && data[j] > x) {
+      data[j + 1] = data[j];
+      --j;
+    }
+    data[j + 1] = x;
+  }
+}
+
+// node -> interior-element incidence (count / fill by (node, elem) items)
+__global__ void k_ninc_count(int K, int* cnt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K || cD.region[t]) return;
+  const int4 w = cD.verts[t];
+  atomicAdd(cnt + w.x, 1);
+  atomicAdd(cnt + w.y, 1);
+  atomicAdd(cnt + w.z, 1);
+  atomicAdd(cnt + w.w, 1);
+}
+
+__global__ void k_ninc_fill(int K, const long long* off, int* cursor, int* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K || cD.region[t]) return;
+  const int4 w = cD.verts[t];
+  const int v[4] = {w.x, w.y, w.z, w.w};
+  for (int i = 0; i < 4; ++i) out[off[v[i]] + atomicAdd(cursor + v[i], 1)] = t;
+}
+
+// per-node patch volume over all elements -> power-of-two fixed-point scale
+__global__ void k_scales(int J, const long long* aoff, const int* ael, double cbound,
+                         double* scale, double* iscale) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  double patch = 0;
+  for (long long k = aoff[i]; k < aoff[i + 1]; ++k) patch += cD.vol[ael[k]];
+  const double bound = cbound * (patch > 0 ? patch : 1e-300);
+  int ex;
+  frexp(bound, &ex);  // bound < 2^ex
+  scale[i] = ldexp(1.0, 61 - ex);
+  iscale[i] = ldexp(1.0, ex - 61);
+}
+
+__global__ void k_all_inc_count(int K, int* cnt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  const int4 w = cD.verts[t];
+  atomicAdd(cnt + w.x, 1);
+  atomicAdd(cnt + w.y, 1);
+  atomicAdd(cnt + w.z, 1);
+  atomicAdd(cnt + w.w, 1);
+}
+
+__global__ void k_all_inc_fill(int K, const long long* off, int* cursor, int* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  const int4 w = cD.verts[t];
+  const int v[4] = {w.x, w.y, w.z, w.w};
+  for (int i = 0; i < 4; ++i) out[off[v[i]] + atomicAdd(cursor + v[i], 1)] = t;
+}
+
+// ---------------------------------------------------------------------------
+// K1: element pairs
+
+// Class codes (5 bits per quadrature point): 0 none, 1 whole element,
+// 2 Monte Carlo cap over the whole element (fullcaps, all vertices outside),
+// 16|mask straddling element with inside-vertex mask 1..14.
+enum : unsigned { kNone = 0, kWhole = 1, kOutCap = 2, kStraddle = 16 };
+
+// Does a nocaps straddler emit at least one inner sub-simplex (volume > tau)?
+// Cheap certificate first: the inner polytope contains a tet of volume
+// >= (depth/diam)^(4-m) vol(T'), depth = delta - |v - x_q| of the deepest
+// inside vertex, and its <= 3 pieces sum to the polytope; otherwise run the
+// exact straddle_inner.
+__device__ __forceinline__ bool inner_pieces_exist(const Vd v[4], int mask, Vd xq, double diam,
+                                                   double vol, double tau) {
+  const int m = __popc(mask);
+  double dmax = 0;
+  for (int i = 0; i < 4; ++i)
+    if (mask >> i & 1) dmax = fmax(dmax, cD.delta - sqrt(vnorm2(vsub(v[i], xq))));
+  const double s = dmax / diam;
+  double f = s;
+  if (m <= 2) f *= s;
+  if (m == 1) f *= s;
+  if (s > 1e-6 && f * vol > 8.0 * tau) return true;
+  Tet pcs[3];
+  return straddle_inner(v, mask, xq, cD.delta, tau, pcs) > 0;
+}
+
+__device__ __forceinline__ bool any_pieces_fullcaps(const Vd v[4], int mask, Vd xq, double vol,
+                                                    double tau) {
+  if (vol > 64.0 * tau) return true;  // inner + outer polytopes cover T'
+  Tet pcs[3];
+  if (straddle_inner(v, mask, xq, cD.delta, tau, pcs) > 0) return true;
+  return straddle_outer(v, mask, xq, cD.delta, tau, pcs) > 0;
+}
+
+// The reference's per-(T,q,T') decision (assembly.cpp:722-759).
+__device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, const Vd v[4],
+                                                  double diam, double vol, double tau) {
+  const double delta = cD.delta;
+  const double gap = vdist(cen, xq);
+  if (gap >= rad + delta) return kNone;
+  if (cD.strategy == NLFEM_STRATEGY_BARYCENTER) return gap < delta ? kWhole : kNone;
+  if (gap + rad < cD.inside_cut) return kWhole;
+  const int mask = inside_mask(v, xq, delta);
+  if (mask == 15) return kWhole;
+  if (mask == 0) {
+    if (cD.strategy == NLFEM_STRATEGY_FULLCAPS && distance_point_simplex(xq, v) < delta)
+      return kOutCap;
+    return kNone;
+  }
+  if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
+    return inner_pieces_exist(v, mask, xq, diam, vol, tau) ? (kStraddle | mask) : kNone;
+  return any_pieces_fullcaps(v, mask, xq, vol, tau) ? (kStraddle | mask) : kNone;
+}
+
+struct OuterT {
+  int T;
+  Vd c;
+  Vd xq[4];
+  double R;
+};
+
+__device__ __forceinline__ void outer_setup(int T, OuterT& o) {
+  Vd v[4];
+  double r;
+  load_elem(T, o.c, r, v);
+  double spread = 0;
+  for (int k = 0; k < 4; ++k) {
+    o.xq[k] = quad_point(v, k);
+    spread = fmax(spread, vdist(o.xq[k], o.c));
+  }
+  o.T = T;
+  o.R = cD.delta + spread;
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_pairs(const long long* pair_off, int* pair_count,
+                                               int* partner, unsigned* info,
+                                               unsigned long long* item_count, int* err_elem) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= cD.KI) return;
+  OuterT o;
+  outer_setup(cD.interior[warp], o);
+  const double reach = o.R + cD.rmax;
+  const int x0 = cell_of(o.c.x - reach, cD.gox, cD.ginv, cD.gx);
+  const int x1 = cell_of(o.c.x + reach, cD.gox, cD.ginv, cD.gx);
+  const int y0 = cell_of(o.c.y - reach, cD.goy, cD.ginv, cD.gy);
+  const int y1 = cell_of(o.c.y + reach, cD.goy, cD.ginv, cD.gy);
+  const int z0 = cell_of(o.c.z - reach, cD.goz, cD.ginv, cD.gz);
+  const int z1 = cell_of(o.c.z + reach, cD.goz, cD.ginv, cD.gz);
+  long long out = FILL ? pair_off[warp] : 0;
+  int cnt = 0;
+  unsigned items = 0;
+  const double reach2 = reach * reach * (1.0 + 1e-9);
+  for (int z = z0; z <= z1; ++z) {
+    const double zl = cD.goz + z * cD.hg, zh = zl + cD.hg;
+    const double dz = o.c.z < zl ? zl - o.c.z : (o.c.z > zh ? o.c.z - zh : 0.0);
+    for (int y = y0; y <= y1; ++y) {
+      const double yl = cD.goy + y * cD.hg, yh = yl + cD.hg;
+      const double dy = o.c.y < yl ? yl - o.c.y : (o.c.y > yh ? o.c.y - yh : 0.0);
+      if (dy * dy + dz * dz > reach2) continue;  // row of cells beyond reach
+      const int row = (z * cD.gy + y) * cD.gx;
+      const int e0 = cD.cell_start[row + x0], e1 = cD.cell_start[row + x1 + 1];
+      for (int base = e0; base < e1; base += 32) {
+        const int e = base + lane;
+        unsigned code = 0;
+        int Tp = -1;
+        if (e < e1) {
+          Tp = cD.cell_elems[e];
+          const double4 a = cD.erec[4 * Tp];
+          const Vd cp = {a.x, a.y, a.z};
+          const double thr = a.w + o.R;
+          if (vnorm2(vsub(cp, o.c)) < thr * thr * (1.0 + 1e-10)) {
+            Vd v[4];
+            load_verts(Tp, v);
+            const double vol = cD.vol[Tp], tau = cD.tau[Tp];
+            double dia = 0;  // ElementTable::diam (ball_approx.cpp:61-67)
+            for (int i = 0; i < 4; ++i)
+              for (int j = i + 1; j < 4; ++j) dia = fmax(dia, vnorm2(vsub(v[i], v[j])));
+            dia = sqrt(dia);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              code |= classify_item(o.xq[k], cp, a.w, v, dia, vol, tau) << (5 * k);
+            if (!FILL) {
+              const int4 nb = cD.nbr[Tp];
+              if (nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) {
+                const int nbv[4] = {nb.x, nb.y, nb.z, nb.w};
+                for (int k = 0; k < 4; ++k)
+                  for (int f = 0; f < 4; ++f)
+                    if (nbv[f] < 0 && facet_distance(v, f, o.xq[k]) < cD.delta - cD.slack)
+                      atomicMin(err_elem, Tp);
+              }
+            }
+          }
+        }
+        const bool keep = code != 0;
+        const unsigned bal = __ballot_sync(FULLMASK, keep);
+        if (FILL && keep) {
+          const long long pos = out + cnt + __popc(bal & ((1u << lane) - 1));
+          partner[pos] = Tp;
+          info[pos] = code;
+        }
+        if (!FILL && keep)
+          for (int k = 0; k < 4; ++k) items += ((code >> (5 * k)) & 31) != 0;
+        cnt += __popc(bal);
+      }
+    }
+  }
+  if (!FILL) {
+    for (int s = 16; s > 0; s >>= 1) items += __shfl_xor_sync(FULLMASK, items, s);
+    if (lane == 0) {
+      pair_count[warp] = cnt;
+      atomicAdd(item_count, (unsigned long long)items);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: pattern
+
+constexpr int kHE = 8192;   // element hash slots per node block
+constexpr int kHN = 4096;   // node hash slots
+constexpr int kRowMax = 4096;
+
+__device__ __forceinline__ unsigned hash32(unsigned x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+// insert key into an open-addressing table of ints (-1 = empty); returns true
+// when newly inserted, sets *ovf when full.
+__device__ __forceinline__ bool hset_insert(int* tab, int cap, int key, int* ovf) {
+  unsigned h = hash32((unsigned)key) & (cap - 1);
+  for (int probe = 0; probe < cap; ++probe) {
+    const int prev = atomicCAS(tab + h, -1, key);
+    if (prev == -1) return true;
+    if (prev == key) return false;
+    h = (h + 1) & (cap - 1);
+  }
+  *ovf = 1;
+  return false;
+}
+
+// block-wide bitonic sort of n <= kRowMax ints in shared memory (ascending)
+__device__ void block_sort(int* a, int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  for (int i = n + threadIdx.x; i < p; i += blockDim.x) a[i] = 0x7fffffff;
+  __syncthreads();
+  for (int k = 2; k <= p; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < p; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const int x = a[i], y = a[ixj];
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// R(i) = sorted nodes of interior partners of every interior T containing node i.
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const int* partner,
+                                              int* rlen, const long long* roff, int* rcols,
+                                              int* ovf) {
+  extern __shared__ int sm[];
+  int* tabE = sm;
+  int* tabN = sm + kHE;
+  int* list = tabN + kHN;
+  __shared__ int nlist;
+  for (int i = blockIdx.x; i < cD.J; i += gridDim.x) {
+    const int a = cD.ni_off[i], b = cD.ni_off[i + 1];
+    if (a == b) {
+      if (!FILL && threadIdx.x == 0) rlen[i] = 0;
+      continue;
+    }
+    for (int s = threadIdx.x; s < kHE; s += blockDim.x) tabE[s] = -1;
+    for (int s = threadIdx.x; s < kHN; s += blockDim.x) tabN[s] = -1;
+    if (threadIdx.x == 0) nlist = 0;
+    __syncthreads();
+    for (int k = a; k < b; ++k) {
+      const int T = cD.ni_el[k];
+      // position of T in the interior list: interior ids ascending -> binary search
+      int lo = 0, hi = cD.KI - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cD.interior[mid] < T) lo = mid + 1;
+        else hi = mid;
+      }
+      const long long p0 = pair_off[lo], p1 = pair_off[lo + 1];
+      for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const int Tp = partner[p];
+        if (cD.region[Tp] == 0) hset_insert(tabE, kHE, Tp, ovf);
+      }
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < kHE; s += blockDim.x) {
+      const int Tp = tabE[s];
+      if (Tp < 0) continue;
+      const int4 w = cD.verts[Tp];
+      const int vv[4] = {w.x, w.y, w.z, w.w};
+      for (int q = 0; q < 4; ++q)
+        if (hset_insert(tabN, kHN, vv[q], ovf)) {
+          const int pos = atomicAdd(&nlist, 1);
+          if (pos < kRowMax) list[pos] = vv[q];
+          else *ovf = 1;
+        }
+    }
+    __syncthreads();
+    const int n = nlist < kRowMax ? nlist : kRowMax;
+    if (!FILL) {
+      if (threadIdx.x == 0) rlen[i] = n;
+    } else {
+      block_sort(list, n);
+      const long long o = roff[i];
+      for (int s = threadIdx.x; s < n; s += blockDim.x) rcols[o + s] = list[s];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_col_count(long long n, const int* cols, int* cnt) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) atomicAdd(cnt + cols[k], 1);
+}
+
+__global__ void k_transpose_fill(int J, const long long* roff, const int* rcols,
+                                 const long long* toff, int* cursor, int* tcols) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  for (long long k = roff[i]; k < roff[i + 1]; ++k) {
+    const int j = rcols[k];
+    tcols[toff[j] + atomicAdd(cursor + j, 1)] = i;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sort_rows(int J, const long long* off, int* cols,
+                                                   int* ovf) {
+  extern __shared__ int sm[];
+  for (int i = blockIdx.x; i < J; i += gridDim.x) {
+    const long long a = off[i];
+    const int n = (int)(off[i + 1] - a);
+    if (n <= 1) continue;
+    if (n > kRowMax) {
+      if (threadIdx.x == 0) *ovf = 1;
+      continue;
+    }
+    for (int s = threadIdx.x; s < n; s += blockDim.x) sm[s] = cols[a + s];
+    __syncthreads();
+    block_sort(sm, n);
+    for (int s = threadIdx.x; s < n; s += blockDim.x) cols[a + s] = sm[s];
+    __syncthreads();
+  }
+}
+
+// S(i) = R(i) ∪ R^T(i), both sorted
+template <bool FILL>
+__global__ void k_union(int J, const long long* roff, const int* rcols, const long long* toff,
+                        const int* tcols, int* slen, const long long* soff, int* scols,
+                        int* maxlen) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  long long a = roff[i];
+  const long long ae = roff[i + 1];
+  long long b = toff[i];
+  const long long be = toff[i + 1];
+  long long o = FILL ? soff[i] : 0;
+  int n = 0;
+  while (a < ae || b < be) {
+    int x;
+    if (b >= be || (a < ae && rcols[a] < tcols[b])) x = rcols[a++];
+    else if (a >= ae || tcols[b] < rcols[a]) x = tcols[b++];
+    else {
+      x = rcols[a++];
+      ++b;
+    }
+    if (FILL) scols[o + n] = x;
+    ++n;
+  }
+  if (!FILL) {
+    slen[i] = n;
+    atomicMax(maxlen, n);
+  }
+}
+
+__device__ __forceinline__ long long find_slot(const long long* soff, const int* scols, int i,
+                                               int j) {
+  long long lo = soff[i], hi = soff[i + 1] - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (scols[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo <= hi && scols[lo] == j) ? lo : -1;
+}
+
+__global__ void k_mirror(int J, const long long* soff, const int* scols, long long* mirror,
+                         int* ovf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  for (long long k = soff[i]; k < soff[i + 1]; ++k) {
+    const int j = scols[k];
+    const long long m = find_slot(soff, scols, j, i);
+    if (m < 0) *ovf = 2;
+    mirror[k] = m;
+  }
+}
+
+// the 10 (b <= b') slots of each interior element's node pairs, stored at
+// row min(M_b, M_b')
+__global__ void k_edge_slots(const long long* soff, const int* scols, long long* eslot,
+                             int* ovf) {
+  const int ii = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ii >= cD.KI) return;
+  const int4 w = cD.verts[cD.interior[ii]];
+  const int v[4] = {w.x, w.y, w.z, w.w};
+  int k = 0;
+  for (int b = 0; b < 4; ++b)
+    for (int c = b; c < 4; ++c, ++k) {
+      const int lo = min(v[b], v[c]), hi = max(v[b], v[c]);
+      const long long s = find_slot(soff, scols, lo, hi);
+      if (s < 0) *ovf = 3;
+      eslot[10 * (long long)ii + k] = s;
+    }
+}
+
+// output pattern: rows = unknown nodes (dof order), columns = unknown nodes
+template <bool FILL>
+__global__ void k_outpat(const long long* soff, const int* scols, int* olen,
+                         const long long* ooff, int* ocols, long long* omap, const int* dof_node) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= cD.unknowns) return;
+  const int i = dof_node[d];
+  int n = 0;
+  const long long o = FILL ? ooff[d] : 0;
+  for (long long k = soff[i]; k < soff[i + 1]; ++k) {
+    const int dj = cD.dof[scols[k]];
+    if (dj < 0) continue;
+    if (FILL) {
+      ocols[o + n] = dj;
+      omap[o + n] = k;
+    }
+    ++n;
+  }
+  if (!FILL) olen[d] = n;
+}
+
+// ---------------------------------------------------------------------------
+// K3/K4: integration + scatter
+
+constexpr int kIntThreads = 128;
+
+struct McSlot {
+  nlfem_mc_frame fr[3];
+  double w[3];
+  double c0[3];  // x_q - v0(T')
+  int Tp, nsub, constr, q;
+};
+
+__device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot, double v,
+                                          double scale) {
+  const long long x = __double2ll_rn(v * scale);
+  if (x != 0) atomicAdd(V + slot, (unsigned long long)x);
+}
+
+// butterfly sum over the warp (fixed tree -> deterministic)
+__device__ __forceinline__ double wsum(double v) {
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULLMASK, v, s);
+  return v;
+}
+
+// S2 index of (b, c), b <= c
+__device__ __forceinline__ int s2i(int b, int c) { return b * 4 - (b * (b - 1)) / 2 + (c - b); }
+
+struct PairAcc {
+  double S0[4], S1[4][4], S2[10], Sg[4];
+};
+
+__device__ __forceinline__ void acc_point_interior(PairAcc& A, int q, double w, const double l[4]) {
+  A.S0[q] += w;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const double wb = w * l[b];
+    A.S1[q][b] += wb;
+#pragma unroll
+    for (int c = b; c < 4; ++c) A.S2[s2i(b, c)] += wb * l[c];
+  }
+}
+
+// ElementTable::bary (reference ball_approx.cpp:100-115)
+__device__ __forceinline__ void bary(const double inv[9], Vd v0, Vd p, double l[4]) {
+  const Vd d = vsub(p, v0);
+  l[1] = inv[0] * d.x + inv[1] * d.y + inv[2] * d.z;
+  l[2] = inv[3] * d.x + inv[4] * d.y + inv[5] * d.z;
+  l[3] = inv[6] * d.x + inv[7] * d.y + inv[8] * d.z;
+  l[0] = 1.0 - l[1] - l[2] - l[3];
+}
+
+__global__ void __launch_bounds__(kIntThreads) k_integrate(
+    const long long* pair_off, const int* partner, const unsigned* info, const long long* soff,
+    const int* scols, const long long* eslot, unsigned long long* V, double* rhsT,
+    unsigned long long* mc_stats, int rowcap) {
+  extern __shared__ unsigned char smraw[];
+  McSlot* slots = reinterpret_cast<McSlot*>(smraw);
+  int* rows = reinterpret_cast<int*>(slots + kIntThreads);  // 4 staged rows
+  __shared__ long long rbase[4];
+  __shared__ int rlen[4];
+  __shared__ double red[kIntThreads / 32][14];
+
+  const int ii = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int T = cD.interior[ii];
+  Vd vT[4], cT;
+  double rT;
+  load_elem(T, cT, rT, vT);
+  const int4 wT = cD.verts[T];
+  const int NT[4] = {wT.x, wT.y, wT.z, wT.w};
+  const double wq = 0.25 * cD.vol[T];  // rule.w[k] * vol (reference assembly.cpp:702)
+  const double C = cD.C;
+  Vd xq[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) xq[k] = quad_point(vT, k);
+
+  // stage the four T-node rows of the node pattern (sorted columns)
+  if (threadIdx.x < 4) {
+    rbase[threadIdx.x] = soff[NT[threadIdx.x]];
+    rlen[threadIdx.x] = (int)(soff[NT[threadIdx.x] + 1] - soff[NT[threadIdx.x]]);
+  }
+  __syncthreads();
+  for (int a = 0; a < 4; ++a)
+    for (int s = threadIdx.x; s < rlen[a]; s += blockDim.x) rows[a * rowcap + s] = scols[rbase[a] + s];
+  __syncthreads();
+
+  double DT[10];
+  double rhsc[4];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) DT[k] = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) rhsc[a] = 0;
+  unsigned long long n_samp = 0, n_hit = 0;
+
+  const long long p0 = pair_off[ii], p1 = pair_off[ii + 1];
+  const long long np = p1 - p0;
+  const int rounds = (int)((np + kIntThreads - 1) / kIntThreads);
+  const bool fullcaps = cD.strategy == NLFEM_STRATEGY_FULLCAPS;
+
+  for (int rd = 0; rd < rounds; ++rd) {
+    const long long p = p0 + (long long)rd * kIntThreads + threadIdx.x;
+    const bool valid = p < p1;
+    PairAcc A;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      A.S0[q] = 0;
+      A.Sg[q] = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) A.S1[q][b] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 10; ++k) A.S2[k] = 0;
+
+    int Tp = 0;
+    unsigned code = 0;
+    Vd vP[4], cP;
+    double rP = 0, volP = 0, tauP = 0;
+    double invP[9];
+    bool constr = false;
+    int4 wP = make_int4(0, 0, 0, 0);
+    if (valid) {
+      Tp = partner[p];
+      code = info[p];
+      load_elem(Tp, cP, rP, vP);
+      volP = cD.vol[Tp];
+      tauP = cD.tau[Tp];
+      constr = cD.region[Tp] != 0;
+      wP = cD.verts[Tp];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) invP[k] = cD.inv[9 * (long long)Tp + k];
+    }
+
+    // ---- thread level: whole elements and Gauss sub-simplices
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned c = (code >> (5 * q)) & 31;
+      if (c == kWhole) {
+        if (constr) {
+          // constraint parent: measure and g average (reference assembly.cpp:350-359)
+          A.S0[q] += volP;
+          for (int k = 0; k < 4; ++k) A.Sg[q] += volP * 0.25 * poly_eval(cD.g, quad_point(vP, k));
+        } else {
+          // exact basis moments of a whole element (reference assembly.cpp:361-369)
+          A.S0[q] += volP;
+          const double s1 = volP / 4, off = volP / 20.0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            A.S1[q][b] += s1;
+#pragma unroll
+            for (int cc = b; cc < 4; ++cc) A.S2[s2i(b, cc)] += off * (b == cc ? 2.0 : 1.0);
+          }
+        }
+      } else if (c & kStraddle) {
+        Tet pcs[3];
+        const int n = straddle_inner(vP, (int)(c & 15), xq[q], cD.delta, tauP, pcs);
+        for (int s = 0; s < n; ++s) {
+          const double vs = tet_volume(pcs[s].v[0], pcs[s].v[1], pcs[s].v[2], pcs[s].v[3]);
+          for (int k = 0; k < 4; ++k) {
+            const Vd y = quad_point(pcs[s].v, k);
+            const double w = vs * 0.25;
+            if (constr) {
+              A.S0[q] += w;
+              A.Sg[q] += w * poly_eval(cD.g, y);
+            } else {
+              double l[4];
+              bary(invP, vP[0], y, l);
+              acc_point_interior(A, q, w, l);
+            }
+          }
+        }
+      }
+    }
+
+    // ---- warp level: Monte Carlo caps (fullcaps)
+    if (fullcaps) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned c = (code >> (5 * q)) & 31;
+        int nsub = 0;
+        McSlot& my = slots[threadIdx.x];
+        if (c == kOutCap) {
+          nsub = 1;
+          nlfem_mc_frame fr;
+          const double v0[3] = {vP[0].x, vP[0].y, vP[0].z}, v1[3] = {vP[1].x, vP[1].y, vP[1].z},
+                       v2[3] = {vP[2].x, vP[2].y, vP[2].z}, v3[3] = {vP[3].x, vP[3].y, vP[3].z},
+                       x[3] = {xq[q].x, xq[q].y, xq[q].z};
+          nlfem_mc_make_frame(v0, v1, v2, v3, x, &fr);
+          my.fr[0] = fr;
+          my.w[0] = tet_volume(vP[0], vP[1], vP[2], vP[3]) / cD.mc;
+        } else if (c & kStraddle) {
+          Tet pcs[3];
+          nsub = straddle_outer(vP, (int)(c & 15), xq[q], cD.delta, tauP, pcs);
+          for (int s = 0; s < nsub; ++s) {
+            const Vd* u = pcs[s].v;
+            const double v0[3] = {u[0].x, u[0].y, u[0].z}, v1[3] = {u[1].x, u[1].y, u[1].z},
+                         v2[3] = {u[2].x, u[2].y, u[2].z}, v3[3] = {u[3].x, u[3].y, u[3].z},
+                         x[3] = {xq[q].x, xq[q].y, xq[q].z};
+            nlfem_mc_make_frame(v0, v1, v2, v3, x, &my.fr[s]);
+            my.w[s] = tet_volume(u[0], u[1], u[2], u[3]) / cD.mc;
+          }
+        }
+        if (nsub > 0) {
+          my.nsub = nsub;
+          my.Tp = Tp;
+          my.constr = constr;
+          my.c0[0] = xq[q].x - vP[0].x;
+          my.c0[1] = xq[q].y - vP[0].y;
+          my.c0[2] = xq[q].z - vP[0].z;
+        }
+        unsigned pend = __ballot_sync(FULLMASK, nsub > 0);
+        __syncwarp();
+        while (pend) {
+          const int L = __ffs(pend) - 1;
+          pend &= pend - 1;
+          const McSlot& it = slots[wid * 32 + L];
+          const int ns = it.nsub, cons = it.constr, tp = it.Tp;
+          const int gps = (cD.mc + 3) >> 2;  // sample blocks per sub-simplex
+          const int G = ns * gps;
+          double n0 = 0, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
+          unsigned hits = 0;
+          for (int gI = lane; gI < G; gI += 32) {
+            const int sub = (gI >= gps) + (gI >= 2 * gps);
+            const int j = gI - sub * gps;
+            uint32_t W[12];
+            nlfem_mc_block(cD.seed, (uint32_t)T, (uint32_t)tp, (uint32_t)q, (uint32_t)sub,
+                           (uint32_t)j, W);
+            const nlfem_mc_frame fr = it.fr[sub];
+            const double w = it.w[sub];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (4 * j + i >= cD.mc) break;
+              double r[3];
+              if (nlfem_mc_point(W[3 * i], W[3 * i + 1], W[3 * i + 2], &fr, cD.dd, r)) {
+                ++hits;
+                if (cons) {
+                  n0 += w;
+                  sg += w * poly_eval(cD.g, {xq[q].x + r[0], xq[q].y + r[1], xq[q].z + r[2]});
+                } else {
+                  const double rx = r[0] + it.c0[0], ry = r[1] + it.c0[1], rz = r[2] + it.c0[2];
+                  n0 += w;
+                  const double tx = w * rx, ty = w * ry, tz = w * rz;
+                  m1x += tx;
+                  m1y += ty;
+                  m1z += tz;
+                  m2[0] = fma(tx, rx, m2[0]);
+                  m2[1] = fma(tx, ry, m2[1]);
+                  m2[2] = fma(tx, rz, m2[2]);
+                  m2[3] = fma(ty, ry, m2[3]);
+                  m2[4] = fma(ty, rz, m2[4]);
+                  m2[5] = fma(tz, rz, m2[5]);
+                }
+              }
+            }
+          }
+          n_hit += hits;
+          n0 = wsum(n0);
+          if (cons) {
+            sg = wsum(sg);
+            if (lane == L) {
+              A.S0[q] += n0;
+              A.Sg[q] += sg;
+            }
+          } else {
+            m1x = wsum(m1x);
+            m1y = wsum(m1y);
+            m1z = wsum(m1z);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) m2[k] = wsum(m2[k]);
+            if (lane == L) {
+              // lambda(y) = e_0 + J (y - v0), J rows from inv_edges
+              double Jr[4][3];
+              Jr[1][0] = invP[0]; Jr[1][1] = invP[1]; Jr[1][2] = invP[2];
+              Jr[2][0] = invP[3]; Jr[2][1] = invP[4]; Jr[2][2] = invP[5];
+              Jr[3][0] = invP[6]; Jr[3][1] = invP[7]; Jr[3][2] = invP[8];
+              for (int a = 0; a < 3; ++a) Jr[0][a] = -(Jr[1][a] + Jr[2][a] + Jr[3][a]);
+              const double M[3][3] = {{m2[0], m2[1], m2[2]}, {m2[1], m2[3], m2[4]},
+                                      {m2[2], m2[4], m2[5]}};
+              double jm[4];
+              double JM[4][3];
+              for (int b = 0; b < 4; ++b) {
+                jm[b] = Jr[b][0] * m1x + Jr[b][1] * m1y + Jr[b][2] * m1z;
+                for (int a = 0; a < 3; ++a)
+                  JM[b][a] = Jr[b][0] * M[0][a] + Jr[b][1] * M[1][a] + Jr[b][2] * M[2][a];
+              }
+              A.S0[q] += n0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                A.S1[q][b] += (b == 0 ? n0 : 0.0) + jm[b];
+#pragma unroll
+                for (int cc = b; cc < 4; ++cc) {
+                  double s2 = JM[b][0] * Jr[cc][0] + JM[b][1] * Jr[cc][1] + JM[b][2] * Jr[cc][2];
+                  if (b == 0) s2 += jm[cc];
+                  if (cc == 0) s2 += jm[b];
+                  if (b == 0 && cc == 0) s2 += n0;
+                  A.S2[s2i(b, cc)] += s2;
+                }
+              }
+            }
+          }
+          if (lane == L) n_samp += (unsigned long long)ns * (unsigned long long)cD.mc;
+          __syncwarp();
+        }
+        __syncwarp();
+      }
+    }
+
+    // ---- element-pair blocks -> fixed point scatter
+    if (valid) {
+      if (constr) {
+        // constraint parent (reference assembly.cpp:416-427): 2C w S0 c c^T, rhs 2C w Sg c
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double base = wq * 2.0 * C;
+          for (int a = 0; a < 4; ++a) {
+            rhsc[a] += base * A.Sg[q] * qbary(q, a);
+            for (int b = a; b < 4; ++b) DT[s2i(a, b)] += base * A.S0[q] * qbary(q, a) * qbary(q, b);
+          }
+        }
+      } else {
+        const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
+        // T x T' cross block: X[a][b] = -C w sum_q c_{q,a} S1_q[b] at (N_a, M_b)
+        for (int b = 0; b < 4; ++b) {
+          for (int a = 0; a < 4; ++a) {
+            double x = 0;
+            for (int q = 0; q < 4; ++q) x += qbary(q, a) * A.S1[q][b];
+            x = -C * wq * x;
+            // slot of column NP[b] in staged row a
+            const int* rw = rows + a * rowcap;
+            int lo = 0, hi = rlen[a] - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (rw[mid] < NP[b]) lo = mid + 1;
+              else hi = mid;
+            }
+            const double v = NT[a] == NP[b] ? 2.0 * x : x;
+            red_fixed(V, rbase[a] + lo, v, cD.scale[NT[a]]);
+          }
+        }
+        // T' x T' block: C w sum_q S2_q at (M_b, M_c)
+        const long long* es = eslot;  // indexed by interior position of T'
+        int lo = 0, hi = cD.KI - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (cD.interior[mid] < Tp) lo = mid + 1;
+          else hi = mid;
+        }
+        for (int b = 0; b < 4; ++b)
+          for (int cc = b; cc < 4; ++cc) {
+            const int k = s2i(b, cc);
+            const int rowN = min(NP[b], NP[cc]);
+            red_fixed(V, es[10 * (long long)lo + k], C * wq * A.S2[k], cD.scale[rowN]);
+          }
+        // T x T block: C w S0_q c c^T, accumulated per outer element
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          for (int a = 0; a < 4; ++a)
+            for (int b = a; b < 4; ++b)
+              DT[s2i(a, b)] += C * wq * A.S0[q] * qbary(q, a) * qbary(q, b);
+      }
+    }
+  }
+
+  // ---- per outer element: D_T block and rhs (fixed-order CTA reduction)
+  for (int k = 0; k < 10; ++k) DT[k] = wsum(DT[k]);
+  for (int a = 0; a < 4; ++a) rhsc[a] = wsum(rhsc[a]);
+  if (lane == 0) {
+    for (int k = 0; k < 10; ++k) red[wid][k] = DT[k];
+    for (int a = 0; a < 4; ++a) red[wid][10 + a] = rhsc[a];
+  }
+  unsigned long long ns = n_samp, nh = n_hit;
+  for (int s = 16; s > 0; s >>= 1) {
+    ns += __shfl_xor_sync(FULLMASK, ns, s);
+    nh += __shfl_xor_sync(FULLMASK, nh, s);
+  }
+  if (lane == 0 && (ns | nh)) {
+    atomicAdd(mc_stats, ns);
+    atomicAdd(mc_stats + 1, nh);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot[14];
+    for (int k = 0; k < 14; ++k) {
+      tot[k] = 0;
+      for (int w = 0; w < kIntThreads / 32; ++w) tot[k] += red[w][k];
+    }
+    int k = 0;
+    for (int a = 0; a < 4; ++a)
+      for (int b = a; b < 4; ++b, ++k) {
+        const int lo = min(NT[a], NT[b]), hi = max(NT[a], NT[b]);
+        // slot of (lo, hi): lo is a T node -> staged row of lo
+        int ra = 0;
+        for (int r = 0; r < 4; ++r)
+          if (NT[r] == lo) ra = r;
+        const int* rw = rows + ra * rowcap;
+        int l2 = 0, h2 = rlen[ra] - 1;
+        while (l2 < h2) {
+          const int mid = (l2 + h2) >> 1;
+          if (rw[mid] < hi) l2 = mid + 1;
+          else h2 = mid;
+        }
+        red_fixed(V, rbase[ra] + l2, tot[k], cD.scale[lo]);
+      }
+    // load vector: f term (reference assembly.cpp:703-709) + constraint terms
+    for (int a = 0; a < 4; ++a) {
+      double r = 0;
+      for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, xq[q]);
+      rhsT[4 * (long long)ii + a] = r + tot[10 + a];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: fixed point -> CSR values, constraint folding
+
+__global__ void k_finalize(const long long* soff, const int* scols, const long long* mirror,
+                           const unsigned long long* V, const long long* ooff,
+                           const long long* omap, double* values, const double* rhsT,
+                           double* rhs, const int* dof_node) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= cD.unknowns) return;
+  const int d = warp;
+  const int i = dof_node[d];
+  const double si = cD.iscale[i];
+  // matrix entries of output row d
+  for (long long o = ooff[d] + lane; o < ooff[d + 1]; o += 32) {
+    const long long k = omap[o];
+    const int j = scols[k];
+    double v = (double)(long long)V[k] * si;
+    if (j != i) v += (double)(long long)V[mirror[k]] * cD.iscale[j];
+    values[o] = v;
+  }
+  // folding of constrained columns: rhs_i -= A_ij g(x_j) (dense-oracle form,
+  // reference tests/support/oracles.cpp:274-292)
+  double fold = 0;
+  for (long long k = soff[i] + lane; k < soff[i + 1]; k += 32) {
+    const int j = scols[k];
+    if (cD.dof[j] >= 0) continue;
+    double v = (double)(long long)V[k] * si;
+    if (j != i) v += (double)(long long)V[mirror[k]] * cD.iscale[j];
+    const Vd x = {cD.node[3 * (long long)j], cD.node[3 * (long long)j + 1], cD.node[3 * (long long)j + 2]};
+    fold += v * poly_eval(cD.g, x);
+  }
+  fold = wsum(fold);
+  if (lane == 0) {
+    double r = 0;
+    for (int k = cD.ni_off[i]; k < cD.ni_off[i + 1]; ++k) {
+      const int T = cD.ni_el[k];
+      int lo = 0, hi = cD.KI - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cD.interior[mid] < T) lo = mid + 1;
+        else hi = mid;
+      }
+      const int4 w = cD.verts[T];
+      const int a = w.x == i ? 0 : (w.y == i ? 1 : (w.z == i ? 2 : 3));
+      r += rhsT[4 * (long long)lo + a];
+    }
+    rhs[d] = r - fold;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t m) {
+    if (m <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    const size_t bytes = std::max<size_t>(m, 1) * sizeof(T);
+    CK(cudaMalloc(&p, bytes));
+    n = std::max<size_t>(m, 1);
+  }
+  void upload(const T* h, size_t m, cudaStream_t s) {
+    ensure(m);
+    if (m) CK(cudaMemcpyAsync(p, h, m * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+struct nlfem_gpu_session {
+  int device = 0;
+  Dev dev{};
+  int K = 0, J = 0, KI = 0, unknowns = 0;
+  std::vector<int> h_interior, h_dof_node;
+  // mesh buffers
+  DBuf<double> node, center, radius, vol, tau, inv;
+  DBuf<int4> verts, nbr;
+  DBuf<uint8_t> region;
+  DBuf<int> interior, dof, dof_node;
+  DBuf<double4> erec;
+  // grid / incidence
+  DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
+  DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp;
+  DBuf<int> cell_start, ni_off;
+  DBuf<double> scale, iscale;
+  // pairs
+  DBuf<int> pair_count, partner, err_elem, ovf;
+  DBuf<unsigned> info;
+  DBuf<long long> pair_off;
+  DBuf<unsigned long long> counters;
+  // pattern
+  DBuf<int> rlen, rcols, tcnt, tcols, slen, scols, olen, ocols;
+  DBuf<long long> roff, toff, soff, mirror, eslot, ooff, omap;
+  // values
+  DBuf<unsigned long long> V;
+  DBuf<double> rhsT, values, rhs;
+  // results of the last run
+  long long npairs = 0, nnz_s = 0, nnz_out = 0;
+  long long launches = 0;
+  unsigned long long items = 0, mc_samples = 0, mc_hits = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+
+namespace {
+
+void scan64(nlfem_gpu_session& S, const void* in, bool in_is_int, long long n, long long* out,
+            cudaStream_t st) {
+  // exclusive scan of n counts into out[0..n], out[n] = total
+  const long long nb = (n + kScanBlock - 1) / kScanBlock;
+  std::vector<long long> dummy;
+  DBuf<long long> sums, sums_scan;
+  sums.ensure(nb + 1);
+  sums_scan.ensure(nb + 1);
+  if (n > 0) {
+    if (in_is_int)
+      k_scan_block<int><<<(unsigned)nb, kScanBlock, 0, st>>>((const int*)in, out, sums.p, n);
+    else
+      k_scan_block<long long><<<(unsigned)nb, kScanBlock, 0, st>>>((const long long*)in, out,
+                                                                    sums.p, n);
+    ++S.launches;
+    if (nb > 1) {
+      scan64(S, sums.p, false, nb, sums_scan.p, st);
+      k_scan_add<<<(unsigned)nb, kScanBlock, 0, st>>>(out, sums_scan.p, n);
+      ++S.launches;
+      // total = scanned[nb-1] + sums[nb-1] -> already in sums_scan[nb]
+      CK(cudaMemcpyAsync(out + n, sums_scan.p + nb, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+    } else {
+      CK(cudaMemcpyAsync(out + n, sums.p, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    CK(cudaMemsetAsync(out, 0, sizeof(long long), st));
+  }
+  CK(cudaStreamSynchronize(st));  // sums buffers are freed on return
+}
+
+long long read_ll(const long long* d, cudaStream_t st) {
+  long long h = 0;
+  CK(cudaMemcpyAsync(&h, d, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+__global__ void k_ll_to_int(long long n, const long long* a, int* b) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (int)a[i];
+}
+
+inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void check_config(const nlfem_gpu_kernel* k, const nlfem_gpu_config* cfg) {
+  if (!(k->delta > 0)) throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: delta must be positive"};
+  if (cfg->mc_samples <= 0)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: mc_samples must be positive"};
+  if (cfg->strategy != NLFEM_STRATEGY_BARYCENTER && cfg->strategy != NLFEM_STRATEGY_NOCAPS &&
+      cfg->strategy != NLFEM_STRATEGY_FULLCAPS)
+    throw Fail{NLFEM_GPU_EUNSUPPORTED,
+               "strategy not implemented on the GPU path (barycenter, nocaps, fullcaps only)"};
+  if (cfg->sampler != NLFEM_SAMPLER_PHILOX)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown sampler"};
+}
+
+void poly_to_dev(const nlfem_gpu_poly* p, Poly& d) {
+  if (!p) {
+    d.n = 0;
+    return;
+  }
+  if (p->nterms > kMaxTerms) throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: polynomial too long"};
+  d.n = p->nterms;
+  for (int t = 0; t < p->nterms; ++t) {
+    d.c[t] = p->coef[t];
+    for (int a = 0; a < 3; ++a) d.e[t][a] = p->exps[3 * t + a];
+  }
+}
+
+void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu_dofs* dofs,
+                  const nlfem_gpu_kernel* k, const nlfem_gpu_poly* f, const nlfem_gpu_poly* g,
+                  const nlfem_gpu_config* cfg) {
+  check_config(k, cfg);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Fail{NLFEM_GPU_ENODEVICE, "no CUDA device available (the GPU path has no CPU fallback)"};
+  if (cfg->device >= 0) CK(cudaSetDevice(cfg->device));
+  CK(cudaGetDevice(&S.device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, S.device));
+  if (prop.major < 10)
+    throw Fail{NLFEM_GPU_ENODEVICE, "device is not sm_100 class (built for sm_100a only)"};
+  CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 8; ++i) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    S.ev.push_back(e);
+  }
+  S.K = m->elem_count;
+  S.J = m->node_count;
+  S.unknowns = dofs->unknowns;
+  if (dofs->node_count != m->node_count)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: dof map does not match the mesh"};
+  cudaStream_t st = S.stream;
+  S.node.upload(m->node_xyz, 3 * (size_t)S.J, st);
+  S.center.upload(m->center, 3 * (size_t)S.K, st);
+  S.radius.upload(m->radius, S.K, st);
+  S.vol.upload(m->volume, S.K, st);
+  S.inv.upload(m->inv_edges, 9 * (size_t)S.K, st);
+  S.verts.upload(reinterpret_cast<const int4*>(m->verts), S.K, st);
+  S.nbr.upload(reinterpret_cast<const int4*>(m->neighbor), S.K, st);
+  S.region.upload(m->region, S.K, st);
+  S.dof.upload(dofs->dof_of_node, S.J, st);
+  // host-side per-element volume floor tau = 1e-14 * diam^3 (reference core.hpp:85)
+  std::vector<double> tau(S.K);
+  double rmax = 0, dmax = 0;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  double volsum = 0;
+  S.h_interior.clear();
+  for (int t = 0; t < S.K; ++t) {
+    tau[t] = 1e-14 * std::pow(m->diam[t], 3);
+    rmax = std::max(rmax, m->radius[t]);
+    dmax = std::max(dmax, m->diam[t]);
+    volsum += m->volume[t];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], m->center[3 * t + a]);
+      hi[a] = std::max(hi[a], m->center[3 * t + a]);
+    }
+    if (!m->region[t]) S.h_interior.push_back(t);
+  }
+  S.KI = (int)S.h_interior.size();
+  S.tau.upload(tau.data(), S.K, st);
+  S.interior.upload(S.h_interior.data(), S.KI, st);
+  S.h_dof_node.assign(S.unknowns, 0);
+  for (int v = 0; v < S.J; ++v)
+    if (dofs->dof_of_node[v] >= 0) S.h_dof_node[dofs->dof_of_node[v]] = v;
+  S.dof_node.upload(S.h_dof_node.data(), S.unknowns, st);
+
+  Dev& D = S.dev;
+  D.K = S.K;
+  D.J = S.J;
+  D.KI = S.KI;
+  D.unknowns = S.unknowns;
+  D.strategy = cfg->strategy;
+  D.mc = cfg->mc_samples;
+  D.seed = cfg->seed;
+  D.C = k->C;
+  D.delta = k->delta;
+  D.slack = 1e-10 * k->delta;                           // eps_geo (core.hpp:83)
+  D.inside_cut = k->delta - D.slack - 1e-12 * k->delta;  // assembly.cpp:659
+  D.dd = k->delta * k->delta;
+  poly_to_dev(f, D.f);
+  poly_to_dev(g, D.g);
+  // uniform grid: cell edge ~ cube root of 6 mean element volumes (one lattice
+  // cube holds 6 Kuhn tets), so a cell holds ~6 centers
+  const double hg = std::max(std::cbrt(6.0 * volsum / std::max(S.K, 1)), 1e-300);
+  D.hg = hg;
+  D.ginv = 1.0 / hg;
+  D.gox = lo[0];
+  D.goy = lo[1];
+  D.goz = lo[2];
+  D.gx = std::max(1, (int)std::floor((hi[0] - lo[0]) / hg) + 1);
+  D.gy = std::max(1, (int)std::floor((hi[1] - lo[1]) / hg) + 1);
+  D.gz = std::max(1, (int)std::floor((hi[2] - lo[2]) / hg) + 1);
+  D.rmax = rmax;
+  S.erec.ensure(4 * (size_t)S.K);
+  D.erec = S.erec.p;
+  D.verts = S.verts.p;
+  D.nbr = S.nbr.p;
+  D.vol = S.vol.p;
+  D.tau = S.tau.p;
+  D.inv = S.inv.p;
+  D.region = S.region.p;
+  D.interior = S.interior.p;
+  D.dof = S.dof.p;
+  D.node = S.node.p;
+  // fixed-point bound per row: 8 C Vmax patch_i, Vmax = |B(delta + 2 dmax)|
+  (void)dmax;
+  CK(cudaStreamSynchronize(st));
+}
+
+// mesh-derived acceleration structures (inside the timed run: the reference's
+// equivalent -- interior list, g_node -- is inside its assemble() too)
+void run_prep(nlfem_gpu_session& S) {
+  cudaStream_t st = S.stream;
+  Dev& D = S.dev;
+  const int K = S.K, J = S.J;
+  const long long ncell = (long long)D.gx * D.gy * D.gz;
+  CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
+  k_erec<<<nblk(K, 256), 256, 0, st>>>(K, S.node.p, S.verts.p, S.center.p, S.radius.p, S.erec.p);
+  ++S.launches;
+  // grid
+  S.cell_key.ensure(K);
+  S.cell_cnt.ensure(ncell);
+  S.cell_elems.ensure(K);
+  S.cursor.ensure(std::max<long long>(ncell, J));
+  S.cell_start64.ensure(ncell + 1);
+  S.cell_start.ensure(ncell + 1);
+  CK(cudaMemsetAsync(S.cell_cnt.p, 0, ncell * sizeof(int), st));
+  k_cell_count<<<nblk(K, 256), 256, 0, st>>>(K, S.cell_key.p, S.cell_cnt.p);
+  ++S.launches;
+  scan64(S, S.cell_cnt.p, true, ncell, S.cell_start64.p, st);
+  CK(cudaMemsetAsync(S.cursor.p, 0, ncell * sizeof(int), st));
+  k_fill_by_key<<<nblk(K, 256), 256, 0, st>>>(K, S.cell_key.p, S.cell_start64.p, S.cursor.p,
+                                              S.cell_elems.p);
+  k_sort_segments<<<nblk(ncell, 256), 256, 0, st>>>((int)ncell, S.cell_start64.p, S.cell_elems.p);
+  k_ll_to_int<<<nblk(ncell + 1, 256), 256, 0, st>>>(ncell + 1, S.cell_start64.p, S.cell_start.p);
+  S.launches += 3;
+  // node -> interior elements
+  S.ni_cnt.ensure(J);
+  S.ni_off64.ensure(J + 1);
+  S.ni_off.ensure(J + 1);
+  CK(cudaMemsetAsync(S.ni_cnt.p, 0, J * sizeof(int), st));
+  k_ninc_count<<<nblk(K, 256), 256, 0, st>>>(K, S.ni_cnt.p);
+  ++S.launches;
+  scan64(S, S.ni_cnt.p, true, J, S.ni_off64.p, st);
+  const long long nin = read_ll(S.ni_off64.p + J, st);
+  S.ni_el.ensure(nin);
+  CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
+  k_ninc_fill<<<nblk(K, 256), 256, 0, st>>>(K, S.ni_off64.p, S.cursor.p, S.ni_el.p);
+  k_sort_segments<<<nblk(J, 256), 256, 0, st>>>(J, S.ni_off64.p, S.ni_el.p);
+  k_ll_to_int<<<nblk(J + 1, 256), 256, 0, st>>>(J + 1, S.ni_off64.p, S.ni_off.p);
+  S.launches += 3;
+  // node -> all elements (patch volumes for the fixed-point scales)
+  S.ai_cnt.ensure(J);
+  S.ai_off64.ensure(J + 1);
+  CK(cudaMemsetAsync(S.ai_cnt.p, 0, J * sizeof(int), st));
+  k_all_inc_count<<<nblk(K, 256), 256, 0, st>>>(K, S.ai_cnt.p);
+  ++S.launches;
+  scan64(S, S.ai_cnt.p, true, J, S.ai_off64.p, st);
+  S.ai_el.ensure(4 * (size_t)K);
+  CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
+  k_all_inc_fill<<<nblk(K, 256), 256, 0, st>>>(K, S.ai_off64.p, S.cursor.p, S.ai_el.p);
+  ++S.launches;
+  S.scale.ensure(J);
+  S.iscale.ensure(J);
+  D.cell_start = S.cell_start.p;
+  D.cell_elems = S.cell_elems.p;
+  D.ni_off = S.ni_off.p;
+  D.ni_el = S.ni_el.p;
+  D.scale = S.scale.p;
+  D.iscale = S.iscale.p;
+  CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
+  // fixed-point bound per row: 8 C Vmax patch_i, Vmax = |B(delta + 2 dmax)|,
+  // dmax <= 2 rmax
+  const double dmax = 2 * D.rmax;
+  const double rr = D.delta + 2 * dmax;
+  const double cbound = 8.0 * D.C * (4.0 / 3.0 * M_PI * rr * rr * rr);
+  k_scales<<<nblk(J, 256), 256, 0, st>>>(J, S.ai_off64.p, S.ai_el.p, cbound, S.scale.p, S.iscale.p);
+  ++S.launches;
+}
+
+void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
+  cudaStream_t st = S.stream;
+  Dev& D = S.dev;
+  const auto wall0 = std::chrono::steady_clock::now();
+  S.launches = 0;
+  if (user) {
+    // order after work the caller queued on its stream
+    CK(cudaEventRecord(S.ev[7], user));
+    CK(cudaStreamWaitEvent(st, S.ev[7], 0));
+  }
+  CK(cudaEventRecord(S.ev[0], st));
+  run_prep(S);
+  CK(cudaEventRecord(S.ev[1], st));
+
+  // ---- K1: pairs (count, scan, fill)
+  const int KI = S.KI, J = S.J;
+  S.pair_count.ensure(KI);
+  S.pair_off.ensure(KI + 1);
+  S.err_elem.ensure(1);
+  S.ovf.ensure(1);
+  S.counters.ensure(4);
+  const int big = 0x7fffffff;
+  CK(cudaMemcpyAsync(S.err_elem.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(S.counters.p, 0, 4 * sizeof(unsigned long long), st));
+  const unsigned pblocks = nblk((long long)KI * 32, 128);
+  k_pairs<false><<<pblocks, 128, 0, st>>>(nullptr, S.pair_count.p, nullptr, nullptr,
+                                          S.counters.p, S.err_elem.p);
+  ++S.launches;
+  int err_elem = big;
+  CK(cudaMemcpyAsync(&err_elem, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  scan64(S, S.pair_count.p, true, KI, S.pair_off.p, st);
+  if (err_elem != big)
+    throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
+               "BallExitsMesh: ball reaches past an unglued facet of element " +
+                   std::to_string(err_elem)};
+  S.npairs = read_ll(S.pair_off.p + KI, st);
+  S.partner.ensure(S.npairs);
+  S.info.ensure(S.npairs);
+  k_pairs<true><<<pblocks, 128, 0, st>>>(S.pair_off.p, nullptr, S.partner.p, S.info.p, nullptr,
+                                         nullptr);
+  ++S.launches;
+  CK(cudaEventRecord(S.ev[2], st));
+
+  // ---- K5: pattern
+  const size_t rows_smem = (kHE + kHN + kRowMax) * sizeof(int);
+  CK(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  S.rlen.ensure(J);
+  S.roff.ensure(J + 1);
+  const unsigned rgrid = (unsigned)std::min<long long>(J, 148LL * 16);
+  k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
+                                               nullptr, S.ovf.p);
+  ++S.launches;
+  scan64(S, S.rlen.p, true, J, S.roff.p, st);
+  const long long nR = read_ll(S.roff.p + J, st);
+  S.rcols.ensure(nR);
+  k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
+                                              S.rcols.p, S.ovf.p);
+  ++S.launches;
+  // transpose
+  S.tcnt.ensure(J);
+  S.toff.ensure(J + 1);
+  S.tcols.ensure(nR);
+  CK(cudaMemsetAsync(S.tcnt.p, 0, J * sizeof(int), st));
+  k_col_count<<<nblk(nR, 256), 256, 0, st>>>(nR, S.rcols.p, S.tcnt.p);
+  ++S.launches;
+  scan64(S, S.tcnt.p, true, J, S.toff.p, st);
+  S.cursor.ensure(J);
+  CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
+  k_transpose_fill<<<nblk(J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.cursor.p,
+                                                 S.tcols.p);
+  CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(kRowMax * sizeof(int))));
+  k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p);
+  S.launches += 2;
+  // union
+  S.slen.ensure(J);
+  S.soff.ensure(J + 1);
+  CK(cudaMemsetAsync(S.counters.p + 3, 0, sizeof(unsigned long long), st));
+  int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 3);
+  k_union<false><<<nblk(J, 128), 128, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+                                               S.slen.p, nullptr, nullptr, d_maxlen);
+  ++S.launches;
+  scan64(S, S.slen.p, true, J, S.soff.p, st);
+  S.nnz_s = read_ll(S.soff.p + J, st);
+  S.scols.ensure(S.nnz_s);
+  k_union<true><<<nblk(J, 128), 128, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+                                              nullptr, S.soff.p, S.scols.p, nullptr);
+  int maxlen = 0;
+  CK(cudaMemcpyAsync(&maxlen, d_maxlen, sizeof(int), cudaMemcpyDeviceToHost, st));
+  S.mirror.ensure(S.nnz_s);
+  k_mirror<<<nblk(J, 128), 128, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
+  S.eslot.ensure(10 * (size_t)KI);
+  k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p);
+  S.launches += 3;
+  // output pattern
+  const int U = S.unknowns;
+  S.olen.ensure(U);
+  S.ooff.ensure(U + 1);
+  k_outpat<false><<<nblk(U, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr, nullptr,
+                                                nullptr, S.dof_node.p);
+  ++S.launches;
+  scan64(S, S.olen.p, true, U, S.ooff.p, st);
+  S.nnz_out = read_ll(S.ooff.p + U, st);
+  S.ocols.ensure(S.nnz_out);
+  S.omap.ensure(S.nnz_out);
+  k_outpat<true><<<nblk(U, 128), 128, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p, S.ocols.p,
+                                               S.omap.p, S.dof_node.p);
+  ++S.launches;
+  int ovf = 0;
+  CK(cudaMemcpyAsync(&ovf, S.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ovf)
+    throw Fail{NLFEM_GPU_BAD_CONFIG,
+               "BadConfig: interaction neighbourhood too large for the pattern kernels (code " +
+                   std::to_string(ovf) + ")"};
+  CK(cudaEventRecord(S.ev[3], st));
+
+  // ---- K3/K4: integrate + scatter
+  S.V.ensure(S.nnz_s);
+  S.rhsT.ensure(4 * (size_t)KI);
+  CK(cudaMemsetAsync(S.V.p, 0, S.nnz_s * sizeof(unsigned long long), st));
+  const int rowcap = std::max(maxlen, 1);
+  const size_t ismem = kIntThreads * sizeof(McSlot) + 4 * (size_t)rowcap * sizeof(int);
+  if (ismem > 200 * 1024)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
+  CK(cudaFuncSetAttribute(k_integrate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
+  if (KI > 0) {
+    k_integrate<<<KI, kIntThreads, ismem, st>>>(S.pair_off.p, S.partner.p, S.info.p, S.soff.p,
+                                                S.scols.p, S.eslot.p, S.V.p, S.rhsT.p,
+                                                S.counters.p + 1, rowcap);
+    ++S.launches;
+  }
+  CK(cudaEventRecord(S.ev[4], st));
+
+  // ---- K6: finalize
+  S.values.ensure(S.nnz_out);
+  S.rhs.ensure(U);
+  if (U > 0) {
+    k_finalize<<<nblk((long long)U * 32, 128), 128, 0, st>>>(
+        S.soff.p, S.scols.p, S.mirror.p, S.V.p, S.ooff.p, S.omap.p, S.values.p, S.rhsT.p,
+        S.rhs.p, S.dof_node.p);
+    ++S.launches;
+  }
+  CK(cudaEventRecord(S.ev[5], st));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  unsigned long long cnt[4];
+  CK(cudaMemcpy(cnt, S.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+  S.items = cnt[0];
+  S.mc_samples = cnt[1];
+  S.mc_hits = cnt[2];
+  if (user) {
+    CK(cudaEventRecord(S.ev[6], st));
+    CK(cudaStreamWaitEvent(user, S.ev[6], 0));
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    float ms[6];
+    for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], S.ev[i], S.ev[i + 1]));
+    CK(cudaEventElapsedTime(&ms[5], S.ev[0], S.ev[5]));
+    for (int i = 0; i < 5; ++i) stats->phase_ms[i] = ms[i];
+    stats->device_ms = ms[5];
+    stats->threads = 1;
+    stats->blocks = (KI + 31) / 32;
+    stats->mc_samples = S.mc_samples;
+    stats->mc_hits = S.mc_hits;
+    stats->element_pairs = S.npairs;
+    stats->items = (long long)S.items;
+    stats->nnz_ext = S.nnz_s;
+    stats->seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  }
+}
+
+int guard(char* err, size_t errlen, const std::function<void()>& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const Fail& f) {
+    put_err(err, errlen, f.msg);
+    return f.code;
+  } catch (const std::bad_alloc&) {
+    put_err(err, errlen, "out of host memory");
+    return NLFEM_GPU_ENOMEM;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return NLFEM_GPU_ENODEVICE;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* nlfem_gpu_version(void) { return "nlfem_gpu 0.1 sm_100a (barycenter, nocaps, fullcaps)"; }
+
+int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
+                             const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
+                             const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
+                             nlfem_gpu_session** out, char* err, size_t errlen) {
+  *out = nullptr;
+  auto* S = new nlfem_gpu_session;
+  const int rc = guard(err, errlen, [&] { session_init(*S, mesh, dofs, kernel, f, g, cfg); });
+  if (rc) {
+    nlfem_gpu_session_destroy(S);
+    return rc;
+  }
+  *out = S;
+  return 0;
+}
+
+int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* stats, char* err,
+                          size_t errlen) {
+  return guard(err, errlen, [&] { run_all(*s, static_cast<cudaStream_t>(stream), stats); });
+}
+
+int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* err,
+                               size_t errlen) {
+  return guard(err, errlen, [&] {
+    const int U = s->unknowns;
+    out->rows = U;
+    out->nnz = s->nnz_out;
+    out->row_ptr = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (U + 1)));
+    out->col_idx = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<long long>(s->nnz_out, 1)));
+    out->values = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(s->nnz_out, 1)));
+    out->rhs = static_cast<double*>(std::malloc(sizeof(double) * std::max(U, 1)));
+    if (!out->row_ptr || !out->col_idx || !out->values || !out->rhs)
+      throw Fail{NLFEM_GPU_ENOMEM, "out of host memory"};
+    if (s->nnz_out > (long long)0x7fffffff)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: nnz exceeds int32 row pointers"};
+    std::vector<long long> off(U + 1);
+    CK(cudaMemcpy(off.data(), s->ooff.p, sizeof(long long) * (U + 1), cudaMemcpyDeviceToHost));
+    for (int i = 0; i <= U; ++i) out->row_ptr[i] = (int32_t)off[i];
+    CK(cudaMemcpy(out->col_idx, s->ocols.p, sizeof(int32_t) * s->nnz_out, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out->values, s->values.p, sizeof(double) * s->nnz_out, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out->rhs, s->rhs.p, sizeof(double) * U, cudaMemcpyDeviceToHost));
+  });
+}
+
+int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* outer_offsets,
+                            int32_t* partner, uint32_t* info, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    *npairs = s->npairs;
+    if (!outer_offsets) return;
+    std::vector<long long> off(s->KI + 1);
+    CK(cudaMemcpy(off.data(), s->pair_off.p, sizeof(long long) * (s->KI + 1), cudaMemcpyDeviceToHost));
+    for (int i = 0; i <= s->KI; ++i) outer_offsets[i] = off[i];
+    if (s->npairs) {
+      CK(cudaMemcpy(partner, s->partner.p, sizeof(int32_t) * s->npairs, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(info, s->info.p, sizeof(uint32_t) * s->npairs, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s) { return s ? s->launches : 0; }
+
+void nlfem_gpu_session_destroy(nlfem_gpu_session* s) {
+  if (!s) return;
+  for (auto e : s->ev) cudaEventDestroy(e);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int nlfem_gpu_assemble(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
+                       const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
+                       const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
+                       nlfem_gpu_csr* out, nlfem_gpu_stats* stats, char* err, size_t errlen) {
+  const auto t0 = std::chrono::steady_clock::now();
+  nlfem_gpu_session* s = nullptr;
+  int rc = nlfem_gpu_session_create(mesh, dofs, kernel, f, g, cfg, &s, err, errlen);
+  if (rc) return rc;
+  rc = nlfem_gpu_session_run(s, nullptr, stats, err, errlen);
+  if (!rc) rc = nlfem_gpu_session_download(s, out, err, errlen);
+  nlfem_gpu_session_destroy(s);
+  if (!rc && stats)
+    stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+void nlfem_gpu_free_csr(nlfem_gpu_csr* csr) {
+  if (!csr) return;
+  std::free(csr->row_ptr);
+  std::free(csr->col_idx);
+  std::free(csr->values);
+  std::free(csr->rhs);
+  csr->row_ptr = csr->col_idx = nullptr;
+  csr->values = csr->rhs = nullptr;
+}
+
+}  // extern "C"
