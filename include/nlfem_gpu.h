@@ -127,6 +127,11 @@ typedef struct {
   int64_t nnz_ext;         /* node-pattern size incl. constrained columns     */
   double device_ms;        /* device pipeline time (CUDA events)              */
   double phase_ms[8];      /* prep, pairs, pattern, integrate, finalize, ...  */
+  uint64_t ledger_flops;   /* algorithmic FP64 FLOPs of the integration kernel,
+                              SURVEY.md 8(d) ledger (whole 39/133, crossing 38,
+                              straddle volume 24, Gauss sub-simplex 360/160, MC
+                              sub-simplex setup 25, sample 35, hit +62/+12)   */
+  uint64_t mc_subsimplices;
 } nlfem_gpu_stats;
 
 /* One-shot drop-in: host arrays in, host CSR out (upload + device pipeline +
@@ -162,6 +167,11 @@ int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* oute
 /* Kernel launches of the last run (for the bench's gpu_launches key). */
 int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s);
 void nlfem_gpu_session_destroy(nlfem_gpu_session* s);
+
+/* FP64 (non-tensor) DFMA throughput of the device, measured by a short
+ * microbenchmark: the roofline denominator for the integration kernels
+ * (MEASURED_PEAKS.json has no FP64 figure). */
+int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen);
 
 /* Build / version string (e.g. "nlfem_gpu sm_100a ..."). */
 const char* nlfem_gpu_version(void);

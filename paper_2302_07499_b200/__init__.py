@@ -83,7 +83,8 @@ class Stats(C.Structure):
     _fields_ = [("seconds", C.c_double), ("threads", C.c_int32), ("blocks", C.c_int32),
                 ("mc_samples", C.c_uint64), ("mc_hits", C.c_uint64),
                 ("element_pairs", C.c_int64), ("items", C.c_int64), ("nnz_ext", C.c_int64),
-                ("device_ms", C.c_double), ("phase_ms", C.c_double * 8)]
+                ("device_ms", C.c_double), ("phase_ms", C.c_double * 8),
+                ("ledger_flops", C.c_uint64), ("mc_subsimplices", C.c_uint64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}
@@ -106,6 +107,8 @@ def lib():
     vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     P = C.POINTER
     L.nlfem_gpu_version.restype = C.c_char_p
+    L.nlfem_gpu_fp64_peak.restype = C.c_int
+    L.nlfem_gpu_fp64_peak.argtypes = [i32, P(dbl), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_assemble.restype = C.c_int
     L.nlfem_gpu_assemble.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
                                      P(_Config), P(_Csr), P(Stats), C.c_char_p, C.c_size_t]
@@ -143,6 +146,7 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
     "nlfem_gpu_session_run", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
+    "nlfem_gpu_fp64_peak",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
 ]
@@ -159,6 +163,14 @@ def _check(rc: int, err) -> None:
 
 
 # --------------------------------------------------------------------------- host setup
+
+def fp64_peak_tflops(device: int = -1) -> float:
+    """Measured FP64 DFMA throughput of the device (TFLOP/s)."""
+    v = C.c_double()
+    err = C.create_string_buffer(512)
+    _check(lib().nlfem_gpu_fp64_peak(device, C.byref(v), err, 512), err)
+    return v.value
+
 
 def strategy_names() -> list[str]:
     return list(STRATEGIES)
@@ -301,6 +313,7 @@ def forcing_terms(delta: float, uterms, normalization: str = "mass") -> np.ndarr
 
 
 def _poly_struct(terms: np.ndarray):
+    terms = np.asarray(terms, np.float64).reshape(-1, 4)
     coef = np.ascontiguousarray(terms[:, 0], np.float64)
     exps = np.ascontiguousarray(terms[:, 1:], np.int32)
     return _Poly(len(terms), _p(coef), _p(exps)), (coef, exps)
@@ -398,14 +411,23 @@ class Session:
 
 def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
              normalization: str = "mass", problem_terms=None, seed: int = 0x5EED,
-             mc_samples: int = 200, device: int = -1) -> tuple[dict, dict]:
-    """One call through nlfem_gpu_assemble (host arrays in, host CSR out)."""
+             mc_samples: int = 200, device: int = -1, f_terms=None,
+             g_terms=None) -> tuple[dict, dict]:
+    """One call through nlfem_gpu_assemble (host arrays in, host CSR out).
+
+    f_terms / g_terms override the manufactured forcing and constraint data
+    with arbitrary polynomials (rows c, e0, e1, e2; may be empty = zero), the
+    analogue of passing arbitrary f, g to nlfem::assemble."""
     if strategy not in STRATEGIES:
         raise NlfemError(8, f"BadConfig: unknown strategy '{strategy}'")
     L = lib()
     Cn = kernel_constant(delta, normalization)
     u = default_problem_terms() if problem_terms is None else _check_terms(problem_terms)
     f = forcing_terms(delta, u, normalization)
+    if f_terms is not None:
+        f = np.asarray(f_terms, np.float64).reshape(-1, 4)
+    if g_terms is not None:
+        u = np.asarray(g_terms, np.float64).reshape(-1, 4)
     m, d = table._structs()
     fp, fk = _poly_struct(f)
     gp, gk = _poly_struct(u)

@@ -729,6 +729,7 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
     const long long* pair_off, const int* partner, const unsigned* info, const long long* soff,
     const int* scols, const long long* eslot, unsigned long long* V, double* rhsT,
     unsigned long long* mc_stats, int rowcap) {
+  // mc_stats: [0] draws, [1] hits, [2] ledger FLOPs, [3] MC sub-simplices
   extern __shared__ unsigned char smraw[];
   McSlot* slots = reinterpret_cast<McSlot*>(smraw);
   int* rows = reinterpret_cast<int*>(slots + kIntThreads);  // 4 staged rows
@@ -766,7 +767,7 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
   for (int k = 0; k < 10; ++k) DT[k] = 0;
 #pragma unroll
   for (int a = 0; a < 4; ++a) rhsc[a] = 0;
-  unsigned long long n_samp = 0, n_hit = 0;
+  unsigned long long n_samp = 0, n_hit = 0, led = 0, nsubs = 0;
 
   const long long p0 = pair_off[ii], p1 = pair_off[ii + 1];
   const long long np = p1 - p0;
@@ -811,6 +812,7 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
     for (int q = 0; q < 4; ++q) {
       const unsigned c = (code >> (5 * q)) & 31;
       if (c == kWhole) {
+        led += constr ? 133 : 39;
         if (constr) {
           // constraint parent: measure and g average (reference assembly.cpp:350-359)
           A.S0[q] += volP;
@@ -829,6 +831,11 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
       } else if (c & kStraddle) {
         Tet pcs[3];
         const int n = straddle_inner(vP, (int)(c & 15), xq[q], cD.delta, tauP, pcs);
+        {
+          const int m = __popc(c & 15);
+          led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3));
+          led += (unsigned long long)n * (constr ? 160 : 360);
+        }
         for (int s = 0; s < n; ++s) {
           const double vs = tet_volume(pcs[s].v[0], pcs[s].v[1], pcs[s].v[2], pcs[s].v[3]);
           for (int k = 0; k < 4; ++k) {
@@ -866,6 +873,8 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
         } else if (c & kStraddle) {
           Tet pcs[3];
           nsub = straddle_outer(vP, (int)(c & 15), xq[q], cD.delta, tauP, pcs);
+          const int m = __popc(c & 15);
+          led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
           for (int s = 0; s < nsub; ++s) {
             const Vd* u = pcs[s].v;
             const double v0[3] = {u[0].x, u[0].y, u[0].z}, v1[3] = {u[1].x, u[1].y, u[1].z},
@@ -929,6 +938,7 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
             }
           }
           n_hit += hits;
+          led += (unsigned long long)hits * (cons ? 12 : 62);
           n0 = wsum(n0);
           if (cons) {
             sg = wsum(sg);
@@ -973,7 +983,11 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
               }
             }
           }
-          if (lane == L) n_samp += (unsigned long long)ns * (unsigned long long)cD.mc;
+          if (lane == L) {
+            n_samp += (unsigned long long)ns * (unsigned long long)cD.mc;
+            led += (unsigned long long)ns * (25ull + 35ull * (unsigned long long)cD.mc);
+            nsubs += ns;
+          }
           __syncwarp();
         }
         __syncwarp();
@@ -1043,14 +1057,20 @@ __global__ void __launch_bounds__(kIntThreads) k_integrate(
     for (int k = 0; k < 10; ++k) red[wid][k] = DT[k];
     for (int a = 0; a < 4; ++a) red[wid][10 + a] = rhsc[a];
   }
-  unsigned long long ns = n_samp, nh = n_hit;
+  unsigned long long ns = n_samp, nh = n_hit, nl = led, nq = nsubs;
   for (int s = 16; s > 0; s >>= 1) {
     ns += __shfl_xor_sync(FULLMASK, ns, s);
     nh += __shfl_xor_sync(FULLMASK, nh, s);
+    nl += __shfl_xor_sync(FULLMASK, nl, s);
+    nq += __shfl_xor_sync(FULLMASK, nq, s);
   }
-  if (lane == 0 && (ns | nh)) {
-    atomicAdd(mc_stats, ns);
-    atomicAdd(mc_stats + 1, nh);
+  if (lane == 0) {
+    if (ns | nh) {
+      atomicAdd(mc_stats, ns);
+      atomicAdd(mc_stats + 1, nh);
+    }
+    atomicAdd(mc_stats + 2, nl);
+    if (nq) atomicAdd(mc_stats + 3, nq);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1137,6 +1157,20 @@ __global__ void k_finalize(const long long* soff, const int* scols, const long l
 }
 
 // ---------------------------------------------------------------------------
+// FP64 DFMA throughput microbenchmark (roofline denominator)
+
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+         x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+    x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 template <class T>
@@ -1193,7 +1227,7 @@ struct nlfem_gpu_session {
   // results of the last run
   long long npairs = 0, nnz_s = 0, nnz_out = 0;
   long long launches = 0;
-  unsigned long long items = 0, mc_samples = 0, mc_hits = 0;
+  unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> ev;
 };
@@ -1462,11 +1496,11 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   S.pair_off.ensure(KI + 1);
   S.err_elem.ensure(1);
   S.ovf.ensure(1);
-  S.counters.ensure(4);
+  S.counters.ensure(8);
   const int big = 0x7fffffff;
   CK(cudaMemcpyAsync(S.err_elem.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
-  CK(cudaMemsetAsync(S.counters.p, 0, 4 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), st));
   const unsigned pblocks = nblk((long long)KI * 32, 128);
   k_pairs<false><<<pblocks, 128, 0, st>>>(nullptr, S.pair_count.p, nullptr, nullptr,
                                           S.counters.p, S.err_elem.p);
@@ -1521,8 +1555,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   // union
   S.slen.ensure(J);
   S.soff.ensure(J + 1);
-  CK(cudaMemsetAsync(S.counters.p + 3, 0, sizeof(unsigned long long), st));
-  int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 3);
+  CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
+  int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
   k_union<false><<<nblk(J, 128), 128, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
                                                S.slen.p, nullptr, nullptr, d_maxlen);
   ++S.launches;
@@ -1590,11 +1624,13 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   CK(cudaEventRecord(S.ev[5], st));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
-  unsigned long long cnt[4];
+  unsigned long long cnt[8];
   CK(cudaMemcpy(cnt, S.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
   S.items = cnt[0];
   S.mc_samples = cnt[1];
   S.mc_hits = cnt[2];
+  S.ledger = cnt[3];
+  S.mc_subs = cnt[4];
   if (user) {
     CK(cudaEventRecord(S.ev[6], st));
     CK(cudaStreamWaitEvent(user, S.ev[6], 0));
@@ -1613,6 +1649,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
     stats->element_pairs = S.npairs;
     stats->items = (long long)S.items;
     stats->nnz_ext = S.nnz_s;
+    stats->ledger_flops = S.ledger;
+    stats->mc_subsimplices = S.mc_subs;
     stats->seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   }
@@ -1636,6 +1674,32 @@ int guard(char* err, size_t errlen, const std::function<void()>& fn) {
 }  // namespace
 
 extern "C" {
+
+int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    if (device >= 0) CK(cudaSetDevice(device));
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf<double> out;
+    out.ensure(1);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int iters = 1 << 14, blocks = sms * 8, threads = 256;
+    k_dfma_peak<<<blocks, threads>>>(out.p, 256, 0.999999, 1e-7);  // warm-up
+    CK(cudaEventRecord(e0));
+    k_dfma_peak<<<blocks, threads>>>(out.p, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+  });
+}
 
 const char* nlfem_gpu_version(void) { return "nlfem_gpu 0.1 sm_100a (barycenter, nocaps, fullcaps)"; }
 

@@ -1,0 +1,104 @@
+"""The CPU oracle (oracle/restated.cpp) pinned against the reference.
+
+Mode R must reproduce the unmodified reference bit for bit: against the
+committed golden fixtures (generated from oracle/_ref by
+tests/golden/make_golden.py) everywhere, and against the live reference
+library when it is present.  Mode P (the GPU's Philox stream) shares every
+line except the sampler."""
+import numpy as np
+import pytest
+
+import paper_2302_07499_b200 as P
+from oracle import port, ref
+from tests.helpers import SEED, U2, golden_names, load_golden, rhs_rel_err, row_rel_err, same_pattern
+
+
+def _table(g):
+    return P.ElementTable(g["coords"], g["cells"], g["region"])
+
+
+def _run(table, delta, strat, mc, sampler, threads=0):
+    return port.assemble(table, delta, strat, P.kernel_constant(delta, "moment2"),
+                         P.forcing_terms(delta, U2, "moment2"), P.normalize_terms(U2),
+                         seed=SEED, mc_samples=mc, sampler=sampler, threads=threads)
+
+
+def test_philox_known_answers():
+    # Random123 Philox4x32-10 KATs
+    assert [hex(x) for x in port.philox([0, 0, 0, 0], (0, 0))] == \
+        ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
+    assert [hex(x) for x in port.philox([0xFFFFFFFF] * 4, (0xFFFFFFFF, 0xFFFFFFFF))] == \
+        ["0x408f276d", "0x41c83b0e", "0xa20bc7c6", "0x6d5451fd"]
+    assert [hex(x) for x in port.philox([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+                                        (0xA4093822, 0x299F31D0))] == \
+        ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("strat", ["barycenter", "nocaps", "fullcaps"])
+def test_mode_r_matches_reference_golden(name, strat):
+    g = load_golden(name)
+    o = _run(_table(g), float(g["delta"]), strat, int(g["mc_samples"]), "R", threads=2)
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(o[k], g[f"{strat}_{k}"]), (name, strat, k)
+    assert [o["mc_samples"], o["mc_hits"]] == list(g[f"{strat}_mc"])
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_mode_r_matches_live_reference():
+    m = P.generate_mesh(3, 5, 0.3, jitter_seed=3)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    r = ref.Problem(m["coords"], m["cells"], m["region"])
+    for strat, mc in (("nocaps", 1), ("fullcaps", 12)):
+        o = _run(t, 0.3, strat, mc, "R")
+        s = r.assemble(0.3, strat, U2, threads=3, seed=SEED, mc_samples=mc)
+        for k in ("row_ptr", "col_idx", "values", "rhs"):
+            assert np.array_equal(o[k], s[k]), (strat, k)
+        assert (o["mc_samples"], o["mc_hits"]) == (s["mc_samples"], s["mc_hits"])
+
+
+def test_mode_p_same_regions_and_thread_invariant():
+    g = load_golden("lat4_d030")
+    t = _table(g)
+    a = _run(t, 0.3, "fullcaps", 16, "P", threads=1)
+    b = _run(t, 0.3, "fullcaps", 16, "P", threads=5)
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(a[k], b[k])
+    assert same_pattern(a, {"row_ptr": g["fullcaps_row_ptr"], "col_idx": g["fullcaps_col_idx"]})
+    # same Monte Carlo regions as the reference: identical draw count
+    assert a["mc_samples"] == int(g["fullcaps_mc"][0])
+    hit_ref = int(g["fullcaps_mc"][1]) / int(g["fullcaps_mc"][0])
+    assert abs(a["mc_hits"] / a["mc_samples"] - hit_ref) < 0.01
+
+
+def test_mode_p_solution_error_close_to_reference():
+    g = load_golden("lat6_d025")
+    t = _table(g)
+    o = _run(t, 0.25, "fullcaps", 8, "P")
+    sol = port.solve_l2(t, o, U2)
+    assert sol["converged"]
+    assert abs(sol["l2"] / float(g["fullcaps_l2"]) - 1) < 0.01
+
+
+def test_oracle_l2_matches_reference_harness():
+    g = load_golden("lat4_d030")
+    t = _table(g)
+    s = {k: g[f"nocaps_{k}"] for k in ("row_ptr", "col_idx", "values", "rhs")}
+    sol = port.solve_l2(t, s, U2)
+    assert abs(sol["l2"] - float(g["nocaps_l2"])) <= 1e-9 * float(g["nocaps_l2"])
+
+
+def test_ball_exits_mesh():
+    m = P.generate_mesh(3, 4, 0.25)   # layer of 1 cell = 0.25
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    with pytest.raises(port.OracleError) as ei:
+        _run(t, 0.3, "nocaps", 1, "R")
+    assert ei.value.code == 5 and "unglued facet" in str(ei.value)
+
+
+def test_bad_config():
+    g = load_golden("lat4_d030")
+    t = _table(g)
+    with pytest.raises(port.OracleError) as ei:
+        _run(t, 0.3, "fullcaps", 0, "P")
+    assert ei.value.code == 8
