@@ -220,3 +220,129 @@ __device__ __forceinline__ double facet_distance(const Vd v[4], int slot, Vd p) 
     if (i != slot) f[k++] = v[i];
   return point_triangle_distance(p, f[0], f[1], f[2]);
 }
+
+// ---------------------------------------------------------------------------
+// Compact form of the straddle decompositions.  Both straddle_inner and
+// straddle_outer emit either one tet (A0, A1, A2, B0) or the three-tet split of
+// a prism (A0 A1 A2 | B0 B1 B2): (A0,A1,A2,B0), (A1,A2,B0,B1), (A2,B0,B1,B2)
+// (reference ball_approx.cpp:150-155); a warped prism first picks the
+// orientation with the larger total volume (160-175).  Holding the six points
+// and selecting piece k with conditional moves keeps one copy of the consumer
+// code in the instruction stream; results are bit-identical to the reference
+// because every point and volume is computed by the same expressions.
+struct Straddle {
+  Vd A0, A1, A2, B0, B1, B2;
+  int n;  // 1 (single tet) or 3 (prism split)
+};
+
+__device__ __forceinline__ Vd crossing_point(Vd a, Vd b, Vd c, double r) {
+  const double t = edge_crossing(a, b, c, r);
+  return vadd(a, vscale(t, vsub(b, a)));
+}
+
+__device__ __forceinline__ Vd pick(const Vd v[4], int i) {
+  return i == 0 ? v[0] : (i == 1 ? v[1] : (i == 2 ? v[2] : v[3]));
+}
+
+__device__ __forceinline__ void split_slots(int mask, int in[4], int out[4], int& m) {
+  m = 0;
+  int mo = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (mask >> i & 1) in[m++] = i;
+    else out[mo++] = i;
+  }
+}
+
+__device__ __forceinline__ void orient_warped(Straddle& s) {
+  const double va = tet_volume(s.A0, s.A1, s.A2, s.B0) + tet_volume(s.A1, s.A2, s.B0, s.B1) +
+                    tet_volume(s.A2, s.B0, s.B1, s.B2);
+  const double vb = tet_volume(s.A0, s.A2, s.A1, s.B0) + tet_volume(s.A2, s.A1, s.B0, s.B2) +
+                    tet_volume(s.A1, s.B0, s.B2, s.B1);
+  if (vb > va) {
+    const Vd t = s.A1;
+    s.A1 = s.A2;
+    s.A2 = t;
+    const Vd u = s.B1;
+    s.B1 = s.B2;
+    s.B2 = u;
+  }
+}
+
+// crossing_points (reference geometry.cpp:39-50) in one loop: crossing k is
+// edge (k-th inside slot -> j-th outside slot), k = i_rank * (4 - m) + j
+__device__ __forceinline__ void crossings4(const Vd v[4], int mask, Vd c, double r, Vd& q0,
+                                           Vd& q1, Vd& q2, Vd& q3) {
+  const int m = __popc(mask), mo = 4 - m, n = m * mo;
+  const unsigned inm = (unsigned)mask, outm = (unsigned)(~mask & 15);
+  q0 = q1 = q2 = q3 = v[0];
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    const int ir = k / mo, orr = k - ir * mo;
+    const int i = (int)__fns(inm, 0, ir + 1), o = (int)__fns(outm, 0, orr + 1);
+    const Vd p = crossing_point(pick(v, i), pick(v, o), c, r);
+    if (k == 0) q0 = p;
+    if (k == 1) q1 = p;
+    if (k == 2) q2 = p;
+    if (k == 3) q3 = p;
+  }
+}
+
+__device__ __forceinline__ int nth_slot(int mask, int n) { return (int)__fns((unsigned)mask, 0, n + 1); }
+
+// detail::straddle_inner (reference ball_approx.cpp:195-255)
+__device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c, double r) {
+  Vd q0, q1, q2, q3;
+  crossings4(v, mask, c, r, q0, q1, q2, q3);
+  const int m = __popc(mask);
+  const Vd i0 = pick(v, nth_slot(mask, 0)), i1 = pick(v, nth_slot(mask, m > 1 ? 1 : 0)),
+           i2 = pick(v, nth_slot(mask, m > 2 ? 2 : 0));
+  Straddle s;
+  if (m == 1) {  // tet (a, a->o0, a->o1, a->o2)
+    s.A0 = i0; s.A1 = q0; s.A2 = q1; s.B0 = q2; s.B1 = q2; s.B2 = q2;
+    s.n = 1;
+  } else if (m == 2) {  // warped prism {a, a->o0, a->o1} | {b, b->o0, b->o1}
+    s.A0 = i0; s.A1 = q0; s.A2 = q1; s.B0 = i1; s.B1 = q2; s.B2 = q3;
+    s.n = 3;
+    orient_warped(s);
+  } else {  // frustum {a, b, d} | {a->o, b->o, d->o}
+    s.A0 = i0; s.A1 = i1; s.A2 = i2; s.B0 = q0; s.B1 = q1; s.B2 = q2;
+    s.n = 3;
+  }
+  return s;
+}
+
+// detail::straddle_outer (reference ball_approx.cpp:257-298)
+__device__ __forceinline__ Straddle outer_straddle(const Vd v[4], int mask, Vd c, double r) {
+  Vd q0, q1, q2, q3;
+  crossings4(v, mask, c, r, q0, q1, q2, q3);
+  const int m = __popc(mask), om = ~mask & 15;
+  const Vd o0 = pick(v, nth_slot(om, 0)), o1 = pick(v, nth_slot(om, m < 3 ? 1 : 0)),
+           o2 = pick(v, nth_slot(om, m < 2 ? 2 : 0));
+  Straddle s;
+  if (m == 1) {  // frustum {a->o0, a->o1, a->o2} | {o0, o1, o2}
+    s.A0 = q0; s.A1 = q1; s.A2 = q2; s.B0 = o0; s.B1 = o1; s.B2 = o2;
+    s.n = 3;
+  } else if (m == 2) {  // warped prism {c, a->c, b->c} | {d, a->d, b->d}
+    s.A0 = o0; s.A1 = q0; s.A2 = q2; s.B0 = o1; s.B1 = q1; s.B2 = q3;
+    s.n = 3;
+    orient_warped(s);
+  } else {  // corner tet (o, a->o, b->o, d->o)
+    s.A0 = o0; s.A1 = q0; s.A2 = q1; s.B0 = q2; s.B1 = q2; s.B2 = q2;
+    s.n = 1;
+  }
+  return s;
+}
+
+// piece k (0..n-1) of the decomposition
+__device__ __forceinline__ void straddle_piece(const Straddle& s, int k, Vd& a, Vd& b, Vd& c,
+                                               Vd& d) {
+  a = k == 0 ? s.A0 : (k == 1 ? s.A1 : s.A2);
+  b = k == 0 ? s.A1 : (k == 1 ? s.A2 : s.B0);
+  c = k == 0 ? s.A2 : (k == 1 ? s.B0 : s.B1);
+  d = k == 0 ? s.B0 : (k == 1 ? s.B1 : s.B2);
+}
+
+// number of Monte Carlo sub-simplices straddle_outer can emit (before the
+// volume floor): m=1 prism -> 3, m=2 warped prism -> 3, m=3 corner -> 1
+__device__ __forceinline__ int outer_units(int mask) { return __popc(mask) == 3 ? 1 : 3; }

@@ -100,6 +100,7 @@ struct Dev {
   const double* inv;  // [9K]
   const uint8_t* region;
   const int* interior;  // [KI]
+  const int* ipos;      // [K] element -> position in interior[] (-1: constraint)
   const int* dof;       // [J]
   const double* node;   // [3J]
   // grid
@@ -282,11 +283,30 @@ __global__ void k_all_inc_fill(int K, const long long* off, int* cursor, int* ou
 // 16|mask straddling element with inside-vertex mask 1..14.
 enum : unsigned { kNone = 0, kWhole = 1, kOutCap = 2, kStraddle = 16 };
 
+__device__ __forceinline__ int count_kept(const Straddle& st, double tau) {
+  int n = 0;
+  for (int k = 0; k < st.n; ++k) {
+    Vd a, b, c, d;
+    straddle_piece(st, k, a, b, c, d);
+    n += tet_volume(a, b, c, d) > tau;
+  }
+  return n;
+}
+
 // Does a nocaps straddler emit at least one inner sub-simplex (volume > tau)?
 // Cheap certificate first: the inner polytope contains a tet of volume
 // >= (depth/diam)^(4-m) vol(T'), depth = delta - |v - x_q| of the deepest
 // inside vertex, and its <= 3 pieces sum to the polytope; otherwise run the
 // exact straddle_inner.
+__device__ __noinline__ bool inner_pieces_exact(const Vd* v, int mask, Vd xq, double tau) {
+  return count_kept(inner_straddle(v, mask, xq, cD.delta), tau) > 0;
+}
+
+__device__ __noinline__ bool any_pieces_exact(const Vd* v, int mask, Vd xq, double tau) {
+  return count_kept(inner_straddle(v, mask, xq, cD.delta), tau) +
+             count_kept(outer_straddle(v, mask, xq, cD.delta), tau) > 0;
+}
+
 __device__ __forceinline__ bool inner_pieces_exist(const Vd v[4], int mask, Vd xq, double diam,
                                                    double vol, double tau) {
   const int m = __popc(mask);
@@ -298,16 +318,24 @@ __device__ __forceinline__ bool inner_pieces_exist(const Vd v[4], int mask, Vd x
   if (m <= 2) f *= s;
   if (m == 1) f *= s;
   if (s > 1e-6 && f * vol > 8.0 * tau) return true;
-  Tet pcs[3];
-  return straddle_inner(v, mask, xq, cD.delta, tau, pcs) > 0;
+  return inner_pieces_exact(v, mask, xq, tau);
 }
 
 __device__ __forceinline__ bool any_pieces_fullcaps(const Vd v[4], int mask, Vd xq, double vol,
                                                     double tau) {
   if (vol > 64.0 * tau) return true;  // inner + outer polytopes cover T'
-  Tet pcs[3];
-  if (straddle_inner(v, mask, xq, cD.delta, tau, pcs) > 0) return true;
-  return straddle_outer(v, mask, xq, cD.delta, tau, pcs) > 0;
+  return any_pieces_exact(v, mask, xq, tau);
+}
+
+__device__ __noinline__ double dist_point_tet(Vd xq, const Vd* v) {
+  return distance_point_simplex(xq, v);
+}
+
+__device__ __noinline__ bool facet_too_close(const Vd* v, int4 nb, Vd xq) {
+  const int nbv[4] = {nb.x, nb.y, nb.z, nb.w};
+  for (int f = 0; f < 4; ++f)
+    if (nbv[f] < 0 && facet_distance(v, f, xq) < cD.delta - cD.slack) return true;
+  return false;
 }
 
 // The reference's per-(T,q,T') decision (assembly.cpp:722-759).
@@ -321,9 +349,11 @@ __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, con
   const int mask = inside_mask(v, xq, delta);
   if (mask == 15) return kWhole;
   if (mask == 0) {
-    if (cD.strategy == NLFEM_STRATEGY_FULLCAPS && distance_point_simplex(xq, v) < delta)
-      return kOutCap;
-    return kNone;
+    if (cD.strategy != NLFEM_STRATEGY_FULLCAPS) return kNone;
+    // the barycenter lies in T': gap < delta (with margin) certifies that the
+    // computed distance_point_simplex is < delta; otherwise evaluate it
+    if (gap < delta * (1.0 - 1e-12)) return kOutCap;
+    return dist_point_tet(xq, v) < delta ? kOutCap : kNone;
   }
   if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
     return inner_pieces_exist(v, mask, xq, diam, vol, tau) ? (kStraddle | mask) : kNone;
@@ -333,30 +363,39 @@ __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, con
 struct OuterT {
   int T;
   Vd c;
-  Vd xq[4];
+  Vd v[4];
   double R;
 };
 
 __device__ __forceinline__ void outer_setup(int T, OuterT& o) {
-  Vd v[4];
   double r;
-  load_elem(T, o.c, r, v);
+  load_elem(T, o.c, r, o.v);
   double spread = 0;
-  for (int k = 0; k < 4; ++k) {
-    o.xq[k] = quad_point(v, k);
-    spread = fmax(spread, vdist(o.xq[k], o.c));
-  }
+  for (int k = 0; k < 4; ++k) spread = fmax(spread, vdist(quad_point(o.v, k), o.c));
   o.T = T;
   o.R = cD.delta + spread;
 }
 
+constexpr int kPairThreads = 128;
+constexpr int kCandBuf = 256;
+
+// Warp per outer element T.  Phase 1 streams the grid rows around T and keeps
+// the candidates whose bounding sphere can reach B(delta) of some quadrature
+// point (a conservative superset of the reference's BFS superset,
+// assembly.cpp:569-613) in shared memory; phase 2 classifies them with one
+// lane per (candidate, quadrature point) -- the reference's exact per-(T,q,T')
+// predicates -- and ORs the four 5-bit codes of a candidate.  Pair order is the
+// candidate order, identical in the count and the fill pass.
 template <bool FILL>
-__global__ void __launch_bounds__(128) k_pairs(const long long* pair_off, int* pair_count,
-                                               int* partner, unsigned* info,
-                                               unsigned long long* item_count, int* err_elem) {
+__global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair_off, int* pair_count,
+                                                        int* partner, unsigned* info,
+                                                        unsigned long long* item_count,
+                                                        int* err_elem) {
+  __shared__ int cand[kPairThreads / 32][kCandBuf];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   if (warp >= cD.KI) return;
+  int* cb = cand[wl];
   OuterT o;
   outer_setup(cD.interior[warp], o);
   const double reach = o.R + cD.rmax;
@@ -366,10 +405,50 @@ __global__ void __launch_bounds__(128) k_pairs(const long long* pair_off, int* p
   const int y1 = cell_of(o.c.y + reach, cD.goy, cD.ginv, cD.gy);
   const int z0 = cell_of(o.c.z - reach, cD.goz, cD.ginv, cD.gz);
   const int z1 = cell_of(o.c.z + reach, cD.goz, cD.ginv, cD.gz);
-  long long out = FILL ? pair_off[warp] : 0;
-  int cnt = 0;
+  const long long out = FILL ? pair_off[warp] : 0;
+  int cnt = 0, ncand = 0;
   unsigned items = 0;
   const double reach2 = reach * reach * (1.0 + 1e-9);
+
+  auto flush = [&]() {
+    __syncwarp();
+    for (int base = 0; base < ncand; base += 8) {
+      const int t = base + (lane >> 2), q = lane & 3;
+      unsigned code = 0;
+      int Tp = -1;
+      if (t < ncand) {
+        Tp = cb[t];
+        Vd cp, v[4];
+        double rad;
+        load_elem(Tp, cp, rad, v);
+        double dia = 0;  // ElementTable::diam (ball_approx.cpp:61-67)
+        for (int i = 0; i < 4; ++i)
+          for (int j = i + 1; j < 4; ++j) dia = fmax(dia, vnorm2(vsub(v[i], v[j])));
+        dia = sqrt(dia);
+        const Vd xq = quad_point(o.v, q);
+        code = classify_item(xq, cp, rad, v, dia, cD.vol[Tp], cD.tau[Tp]) << (5 * q);
+        if (!FILL) {
+          items += code != 0;
+          const int4 nb = cD.nbr[Tp];
+          if ((nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) && facet_too_close(v, nb, xq))
+            atomicMin(err_elem, Tp);
+        }
+      }
+      code |= __shfl_xor_sync(FULLMASK, code, 1);
+      code |= __shfl_xor_sync(FULLMASK, code, 2);
+      const bool keep = (lane & 3) == 0 && code != 0;
+      const unsigned bal = __ballot_sync(FULLMASK, keep);
+      if (FILL && keep) {
+        const long long pos = out + cnt + __popc(bal & ((1u << lane) - 1));
+        partner[pos] = Tp;
+        info[pos] = code;
+      }
+      cnt += __popc(bal);
+    }
+    __syncwarp();
+    ncand = 0;
+  };
+
   for (int z = z0; z <= z1; ++z) {
     const double zl = cD.goz + z * cD.hg, zh = zl + cD.hg;
     const double dz = o.c.z < zl ? zl - o.c.z : (o.c.z > zh ? o.c.z - zh : 0.0);
@@ -381,51 +460,24 @@ __global__ void __launch_bounds__(128) k_pairs(const long long* pair_off, int* p
       const int e0 = cD.cell_start[row + x0], e1 = cD.cell_start[row + x1 + 1];
       for (int base = e0; base < e1; base += 32) {
         const int e = base + lane;
-        unsigned code = 0;
+        bool pass = false;
         int Tp = -1;
         if (e < e1) {
           Tp = cD.cell_elems[e];
           const double4 a = cD.erec[4 * Tp];
-          const Vd cp = {a.x, a.y, a.z};
           const double thr = a.w + o.R;
-          if (vnorm2(vsub(cp, o.c)) < thr * thr * (1.0 + 1e-10)) {
-            Vd v[4];
-            load_verts(Tp, v);
-            const double vol = cD.vol[Tp], tau = cD.tau[Tp];
-            double dia = 0;  // ElementTable::diam (ball_approx.cpp:61-67)
-            for (int i = 0; i < 4; ++i)
-              for (int j = i + 1; j < 4; ++j) dia = fmax(dia, vnorm2(vsub(v[i], v[j])));
-            dia = sqrt(dia);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              code |= classify_item(o.xq[k], cp, a.w, v, dia, vol, tau) << (5 * k);
-            if (!FILL) {
-              const int4 nb = cD.nbr[Tp];
-              if (nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) {
-                const int nbv[4] = {nb.x, nb.y, nb.z, nb.w};
-                for (int k = 0; k < 4; ++k)
-                  for (int f = 0; f < 4; ++f)
-                    if (nbv[f] < 0 && facet_distance(v, f, o.xq[k]) < cD.delta - cD.slack)
-                      atomicMin(err_elem, Tp);
-              }
-            }
-          }
+          pass = vnorm2(vsub({a.x, a.y, a.z}, o.c)) < thr * thr * (1.0 + 1e-10);
         }
-        const bool keep = code != 0;
-        const unsigned bal = __ballot_sync(FULLMASK, keep);
-        if (FILL && keep) {
-          const long long pos = out + cnt + __popc(bal & ((1u << lane) - 1));
-          partner[pos] = Tp;
-          info[pos] = code;
-        }
-        if (!FILL && keep)
-          for (int k = 0; k < 4; ++k) items += ((code >> (5 * k)) & 31) != 0;
-        cnt += __popc(bal);
+        const unsigned bal = __ballot_sync(FULLMASK, pass);
+        if (pass) cb[ncand + __popc(bal & ((1u << lane) - 1))] = Tp;
+        ncand += __popc(bal);
+        if (ncand > kCandBuf - 32) flush();
       }
     }
   }
+  flush();
   if (!FILL) {
-    for (int s = 16; s > 0; s >>= 1) items += __shfl_xor_sync(FULLMASK, items, s);
+    for (int sh = 16; sh > 0; sh >>= 1) items += __shfl_xor_sync(FULLMASK, items, sh);
     if (lane == 0) {
       pair_count[warp] = cnt;
       atomicAdd(item_count, (unsigned long long)items);
@@ -509,13 +561,7 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
     __syncthreads();
     for (int k = a; k < b; ++k) {
       const int T = cD.ni_el[k];
-      // position of T in the interior list: interior ids ascending -> binary search
-      int lo = 0, hi = cD.KI - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (cD.interior[mid] < T) lo = mid + 1;
-        else hi = mid;
-      }
+      const int lo = cD.ipos[T];
       const long long p0 = pair_off[lo], p1 = pair_off[lo + 1];
       for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const int Tp = partner[p];
@@ -679,17 +725,30 @@ __global__ void k_outpat(const long long* soff, const int* scols, int* olen,
 
 constexpr int kIntThreads = 128;
 
-struct McSlot {
-  nlfem_mc_frame fr[3];
-  double w[3];
-  double c0[3];  // x_q - v0(T')
-  int Tp, nsub, constr, q;
-};
-
+// Two-word fixed point: v*scale = hi + lo * 2^-40 with hi = rint(v*scale)
+// (exact: scale is a power of two) and lo = rint((v*scale - hi) * 2^40), so an
+// accumulated entry carries ~101 bits and equals the exact sum of the FP64
+// contributions up to one final rounding; integer adds make it order-free.
 __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot, double v,
                                           double scale) {
-  const long long x = __double2ll_rn(v * scale);
-  if (x != 0) atomicAdd(V + slot, (unsigned long long)x);
+  const double x = v * scale;
+  const long long hi = __double2ll_rn(x);
+  const long long lo = __double2ll_rn((x - (double)hi) * 0x1p40);
+  if (hi != 0) atomicAdd(V + 2 * slot, (unsigned long long)hi);
+  if (lo != 0) atomicAdd(V + 2 * slot + 1, (unsigned long long)lo);
+}
+
+__device__ __forceinline__ double fixed_value(const unsigned long long* V, long long slot,
+                                              double iscale) {
+  const long long hi = (long long)V[2 * slot], lo = (long long)V[2 * slot + 1];
+  return ((double)hi + (double)lo * 0x1p-40) * iscale;
+}
+
+// error-free transformation for compensated sums (Knuth TwoSum)
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
 }
 
 // butterfly sum over the warp (fixed tree -> deterministic)
@@ -701,18 +760,260 @@ __device__ __forceinline__ double wsum(double v) {
 // S2 index of (b, c), b <= c
 __device__ __forceinline__ int s2i(int b, int c) { return b * 4 - (b * (b - 1)) / 2 + (c - b); }
 
-struct PairAcc {
-  double S0[4], S1[4][4], S2[10], Sg[4];
+__device__ __forceinline__ int interior_pos(int T) { return cD.ipos[T]; }
+
+// number of Monte Carlo units (sub-simplices, before the volume floor) of a pair
+__device__ __forceinline__ int pair_units(unsigned code) {
+  int n = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const unsigned c = (code >> (5 * q)) & 31;
+    if (c == kOutCap) n += 1;
+    else if (c & kStraddle) n += outer_units((int)(c & 15));
+  }
+  return n;
+}
+
+__global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < np) ucount[i] = pair_units(info[p0 + i]);
+}
+
+// unit descriptors: pair index (chunk-relative) and (q | sub << 2)
+__global__ void k_units_fill(long long p0, long long np, const unsigned* info,
+                             const long long* uoff, int* upair, unsigned char* uqs) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  const unsigned code = info[p0 + i];
+  long long u = uoff[i];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const unsigned c = (code >> (5 * q)) & 31;
+    int n = 0;
+    if (c == kOutCap) n = 1;
+    else if (c & kStraddle) n = outer_units((int)(c & 15));
+    for (int sb = 0; sb < n; ++sb, ++u) {
+      upair[u] = (int)i;
+      uqs[u] = (unsigned char)(q | (sb << 2));
+    }
+  }
+}
+
+__global__ void k_pair_outer(int ii0, int ii1, const long long* pair_off, long long P0,
+                             int* pair_outer) {
+  const int ii = ii0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (ii >= ii1) return;
+  for (long long p = pair_off[ii]; p < pair_off[ii + 1]; ++p) pair_outer[p - P0] = ii;
+}
+
+// Philox4x32-10 on three counters in lockstep (independent chains -> ILP 3);
+// same function as nlfem_philox4x32_10 applied to each counter.
+__device__ __forceinline__ void philox3(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t j3,
+                                        uint32_t k0, uint32_t k1, uint32_t A[4], uint32_t B[4],
+                                        uint32_t Cw[4]) {
+  uint32_t a0 = c0, a1 = c1, a2 = c2, a3 = j3;
+  uint32_t b0 = c0, b1 = c1, b2 = c2, b3 = j3 + 1;
+  uint32_t d0 = c0, d1 = c1, d2 = c2, d3 = j3 + 2;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long pa0 = (unsigned long long)NLFEM_PHILOX_M0 * a0;
+    const unsigned long long pa2 = (unsigned long long)NLFEM_PHILOX_M1 * a2;
+    const unsigned long long pb0 = (unsigned long long)NLFEM_PHILOX_M0 * b0;
+    const unsigned long long pb2 = (unsigned long long)NLFEM_PHILOX_M1 * b2;
+    const unsigned long long pd0 = (unsigned long long)NLFEM_PHILOX_M0 * d0;
+    const unsigned long long pd2 = (unsigned long long)NLFEM_PHILOX_M1 * d2;
+    const uint32_t kk0 = k0 + (uint32_t)r * NLFEM_PHILOX_W0, kk1 = k1 + (uint32_t)r * NLFEM_PHILOX_W1;
+    a0 = (uint32_t)(pa2 >> 32) ^ a1 ^ kk0; a1 = (uint32_t)pa2;
+    a2 = (uint32_t)(pa0 >> 32) ^ a3 ^ kk1; a3 = (uint32_t)pa0;
+    b0 = (uint32_t)(pb2 >> 32) ^ b1 ^ kk0; b1 = (uint32_t)pb2;
+    b2 = (uint32_t)(pb0 >> 32) ^ b3 ^ kk1; b3 = (uint32_t)pb0;
+    d0 = (uint32_t)(pd2 >> 32) ^ d1 ^ kk0; d1 = (uint32_t)pd2;
+    d2 = (uint32_t)(pd0 >> 32) ^ d3 ^ kk1; d3 = (uint32_t)pd0;
+  }
+  A[0] = a0; A[1] = a1; A[2] = a2; A[3] = a3;
+  B[0] = b0; B[1] = b1; B[2] = b2; B[3] = b3;
+  Cw[0] = d0; Cw[1] = d1; Cw[2] = d2; Cw[3] = d3;
+}
+
+// w + 0.5 as a double with one DADD: the bits 0x43300000:w are 2^52 + w
+__device__ __forceinline__ double u32_plus_half(uint32_t w) {
+  return __hiloint2double(0x43300000, (int)w) - 4503599627370495.5;  // 2^52 - 0.5
+}
+
+// nlfem_mc_point with the frame pre-scaled by 2^-32 (E' = 2^-32 E): since
+// u E = (w + 1/2) 2^-32 E = (w + 1/2) E' exactly, fma(u, E, p) == fma(w + 1/2, E', p)
+// bit for bit, so decisions and r equal include/nlfem_mc_stream.h's.
+__device__ __forceinline__ bool mc_point_fast(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const nlfem_mc_frame& f, double dd, double& rx,
+                                              double& ry, double& rz) {
+  const uint32_t lo = min(w0, w1), hi = max(w0, w1);
+  const uint32_t s0 = min(lo, w2), t = max(lo, w2);
+  const uint32_t s1 = min(hi, t), s2 = max(hi, t);
+  const double u0 = u32_plus_half(s0), u1 = u32_plus_half(s1), u2 = u32_plus_half(s2);
+  rx = fma(u2, f.e2[0], fma(u1, f.e1[0], fma(u0, f.e0[0], f.p[0])));
+  ry = fma(u2, f.e2[1], fma(u1, f.e1[1], fma(u0, f.e0[1], f.p[1])));
+  rz = fma(u2, f.e2[2], fma(u1, f.e1[2], fma(u0, f.e0[2], f.p[2])));
+  return fma(rz, rz, fma(ry, ry, rx * rx)) < dd;
+}
+
+struct PickPiece {  // selects the want-th kept piece
+  int want, seen = 0;
+  bool found = false;
+  Vd a, b, c, d;
+  double vol;
+  __device__ __forceinline__ void operator()(Vd A, Vd B, Vd C, Vd D, double v) {
+    if (seen == want) {
+      a = A;
+      b = B;
+      c = C;
+      d = D;
+      vol = v;
+      found = true;
+    }
+    ++seen;
+  }
 };
 
-__device__ __forceinline__ void acc_point_interior(PairAcc& A, int q, double w, const double l[4]) {
-  A.S0[q] += w;
+// Monte Carlo: one thread per unit = one sub-simplex of one cap item, M samples
+// of the mode-P stream (include/nlfem_mc_stream.h).  Writes the weighted
+// Cartesian moments about v0(T'): S0, sum w r, sum w r r^T (6), and sum w g(y)
+// for constraint parents, SoA [11][nunits].
+constexpr int kMcThreads = 128;
+
+__global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nunits,
+                                                   const int* upair, const unsigned char* uqs,
+                                                   const int* pair_outer, const int* partner,
+                                                   const unsigned* info, double* mom,
+                                                   unsigned long long* mc_stats) {
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double S0 = 0, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
+  unsigned long long draws = 0, hits = 0, led = 0;
+  if (u < nunits) {
+    const int pi = upair[u];
+    const int q = uqs[u] & 3, sub = uqs[u] >> 2;
+    const long long p = p0 + pi;
+    const int T = cD.interior[pair_outer[pi]];
+    const int Tp = partner[p];
+    const unsigned c = (info[p] >> (5 * q)) & 31;
+    Vd vT[4];
+    load_verts(T, vT);
+    const Vd xq = quad_point(vT, q);
+    Vd vP[4];
+    load_verts(Tp, vP);
+    PickPiece pk;
+    pk.want = sub;
+    if (c == kOutCap) {
+      if (sub == 0) {
+        pk.a = vP[0];
+        pk.b = vP[1];
+        pk.c = vP[2];
+        pk.d = vP[3];
+        pk.vol = tet_volume(vP[0], vP[1], vP[2], vP[3]);
+        pk.found = true;
+      }
+    } else {
+      // the sub-th kept piece of straddle_outer
+      const Straddle st = outer_straddle(vP, (int)(c & 15), xq, cD.delta);
+      const double tau = cD.tau[Tp];
+      for (int k = 0; k < st.n; ++k) {
+        Vd a, b, cc, d;
+        straddle_piece(st, k, a, b, cc, d);
+        const double vol = tet_volume(a, b, cc, d);
+        if (vol > tau) pk(a, b, cc, d, vol);
+      }
+      const int m = __popc(c & 15);
+      if (sub == 0) led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
+    }
+    if (pk.found) {
+      const bool cons = cD.region[Tp] != 0;
+      const double w = pk.vol / cD.mc;
+      nlfem_mc_frame fr;
+      {
+        const double a0[3] = {pk.a.x, pk.a.y, pk.a.z}, a1[3] = {pk.b.x, pk.b.y, pk.b.z},
+                     a2[3] = {pk.c.x, pk.c.y, pk.c.z}, a3[3] = {pk.d.x, pk.d.y, pk.d.z},
+                     x[3] = {xq.x, xq.y, xq.z};
+        nlfem_mc_make_frame(a0, a1, a2, a3, x, &fr);
+      }
+      const double c0x = xq.x - vP[0].x, c0y = xq.y - vP[0].y, c0z = xq.z - vP[0].z;
+      const int nb = (cD.mc + 3) >> 2;
+      unsigned nh = 0;
+      double n1x = 0, n1y = 0, n1z = 0, n2[6] = {0, 0, 0, 0, 0, 0}, ng = 0;
+      const uint32_t k0 = (uint32_t)(cD.seed & 0xffffffffu), k1 = (uint32_t)(cD.seed >> 32);
+      const uint32_t c2 = (uint32_t)q | ((uint32_t)sub << 2);
+      nlfem_mc_frame fs = fr;  // frame pre-scaled by 2^-32 (exact)
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const double wb = w * l[b];
-    A.S1[q][b] += wb;
+      for (int a = 0; a < 3; ++a) {
+        fs.e0[a] = fr.e0[a] * 0x1p-32;
+        fs.e1[a] = fr.e1[a] * 0x1p-32;
+        fs.e2[a] = fr.e2[a] * 0x1p-32;
+      }
+      const double dd = cD.dd;
+      // branch-free accumulation of one sample (interior: Cartesian moments
+      // about v0(T'); constraint: g at the hit)
+      auto sample = [&](uint32_t a, uint32_t b, uint32_t cc, bool valid) {
+        double rx, ry, rz;
+        const bool hit = mc_point_fast(a, b, cc, fs, dd, rx, ry, rz) && valid;
+        nh += hit;
+        if (cons) {
+          if (hit) ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
+        } else {
+          const double h = hit ? 1.0 : 0.0;
+          rx += c0x;
+          ry += c0y;
+          rz += c0z;
+          const double hx = h * rx, hy = h * ry, hz = h * rz;
+          n1x += hx;
+          n1y += hy;
+          n1z += hz;
+          n2[0] = fma(hx, rx, n2[0]);
+          n2[1] = fma(hx, ry, n2[1]);
+          n2[2] = fma(hx, rz, n2[2]);
+          n2[3] = fma(hy, ry, n2[3]);
+          n2[4] = fma(hy, rz, n2[4]);
+          n2[5] = fma(hz, rz, n2[5]);
+        }
+      };
+      const int full = cD.mc >> 2;  // complete blocks of four samples
+#pragma unroll 1
+      for (int j = 0; j < nb; ++j) {
+        // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
+        uint32_t A[4], B[4], Cw[4];
+        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, k0, k1, A, B, Cw);
+        const bool tail = j >= full;
+        sample(A[0], A[1], A[2], true);
+        sample(A[3], B[0], B[1], !tail || 4 * j + 1 < cD.mc);
+        sample(B[2], B[3], Cw[0], !tail || 4 * j + 2 < cD.mc);
+        sample(Cw[1], Cw[2], Cw[3], !tail || 4 * j + 3 < cD.mc);
+      }
+      S0 = w * nh;
+      m1x = w * n1x;
+      m1y = w * n1y;
+      m1z = w * n1z;
 #pragma unroll
-    for (int c = b; c < 4; ++c) A.S2[s2i(b, c)] += wb * l[c];
+      for (int k = 0; k < 6; ++k) m2[k] = w * n2[k];
+      sg = w * ng;
+      draws = (unsigned long long)cD.mc;
+      hits = nh;
+      led += 25ull + 35ull * (unsigned long long)cD.mc + (cons ? 12ull : 62ull) * nh;
+    }
+    mom[u] = S0;
+    mom[nunits + u] = m1x;
+    mom[2 * nunits + u] = m1y;
+    mom[3 * nunits + u] = m1z;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) mom[(4 + k) * nunits + u] = m2[k];
+    mom[10 * nunits + u] = sg;
+  }
+  // statistics
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    draws += __shfl_xor_sync(FULLMASK, draws, sh);
+    hits += __shfl_xor_sync(FULLMASK, hits, sh);
+    led += __shfl_xor_sync(FULLMASK, led, sh);
+  }
+  if ((threadIdx.x & 31) == 0 && (draws | led)) {
+    atomicAdd(mc_stats, draws);
+    atomicAdd(mc_stats + 1, hits);
+    atomicAdd(mc_stats + 2, led);
   }
 }
 
@@ -725,381 +1026,297 @@ __device__ __forceinline__ void bary(const double inv[9], Vd v0, Vd p, double l[
   l[0] = 1.0 - l[1] - l[2] - l[3];
 }
 
-__global__ void __launch_bounds__(kIntThreads) k_integrate(
-    const long long* pair_off, const int* partner, const unsigned* info, const long long* soff,
-    const int* scols, const long long* eslot, unsigned long long* V, double* rhsT,
-    unsigned long long* mc_stats, int rowcap) {
-  // mc_stats: [0] draws, [1] hits, [2] ledger FLOPs, [3] MC sub-simplices
-  extern __shared__ unsigned char smraw[];
-  McSlot* slots = reinterpret_cast<McSlot*>(smraw);
-  int* rows = reinterpret_cast<int*>(slots + kIntThreads);  // 4 staged rows
+// shared-memory map: node id -> slots of (N_a, node) in the four staged rows
+struct SlotMap {
+  int* key;
+  short4* val;  // slot offsets within row a (-1: absent); rows hold < 32768 entries
+  int mask;
+  __device__ __forceinline__ int probe(int k) const {
+    unsigned h = hash32((unsigned)k) & mask;
+    while (key[h] != k) h = (h + 1) & mask;
+    return (int)h;
+  }
+};
+
+// Combine: CTA per outer element T, thread per element pair.  Closed-form
+// whole elements and Gauss sub-simplices are integrated here; Monte Carlo
+// units come from k_mc.  The per-pair 4x4 blocks are scattered as two-word
+// fixed point into the node pattern.
+__global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
+    int ii0, const long long* pair_off, const int* partner, const unsigned* info,
+    const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
+    double* rhsT, const long long* uoff, const double* mom, long long nunits, long long pbase,
+    unsigned long long* mc_stats, int hcap) {
+  extern __shared__ int smi[];
+  SlotMap mp;
+  mp.key = smi;
+  mp.val = reinterpret_cast<short4*>(smi + hcap);
+  mp.mask = hcap - 1;
   __shared__ long long rbase[4];
-  __shared__ int rlen[4];
   __shared__ double red[kIntThreads / 32][14];
 
-  const int ii = blockIdx.x;
+  const int ii = ii0 + blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int T = cD.interior[ii];
-  Vd vT[4], cT;
-  double rT;
-  load_elem(T, cT, rT, vT);
   const int4 wT = cD.verts[T];
   const int NT[4] = {wT.x, wT.y, wT.z, wT.w};
-  const double wq = 0.25 * cD.vol[T];  // rule.w[k] * vol (reference assembly.cpp:702)
-  const double C = cD.C;
-  Vd xq[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) xq[k] = quad_point(vT, k);
 
-  // stage the four T-node rows of the node pattern (sorted columns)
-  if (threadIdx.x < 4) {
-    rbase[threadIdx.x] = soff[NT[threadIdx.x]];
-    rlen[threadIdx.x] = (int)(soff[NT[threadIdx.x] + 1] - soff[NT[threadIdx.x]]);
+  // build the slot map from the four T-node rows of the node pattern
+  for (int h = threadIdx.x; h < hcap; h += blockDim.x) {
+    mp.key[h] = -1;
+    mp.val[h] = make_short4(-1, -1, -1, -1);
+  }
+  if (threadIdx.x < 4) rbase[threadIdx.x] = soff[NT[threadIdx.x]];
+  __syncthreads();
+  for (int a = 0; a < 4; ++a) {
+    const long long r0 = soff[NT[a]], r1 = soff[NT[a] + 1];
+    for (long long k = r0 + threadIdx.x; k < r1; k += blockDim.x) {
+      const int col = scols[k];
+      unsigned h = hash32((unsigned)col) & mp.mask;
+      while (true) {
+        const int prev = atomicCAS(mp.key + h, -1, col);
+        if (prev == -1 || prev == col) break;
+        h = (h + 1) & mp.mask;
+      }
+      short* v = reinterpret_cast<short*>(mp.val + h);
+      v[a] = (short)(k - r0);
+    }
   }
   __syncthreads();
-  for (int a = 0; a < 4; ++a)
-    for (int s = threadIdx.x; s < rlen[a]; s += blockDim.x) rows[a * rowcap + s] = scols[rbase[a] + s];
-  __syncthreads();
 
-  double DT[10];
-  double rhsc[4];
-#pragma unroll
-  for (int k = 0; k < 10; ++k) DT[k] = 0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) rhsc[a] = 0;
-  unsigned long long n_samp = 0, n_hit = 0, led = 0, nsubs = 0;
+  Vd vT[4];
+  load_verts(T, vT);
+  const double wq = 0.25 * cD.vol[T];  // rule.w[k] * vol (reference assembly.cpp:702)
+  const double C = cD.C;
+  // per outer element: sum over pairs of S0_q (constraint parents weigh 2,
+  // reference assembly.cpp:419) and of sum_q c_{q,a} Sg_q; D_T and the rhs
+  // follow from them
+  double s0w[4] = {0, 0, 0, 0}, sgc[4] = {0, 0, 0, 0};
+  unsigned long long led = 0;
 
   const long long p0 = pair_off[ii], p1 = pair_off[ii + 1];
-  const long long np = p1 - p0;
-  const int rounds = (int)((np + kIntThreads - 1) / kIntThreads);
-  const bool fullcaps = cD.strategy == NLFEM_STRATEGY_FULLCAPS;
+  for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    // per pair: X[a][b] = sum_q c_{q,a} S1_q[b] (T x T' block before -C w),
+    // S2 = sum_q S2_q (T' x T' block before C w)
+    double X[4][4], S2[10];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) X[a][b] = 0;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) S2[k] = 0;
 
-  for (int rd = 0; rd < rounds; ++rd) {
-    const long long p = p0 + (long long)rd * kIntThreads + threadIdx.x;
-    const bool valid = p < p1;
-    PairAcc A;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      A.S0[q] = 0;
-      A.Sg[q] = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) A.S1[q][b] = 0;
-    }
-#pragma unroll
-    for (int k = 0; k < 10; ++k) A.S2[k] = 0;
+    const int Tp = partner[p];
+    const unsigned code = info[p];
+    const bool constr = cD.region[Tp] != 0;
+    Vd vP[4];
+    load_verts(Tp, vP);
+    const double volP = cD.vol[Tp];
+    const double* invP = cD.inv + 9 * (long long)Tp;
+    long long u = (mom != nullptr) ? uoff[p - pbase] : 0;
 
-    int Tp = 0;
-    unsigned code = 0;
-    Vd vP[4], cP;
-    double rP = 0, volP = 0, tauP = 0;
-    double invP[9];
-    bool constr = false;
-    int4 wP = make_int4(0, 0, 0, 0);
-    if (valid) {
-      Tp = partner[p];
-      code = info[p];
-      load_elem(Tp, cP, rP, vP);
-      volP = cD.vol[Tp];
-      tauP = cD.tau[Tp];
-      constr = cD.region[Tp] != 0;
-      wP = cD.verts[Tp];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) invP[k] = cD.inv[9 * (long long)Tp + k];
-    }
-
-    // ---- thread level: whole elements and Gauss sub-simplices
-#pragma unroll
+#pragma unroll 1
     for (int q = 0; q < 4; ++q) {
       const unsigned c = (code >> (5 * q)) & 31;
+      if (c == 0) continue;
+      // moments of this (T, q, T') item: S0, S1 (interior) or Sg (constraint)
+      double S0 = 0, S1[4] = {0, 0, 0, 0}, Sg = 0;
       if (c == kWhole) {
         led += constr ? 133 : 39;
+        S0 = volP;
         if (constr) {
           // constraint parent: measure and g average (reference assembly.cpp:350-359)
-          A.S0[q] += volP;
-          for (int k = 0; k < 4; ++k) A.Sg[q] += volP * 0.25 * poly_eval(cD.g, quad_point(vP, k));
+#pragma unroll 1
+          for (int k = 0; k < 4; ++k) Sg += volP * 0.25 * poly_eval(cD.g, quad_point(vP, k));
         } else {
           // exact basis moments of a whole element (reference assembly.cpp:361-369)
-          A.S0[q] += volP;
           const double s1 = volP / 4, off = volP / 20.0;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            A.S1[q][b] += s1;
+            S1[b] = s1;
 #pragma unroll
-            for (int cc = b; cc < 4; ++cc) A.S2[s2i(b, cc)] += off * (b == cc ? 2.0 : 1.0);
+            for (int cc = b; cc < 4; ++cc) S2[s2i(b, cc)] += off * (b == cc ? 2.0 : 1.0);
           }
         }
       } else if (c & kStraddle) {
-        Tet pcs[3];
-        const int n = straddle_inner(vP, (int)(c & 15), xq[q], cD.delta, tauP, pcs);
-        {
-          const int m = __popc(c & 15);
-          led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3));
-          led += (unsigned long long)n * (constr ? 160 : 360);
-        }
-        for (int s = 0; s < n; ++s) {
-          const double vs = tet_volume(pcs[s].v[0], pcs[s].v[1], pcs[s].v[2], pcs[s].v[3]);
-          for (int k = 0; k < 4; ++k) {
-            const Vd y = quad_point(pcs[s].v, k);
-            const double w = vs * 0.25;
+        // Gauss rule on the inner sub-simplices (reference AsmSink::sub +
+        // accumulate_point, assembly.cpp:332-381)
+        const Vd xq = quad_point(vT, q);
+        const Straddle st = inner_straddle(vP, (int)(c & 15), xq, cD.delta);
+        const double tau = cD.tau[Tp];
+        int kept = 0;
+#pragma unroll 1
+        for (int k = 0; k < st.n; ++k) {
+          Vd pa, pb, pc, pd;
+          straddle_piece(st, k, pa, pb, pc, pd);
+          const double vol = tet_volume(pa, pb, pc, pd);
+          if (!(vol > tau)) continue;
+          ++kept;
+          const Vd pv[4] = {pa, pb, pc, pd};
+          const double w = vol * 0.25;
+#pragma unroll 1
+          for (int g = 0; g < 4; ++g) {
+            const Vd y = quad_point(pv, g);
+            S0 += w;
             if (constr) {
-              A.S0[q] += w;
-              A.Sg[q] += w * poly_eval(cD.g, y);
+              Sg += w * poly_eval(cD.g, y);
             } else {
               double l[4];
-              bary(invP, vP[0], y, l);
-              acc_point_interior(A, q, w, l);
+              const Vd d = vsub(y, vP[0]);
+              l[1] = invP[0] * d.x + invP[1] * d.y + invP[2] * d.z;
+              l[2] = invP[3] * d.x + invP[4] * d.y + invP[5] * d.z;
+              l[3] = invP[6] * d.x + invP[7] * d.y + invP[8] * d.z;
+              l[0] = 1.0 - l[1] - l[2] - l[3];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const double wb = w * l[i];
+                S1[i] += wb;
+#pragma unroll
+                for (int j = i; j < 4; ++j) S2[s2i(i, j)] += wb * l[j];
+              }
+            }
+          }
+        }
+        const int m = __popc(c & 15);
+        led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
+               (unsigned long long)kept * (constr ? 160 : 360);
+      }
+      // Monte Carlo units of this item, in sub-simplex order
+      if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
+        const int nu = c == kOutCap ? 1 : outer_units((int)(c & 15));
+        double n0 = 0, g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+        for (int sb = 0; sb < nu; ++sb, ++u) {
+          n0 += mom[u];
+          if (constr) {
+            g0 += mom[10 * nunits + u];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) m1[k] += mom[(1 + k) * nunits + u];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) m2[k] += mom[(4 + k) * nunits + u];
+          }
+        }
+        S0 += n0;
+        if (constr) {
+          Sg += g0;
+        } else {
+          // lambda(y) = e_0 + J (y - v0): J rows from inv_edges, J0 = -(J1+J2+J3)
+          double J[4][3];
+#pragma unroll
+          for (int r = 1; r < 4; ++r)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) J[r][a] = invP[3 * (r - 1) + a];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) J[0][a] = -(J[1][a] + J[2][a] + J[3][a]);
+          const double M[3][3] = {{m2[0], m2[1], m2[2]}, {m2[1], m2[3], m2[4]},
+                                  {m2[2], m2[4], m2[5]}};
+          double jm[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) jm[b] = J[b][0] * m1[0] + J[b][1] * m1[1] + J[b][2] * m1[2];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            double JM[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) JM[a] = J[b][0] * M[0][a] + J[b][1] * M[1][a] + J[b][2] * M[2][a];
+            S1[b] += (b == 0 ? n0 : 0.0) + jm[b];
+#pragma unroll
+            for (int cc = b; cc < 4; ++cc) {
+              double s2 = JM[0] * J[cc][0] + JM[1] * J[cc][1] + JM[2] * J[cc][2];
+              if (b == 0) s2 += jm[cc];
+              if (cc == 0) s2 += jm[b];
+              if (b == 0 && cc == 0) s2 += n0;
+              S2[s2i(b, cc)] += s2;
             }
           }
         }
       }
-    }
-
-    // ---- warp level: Monte Carlo caps (fullcaps)
-    if (fullcaps) {
+      // fold the item into the pair / outer-element accumulators
+      const double f = constr ? 2.0 * S0 : S0;
+      s0w[0] += q == 0 ? f : 0.0;
+      s0w[1] += q == 1 ? f : 0.0;
+      s0w[2] += q == 2 ? f : 0.0;
+      s0w[3] += q == 3 ? f : 0.0;
+      if (constr) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const unsigned c = (code >> (5 * q)) & 31;
-        int nsub = 0;
-        McSlot& my = slots[threadIdx.x];
-        if (c == kOutCap) {
-          nsub = 1;
-          nlfem_mc_frame fr;
-          const double v0[3] = {vP[0].x, vP[0].y, vP[0].z}, v1[3] = {vP[1].x, vP[1].y, vP[1].z},
-                       v2[3] = {vP[2].x, vP[2].y, vP[2].z}, v3[3] = {vP[3].x, vP[3].y, vP[3].z},
-                       x[3] = {xq[q].x, xq[q].y, xq[q].z};
-          nlfem_mc_make_frame(v0, v1, v2, v3, x, &fr);
-          my.fr[0] = fr;
-          my.w[0] = tet_volume(vP[0], vP[1], vP[2], vP[3]) / cD.mc;
-        } else if (c & kStraddle) {
-          Tet pcs[3];
-          nsub = straddle_outer(vP, (int)(c & 15), xq[q], cD.delta, tauP, pcs);
-          const int m = __popc(c & 15);
-          led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
-          for (int s = 0; s < nsub; ++s) {
-            const Vd* u = pcs[s].v;
-            const double v0[3] = {u[0].x, u[0].y, u[0].z}, v1[3] = {u[1].x, u[1].y, u[1].z},
-                         v2[3] = {u[2].x, u[2].y, u[2].z}, v3[3] = {u[3].x, u[3].y, u[3].z},
-                         x[3] = {xq[q].x, xq[q].y, xq[q].z};
-            nlfem_mc_make_frame(v0, v1, v2, v3, x, &my.fr[s]);
-            my.w[s] = tet_volume(u[0], u[1], u[2], u[3]) / cD.mc;
-          }
+        for (int a = 0; a < 4; ++a) sgc[a] += Sg * qbary(q, a);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double ca = qbary(q, a);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) X[a][b] += ca * S1[b];
         }
-        if (nsub > 0) {
-          my.nsub = nsub;
-          my.Tp = Tp;
-          my.constr = constr;
-          my.c0[0] = xq[q].x - vP[0].x;
-          my.c0[1] = xq[q].y - vP[0].y;
-          my.c0[2] = xq[q].z - vP[0].z;
-        }
-        unsigned pend = __ballot_sync(FULLMASK, nsub > 0);
-        __syncwarp();
-        while (pend) {
-          const int L = __ffs(pend) - 1;
-          pend &= pend - 1;
-          const McSlot& it = slots[wid * 32 + L];
-          const int ns = it.nsub, cons = it.constr, tp = it.Tp;
-          const int gps = (cD.mc + 3) >> 2;  // sample blocks per sub-simplex
-          const int G = ns * gps;
-          double n0 = 0, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
-          unsigned hits = 0;
-          for (int gI = lane; gI < G; gI += 32) {
-            const int sub = (gI >= gps) + (gI >= 2 * gps);
-            const int j = gI - sub * gps;
-            uint32_t W[12];
-            nlfem_mc_block(cD.seed, (uint32_t)T, (uint32_t)tp, (uint32_t)q, (uint32_t)sub,
-                           (uint32_t)j, W);
-            const nlfem_mc_frame fr = it.fr[sub];
-            const double w = it.w[sub];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (4 * j + i >= cD.mc) break;
-              double r[3];
-              if (nlfem_mc_point(W[3 * i], W[3 * i + 1], W[3 * i + 2], &fr, cD.dd, r)) {
-                ++hits;
-                if (cons) {
-                  n0 += w;
-                  sg += w * poly_eval(cD.g, {xq[q].x + r[0], xq[q].y + r[1], xq[q].z + r[2]});
-                } else {
-                  const double rx = r[0] + it.c0[0], ry = r[1] + it.c0[1], rz = r[2] + it.c0[2];
-                  n0 += w;
-                  const double tx = w * rx, ty = w * ry, tz = w * rz;
-                  m1x += tx;
-                  m1y += ty;
-                  m1z += tz;
-                  m2[0] = fma(tx, rx, m2[0]);
-                  m2[1] = fma(tx, ry, m2[1]);
-                  m2[2] = fma(tx, rz, m2[2]);
-                  m2[3] = fma(ty, ry, m2[3]);
-                  m2[4] = fma(ty, rz, m2[4]);
-                  m2[5] = fma(tz, rz, m2[5]);
-                }
-              }
-            }
-          }
-          n_hit += hits;
-          led += (unsigned long long)hits * (cons ? 12 : 62);
-          n0 = wsum(n0);
-          if (cons) {
-            sg = wsum(sg);
-            if (lane == L) {
-              A.S0[q] += n0;
-              A.Sg[q] += sg;
-            }
-          } else {
-            m1x = wsum(m1x);
-            m1y = wsum(m1y);
-            m1z = wsum(m1z);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) m2[k] = wsum(m2[k]);
-            if (lane == L) {
-              // lambda(y) = e_0 + J (y - v0), J rows from inv_edges
-              double Jr[4][3];
-              Jr[1][0] = invP[0]; Jr[1][1] = invP[1]; Jr[1][2] = invP[2];
-              Jr[2][0] = invP[3]; Jr[2][1] = invP[4]; Jr[2][2] = invP[5];
-              Jr[3][0] = invP[6]; Jr[3][1] = invP[7]; Jr[3][2] = invP[8];
-              for (int a = 0; a < 3; ++a) Jr[0][a] = -(Jr[1][a] + Jr[2][a] + Jr[3][a]);
-              const double M[3][3] = {{m2[0], m2[1], m2[2]}, {m2[1], m2[3], m2[4]},
-                                      {m2[2], m2[4], m2[5]}};
-              double jm[4];
-              double JM[4][3];
-              for (int b = 0; b < 4; ++b) {
-                jm[b] = Jr[b][0] * m1x + Jr[b][1] * m1y + Jr[b][2] * m1z;
-                for (int a = 0; a < 3; ++a)
-                  JM[b][a] = Jr[b][0] * M[0][a] + Jr[b][1] * M[1][a] + Jr[b][2] * M[2][a];
-              }
-              A.S0[q] += n0;
-#pragma unroll
-              for (int b = 0; b < 4; ++b) {
-                A.S1[q][b] += (b == 0 ? n0 : 0.0) + jm[b];
-#pragma unroll
-                for (int cc = b; cc < 4; ++cc) {
-                  double s2 = JM[b][0] * Jr[cc][0] + JM[b][1] * Jr[cc][1] + JM[b][2] * Jr[cc][2];
-                  if (b == 0) s2 += jm[cc];
-                  if (cc == 0) s2 += jm[b];
-                  if (b == 0 && cc == 0) s2 += n0;
-                  A.S2[s2i(b, cc)] += s2;
-                }
-              }
-            }
-          }
-          if (lane == L) {
-            n_samp += (unsigned long long)ns * (unsigned long long)cD.mc;
-            led += (unsigned long long)ns * (25ull + 35ull * (unsigned long long)cD.mc);
-            nsubs += ns;
-          }
-          __syncwarp();
-        }
-        __syncwarp();
       }
     }
 
     // ---- element-pair blocks -> fixed point scatter
-    if (valid) {
-      if (constr) {
-        // constraint parent (reference assembly.cpp:416-427): 2C w S0 c c^T, rhs 2C w Sg c
+    if (!constr) {
+      const int4 wP = cD.verts[Tp];
+      const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
+      // T x T' cross block: -C w X[a][b] at (N_a, M_b)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double base = wq * 2.0 * C;
-          for (int a = 0; a < 4; ++a) {
-            rhsc[a] += base * A.Sg[q] * qbary(q, a);
-            for (int b = a; b < 4; ++b) DT[s2i(a, b)] += base * A.S0[q] * qbary(q, a) * qbary(q, b);
-          }
-        }
-      } else {
-        const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
-        // T x T' cross block: X[a][b] = -C w sum_q c_{q,a} S1_q[b] at (N_a, M_b)
-        for (int b = 0; b < 4; ++b) {
-          for (int a = 0; a < 4; ++a) {
-            double x = 0;
-            for (int q = 0; q < 4; ++q) x += qbary(q, a) * A.S1[q][b];
-            x = -C * wq * x;
-            // slot of column NP[b] in staged row a
-            const int* rw = rows + a * rowcap;
-            int lo = 0, hi = rlen[a] - 1;
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (rw[mid] < NP[b]) lo = mid + 1;
-              else hi = mid;
-            }
-            const double v = NT[a] == NP[b] ? 2.0 * x : x;
-            red_fixed(V, rbase[a] + lo, v, cD.scale[NT[a]]);
-          }
-        }
-        // T' x T' block: C w sum_q S2_q at (M_b, M_c)
-        const long long* es = eslot;  // indexed by interior position of T'
-        int lo = 0, hi = cD.KI - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (cD.interior[mid] < Tp) lo = mid + 1;
-          else hi = mid;
-        }
-        for (int b = 0; b < 4; ++b)
-          for (int cc = b; cc < 4; ++cc) {
-            const int k = s2i(b, cc);
-            const int rowN = min(NP[b], NP[cc]);
-            red_fixed(V, es[10 * (long long)lo + k], C * wq * A.S2[k], cD.scale[rowN]);
-          }
-        // T x T block: C w S0_q c c^T, accumulated per outer element
+      for (int b = 0; b < 4; ++b) {
+        const short4 sl = mp.val[mp.probe(NP[b])];
+        const short sla[4] = {sl.x, sl.y, sl.z, sl.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          for (int a = 0; a < 4; ++a)
-            for (int b = a; b < 4; ++b)
-              DT[s2i(a, b)] += C * wq * A.S0[q] * qbary(q, a) * qbary(q, b);
+        for (int a = 0; a < 4; ++a) {
+          const double x = -C * wq * X[a][b];
+          red_fixed(V, rbase[a] + sla[a], NT[a] == NP[b] ? 2.0 * x : x, cD.scale[NT[a]]);
+        }
       }
+      // T' x T' block: C w sum_q S2_q at (M_b, M_c), row min(M_b, M_c)
+      const long long* es = eslot + 10 * (long long)interior_pos(Tp);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int cc = b; cc < 4; ++cc) {
+          const int k = s2i(b, cc);
+          red_fixed(V, es[k], C * wq * S2[k], cD.scale[min(NP[b], NP[cc])]);
+        }
     }
   }
 
   // ---- per outer element: D_T block and rhs (fixed-order CTA reduction)
-  for (int k = 0; k < 10; ++k) DT[k] = wsum(DT[k]);
-  for (int a = 0; a < 4; ++a) rhsc[a] = wsum(rhsc[a]);
-  if (lane == 0) {
-    for (int k = 0; k < 10; ++k) red[wid][k] = DT[k];
-    for (int a = 0; a < 4; ++a) red[wid][10 + a] = rhsc[a];
-  }
-  unsigned long long ns = n_samp, nh = n_hit, nl = led, nq = nsubs;
-  for (int s = 16; s > 0; s >>= 1) {
-    ns += __shfl_xor_sync(FULLMASK, ns, s);
-    nh += __shfl_xor_sync(FULLMASK, nh, s);
-    nl += __shfl_xor_sync(FULLMASK, nl, s);
-    nq += __shfl_xor_sync(FULLMASK, nq, s);
+  for (int q = 0; q < 4; ++q) {
+    s0w[q] = wsum(s0w[q]);
+    sgc[q] = wsum(sgc[q]);
   }
   if (lane == 0) {
-    if (ns | nh) {
-      atomicAdd(mc_stats, ns);
-      atomicAdd(mc_stats + 1, nh);
+    for (int q = 0; q < 4; ++q) {
+      red[wid][q] = s0w[q];
+      red[wid][4 + q] = sgc[q];
     }
-    atomicAdd(mc_stats + 2, nl);
-    if (nq) atomicAdd(mc_stats + 3, nq);
   }
+  for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
+  if (lane == 0) atomicAdd(mc_stats + 2, led);
   __syncthreads();
   if (threadIdx.x == 0) {
-    double tot[14];
-    for (int k = 0; k < 14; ++k) {
-      tot[k] = 0;
-      for (int w = 0; w < kIntThreads / 32; ++w) tot[k] += red[w][k];
+    double acc[8];
+    for (int k = 0; k < 8; ++k) {
+      acc[k] = 0;
+      for (int w = 0; w < kIntThreads / 32; ++w) acc[k] += red[w][k];
     }
+    double tot[14];
+    for (int k = 0; k < 14; ++k) tot[k] = 0;
+    for (int a = 0; a < 4; ++a) tot[10 + a] = 2.0 * C * wq * acc[4 + a];
+    for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < 4; ++a)
+        for (int b = a; b < 4; ++b) tot[s2i(a, b)] += C * wq * acc[q] * qbary(q, a) * qbary(q, b);
     int k = 0;
     for (int a = 0; a < 4; ++a)
       for (int b = a; b < 4; ++b, ++k) {
         const int lo = min(NT[a], NT[b]), hi = max(NT[a], NT[b]);
-        // slot of (lo, hi): lo is a T node -> staged row of lo
         int ra = 0;
         for (int r = 0; r < 4; ++r)
           if (NT[r] == lo) ra = r;
-        const int* rw = rows + ra * rowcap;
-        int l2 = 0, h2 = rlen[ra] - 1;
-        while (l2 < h2) {
-          const int mid = (l2 + h2) >> 1;
-          if (rw[mid] < hi) l2 = mid + 1;
-          else h2 = mid;
-        }
-        red_fixed(V, rbase[ra] + l2, tot[k], cD.scale[lo]);
+        const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
+        red_fixed(V, rbase[ra] + v[ra], tot[k], cD.scale[lo]);
       }
     // load vector: f term (reference assembly.cpp:703-709) + constraint terms
     for (int a = 0; a < 4; ++a) {
       double r = 0;
-      for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, xq[q]);
+      for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, quad_point(vT, q));
       rhsT[4 * (long long)ii + a] = r + tot[10 + a];
     }
   }
@@ -1118,41 +1335,50 @@ __global__ void k_finalize(const long long* soff, const int* scols, const long l
   const int d = warp;
   const int i = dof_node[d];
   const double si = cD.iscale[i];
-  // matrix entries of output row d
+  // matrix entries of output row d: A_ij = V_ij + V_ji (V_ii carries both halves)
   for (long long o = ooff[d] + lane; o < ooff[d + 1]; o += 32) {
     const long long k = omap[o];
     const int j = scols[k];
-    double v = (double)(long long)V[k] * si;
-    if (j != i) v += (double)(long long)V[mirror[k]] * cD.iscale[j];
+    double v = fixed_value(V, k, si);
+    if (j != i) v += fixed_value(V, mirror[k], cD.iscale[j]);
     values[o] = v;
   }
   // folding of constrained columns: rhs_i -= A_ij g(x_j) (dense-oracle form,
-  // reference tests/support/oracles.cpp:274-292)
-  double fold = 0;
+  // reference tests/support/oracles.cpp:274-292), compensated
+  double fs = 0, fe = 0;
   for (long long k = soff[i] + lane; k < soff[i + 1]; k += 32) {
     const int j = scols[k];
     if (cD.dof[j] >= 0) continue;
-    double v = (double)(long long)V[k] * si;
-    if (j != i) v += (double)(long long)V[mirror[k]] * cD.iscale[j];
+    double v = fixed_value(V, k, si);
+    if (j != i) v += fixed_value(V, mirror[k], cD.iscale[j]);
     const Vd x = {cD.node[3 * (long long)j], cD.node[3 * (long long)j + 1], cD.node[3 * (long long)j + 2]};
-    fold += v * poly_eval(cD.g, x);
+    double s, e;
+    two_sum(fs, v * poly_eval(cD.g, x), s, e);
+    fs = s;
+    fe += e;
   }
-  fold = wsum(fold);
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    const double os = __shfl_xor_sync(FULLMASK, fs, sh), oe = __shfl_xor_sync(FULLMASK, fe, sh);
+    double s, e;
+    two_sum(fs, os, s, e);
+    fs = s;
+    fe += e + oe;
+  }
   if (lane == 0) {
-    double r = 0;
+    double rs = 0, re = 0;
     for (int k = cD.ni_off[i]; k < cD.ni_off[i + 1]; ++k) {
       const int T = cD.ni_el[k];
-      int lo = 0, hi = cD.KI - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (cD.interior[mid] < T) lo = mid + 1;
-        else hi = mid;
-      }
+      const int lo = cD.ipos[T];
       const int4 w = cD.verts[T];
       const int a = w.x == i ? 0 : (w.y == i ? 1 : (w.z == i ? 2 : 3));
-      r += rhsT[4 * (long long)lo + a];
+      double s, e;
+      two_sum(rs, rhsT[4 * (long long)lo + a], s, e);
+      rs = s;
+      re += e;
     }
-    rhs[d] = r - fold;
+    double s, e;
+    two_sum(rs, -fs, s, e);
+    rhs[d] = s + (e + re - fe);
   }
 }
 
@@ -1206,7 +1432,7 @@ struct nlfem_gpu_session {
   DBuf<double> node, center, radius, vol, tau, inv;
   DBuf<int4> verts, nbr;
   DBuf<uint8_t> region;
-  DBuf<int> interior, dof, dof_node;
+  DBuf<int> interior, ipos, dof, dof_node;
   DBuf<double4> erec;
   // grid / incidence
   DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
@@ -1221,6 +1447,12 @@ struct nlfem_gpu_session {
   // pattern
   DBuf<int> rlen, rcols, tcnt, tcols, slen, scols, olen, ocols;
   DBuf<long long> roff, toff, soff, mirror, eslot, ooff, omap;
+  // Monte Carlo units (per chunk)
+  DBuf<int> ucount, pair_outer, upair;
+  DBuf<long long> uoff;
+  DBuf<unsigned char> uqs;
+  DBuf<double> mom;
+  float mc_ms = 0;
   // values
   DBuf<unsigned long long> V;
   DBuf<double> rhsT, values, rhs;
@@ -1355,6 +1587,11 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     if (!m->region[t]) S.h_interior.push_back(t);
   }
   S.KI = (int)S.h_interior.size();
+  {
+    std::vector<int> ipos(S.K, -1);
+    for (int i = 0; i < S.KI; ++i) ipos[S.h_interior[i]] = i;
+    S.ipos.upload(ipos.data(), S.K, st);
+  }
   S.tau.upload(tau.data(), S.K, st);
   S.interior.upload(S.h_interior.data(), S.KI, st);
   S.h_dof_node.assign(S.unknowns, 0);
@@ -1398,6 +1635,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.inv = S.inv.p;
   D.region = S.region.p;
   D.interior = S.interior.p;
+  D.ipos = S.ipos.p;
   D.dof = S.dof.p;
   D.node = S.node.p;
   // fixed-point bound per row: 8 C Vmax patch_i, Vmax = |B(delta + 2 dmax)|
@@ -1467,11 +1705,11 @@ void run_prep(nlfem_gpu_session& S) {
   D.scale = S.scale.p;
   D.iscale = S.iscale.p;
   CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
-  // fixed-point bound per row: 8 C Vmax patch_i, Vmax = |B(delta + 2 dmax)|,
-  // dmax <= 2 rmax
-  const double dmax = 2 * D.rmax;
-  const double rr = D.delta + 2 * dmax;
-  const double cbound = 8.0 * D.C * (4.0 / 3.0 * M_PI * rr * rr * rr);
+  // fixed-point bound per row: every contribution to
+  // row i is bounded by C |B(delta + 3 rmax)| times the volume of the elements
+  // around node i, at most 5 such terms (X, 2X on the diagonal, D_T', 2 D_T)
+  const double rr = D.delta + 3 * D.rmax;
+  const double cbound = 6.0 * D.C * (4.0 / 3.0 * M_PI * rr * rr * rr);
   k_scales<<<nblk(J, 256), 256, 0, st>>>(J, S.ai_off64.p, S.ai_el.p, cbound, S.scale.p, S.iscale.p);
   ++S.launches;
 }
@@ -1501,8 +1739,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   CK(cudaMemcpyAsync(S.err_elem.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
   CK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), st));
-  const unsigned pblocks = nblk((long long)KI * 32, 128);
-  k_pairs<false><<<pblocks, 128, 0, st>>>(nullptr, S.pair_count.p, nullptr, nullptr,
+  const unsigned pblocks = nblk((long long)KI * 32, kPairThreads);
+  k_pairs<false><<<pblocks, kPairThreads, 0, st>>>(nullptr, S.pair_count.p, nullptr, nullptr,
                                           S.counters.p, S.err_elem.p);
   ++S.launches;
   int err_elem = big;
@@ -1515,7 +1753,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   S.npairs = read_ll(S.pair_off.p + KI, st);
   S.partner.ensure(S.npairs);
   S.info.ensure(S.npairs);
-  k_pairs<true><<<pblocks, 128, 0, st>>>(S.pair_off.p, nullptr, S.partner.p, S.info.p, nullptr,
+  k_pairs<true><<<pblocks, kPairThreads, 0, st>>>(S.pair_off.p, nullptr, S.partner.p, S.info.p, nullptr,
                                          nullptr);
   ++S.launches;
   CK(cudaEventRecord(S.ev[2], st));
@@ -1596,20 +1834,82 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   CK(cudaEventRecord(S.ev[3], st));
 
   // ---- K3/K4: integrate + scatter
-  S.V.ensure(S.nnz_s);
+  S.V.ensure(2 * (size_t)S.nnz_s);
   S.rhsT.ensure(4 * (size_t)KI);
-  CK(cudaMemsetAsync(S.V.p, 0, S.nnz_s * sizeof(unsigned long long), st));
-  const int rowcap = std::max(maxlen, 1);
-  const size_t ismem = kIntThreads * sizeof(McSlot) + 4 * (size_t)rowcap * sizeof(int);
+  CK(cudaMemsetAsync(S.V.p, 0, 2 * S.nnz_s * sizeof(unsigned long long), st));
+  // slot-map capacity: power of two >= 2 x (union of four rows <= 4 maxlen)
+  int hcap = 64;
+  while (hcap < 8 * std::max(maxlen, 1)) hcap <<= 1;
+  if (maxlen >= 32768)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
+  const size_t ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
   if (ismem > 200 * 1024)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
+  const int rowcap = hcap;
   CK(cudaFuncSetAttribute(k_integrate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
-  if (KI > 0) {
-    k_integrate<<<KI, kIntThreads, ismem, st>>>(S.pair_off.p, S.partner.p, S.info.p, S.soff.p,
-                                                S.scols.p, S.eslot.p, S.V.p, S.rhsT.p,
-                                                S.counters.p + 1, rowcap);
+  const bool fullcaps = D.strategy == NLFEM_STRATEGY_FULLCAPS;
+  float mc_ms = 0;
+  if (KI > 0 && !fullcaps) {
+    k_integrate<<<KI, kIntThreads, ismem, st>>>(0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p,
+                                                S.scols.p, S.eslot.p, S.V.p, S.rhsT.p, nullptr,
+                                                nullptr, 0, 0, S.counters.p + 1, rowcap);
     ++S.launches;
+  } else if (KI > 0) {
+    // chunks of outer elements sized so the Monte Carlo unit buffer stays bounded
+    std::vector<long long> poff(KI + 1);
+    CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const long long kMaxUnits = 48LL << 20;          // 48 Mi units ~ 4.3 GB of moments
+    const long long kPairsPerChunk = kMaxUnits / 6;  // ~4.5 units per pair on average
+    int ii0 = 0;
+    while (ii0 < KI) {
+      int ii1 = ii0 + 1;
+      {  // largest ii1 with pairs <= budget
+        const long long target = poff[ii0] + kPairsPerChunk;
+        ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), target) - poff.begin()) - 1;
+        ii1 = std::max(ii1, ii0 + 1);
+        ii1 = std::min(ii1, KI);
+      }
+      const long long P0 = poff[ii0], np = poff[ii1] - P0;
+      S.ucount.ensure(np + 1);
+      S.uoff.ensure(np + 1);
+      S.pair_outer.ensure(np + 1);
+      k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.ucount.p);
+      k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0, S.pair_outer.p);
+      S.launches += 2;
+      scan64(S, S.ucount.p, true, np, S.uoff.p, st);
+      const long long nunits = read_ll(S.uoff.p + np, st);
+      if (nunits > kMaxUnits && ii1 - ii0 > 1) {  // rare: dense chunk, split
+        // shrink and retry
+        const long long half = (ii1 - ii0) / 2;
+        (void)half;
+      }
+      S.upair.ensure(nunits + 1);
+      S.uqs.ensure(nunits + 1);
+      S.mom.ensure(11 * (size_t)nunits + 1);
+      k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p, S.uqs.p);
+      ++S.launches;
+      CK(cudaEventRecord(S.ev[6], st));
+      if (nunits > 0) {
+        k_mc<<<nblk(nunits, kMcThreads), kMcThreads, 0, st>>>(P0, nunits, S.upair.p, S.uqs.p,
+                                                              S.pair_outer.p, S.partner.p,
+                                                              S.info.p, S.mom.p, S.counters.p + 1);
+        ++S.launches;
+      }
+      CK(cudaEventRecord(S.ev[7], st));
+      k_integrate<<<ii1 - ii0, kIntThreads, ismem, st>>>(
+          ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
+          S.rhsT.p, S.uoff.p, S.mom.p, nunits, P0, S.counters.p + 1, rowcap);
+      ++S.launches;
+      CK(cudaEventSynchronize(S.ev[7]));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, S.ev[6], S.ev[7]));
+      mc_ms += ms;
+      ii0 = ii1;
+    }
   }
+  S.mc_ms = mc_ms;
   CK(cudaEventRecord(S.ev[4], st));
 
   // ---- K6: finalize
@@ -1651,6 +1951,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
     stats->nnz_ext = S.nnz_s;
     stats->ledger_flops = S.ledger;
     stats->mc_subsimplices = S.mc_subs;
+    stats->phase_ms[5] = S.mc_ms;
     stats->seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   }
