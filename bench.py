@@ -50,6 +50,9 @@ CONFIGS = {
     "C3n": dict(res=48, delta=3 / 48, strategy="nocaps", mc=1, jitter=7),
     "C3f": dict(res=48, delta=3 / 48, strategy="fullcaps", mc=128, jitter=7),
     "C4": dict(res=96, delta=3 / 96, strategy="fullcaps", mc=128, jitter=None),
+    # smaller same-delta/h variants for profiling
+    "P3n": dict(res=24, delta=3 / 24, strategy="nocaps", mc=1, jitter=7),
+    "P3f": dict(res=24, delta=3 / 24, strategy="fullcaps", mc=128, jitter=7),
 }
 def describe(name, cfg):
     d = dict(cfg)
@@ -297,7 +300,7 @@ def main():
                    "l2": "flushed between steps (256 MiB write; inputs smaller than L2)",
                    "parallelism": f"replicas x{world}"},
         "fp64_gflops_ledger": st.ledger_flops / (t_total / args.steps * 1e-3) / 1e9,
-        "phase_ms": [round(x, 3) for x in st.phase_ms[:5]],
+        "phase_ms": [round(x, 3) for x in st.phase_ms[:6]],
         "roofline": {"kernel": "k_integrate", "bound": "fp64", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": "nlfem_gpu_fp64_peak() DFMA microbenchmark, this run (burst)",

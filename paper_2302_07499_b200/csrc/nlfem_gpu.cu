@@ -342,17 +342,40 @@ __device__ __noinline__ bool facet_too_close(const Vd* v, int4 nb, Vd xq) {
 __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, const Vd v[4],
                                                   double diam, double vol, double tau) {
   const double delta = cD.delta;
-  const double gap = vdist(cen, xq);
-  if (gap >= rad + delta) return kNone;
-  if (cD.strategy == NLFEM_STRATEGY_BARYCENTER) return gap < delta ? kWhole : kNone;
-  if (gap + rad < cD.inside_cut) return kWhole;
+  // The reference compares gap = sqrt(|c - x_q|^2) against thresholds.  A
+  // squared comparison with a 1e-12 relative margin decides the same way
+  // whenever it is conclusive (sqrt and the square are correctly rounded);
+  // otherwise fall through to the reference's exact expression.
+  const double g2 = vnorm2(vsub(cen, xq));
+  const double t1 = rad + delta;
+  if (g2 >= t1 * t1 * (1.0 + 1e-12)) return kNone;
+  double gap = -1.0;  // computed lazily
+  if (!(g2 < t1 * t1 * (1.0 - 1e-12))) {
+    gap = sqrt(g2);
+    if (gap >= rad + delta) return kNone;
+  }
+  if (cD.strategy == NLFEM_STRATEGY_BARYCENTER) {
+    if (g2 < delta * delta * (1.0 - 1e-12)) return kWhole;
+    if (g2 >= delta * delta * (1.0 + 1e-12)) return kNone;
+    if (gap < 0) gap = sqrt(g2);
+    return gap < delta ? kWhole : kNone;
+  }
+  // fast inside cut: gap + rad < inside_cut
+  const double t2 = cD.inside_cut - rad;
+  if (t2 > 0) {
+    if (g2 < t2 * t2 * (1.0 - 1e-12)) return kWhole;
+    if (!(g2 >= t2 * t2 * (1.0 + 1e-12))) {
+      if (gap < 0) gap = sqrt(g2);
+      if (gap + rad < cD.inside_cut) return kWhole;
+    }
+  }
   const int mask = inside_mask(v, xq, delta);
   if (mask == 15) return kWhole;
   if (mask == 0) {
     if (cD.strategy != NLFEM_STRATEGY_FULLCAPS) return kNone;
     // the barycenter lies in T': gap < delta (with margin) certifies that the
     // computed distance_point_simplex is < delta; otherwise evaluate it
-    if (gap < delta * (1.0 - 1e-12)) return kOutCap;
+    if (g2 < delta * delta * (1.0 - 1e-11)) return kOutCap;
     return dist_point_tet(xq, v) < delta ? kOutCap : kNone;
   }
   if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
@@ -723,8 +746,6 @@ __global__ void k_outpat(const long long* soff, const int* scols, int* olen,
 // ---------------------------------------------------------------------------
 // K3/K4: integration + scatter
 
-constexpr int kIntThreads = 128;
-
 // Two-word fixed point: v*scale = hi + lo * 2^-40 with hi = rint(v*scale)
 // (exact: scale is a power of two) and lo = rint((v*scale - hi) * 2^40), so an
 // accumulated entry carries ~101 bits and equals the exact sum of the FP64
@@ -774,18 +795,87 @@ __device__ __forceinline__ int pair_units(unsigned code) {
   return n;
 }
 
-__global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < np) ucount[i] = pair_units(info[p0 + i]);
+// Warp-aggregated reservation in one of two lists: every lane asks for n
+// slots in list `kind` (0/1); one atomic per warp and list.  Whole warps must
+// call it (inactive lanes pass n = 0).
+__device__ __forceinline__ int reserve2(int* counters, int kind, int n) {
+  const int lane = threadIdx.x & 31;
+  int a = kind ? 0 : n, b = kind ? n : 0;
+  int ia = a, ib = b;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int ta = __shfl_up_sync(FULLMASK, ia, off), tb = __shfl_up_sync(FULLMASK, ib, off);
+    if (lane >= off) {
+      ia += ta;
+      ib += tb;
+    }
+  }
+  int base_a = 0, base_b = 0;
+  if (lane == 31) {
+    if (ia) base_a = atomicAdd(counters, ia);
+    if (ib) base_b = atomicAdd(counters + 1, ib);
+  }
+  base_a = __shfl_sync(FULLMASK, base_a, 31);
+  base_b = __shfl_sync(FULLMASK, base_b, 31);
+  return kind ? base_b + ib - b : base_a + ia - a;
 }
 
-// unit descriptors: pair index (chunk-relative) and (q | sub << 2)
-__global__ void k_units_fill(long long p0, long long np, const unsigned* info,
-                             const long long* uoff, int* upair, unsigned char* uqs) {
+__global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount,
+                              int* gcount, int mc_units) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= np) return;
   const unsigned code = info[p0 + i];
-  long long u = uoff[i];
+  ucount[i] = mc_units ? pair_units(code) : 0;
+  int g = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) g += ((code >> (5 * q)) & kStraddle) != 0;
+  gcount[i] = g;
+}
+
+// Gauss units: one per straddling (T, q, T') item; same list split by parent kind
+__global__ void k_gunits_fill(long long p0, long long np, const unsigned* info,
+                              const long long* goff, int* gpair, unsigned char* gq,
+                              const int* partner, int* list_int, int* list_con, int* nlist) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = i < np;
+  long long u = act ? goff[i] : 0;
+  const int nu = act ? (int)(goff[i + 1] - u) : 0;
+  const bool cons = act && nu > 0 && cD.region[partner[p0 + i]] != 0;
+  const int base = reserve2(nlist, cons ? 1 : 0, nu);
+  if (!act || nu == 0) return;
+  const unsigned code = info[p0 + i];
+  int* lst = cons ? list_con : list_int;
+  int k = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if ((code >> (5 * q)) & kStraddle) {
+      gpair[u] = (int)i;
+      gq[u] = (unsigned char)q;
+      lst[base + k] = (int)u;
+      ++u;
+      ++k;
+    }
+}
+
+// unit descriptors: pair index (chunk-relative) and (q | sub << 2); unit ids
+// are also listed per parent kind (interior / constraint) so each Monte Carlo
+// launch runs one code path (list order is irrelevant: every unit writes only
+// its own slot)
+__global__ void k_units_fill(long long p0, long long np, const unsigned* info,
+                             const long long* uoff, int* upair, unsigned char* uqs,
+                             const int* partner, int* list_int, int* list_con, int* nlist) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = i < np;
+  long long u = act ? uoff[i] : 0;
+  const int nu = act ? (int)(uoff[i + 1] - u) : 0;
+  const bool cons = act && nu > 0 && cD.region[partner[p0 + i]] != 0;
+  const int base = reserve2(nlist, cons ? 1 : 0, nu);
+  if (!act) return;
+  const unsigned code = info[p0 + i];
+  {
+    int* lst = cons ? list_con : list_int;
+    for (int k = 0; k < nu; ++k) lst[base + k] = (int)(u + k);
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
@@ -880,15 +970,18 @@ struct PickPiece {  // selects the want-th kept piece
 // for constraint parents, SoA [11][nunits].
 constexpr int kMcThreads = 128;
 
+template <bool CONS>
 __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nunits,
-                                                   const int* upair, const unsigned char* uqs,
-                                                   const int* pair_outer, const int* partner,
-                                                   const unsigned* info, double* mom,
-                                                   unsigned long long* mc_stats) {
-  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  double S0 = 0, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
+                                                      const int* list, int nlist,
+                                                      const int* upair, const unsigned char* uqs,
+                                                      const int* pair_outer, const int* partner,
+                                                      const unsigned* info, double* mom,
+                                                      unsigned long long* mc_stats) {
+  const int li = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long draws = 0, hits = 0, led = 0;
-  if (u < nunits) {
+  if (li < nlist) {
+    const long long u = list[li];
+    double S0 = 0, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
     const int pi = upair[u];
     const int q = uqs[u] & 3, sub = uqs[u] >> 2;
     const long long p = p0 + pi;
@@ -925,8 +1018,8 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
       if (sub == 0) led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
     }
     if (pk.found) {
-      const bool cons = cD.region[Tp] != 0;
-      const double w = pk.vol / cD.mc;
+      const int M = cD.mc;
+      const double w = pk.vol / M;
       nlfem_mc_frame fr;
       {
         const double a0[3] = {pk.a.x, pk.a.y, pk.a.z}, a1[3] = {pk.b.x, pk.b.y, pk.b.z},
@@ -934,12 +1027,6 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
                      x[3] = {xq.x, xq.y, xq.z};
         nlfem_mc_make_frame(a0, a1, a2, a3, x, &fr);
       }
-      const double c0x = xq.x - vP[0].x, c0y = xq.y - vP[0].y, c0z = xq.z - vP[0].z;
-      const int nb = (cD.mc + 3) >> 2;
-      unsigned nh = 0;
-      double n1x = 0, n1y = 0, n1z = 0, n2[6] = {0, 0, 0, 0, 0, 0}, ng = 0;
-      const uint32_t k0 = (uint32_t)(cD.seed & 0xffffffffu), k1 = (uint32_t)(cD.seed >> 32);
-      const uint32_t c2 = (uint32_t)q | ((uint32_t)sub << 2);
       nlfem_mc_frame fs = fr;  // frame pre-scaled by 2^-32 (exact)
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -948,32 +1035,31 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
         fs.e2[a] = fr.e2[a] * 0x1p-32;
       }
       const double dd = cD.dd;
-      // branch-free accumulation of one sample (interior: Cartesian moments
-      // about v0(T'); constraint: g at the hit)
+      const uint32_t k0 = (uint32_t)(cD.seed & 0xffffffffu), k1 = (uint32_t)(cD.seed >> 32);
+      const uint32_t c2 = (uint32_t)q | ((uint32_t)sub << 2);
+      unsigned nh = 0;
+      // interior: sums of r and r r^T over hits, r = y - x_q; constraint: sum g(y)
+      double t1x = 0, t1y = 0, t1z = 0, t2[6] = {0, 0, 0, 0, 0, 0}, ng = 0;
       auto sample = [&](uint32_t a, uint32_t b, uint32_t cc, bool valid) {
         double rx, ry, rz;
         const bool hit = mc_point_fast(a, b, cc, fs, dd, rx, ry, rz) && valid;
         nh += hit;
-        if (cons) {
+        if (CONS) {
           if (hit) ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
         } else {
-          const double h = hit ? 1.0 : 0.0;
-          rx += c0x;
-          ry += c0y;
-          rz += c0z;
-          const double hx = h * rx, hy = h * ry, hz = h * rz;
-          n1x += hx;
-          n1y += hy;
-          n1z += hz;
-          n2[0] = fma(hx, rx, n2[0]);
-          n2[1] = fma(hx, ry, n2[1]);
-          n2[2] = fma(hx, rz, n2[2]);
-          n2[3] = fma(hy, ry, n2[3]);
-          n2[4] = fma(hy, rz, n2[4]);
-          n2[5] = fma(hz, rz, n2[5]);
+          const double hx = hit ? rx : 0.0, hy = hit ? ry : 0.0, hz = hit ? rz : 0.0;
+          t1x += hx;
+          t1y += hy;
+          t1z += hz;
+          t2[0] = fma(hx, rx, t2[0]);
+          t2[1] = fma(hx, ry, t2[1]);
+          t2[2] = fma(hx, rz, t2[2]);
+          t2[3] = fma(hy, ry, t2[3]);
+          t2[4] = fma(hy, rz, t2[4]);
+          t2[5] = fma(hz, rz, t2[5]);
         }
       };
-      const int full = cD.mc >> 2;  // complete blocks of four samples
+      const int nb = (M + 3) >> 2, full = M >> 2;
 #pragma unroll 1
       for (int j = 0; j < nb; ++j) {
         // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
@@ -981,20 +1067,30 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
         philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, k0, k1, A, B, Cw);
         const bool tail = j >= full;
         sample(A[0], A[1], A[2], true);
-        sample(A[3], B[0], B[1], !tail || 4 * j + 1 < cD.mc);
-        sample(B[2], B[3], Cw[0], !tail || 4 * j + 2 < cD.mc);
-        sample(Cw[1], Cw[2], Cw[3], !tail || 4 * j + 3 < cD.mc);
+        sample(A[3], B[0], B[1], !tail || 4 * j + 1 < M);
+        sample(B[2], B[3], Cw[0], !tail || 4 * j + 2 < M);
+        sample(Cw[1], Cw[2], Cw[3], !tail || 4 * j + 3 < M);
       }
       S0 = w * nh;
-      m1x = w * n1x;
-      m1y = w * n1y;
-      m1z = w * n1z;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) m2[k] = w * n2[k];
-      sg = w * ng;
-      draws = (unsigned long long)cD.mc;
+      if (CONS) {
+        sg = w * ng;
+      } else {
+        // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
+        const double c0x = xq.x - vP[0].x, c0y = xq.y - vP[0].y, c0z = xq.z - vP[0].z;
+        const double n = (double)nh;
+        m1x = w * (t1x + n * c0x);
+        m1y = w * (t1y + n * c0y);
+        m1z = w * (t1z + n * c0z);
+        m2[0] = w * (t2[0] + 2.0 * c0x * t1x + n * c0x * c0x);
+        m2[1] = w * (t2[1] + c0x * t1y + c0y * t1x + n * c0x * c0y);
+        m2[2] = w * (t2[2] + c0x * t1z + c0z * t1x + n * c0x * c0z);
+        m2[3] = w * (t2[3] + 2.0 * c0y * t1y + n * c0y * c0y);
+        m2[4] = w * (t2[4] + c0y * t1z + c0z * t1y + n * c0y * c0z);
+        m2[5] = w * (t2[5] + 2.0 * c0z * t1z + n * c0z * c0z);
+      }
+      draws = (unsigned long long)M;
       hits = nh;
-      led += 25ull + 35ull * (unsigned long long)cD.mc + (cons ? 12ull : 62ull) * nh;
+      led += 25ull + 35ull * (unsigned long long)M + (CONS ? 12ull : 62ull) * nh;
     }
     mom[u] = S0;
     mom[nunits + u] = m1x;
@@ -1017,13 +1113,90 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
   }
 }
 
-// ElementTable::bary (reference ball_approx.cpp:100-115)
-__device__ __forceinline__ void bary(const double inv[9], Vd v0, Vd p, double l[4]) {
-  const Vd d = vsub(p, v0);
-  l[1] = inv[0] * d.x + inv[1] * d.y + inv[2] * d.z;
-  l[2] = inv[3] * d.x + inv[4] * d.y + inv[5] * d.z;
-  l[3] = inv[6] * d.x + inv[7] * d.y + inv[8] * d.z;
-  l[0] = 1.0 - l[1] - l[2] - l[3];
+
+// Gauss rule on the inner sub-simplices of one straddling item (reference
+// AsmSink::sub + accumulate_point, assembly.cpp:332-381): thread per item.
+// Output SoA [15][n]: S0, S1[4], S2[10] (upper triangle) for interior parents;
+// S0, Sg for constraint parents (slots 0, 1).
+constexpr int kGaussThreads = 128;
+
+template <bool CONS>
+__global__ void __launch_bounds__(kGaussThreads, 4) k_gauss(long long p0, long long n,
+                                                            const int* list, int nlist,
+                                                            const int* gpair,
+                                                            const unsigned char* gq,
+                                                            const int* pair_outer,
+                                                            const int* partner,
+                                                            const unsigned* info, double* gmom,
+                                                            unsigned long long* stats) {
+  const int li = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long led = 0;
+  if (li < nlist) {
+    const long long u = list[li];
+    const int pi = gpair[u], q = gq[u];
+    const long long p = p0 + pi;
+    const int T = cD.interior[pair_outer[pi]];
+    const int Tp = partner[p];
+    const int mask = (int)((info[p] >> (5 * q)) & 15);
+    Vd vT[4], vP[4];
+    load_verts(T, vT);
+    load_verts(Tp, vP);
+    const Vd xq = quad_point(vT, q);
+    double inv[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) inv[k] = cD.inv[9 * (long long)Tp + k];
+    const Straddle st = inner_straddle(vP, mask, xq, cD.delta);
+    const double tau = cD.tau[Tp];
+    double S0 = 0, Sg = 0, S1[4] = {0, 0, 0, 0}, S2[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int kept = 0;
+#pragma unroll 1
+    for (int k = 0; k < st.n; ++k) {
+      Vd pa, pb, pc, pd;
+      straddle_piece(st, k, pa, pb, pc, pd);
+      const double vol = tet_volume(pa, pb, pc, pd);
+      if (!(vol > tau)) continue;
+      ++kept;
+      const Vd pv[4] = {pa, pb, pc, pd};
+      const double w = vol * 0.25;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const Vd y = quad_point(pv, g);
+        S0 += w;
+        if (CONS) {
+          Sg = fma(w, poly_eval(cD.g, y), Sg);
+        } else {
+          // ElementTable::bary (ball_approx.cpp:100-115), then the moment sums
+          const Vd d = vsub(y, vP[0]);
+          double l[4];
+          l[1] = inv[0] * d.x + inv[1] * d.y + inv[2] * d.z;
+          l[2] = inv[3] * d.x + inv[4] * d.y + inv[5] * d.z;
+          l[3] = inv[6] * d.x + inv[7] * d.y + inv[8] * d.z;
+          l[0] = 1.0 - l[1] - l[2] - l[3];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double wb = w * l[i];
+            S1[i] += wb;
+#pragma unroll
+            for (int j = i; j < 4; ++j) S2[s2i(i, j)] = fma(wb, l[j], S2[s2i(i, j)]);
+          }
+        }
+      }
+    }
+    const int m = __popc(mask);
+    led = 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
+          (unsigned long long)kept * (CONS ? 160 : 360);
+    gmom[u] = S0;
+    if (CONS) {
+      gmom[n + u] = Sg;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gmom[(1 + i) * n + u] = S1[i];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) gmom[(5 + k) * n + u] = S2[k];
+    }
+  }
+  for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
+  if ((threadIdx.x & 31) == 0 && led) atomicAdd(stats + 2, led);
 }
 
 // shared-memory map: node id -> slots of (N_a, node) in the four staged rows
@@ -1038,22 +1211,38 @@ struct SlotMap {
   }
 };
 
-// Combine: CTA per outer element T, thread per element pair.  Closed-form
-// whole elements and Gauss sub-simplices are integrated here; Monte Carlo
-// units come from k_mc.  The per-pair 4x4 blocks are scattered as two-word
-// fixed point into the node pattern.
-__global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
+// Combine: CTA per outer element T, thread per element pair.  Whole elements
+// are closed form here; straddle items (Gauss units) and caps (Monte Carlo
+// units) come precomputed.  The T x T' block of every pair is pre-reduced in
+// shared memory (exact two-word fixed point, integer atomics) over the CTA
+// and flushed once per outer element; the T' x T' block goes straight to the
+// node pattern.
+constexpr int kIntThreads = 256;
+
+__device__ __forceinline__ void smem_fixed(unsigned long long* acc, int slot, double v,
+                                           double scale) {
+  const double x = v * scale;
+  const long long hi = __double2ll_rn(x);
+  const long long lo = __double2ll_rn((x - (double)hi) * 0x1p40);
+  if (hi != 0) atomicAdd(acc + 2 * slot, (unsigned long long)hi);
+  if (lo != 0) atomicAdd(acc + 2 * slot + 1, (unsigned long long)lo);
+}
+
+__global__ void __launch_bounds__(kIntThreads, 2) k_integrate(
     int ii0, const long long* pair_off, const int* partner, const unsigned* info,
     const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
-    double* rhsT, const long long* uoff, const double* mom, long long nunits, long long pbase,
-    unsigned long long* mc_stats, int hcap) {
-  extern __shared__ int smi[];
+    double* rhsT, const long long* uoff, const double* mom, long long nunits,
+    const long long* goff, const double* gmom, long long ngunits, long long pbase,
+    unsigned long long* stats, int hcap, int rowcap) {
+  extern __shared__ unsigned long long sml[];
+  unsigned long long* xacc = sml;  // [4][rowcap][2]
   SlotMap mp;
-  mp.key = smi;
-  mp.val = reinterpret_cast<short4*>(smi + hcap);
+  mp.key = reinterpret_cast<int*>(sml + 8 * (size_t)rowcap);
+  mp.val = reinterpret_cast<short4*>(mp.key + hcap);
   mp.mask = hcap - 1;
   __shared__ long long rbase[4];
-  __shared__ double red[kIntThreads / 32][14];
+  __shared__ int rlen[4];
+  __shared__ double red[kIntThreads / 32][8];
 
   const int ii = ii0 + blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1061,12 +1250,16 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
   const int4 wT = cD.verts[T];
   const int NT[4] = {wT.x, wT.y, wT.z, wT.w};
 
-  // build the slot map from the four T-node rows of the node pattern
+  // slot map of the four T-node rows; zero the row accumulators
   for (int h = threadIdx.x; h < hcap; h += blockDim.x) {
     mp.key[h] = -1;
     mp.val[h] = make_short4(-1, -1, -1, -1);
   }
-  if (threadIdx.x < 4) rbase[threadIdx.x] = soff[NT[threadIdx.x]];
+  for (int k = threadIdx.x; k < 8 * rowcap; k += blockDim.x) xacc[k] = 0;
+  if (threadIdx.x < 4) {
+    rbase[threadIdx.x] = soff[NT[threadIdx.x]];
+    rlen[threadIdx.x] = (int)(soff[NT[threadIdx.x] + 1] - soff[NT[threadIdx.x]]);
+  }
   __syncthreads();
   for (int a = 0; a < 4; ++a) {
     const long long r0 = soff[NT[a]], r1 = soff[NT[a] + 1];
@@ -1078,8 +1271,7 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
         if (prev == -1 || prev == col) break;
         h = (h + 1) & mp.mask;
       }
-      short* v = reinterpret_cast<short*>(mp.val + h);
-      v[a] = (short)(k - r0);
+      reinterpret_cast<short*>(mp.val + h)[a] = (short)(k - r0);
     }
   }
   __syncthreads();
@@ -1088,16 +1280,15 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
   load_verts(T, vT);
   const double wq = 0.25 * cD.vol[T];  // rule.w[k] * vol (reference assembly.cpp:702)
   const double C = cD.C;
+  const double sc[4] = {cD.scale[NT[0]], cD.scale[NT[1]], cD.scale[NT[2]], cD.scale[NT[3]]};
   // per outer element: sum over pairs of S0_q (constraint parents weigh 2,
-  // reference assembly.cpp:419) and of sum_q c_{q,a} Sg_q; D_T and the rhs
-  // follow from them
+  // reference assembly.cpp:419) and of sum_q c_{q,a} Sg_q
   double s0w[4] = {0, 0, 0, 0}, sgc[4] = {0, 0, 0, 0};
   unsigned long long led = 0;
 
   const long long p0 = pair_off[ii], p1 = pair_off[ii + 1];
   for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    // per pair: X[a][b] = sum_q c_{q,a} S1_q[b] (T x T' block before -C w),
-    // S2 = sum_q S2_q (T' x T' block before C w)
+    // per pair: X[a][b] = sum_q c_{q,a} S1_q[b], S2 = sum_q S2_q
     double X[4][4], S2[10];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -1109,23 +1300,23 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
     const int Tp = partner[p];
     const unsigned code = info[p];
     const bool constr = cD.region[Tp] != 0;
-    Vd vP[4];
-    load_verts(Tp, vP);
     const double volP = cD.vol[Tp];
     const double* invP = cD.inv + 9 * (long long)Tp;
     long long u = (mom != nullptr) ? uoff[p - pbase] : 0;
+    long long gu = (gmom != nullptr) ? goff[p - pbase] : 0;
 
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
       const unsigned c = (code >> (5 * q)) & 31;
       if (c == 0) continue;
-      // moments of this (T, q, T') item: S0, S1 (interior) or Sg (constraint)
       double S0 = 0, S1[4] = {0, 0, 0, 0}, Sg = 0;
       if (c == kWhole) {
         led += constr ? 133 : 39;
         S0 = volP;
         if (constr) {
           // constraint parent: measure and g average (reference assembly.cpp:350-359)
+          Vd vP[4];
+          load_verts(Tp, vP);
 #pragma unroll 1
           for (int k = 0; k < 4; ++k) Sg += volP * 0.25 * poly_eval(cD.g, quad_point(vP, k));
         } else {
@@ -1139,47 +1330,16 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
           }
         }
       } else if (c & kStraddle) {
-        // Gauss rule on the inner sub-simplices (reference AsmSink::sub +
-        // accumulate_point, assembly.cpp:332-381)
-        const Vd xq = quad_point(vT, q);
-        const Straddle st = inner_straddle(vP, (int)(c & 15), xq, cD.delta);
-        const double tau = cD.tau[Tp];
-        int kept = 0;
-#pragma unroll 1
-        for (int k = 0; k < st.n; ++k) {
-          Vd pa, pb, pc, pd;
-          straddle_piece(st, k, pa, pb, pc, pd);
-          const double vol = tet_volume(pa, pb, pc, pd);
-          if (!(vol > tau)) continue;
-          ++kept;
-          const Vd pv[4] = {pa, pb, pc, pd};
-          const double w = vol * 0.25;
-#pragma unroll 1
-          for (int g = 0; g < 4; ++g) {
-            const Vd y = quad_point(pv, g);
-            S0 += w;
-            if (constr) {
-              Sg += w * poly_eval(cD.g, y);
-            } else {
-              double l[4];
-              const Vd d = vsub(y, vP[0]);
-              l[1] = invP[0] * d.x + invP[1] * d.y + invP[2] * d.z;
-              l[2] = invP[3] * d.x + invP[4] * d.y + invP[5] * d.z;
-              l[3] = invP[6] * d.x + invP[7] * d.y + invP[8] * d.z;
-              l[0] = 1.0 - l[1] - l[2] - l[3];
+        S0 = gmom[gu];
+        if (constr) {
+          Sg = gmom[ngunits + gu];
+        } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const double wb = w * l[i];
-                S1[i] += wb;
+          for (int i = 0; i < 4; ++i) S1[i] = gmom[(1 + i) * ngunits + gu];
 #pragma unroll
-                for (int j = i; j < 4; ++j) S2[s2i(i, j)] += wb * l[j];
-              }
-            }
-          }
+          for (int k = 0; k < 10; ++k) S2[k] += gmom[(5 + k) * ngunits + gu];
         }
-        const int m = __popc(c & 15);
-        led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
-               (unsigned long long)kept * (constr ? 160 : 360);
+        ++gu;
       }
       // Monte Carlo units of this item, in sub-simplex order
       if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
@@ -1245,16 +1405,15 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
         for (int a = 0; a < 4; ++a) {
           const double ca = qbary(q, a);
 #pragma unroll
-          for (int b = 0; b < 4; ++b) X[a][b] += ca * S1[b];
+          for (int b = 0; b < 4; ++b) X[a][b] = fma(ca, S1[b], X[a][b]);
         }
       }
     }
 
-    // ---- element-pair blocks -> fixed point scatter
     if (!constr) {
       const int4 wP = cD.verts[Tp];
       const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
-      // T x T' cross block: -C w X[a][b] at (N_a, M_b)
+      // T x T' cross block -C w X[a][b] at (N_a, M_b): shared-memory rows
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const short4 sl = mp.val[mp.probe(NP[b])];
@@ -1262,10 +1421,10 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const double x = -C * wq * X[a][b];
-          red_fixed(V, rbase[a] + sla[a], NT[a] == NP[b] ? 2.0 * x : x, cD.scale[NT[a]]);
+          smem_fixed(xacc, a * rowcap + sla[a], NT[a] == NP[b] ? 2.0 * x : x, sc[a]);
         }
       }
-      // T' x T' block: C w sum_q S2_q at (M_b, M_c), row min(M_b, M_c)
+      // T' x T' block C w sum_q S2_q at (M_b, M_c), row min(M_b, M_c)
       const long long* es = eslot + 10 * (long long)interior_pos(Tp);
 #pragma unroll
       for (int b = 0; b < 4; ++b)
@@ -1289,7 +1448,7 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
     }
   }
   for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
-  if (lane == 0) atomicAdd(mc_stats + 2, led);
+  if (lane == 0 && led) atomicAdd(stats + 2, led);
   __syncthreads();
   if (threadIdx.x == 0) {
     double acc[8];
@@ -1311,7 +1470,7 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
         for (int r = 0; r < 4; ++r)
           if (NT[r] == lo) ra = r;
         const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
-        red_fixed(V, rbase[ra] + v[ra], tot[k], cD.scale[lo]);
+        smem_fixed(xacc, ra * rowcap + v[ra], tot[k], sc[ra]);
       }
     // load vector: f term (reference assembly.cpp:703-709) + constraint terms
     for (int a = 0; a < 4; ++a) {
@@ -1320,6 +1479,14 @@ __global__ void __launch_bounds__(kIntThreads, 3) k_integrate(
       rhsT[4 * (long long)ii + a] = r + tot[10 + a];
     }
   }
+  __syncthreads();
+  // flush the four pre-reduced rows (exact integer sums) to the node pattern
+  for (int a = 0; a < 4; ++a)
+    for (int k = threadIdx.x; k < rlen[a]; k += blockDim.x) {
+      const unsigned long long hi = xacc[2 * (a * rowcap + k)], lo = xacc[2 * (a * rowcap + k) + 1];
+      if (hi) atomicAdd(V + 2 * (rbase[a] + k), hi);
+      if (lo) atomicAdd(V + 2 * (rbase[a] + k) + 1, lo);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1448,7 +1615,10 @@ struct nlfem_gpu_session {
   DBuf<int> rlen, rcols, tcnt, tcols, slen, scols, olen, ocols;
   DBuf<long long> roff, toff, soff, mirror, eslot, ooff, omap;
   // Monte Carlo units (per chunk)
-  DBuf<int> ucount, pair_outer, upair;
+  DBuf<int> ucount, gcount, pair_outer, upair, ulist, nlist, gpair, glist;
+  DBuf<long long> goff;
+  DBuf<unsigned char> gq;
+  DBuf<double> gmom;
   DBuf<long long> uoff;
   DBuf<unsigned char> uqs;
   DBuf<double> mom;
@@ -1466,34 +1636,42 @@ struct nlfem_gpu_session {
 
 namespace {
 
+// exclusive scan of n counts into out[0..n], out[n] = total; the block sums
+// of every recursion level live in persistent session scratch (no allocation)
+void scan64_level(nlfem_gpu_session& S, const void* in, bool in_is_int, long long n,
+                  long long* out, cudaStream_t st, size_t scratch_off) {
+  const long long nb = (n + kScanBlock - 1) / kScanBlock;
+  if (n <= 0) {
+    CK(cudaMemsetAsync(out, 0, sizeof(long long), st));
+    return;
+  }
+  long long* sums = S.scan_tmp.p + scratch_off;
+  long long* sums_scan = sums + nb + 1;
+  if (in_is_int)
+    k_scan_block<int><<<(unsigned)nb, kScanBlock, 0, st>>>((const int*)in, out, sums, n);
+  else
+    k_scan_block<long long><<<(unsigned)nb, kScanBlock, 0, st>>>((const long long*)in, out, sums, n);
+  ++S.launches;
+  if (nb > 1) {
+    scan64_level(S, sums, false, nb, sums_scan, st, scratch_off + 2 * (size_t)(nb + 1));
+    k_scan_add<<<(unsigned)nb, kScanBlock, 0, st>>>(out, sums_scan, n);
+    ++S.launches;
+    CK(cudaMemcpyAsync(out + n, sums_scan + nb, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+  } else {
+    CK(cudaMemcpyAsync(out + n, sums, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+  }
+}
+
 void scan64(nlfem_gpu_session& S, const void* in, bool in_is_int, long long n, long long* out,
             cudaStream_t st) {
-  // exclusive scan of n counts into out[0..n], out[n] = total
-  const long long nb = (n + kScanBlock - 1) / kScanBlock;
-  std::vector<long long> dummy;
-  DBuf<long long> sums, sums_scan;
-  sums.ensure(nb + 1);
-  sums_scan.ensure(nb + 1);
-  if (n > 0) {
-    if (in_is_int)
-      k_scan_block<int><<<(unsigned)nb, kScanBlock, 0, st>>>((const int*)in, out, sums.p, n);
-    else
-      k_scan_block<long long><<<(unsigned)nb, kScanBlock, 0, st>>>((const long long*)in, out,
-                                                                    sums.p, n);
-    ++S.launches;
-    if (nb > 1) {
-      scan64(S, sums.p, false, nb, sums_scan.p, st);
-      k_scan_add<<<(unsigned)nb, kScanBlock, 0, st>>>(out, sums_scan.p, n);
-      ++S.launches;
-      // total = scanned[nb-1] + sums[nb-1] -> already in sums_scan[nb]
-      CK(cudaMemcpyAsync(out + n, sums_scan.p + nb, sizeof(long long), cudaMemcpyDeviceToDevice, st));
-    } else {
-      CK(cudaMemcpyAsync(out + n, sums.p, sizeof(long long), cudaMemcpyDeviceToDevice, st));
-    }
-  } else {
-    CK(cudaMemsetAsync(out, 0, sizeof(long long), st));
+  size_t need = 0;
+  for (long long m = n; m > 1; m = (m + kScanBlock - 1) / kScanBlock)
+    need += 2 * (size_t)((m + kScanBlock - 1) / kScanBlock + 1);
+  if (S.scan_tmp.n < need + 16) {
+    CK(cudaStreamSynchronize(st));  // buffer may be in use by queued work
+    S.scan_tmp.ensure(need + 16);
   }
-  CK(cudaStreamSynchronize(st));  // sums buffers are freed on return
+  scan64_level(S, in, in_is_int, n, out, st, 0);
 }
 
 long long read_ll(const long long* d, cudaStream_t st) {
@@ -1837,75 +2015,110 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   S.V.ensure(2 * (size_t)S.nnz_s);
   S.rhsT.ensure(4 * (size_t)KI);
   CK(cudaMemsetAsync(S.V.p, 0, 2 * S.nnz_s * sizeof(unsigned long long), st));
-  // slot-map capacity: power of two >= 2 x (union of four rows <= 4 maxlen)
+  // slot-map capacity: power of two > union of the four rows (<= 4 maxlen)
   int hcap = 64;
-  while (hcap < 8 * std::max(maxlen, 1)) hcap <<= 1;
+  while (hcap <= 4 * std::max(maxlen, 1)) hcap <<= 1;
   if (maxlen >= 32768)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
-  const size_t ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
-  if (ismem > 200 * 1024)
+  const int rowcap = std::max(maxlen, 1);
+  const size_t ismem = 8 * (size_t)rowcap * sizeof(unsigned long long) +
+                       (size_t)hcap * (sizeof(int) + sizeof(short4));
+  if (ismem > 220 * 1024)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
-  const int rowcap = hcap;
   CK(cudaFuncSetAttribute(k_integrate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
-  const bool fullcaps = D.strategy == NLFEM_STRATEGY_FULLCAPS;
+  const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
+  const bool need_gauss = D.strategy != NLFEM_STRATEGY_BARYCENTER;
   float mc_ms = 0;
-  if (KI > 0 && !fullcaps) {
-    k_integrate<<<KI, kIntThreads, ismem, st>>>(0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p,
-                                                S.scols.p, S.eslot.p, S.V.p, S.rhsT.p, nullptr,
-                                                nullptr, 0, 0, S.counters.p + 1, rowcap);
-    ++S.launches;
-  } else if (KI > 0) {
-    // chunks of outer elements sized so the Monte Carlo unit buffer stays bounded
+  if (KI > 0) {
+    // chunks of outer elements sized so the unit buffers stay bounded
     std::vector<long long> poff(KI + 1);
     CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const long long kMaxUnits = 48LL << 20;          // 48 Mi units ~ 4.3 GB of moments
-    const long long kPairsPerChunk = kMaxUnits / 6;  // ~4.5 units per pair on average
+    const long long kPairsPerChunk = need_gauss ? (8LL << 20) : (1LL << 40);
     int ii0 = 0;
     while (ii0 < KI) {
-      int ii1 = ii0 + 1;
-      {  // largest ii1 with pairs <= budget
-        const long long target = poff[ii0] + kPairsPerChunk;
-        ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), target) - poff.begin()) - 1;
-        ii1 = std::max(ii1, ii0 + 1);
-        ii1 = std::min(ii1, KI);
-      }
+      int ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), poff[ii0] + kPairsPerChunk) -
+                      poff.begin()) - 1;
+      ii1 = std::min(std::max(ii1, ii0 + 1), KI);
       const long long P0 = poff[ii0], np = poff[ii1] - P0;
-      S.ucount.ensure(np + 1);
-      S.uoff.ensure(np + 1);
-      S.pair_outer.ensure(np + 1);
-      k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.ucount.p);
-      k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0, S.pair_outer.p);
-      S.launches += 2;
-      scan64(S, S.ucount.p, true, np, S.uoff.p, st);
-      const long long nunits = read_ll(S.uoff.p + np, st);
-      if (nunits > kMaxUnits && ii1 - ii0 > 1) {  // rare: dense chunk, split
-        // shrink and retry
-        const long long half = (ii1 - ii0) / 2;
-        (void)half;
-      }
-      S.upair.ensure(nunits + 1);
-      S.uqs.ensure(nunits + 1);
-      S.mom.ensure(11 * (size_t)nunits + 1);
-      k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p, S.uqs.p);
-      ++S.launches;
-      CK(cudaEventRecord(S.ev[6], st));
-      if (nunits > 0) {
-        k_mc<<<nblk(nunits, kMcThreads), kMcThreads, 0, st>>>(P0, nunits, S.upair.p, S.uqs.p,
-                                                              S.pair_outer.p, S.partner.p,
-                                                              S.info.p, S.mom.p, S.counters.p + 1);
+      long long nunits = 0, ngunits = 0;
+      if (need_gauss) {
+        S.ucount.ensure(np + 1);
+        S.gcount.ensure(np + 1);
+        S.uoff.ensure(np + 1);
+        S.goff.ensure(np + 1);
+        S.pair_outer.ensure(np + 1);
+        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.ucount.p, S.gcount.p,
+                                                     need_mc ? 1 : 0);
+        k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
+                                                           S.pair_outer.p);
+        S.launches += 2;
+        scan64(S, S.gcount.p, true, np, S.goff.p, st);
+        ngunits = read_ll(S.goff.p + np, st);
+        S.gpair.ensure(ngunits + 1);
+        S.gq.ensure(ngunits + 1);
+        S.gmom.ensure(15 * (size_t)ngunits + 1);
+        S.glist.ensure(2 * (size_t)ngunits + 2);
+        S.nlist.ensure(4);
+        CK(cudaMemsetAsync(S.nlist.p, 0, 4 * sizeof(int), st));
+        k_gunits_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.goff.p, S.gpair.p, S.gq.p,
+                                                     S.partner.p, S.glist.p,
+                                                     S.glist.p + ngunits + 1, S.nlist.p + 2);
         ++S.launches;
+        if (need_mc) {
+          scan64(S, S.ucount.p, true, np, S.uoff.p, st);
+          nunits = read_ll(S.uoff.p + np, st);
+          S.upair.ensure(nunits + 1);
+          S.uqs.ensure(nunits + 1);
+          S.mom.ensure(11 * (size_t)nunits + 1);
+          S.ulist.ensure(2 * (size_t)nunits + 2);
+          k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p,
+                                                      S.uqs.p, S.partner.p, S.ulist.p,
+                                                      S.ulist.p + nunits + 1, S.nlist.p);
+          ++S.launches;
+        }
+        int nl[4] = {0, 0, 0, 0};
+        CK(cudaMemcpyAsync(nl, S.nlist.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaEventRecord(S.ev[6], st));
+        if (nl[2] > 0) {
+          k_gauss<false><<<nblk(nl[2], kGaussThreads), kGaussThreads, 0, st>>>(
+              P0, ngunits, S.glist.p, nl[2], S.gpair.p, S.gq.p, S.pair_outer.p, S.partner.p,
+              S.info.p, S.gmom.p, S.counters.p + 1);
+          ++S.launches;
+        }
+        if (nl[3] > 0) {
+          k_gauss<true><<<nblk(nl[3], kGaussThreads), kGaussThreads, 0, st>>>(
+              P0, ngunits, S.glist.p + ngunits + 1, nl[3], S.gpair.p, S.gq.p, S.pair_outer.p,
+              S.partner.p, S.info.p, S.gmom.p, S.counters.p + 1);
+          ++S.launches;
+        }
+        if (nl[0] > 0) {
+          k_mc<false><<<nblk(nl[0], kMcThreads), kMcThreads, 0, st>>>(
+              P0, nunits, S.ulist.p, nl[0], S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
+              S.info.p, S.mom.p, S.counters.p + 1);
+          ++S.launches;
+        }
+        if (nl[1] > 0) {
+          k_mc<true><<<nblk(nl[1], kMcThreads), kMcThreads, 0, st>>>(
+              P0, nunits, S.ulist.p + nunits + 1, nl[1], S.upair.p, S.uqs.p, S.pair_outer.p,
+              S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
+          ++S.launches;
+        }
+        CK(cudaEventRecord(S.ev[7], st));
       }
-      CK(cudaEventRecord(S.ev[7], st));
       k_integrate<<<ii1 - ii0, kIntThreads, ismem, st>>>(
           ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
-          S.rhsT.p, S.uoff.p, S.mom.p, nunits, P0, S.counters.p + 1, rowcap);
+          S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
+          need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
       ++S.launches;
-      CK(cudaEventSynchronize(S.ev[7]));
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, S.ev[6], S.ev[7]));
-      mc_ms += ms;
+      if (need_gauss) {
+        CK(cudaEventSynchronize(S.ev[7]));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, S.ev[6], S.ev[7]));
+        mc_ms += ms;
+      }
       ii0 = ii1;
     }
   }
