@@ -27,7 +27,7 @@ import time
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnlfem_gpu.so")
+LIB_PATH = os.environ.get("NLFEM_GPU_LIB") or os.path.join(_HERE, "libnlfem_gpu.so")
 
 STRATEGIES = ["inside", "overlap", "barycenter", "nocaps", "approxcaps", "fullcaps"]
 GPU_STRATEGIES = ("barycenter", "nocaps", "fullcaps")

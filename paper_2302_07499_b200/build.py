@@ -45,11 +45,12 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out=None) -> str:
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
         os.path.join(INC, f) for f in os.listdir(INC)] + [__file__]
-    if not force and not _stale(LIB, deps):
-        return LIB
+    lib = out or LIB
+    if not force and not _stale(lib, deps):
+        return lib
     objdir = os.path.join(HERE, "_build")
     os.makedirs(objdir, exist_ok=True)
     logpath = os.path.join(objdir, "build.log")
@@ -57,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(logpath, "w") as log:
         for src in CU_SOURCES:
             obj = os.path.join(objdir, src + ".o")
-            _run([NVCC, *NVCC_FLAGS, "-I", INC, "-I", CSRC, "-c",
+            _run([NVCC, *NVCC_FLAGS, *extra_flags, "-I", INC, "-I", CSRC, "-c",
                   os.path.join(CSRC, src), "-o", obj], log)
             objs.append(obj)
         for src in CPP_SOURCES:
@@ -65,11 +66,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             _run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-I", INC,
                   "-c", os.path.join(CSRC, src), "-o", obj], log)
             objs.append(obj)
-        _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB,
+        _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib,
               *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"], log)
     if verbose:
         sys.stdout.write(open(logpath).read())
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -970,8 +970,47 @@ struct PickPiece {  // selects the want-th kept piece
 // for constraint parents, SoA [11][nunits].
 constexpr int kMcThreads = 128;
 
-template <bool CONS>
-__global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nunits,
+// value, gradient and Hessian at x of a polynomial of total degree <= 2
+// (only such g take the moment path in k_mc<true, true>)
+__device__ __forceinline__ void poly2_taylor(const Poly& P, Vd x, double& g0, double gr[3],
+                                             double H[6]) {
+  g0 = poly_eval(P, x);
+  gr[0] = gr[1] = gr[2] = 0;
+  for (int k = 0; k < 6; ++k) H[k] = 0;
+  const double xv[3] = {x.x, x.y, x.z};
+  for (int t = 0; t < P.n; ++t) {
+    const int e0 = P.e[t][0], e1 = P.e[t][1], e2 = P.e[t][2];
+    const int e[3] = {e0, e1, e2};
+    const double c = P.c[t];
+    // d/dx_a of c x^e: c e_a x^(e - 1_a) (degree <= 2 -> at most one other factor)
+    for (int a = 0; a < 3; ++a) {
+      if (!e[a]) continue;
+      double v = c * e[a];
+      for (int b = 0; b < 3; ++b) {
+        const int eb = e[b] - (b == a);
+        for (int i = 0; i < eb; ++i) v *= xv[b];
+      }
+      gr[a] += v;
+    }
+    // Hessian (constant for degree 2): H_aa = 2c (e_a == 2), H_ab = c (e_a = e_b = 1)
+    if (e0 + e1 + e2 == 2) {
+      int k = 0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = a; b < 3; ++b, ++k)
+          H[k] += (a == b) ? (e[a] == 2 ? 2.0 * c : 0.0) : (e[a] == 1 && e[b] == 1 ? c : 0.0);
+    }
+  }
+}
+
+#ifndef NLFEM_MC_MINBLOCKS
+#define NLFEM_MC_MINBLOCKS 6
+#endif
+// CONS: constraint parent (accumulates sum g(y) instead of basis moments).
+// G2: g has total degree <= 2, so sum_hits g(x_q + r) follows exactly from the
+// hit count, sum r and sum r r^T -- the same branch-free moments as interior
+// parents -- instead of one polynomial evaluation per hit.
+template <bool CONS, bool G2>
+__global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nunits,
                                                       const int* list, int nlist,
                                                       const int* upair, const unsigned char* uqs,
                                                       const int* pair_outer, const int* partner,
@@ -1044,10 +1083,15 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
         double rx, ry, rz;
         const bool hit = mc_point_fast(a, b, cc, fs, dd, rx, ry, rz) && valid;
         nh += hit;
-        if (CONS) {
+        if (CONS && !G2) {
           if (hit) ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
         } else {
+#ifdef NLFEM_MC_DMUL
+          const double h = hit ? 1.0 : 0.0;
+          const double hx = h * rx, hy = h * ry, hz = h * rz;
+#else
           const double hx = hit ? rx : 0.0, hy = hit ? ry : 0.0, hz = hit ? rz : 0.0;
+#endif
           t1x += hx;
           t1y += hy;
           t1z += hz;
@@ -1072,7 +1116,15 @@ __global__ void __launch_bounds__(kMcThreads, 4) k_mc(long long p0, long long nu
         sample(Cw[1], Cw[2], Cw[3], !tail || 4 * j + 3 < M);
       }
       S0 = w * nh;
-      if (CONS) {
+      if (CONS && G2) {
+        // sum over hits of g(x_q + r) = n g + grad g . sum r + 1/2 sum H_ab r_a r_b
+        double g0, gr[3], H[6];
+        poly2_taylor(cD.g, xq, g0, gr, H);
+        const double n = (double)nh;
+        const double quad = 0.5 * (H[0] * t2[0] + H[3] * t2[3] + H[5] * t2[5]) +
+                            H[1] * t2[1] + H[2] * t2[2] + H[4] * t2[4];
+        sg = w * (n * g0 + gr[0] * t1x + gr[1] * t1y + gr[2] * t1z + quad);
+      } else if (CONS) {
         sg = w * ng;
       } else {
         // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
@@ -1623,6 +1675,7 @@ struct nlfem_gpu_session {
   DBuf<unsigned char> uqs;
   DBuf<double> mom;
   float mc_ms = 0;
+  int g_deg = 0;  // total degree of g
   // values
   DBuf<unsigned long long> V;
   DBuf<double> rhsT, values, rhs;
@@ -1792,6 +1845,9 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.dd = k->delta * k->delta;
   poly_to_dev(f, D.f);
   poly_to_dev(g, D.g);
+  S.g_deg = 0;
+  for (int t = 0; t < D.g.n; ++t)
+    S.g_deg = std::max(S.g_deg, D.g.e[t][0] + D.g.e[t][1] + D.g.e[t][2]);
   // uniform grid: cell edge ~ cube root of 6 mean element volumes (one lattice
   // cube holds 6 Kuhn tets), so a cell holds ~6 centers
   const double hg = std::max(std::cbrt(6.0 * volsum / std::max(S.K, 1)), 1e-300);
@@ -2095,15 +2151,20 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
           ++S.launches;
         }
         if (nl[0] > 0) {
-          k_mc<false><<<nblk(nl[0], kMcThreads), kMcThreads, 0, st>>>(
+          k_mc<false, false><<<nblk(nl[0], kMcThreads), kMcThreads, 0, st>>>(
               P0, nunits, S.ulist.p, nl[0], S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
               S.info.p, S.mom.p, S.counters.p + 1);
           ++S.launches;
         }
         if (nl[1] > 0) {
-          k_mc<true><<<nblk(nl[1], kMcThreads), kMcThreads, 0, st>>>(
-              P0, nunits, S.ulist.p + nunits + 1, nl[1], S.upair.p, S.uqs.p, S.pair_outer.p,
-              S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
+          if (S.g_deg <= 2)
+            k_mc<true, true><<<nblk(nl[1], kMcThreads), kMcThreads, 0, st>>>(
+                P0, nunits, S.ulist.p + nunits + 1, nl[1], S.upair.p, S.uqs.p, S.pair_outer.p,
+                S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
+          else
+            k_mc<true, false><<<nblk(nl[1], kMcThreads), kMcThreads, 0, st>>>(
+                P0, nunits, S.ulist.p + nunits + 1, nl[1], S.upair.p, S.uqs.p, S.pair_outer.p,
+                S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
           ++S.launches;
         }
         CK(cudaEventRecord(S.ev[7], st));

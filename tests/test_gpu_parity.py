@@ -202,3 +202,22 @@ def test_jittered_nocaps_against_reference_oracle():
     assert same_pattern(out, o)
     assert row_rel_err(out, o) <= TOL_DET
     assert rhs_rel_err(out, o) <= TOL_DET
+
+
+@pytest.mark.parametrize("gterms", [
+    [[1.0, 2, 0, 0], [0.5, 0, 1, 1], [-0.25, 0, 0, 1], [0.1, 0, 0, 0]],   # degree 2: moment path
+    [[1.0, 2, 1, 0], [1.0, 0, 0, 3], [0.3, 1, 0, 0]],                     # degree 3: per-hit path
+])
+def test_fullcaps_custom_g_against_oracle(gterms):
+    g = load_golden("jit5_d040")
+    t = _table(g)
+    f = np.array([[0.5, 0, 0, 0], [1.0, 0, 0, 1]])
+    gg = np.array(gterms)
+    out, st = P.assemble(t, 0.4, "fullcaps", "mass", U2, seed=SEED, mc_samples=12, f_terms=f,
+                         g_terms=P.normalize_terms(gg))
+    o = port.assemble(t, 0.4, "fullcaps", P.kernel_constant(0.4, "mass"), f,
+                      P.normalize_terms(gg), seed=SEED, mc_samples=12, sampler="P")
+    assert same_pattern(out, o)
+    assert row_rel_err(out, o) <= TOL_MC
+    assert rhs_rel_err(out, o) <= TOL_MC
+    assert (st["mc_samples"], st["mc_hits"]) == (o["mc_samples"], o["mc_hits"])
