@@ -233,6 +233,10 @@ __device__ __forceinline__ double facet_distance(const Vd v[4], int slot, Vd p) 
 struct Straddle {
   Vd A0, A1, A2, B0, B1, B2;
   int n;  // 1 (single tet) or 3 (prism split)
+  // barycentric coordinates of the six points in the parent element:
+  // lambda = (1 - t) e_a + t e_b (vertices: a = b, t = 0; crossings: the edge)
+  int la[6], lb[6];
+  double lt[6];
 };
 
 __device__ __forceinline__ Vd crossing_point(Vd a, Vd b, Vd c, double r) {
@@ -266,47 +270,88 @@ __device__ __forceinline__ void orient_warped(Straddle& s) {
     const Vd u = s.B1;
     s.B1 = s.B2;
     s.B2 = u;
+    int ia = s.la[1], ib = s.lb[1];
+    double it = s.lt[1];
+    s.la[1] = s.la[2]; s.lb[1] = s.lb[2]; s.lt[1] = s.lt[2];
+    s.la[2] = ia; s.lb[2] = ib; s.lt[2] = it;
+    ia = s.la[4]; ib = s.lb[4]; it = s.lt[4];
+    s.la[4] = s.la[5]; s.lb[4] = s.lb[5]; s.lt[4] = s.lt[5];
+    s.la[5] = ia; s.lb[5] = ib; s.lt[5] = it;
   }
 }
 
 // crossing_points (reference geometry.cpp:39-50) in one loop: crossing k is
 // edge (k-th inside slot -> j-th outside slot), k = i_rank * (4 - m) + j
-__device__ __forceinline__ void crossings4(const Vd v[4], int mask, Vd c, double r, Vd& q0,
-                                           Vd& q1, Vd& q2, Vd& q3) {
+struct Crossings {
+  Vd q[4];
+  int a[4], b[4];  // edge (inside slot, outside slot)
+  double t[4];
+};
+
+__device__ __forceinline__ void crossings4(const Vd v[4], int mask, Vd c, double r, Crossings& X) {
   const int m = __popc(mask), mo = 4 - m, n = m * mo;
   const unsigned inm = (unsigned)mask, outm = (unsigned)(~mask & 15);
-  q0 = q1 = q2 = q3 = v[0];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    X.q[k] = v[0];
+    X.a[k] = X.b[k] = 0;
+    X.t[k] = 0;
+  }
 #pragma unroll 1
   for (int k = 0; k < n; ++k) {
     const int ir = k / mo, orr = k - ir * mo;
     const int i = (int)__fns(inm, 0, ir + 1), o = (int)__fns(outm, 0, orr + 1);
-    const Vd p = crossing_point(pick(v, i), pick(v, o), c, r);
-    if (k == 0) q0 = p;
-    if (k == 1) q1 = p;
-    if (k == 2) q2 = p;
-    if (k == 3) q3 = p;
+    const Vd a = pick(v, i), b = pick(v, o);
+    const double t = edge_crossing(a, b, c, r);
+    const Vd p = vadd(a, vscale(t, vsub(b, a)));
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (k == j) {
+        X.q[j] = p;
+        X.a[j] = i;
+        X.b[j] = o;
+        X.t[j] = t;
+      }
   }
+}
+
+__device__ __forceinline__ void set_vertex(Straddle& s, int p, int slot) {
+  s.la[p] = slot;
+  s.lb[p] = slot;
+  s.lt[p] = 0.0;
+}
+__device__ __forceinline__ void set_cross(Straddle& s, int p, const Crossings& X, int k) {
+  s.la[p] = X.a[k];
+  s.lb[p] = X.b[k];
+  s.lt[p] = X.t[k];
 }
 
 __device__ __forceinline__ int nth_slot(int mask, int n) { return (int)__fns((unsigned)mask, 0, n + 1); }
 
 // detail::straddle_inner (reference ball_approx.cpp:195-255)
 __device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c, double r) {
-  Vd q0, q1, q2, q3;
-  crossings4(v, mask, c, r, q0, q1, q2, q3);
+  Crossings X;
+  crossings4(v, mask, c, r, X);
   const int m = __popc(mask);
-  const Vd i0 = pick(v, nth_slot(mask, 0)), i1 = pick(v, nth_slot(mask, m > 1 ? 1 : 0)),
-           i2 = pick(v, nth_slot(mask, m > 2 ? 2 : 0));
+  const int s0 = nth_slot(mask, 0), s1 = nth_slot(mask, m > 1 ? 1 : 0),
+            s2 = nth_slot(mask, m > 2 ? 2 : 0);
+  const Vd i0 = pick(v, s0), i1 = pick(v, s1), i2 = pick(v, s2);
   Straddle s;
   if (m == 1) {  // tet (a, a->o0, a->o1, a->o2)
-    s.A0 = i0; s.A1 = q0; s.A2 = q1; s.B0 = q2; s.B1 = q2; s.B2 = q2;
+    s.A0 = i0; s.A1 = X.q[0]; s.A2 = X.q[1]; s.B0 = X.q[2]; s.B1 = X.q[2]; s.B2 = X.q[2];
+    set_vertex(s, 0, s0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 1);
+    set_cross(s, 3, X, 2); set_cross(s, 4, X, 2); set_cross(s, 5, X, 2);
     s.n = 1;
   } else if (m == 2) {  // warped prism {a, a->o0, a->o1} | {b, b->o0, b->o1}
-    s.A0 = i0; s.A1 = q0; s.A2 = q1; s.B0 = i1; s.B1 = q2; s.B2 = q3;
+    s.A0 = i0; s.A1 = X.q[0]; s.A2 = X.q[1]; s.B0 = i1; s.B1 = X.q[2]; s.B2 = X.q[3];
+    set_vertex(s, 0, s0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 1);
+    set_vertex(s, 3, s1); set_cross(s, 4, X, 2); set_cross(s, 5, X, 3);
     s.n = 3;
     orient_warped(s);
   } else {  // frustum {a, b, d} | {a->o, b->o, d->o}
-    s.A0 = i0; s.A1 = i1; s.A2 = i2; s.B0 = q0; s.B1 = q1; s.B2 = q2;
+    s.A0 = i0; s.A1 = i1; s.A2 = i2; s.B0 = X.q[0]; s.B1 = X.q[1]; s.B2 = X.q[2];
+    set_vertex(s, 0, s0); set_vertex(s, 1, s1); set_vertex(s, 2, s2);
+    set_cross(s, 3, X, 0); set_cross(s, 4, X, 1); set_cross(s, 5, X, 2);
     s.n = 3;
   }
   return s;
@@ -314,21 +359,27 @@ __device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c
 
 // detail::straddle_outer (reference ball_approx.cpp:257-298)
 __device__ __forceinline__ Straddle outer_straddle(const Vd v[4], int mask, Vd c, double r) {
-  Vd q0, q1, q2, q3;
-  crossings4(v, mask, c, r, q0, q1, q2, q3);
+  Crossings X;
+  crossings4(v, mask, c, r, X);
   const int m = __popc(mask), om = ~mask & 15;
-  const Vd o0 = pick(v, nth_slot(om, 0)), o1 = pick(v, nth_slot(om, m < 3 ? 1 : 0)),
-           o2 = pick(v, nth_slot(om, m < 2 ? 2 : 0));
+  const int t0 = nth_slot(om, 0), t1 = nth_slot(om, m < 3 ? 1 : 0), t2 = nth_slot(om, m < 2 ? 2 : 0);
+  const Vd o0 = pick(v, t0), o1 = pick(v, t1), o2 = pick(v, t2);
   Straddle s;
   if (m == 1) {  // frustum {a->o0, a->o1, a->o2} | {o0, o1, o2}
-    s.A0 = q0; s.A1 = q1; s.A2 = q2; s.B0 = o0; s.B1 = o1; s.B2 = o2;
+    s.A0 = X.q[0]; s.A1 = X.q[1]; s.A2 = X.q[2]; s.B0 = o0; s.B1 = o1; s.B2 = o2;
+    set_cross(s, 0, X, 0); set_cross(s, 1, X, 1); set_cross(s, 2, X, 2);
+    set_vertex(s, 3, t0); set_vertex(s, 4, t1); set_vertex(s, 5, t2);
     s.n = 3;
   } else if (m == 2) {  // warped prism {c, a->c, b->c} | {d, a->d, b->d}
-    s.A0 = o0; s.A1 = q0; s.A2 = q2; s.B0 = o1; s.B1 = q1; s.B2 = q3;
+    s.A0 = o0; s.A1 = X.q[0]; s.A2 = X.q[2]; s.B0 = o1; s.B1 = X.q[1]; s.B2 = X.q[3];
+    set_vertex(s, 0, t0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 2);
+    set_vertex(s, 3, t1); set_cross(s, 4, X, 1); set_cross(s, 5, X, 3);
     s.n = 3;
     orient_warped(s);
   } else {  // corner tet (o, a->o, b->o, d->o)
-    s.A0 = o0; s.A1 = q0; s.A2 = q1; s.B0 = q2; s.B1 = q2; s.B2 = q2;
+    s.A0 = o0; s.A1 = X.q[0]; s.A2 = X.q[1]; s.B0 = X.q[2]; s.B1 = X.q[2]; s.B2 = X.q[2];
+    set_vertex(s, 0, t0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 1);
+    set_cross(s, 3, X, 2); set_cross(s, 4, X, 2); set_cross(s, 5, X, 2);
     s.n = 1;
   }
   return s;
@@ -341,6 +392,14 @@ __device__ __forceinline__ void straddle_piece(const Straddle& s, int k, Vd& a, 
   b = k == 0 ? s.A1 : (k == 1 ? s.A2 : s.B0);
   c = k == 0 ? s.A2 : (k == 1 ? s.B0 : s.B1);
   d = k == 0 ? s.B0 : (k == 1 ? s.B1 : s.B2);
+}
+
+// barycentric-label indices (into la/lb/lt) of the four vertices of piece k
+__device__ __forceinline__ void straddle_piece_ids(int k, int& p0, int& p1, int& p2, int& p3) {
+  p0 = k;      // A0 | A1 | A2
+  p1 = k + 1;  // A1 | A2 | B0
+  p2 = k + 2;  // A2 | B0 | B1
+  p3 = k + 3;  // B0 | B1 | B2
 }
 
 // number of Monte Carlo sub-simplices straddle_outer can emit (before the

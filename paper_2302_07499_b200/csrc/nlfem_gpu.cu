@@ -97,6 +97,7 @@ struct Dev {
   const int4* nbr;
   const double* vol;
   const double* tau;
+  const double* diam;
   const double* inv;  // [9K]
   const uint8_t* region;
   const int* interior;  // [KI]
@@ -307,18 +308,26 @@ __device__ __noinline__ bool any_pieces_exact(const Vd* v, int mask, Vd xq, doub
              count_kept(outer_straddle(v, mask, xq, cD.delta), tau) > 0;
 }
 
-__device__ __forceinline__ bool inner_pieces_exist(const Vd v[4], int mask, Vd xq, double diam,
-                                                   double vol, double tau) {
-  const int m = __popc(mask);
-  double dmax = 0;
+// Does a nocaps straddler emit at least one inner sub-simplex (volume > tau)?
+// Certificate: the inner polytope contains a tet of volume >= (depth/diam)^(4-m)
+// vol(T'), depth = delta - |v - x_q| of the deepest inside vertex, and its <= 3
+// kept pieces tile the polytope, so some piece exceeds tau once
+// depth > rho = diam * max((8 tau / vol)^(1/3), 1e-6) (the largest of the m-wise
+// thresholds).  Tested on squared distances with a factor-2 margin; otherwise
+// run the exact decomposition.
+__device__ __forceinline__ bool inner_pieces_exist(const Vd v[4], int mask, Vd xq,
+                                                   const double d2[4], double cert2,
+                                                   double tau) {
+#pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (mask >> i & 1) dmax = fmax(dmax, cD.delta - sqrt(vnorm2(vsub(v[i], xq))));
-  const double s = dmax / diam;
-  double f = s;
-  if (m <= 2) f *= s;
-  if (m == 1) f *= s;
-  if (s > 1e-6 && f * vol > 8.0 * tau) return true;
+    if ((mask >> i & 1) && d2[i] < cert2) return true;
   return inner_pieces_exact(v, mask, xq, tau);
+}
+
+__device__ __forceinline__ double cert_threshold2(double diam, double vol, double tau) {
+  const double rho = diam * fmax(cbrt(8.0 * tau / vol), 1e-6);
+  const double t = cD.delta - 2.0 * rho;
+  return t > 0 ? t * t * (1.0 - 1e-12) : 0.0;
 }
 
 __device__ __forceinline__ bool any_pieces_fullcaps(const Vd v[4], int mask, Vd xq, double vol,
@@ -340,7 +349,7 @@ __device__ __noinline__ bool facet_too_close(const Vd* v, int4 nb, Vd xq) {
 
 // The reference's per-(T,q,T') decision (assembly.cpp:722-759).
 __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, const Vd v[4],
-                                                  double diam, double vol, double tau) {
+                                                  double cert2, double vol, double tau) {
   const double delta = cD.delta;
   // The reference compares gap = sqrt(|c - x_q|^2) against thresholds.  A
   // squared comparison with a 1e-12 relative margin decides the same way
@@ -369,7 +378,18 @@ __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, con
       if (gap + rad < cD.inside_cut) return kWhole;
     }
   }
-  const int mask = inside_mask(v, xq, delta);
+  // classify_simplex flags (reference geometry.cpp:8-24), keeping |v - x_q|^2
+  double d2[4];
+  int mask = 0;
+  {
+    const double r_in = delta - 1e-10 * delta;
+    const double r2 = r_in * r_in;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      d2[i] = vnorm2(vsub(v[i], xq));
+      if (d2[i] < r2) mask |= 1 << i;
+    }
+  }
   if (mask == 15) return kWhole;
   if (mask == 0) {
     if (cD.strategy != NLFEM_STRATEGY_FULLCAPS) return kNone;
@@ -379,7 +399,7 @@ __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, con
     return dist_point_tet(xq, v) < delta ? kOutCap : kNone;
   }
   if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
-    return inner_pieces_exist(v, mask, xq, diam, vol, tau) ? (kStraddle | mask) : kNone;
+    return inner_pieces_exist(v, mask, xq, d2, cert2, tau) ? (kStraddle | mask) : kNone;
   return any_pieces_fullcaps(v, mask, xq, vol, tau) ? (kStraddle | mask) : kNone;
 }
 
@@ -399,57 +419,94 @@ __device__ __forceinline__ void outer_setup(int T, OuterT& o) {
   o.R = cD.delta + spread;
 }
 
-constexpr int kPairThreads = 128;
-constexpr int kCandBuf = 256;
+constexpr int kPairThreads = 128;       // 4 warps = 4 consecutive outer elements
+constexpr int kPairWarps = kPairThreads / 32;
+constexpr int kCandChunk = 128;         // candidates staged in shared memory at a time
 
-// Warp per outer element T.  Phase 1 streams the grid rows around T and keeps
-// the candidates whose bounding sphere can reach B(delta) of some quadrature
-// point (a conservative superset of the reference's BFS superset,
-// assembly.cpp:569-613) in shared memory; phase 2 classifies them with one
-// lane per (candidate, quadrature point) -- the reference's exact per-(T,q,T')
-// predicates -- and ORs the four 5-bit codes of a candidate.  Pair order is the
-// candidate order, identical in the count and the fill pass.
+struct CandStage {
+  double4 rec[kCandChunk][4];  // erec of the candidate (center+radius, vertices)
+  double vol[kCandChunk], tau[kCandChunk], cert2[kCandChunk];
+  int id[kCandChunk];
+  unsigned char pass[kCandChunk];  // bit w: passes warp w's superset screen
+  short mine[kPairWarps][kCandChunk];  // per warp: indices of its candidates
+};
+
+// CTA per 4 consecutive outer elements T (one per warp).  The CTA streams the
+// grid rows of the union of their reach boxes once; a candidate T' survives if
+// its bounding sphere can reach B(delta) of some quadrature point of one of the
+// four T (a conservative superset of the reference's BFS superset,
+// assembly.cpp:569-613); survivors are staged in shared memory.  Each warp then
+// classifies its own survivors with one lane per (candidate, quadrature point)
+// -- the reference's exact per-(T,q,T') predicates -- and ORs the four 5-bit
+// codes.  Pair order is the stream order, identical in the count and fill pass.
 template <bool FILL>
-__global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair_off, int* pair_count,
-                                                        int* partner, unsigned* info,
+__global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair_off,
+                                                        int* pair_count, int* partner,
+                                                        unsigned* info,
                                                         unsigned long long* item_count,
                                                         int* err_elem) {
-  __shared__ int cand[kPairThreads / 32][kCandBuf];
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ CandStage sg;
+  __shared__ int nst, xb[6];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  if (warp >= cD.KI) return;
-  int* cb = cand[wl];
+  const int warp = blockIdx.x * kPairWarps + wl;  // outer element index
+  const bool active = warp < cD.KI;
   OuterT o;
-  outer_setup(cD.interior[warp], o);
+  if (active) outer_setup(cD.interior[warp], o);
+  else o.R = -1;
   const double reach = o.R + cD.rmax;
-  const int x0 = cell_of(o.c.x - reach, cD.gox, cD.ginv, cD.gx);
-  const int x1 = cell_of(o.c.x + reach, cD.gox, cD.ginv, cD.gx);
-  const int y0 = cell_of(o.c.y - reach, cD.goy, cD.ginv, cD.gy);
-  const int y1 = cell_of(o.c.y + reach, cD.goy, cD.ginv, cD.gy);
-  const int z0 = cell_of(o.c.z - reach, cD.goz, cD.ginv, cD.gz);
-  const int z1 = cell_of(o.c.z + reach, cD.goz, cD.ginv, cD.gz);
-  const long long out = FILL ? pair_off[warp] : 0;
-  int cnt = 0, ncand = 0;
+  // union of the reach boxes (cell indices)
+  if (threadIdx.x == 0) {
+    xb[0] = xb[2] = xb[4] = 1 << 30;
+    xb[1] = xb[3] = xb[5] = -1;
+  }
+  __syncthreads();
+  if (active && lane == 0) {
+    atomicMin(xb + 0, cell_of(o.c.x - reach, cD.gox, cD.ginv, cD.gx));
+    atomicMax(xb + 1, cell_of(o.c.x + reach, cD.gox, cD.ginv, cD.gx));
+    atomicMin(xb + 2, cell_of(o.c.y - reach, cD.goy, cD.ginv, cD.gy));
+    atomicMax(xb + 3, cell_of(o.c.y + reach, cD.goy, cD.ginv, cD.gy));
+    atomicMin(xb + 4, cell_of(o.c.z - reach, cD.goz, cD.ginv, cD.gz));
+    atomicMax(xb + 5, cell_of(o.c.z + reach, cD.goz, cD.ginv, cD.gz));
+  }
+  __syncthreads();
+  const int x0 = xb[0], x1 = xb[1], y0 = xb[2], y1 = xb[3], z0 = xb[4], z1 = xb[5];
+  // the four outer centers and radii for the union screen (broadcast via smem)
+  __shared__ double oc[kPairWarps][4];
+  if (lane == 0) {
+    oc[wl][0] = o.c.x;
+    oc[wl][1] = o.c.y;
+    oc[wl][2] = o.c.z;
+    oc[wl][3] = active ? o.R : -1.0;
+  }
+  __syncthreads();
+  const long long out = (FILL && active) ? pair_off[warp] : 0;
+  int cnt = 0;
   unsigned items = 0;
-  const double reach2 = reach * reach * (1.0 + 1e-9);
 
-  auto flush = [&]() {
+  // classify the staged chunk for this warp's T
+  auto classify_chunk = [&]() {
+    // indices of staged candidates that pass this warp's screen
+    int nm = 0;
+    for (int base = 0; base < nst; base += 32) {
+      const int k = base + lane;
+      const bool mine = k < nst && ((sg.pass[k] >> wl) & 1);
+      const unsigned bal = __ballot_sync(FULLMASK, mine);
+      if (mine) sg.mine[wl][nm + __popc(bal & ((1u << lane) - 1))] = (short)k;
+      nm += __popc(bal);
+    }
     __syncwarp();
-    for (int base = 0; base < ncand; base += 8) {
+    for (int base = 0; base < nm; base += 8) {
       const int t = base + (lane >> 2), q = lane & 3;
       unsigned code = 0;
       int Tp = -1;
-      if (t < ncand) {
-        Tp = cb[t];
-        Vd cp, v[4];
-        double rad;
-        load_elem(Tp, cp, rad, v);
-        double dia = 0;  // ElementTable::diam (ball_approx.cpp:61-67)
-        for (int i = 0; i < 4; ++i)
-          for (int j = i + 1; j < 4; ++j) dia = fmax(dia, vnorm2(vsub(v[i], v[j])));
-        dia = sqrt(dia);
+      if (t < nm) {
+        const int k = sg.mine[wl][t];
+        Tp = sg.id[k];
+        const double4 a = sg.rec[k][0], b = sg.rec[k][1], e = sg.rec[k][2], d = sg.rec[k][3];
+        const Vd cp = {a.x, a.y, a.z};
+        const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
         const Vd xq = quad_point(o.v, q);
-        code = classify_item(xq, cp, rad, v, dia, cD.vol[Tp], cD.tau[Tp]) << (5 * q);
+        code = classify_item(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]) << (5 * q);
         if (!FILL) {
           items += code != 0;
           const int4 nb = cD.nbr[Tp];
@@ -468,40 +525,79 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
       }
       cnt += __popc(bal);
     }
-    __syncwarp();
-    ncand = 0;
   };
 
+  if (threadIdx.x == 0) nst = 0;
+  __syncthreads();
   for (int z = z0; z <= z1; ++z) {
-    const double zl = cD.goz + z * cD.hg, zh = zl + cD.hg;
-    const double dz = o.c.z < zl ? zl - o.c.z : (o.c.z > zh ? o.c.z - zh : 0.0);
     for (int y = y0; y <= y1; ++y) {
-      const double yl = cD.goy + y * cD.hg, yh = yl + cD.hg;
-      const double dy = o.c.y < yl ? yl - o.c.y : (o.c.y > yh ? o.c.y - yh : 0.0);
-      if (dy * dy + dz * dz > reach2) continue;  // row of cells beyond reach
       const int row = (z * cD.gy + y) * cD.gx;
       const int e0 = cD.cell_start[row + x0], e1 = cD.cell_start[row + x1 + 1];
-      for (int base = e0; base < e1; base += 32) {
-        const int e = base + lane;
-        bool pass = false;
+      for (int base = e0; base < e1; base += kPairThreads) {
+        const int e = base + threadIdx.x;
+        unsigned pm = 0;
         int Tp = -1;
+        double4 a;
         if (e < e1) {
           Tp = cD.cell_elems[e];
-          const double4 a = cD.erec[4 * Tp];
-          const double thr = a.w + o.R;
-          pass = vnorm2(vsub({a.x, a.y, a.z}, o.c)) < thr * thr * (1.0 + 1e-10);
+          a = cD.erec[4 * Tp];
+#pragma unroll
+          for (int w = 0; w < kPairWarps; ++w) {
+            const double thr = a.w + oc[w][3];
+            const double dx = a.x - oc[w][0], dy = a.y - oc[w][1], dz = a.z - oc[w][2];
+            if (oc[w][3] >= 0 && dx * dx + dy * dy + dz * dz < thr * thr * (1.0 + 1e-10))
+              pm |= 1u << w;
+          }
         }
-        const unsigned bal = __ballot_sync(FULLMASK, pass);
-        if (pass) cb[ncand + __popc(bal & ((1u << lane) - 1))] = Tp;
-        ncand += __popc(bal);
-        if (ncand > kCandBuf - 32) flush();
+        // stage survivors (block-wide compaction)
+        const unsigned bal = __ballot_sync(FULLMASK, pm != 0);
+        __shared__ int wcount[kPairWarps], wbase[kPairWarps];
+        if (lane == 0) wcount[wl] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int acc = nst;
+          for (int w = 0; w < kPairWarps; ++w) {
+            wbase[w] = acc;
+            acc += wcount[w];
+          }
+        }
+        __syncthreads();
+        const int tot = wbase[kPairWarps - 1] + wcount[kPairWarps - 1];
+        if (tot > kCandChunk) {
+          // chunk full: classify what is staged, then restart the stage
+          classify_chunk();
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int w = 0; w < kPairWarps; ++w) {
+              wbase[w] = acc;
+              acc += wcount[w];
+            }
+          }
+          __syncthreads();
+        }
+        if (pm) {
+          const int k = wbase[wl] + __popc(bal & ((1u << lane) - 1));
+          sg.id[k] = Tp;
+          sg.rec[k][0] = a;
+          sg.rec[k][1] = cD.erec[4 * Tp + 1];
+          sg.rec[k][2] = cD.erec[4 * Tp + 2];
+          sg.rec[k][3] = cD.erec[4 * Tp + 3];
+          sg.vol[k] = cD.vol[Tp];
+          sg.tau[k] = cD.tau[Tp];
+          sg.cert2[k] = cert_threshold2(cD.diam[Tp], sg.vol[k], sg.tau[k]);
+          sg.pass[k] = (unsigned char)pm;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) nst = wbase[kPairWarps - 1] + wcount[kPairWarps - 1];
+        __syncthreads();
       }
     }
   }
-  flush();
+  classify_chunk();
   if (!FILL) {
     for (int sh = 16; sh > 0; sh >>= 1) items += __shfl_xor_sync(FULLMASK, items, sh);
-    if (lane == 0) {
+    if (active && lane == 0) {
       pair_count[warp] = cnt;
       atomicAdd(item_count, (unsigned long long)items);
     }
@@ -1194,42 +1290,52 @@ __global__ void __launch_bounds__(kGaussThreads, 4) k_gauss(long long p0, long l
     load_verts(T, vT);
     load_verts(Tp, vP);
     const Vd xq = quad_point(vT, q);
-    double inv[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) inv[k] = cD.inv[9 * (long long)Tp + k];
     const Straddle st = inner_straddle(vP, mask, xq, cD.delta);
     const double tau = cD.tau[Tp];
     double S0 = 0, Sg = 0, S1[4] = {0, 0, 0, 0}, S2[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     int kept = 0;
-#pragma unroll 1
-    for (int k = 0; k < st.n; ++k) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k >= st.n) break;
       Vd pa, pb, pc, pd;
       straddle_piece(st, k, pa, pb, pc, pd);
       const double vol = tet_volume(pa, pb, pc, pd);
-      if (!(vol > tau)) continue;
+      if (!(vol > tau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
       ++kept;
-      const Vd pv[4] = {pa, pb, pc, pd};
-      const double w = vol * 0.25;
+      S0 += vol;
+      if (CONS) {
+        // degree-2 Gauss points with g (reference AsmSink::sub, assembly.cpp:372-381)
+        const Vd pv[4] = {pa, pb, pc, pd};
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const Vd y = quad_point(pv, g);
-        S0 += w;
-        if (CONS) {
-          Sg = fma(w, poly_eval(cD.g, y), Sg);
-        } else {
-          // ElementTable::bary (ball_approx.cpp:100-115), then the moment sums
-          const Vd d = vsub(y, vP[0]);
-          double l[4];
-          l[1] = inv[0] * d.x + inv[1] * d.y + inv[2] * d.z;
-          l[2] = inv[3] * d.x + inv[4] * d.y + inv[5] * d.z;
-          l[3] = inv[6] * d.x + inv[7] * d.y + inv[8] * d.z;
-          l[0] = 1.0 - l[1] - l[2] - l[3];
+        for (int g = 0; g < 4; ++g) Sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), Sg);
+      } else {
+        // The reference integrates lambda and lambda lambda^T with the degree-2
+        // rule, which is exact for them; the same values follow in closed form
+        // from the barycentric coordinates L_j of the piece's vertices in T'
+        // (parent vertex e_a; crossing at t on edge a->b: (1-t) e_a + t e_b):
+        //   int lambda = vol/4 sum_j L_j,
+        //   int lambda lambda^T = vol/20 (sum_j L_j L_j^T + (sum_j L_j)(sum_j L_j)^T).
+        double L[4][4], sl[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int a = st.la[k + j], b = st.lb[k + j];
+          const double t = st.lt[k + j];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const double wb = w * l[i];
-            S1[i] += wb;
+            L[j][i] = (i == a ? 1.0 - t : 0.0) + (i == b ? t : 0.0);
+            sl[i] += L[j][i];
+          }
+        }
+        const double v4 = vol * 0.25, v20 = vol / 20.0;
 #pragma unroll
-            for (int j = i; j < 4; ++j) S2[s2i(i, j)] = fma(wb, l[j], S2[s2i(i, j)]);
+        for (int i = 0; i < 4; ++i) {
+          S1[i] = fma(v4, sl[i], S1[i]);
+#pragma unroll
+          for (int jj = i; jj < 4; ++jj) {
+            double mm = sl[i] * sl[jj];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mm = fma(L[j][i], L[j][jj], mm);
+            S2[s2i(i, jj)] = fma(v20, mm, S2[s2i(i, jj)]);
           }
         }
       }
@@ -1269,7 +1375,13 @@ struct SlotMap {
 // shared memory (exact two-word fixed point, integer atomics) over the CTA
 // and flushed once per outer element; the T' x T' block goes straight to the
 // node pattern.
-constexpr int kIntThreads = 256;
+#ifndef NLFEM_INT_THREADS
+#define NLFEM_INT_THREADS 256
+#endif
+#ifndef NLFEM_INT_MINBLOCKS
+#define NLFEM_INT_MINBLOCKS 2
+#endif
+constexpr int kIntThreads = NLFEM_INT_THREADS;
 
 __device__ __forceinline__ void smem_fixed(unsigned long long* acc, int slot, double v,
                                            double scale) {
@@ -1280,7 +1392,7 @@ __device__ __forceinline__ void smem_fixed(unsigned long long* acc, int slot, do
   if (lo != 0) atomicAdd(acc + 2 * slot + 1, (unsigned long long)lo);
 }
 
-__global__ void __launch_bounds__(kIntThreads, 2) k_integrate(
+__global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
     int ii0, const long long* pair_off, const int* partner, const unsigned* info,
     const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
     double* rhsT, const long long* uoff, const double* mom, long long nunits,
@@ -1648,7 +1760,7 @@ struct nlfem_gpu_session {
   int K = 0, J = 0, KI = 0, unknowns = 0;
   std::vector<int> h_interior, h_dof_node;
   // mesh buffers
-  DBuf<double> node, center, radius, vol, tau, inv;
+  DBuf<double> node, center, radius, vol, tau, inv, diam;
   DBuf<int4> verts, nbr;
   DBuf<uint8_t> region;
   DBuf<int> interior, ipos, dof, dof_node;
@@ -1795,6 +1907,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   S.center.upload(m->center, 3 * (size_t)S.K, st);
   S.radius.upload(m->radius, S.K, st);
   S.vol.upload(m->volume, S.K, st);
+  S.diam.upload(m->diam, S.K, st);
   S.inv.upload(m->inv_edges, 9 * (size_t)S.K, st);
   S.verts.upload(reinterpret_cast<const int4*>(m->verts), S.K, st);
   S.nbr.upload(reinterpret_cast<const int4*>(m->neighbor), S.K, st);
@@ -1866,6 +1979,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.nbr = S.nbr.p;
   D.vol = S.vol.p;
   D.tau = S.tau.p;
+  D.diam = S.diam.p;
   D.inv = S.inv.p;
   D.region = S.region.p;
   D.interior = S.interior.p;
@@ -1973,7 +2087,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   CK(cudaMemcpyAsync(S.err_elem.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
   CK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), st));
-  const unsigned pblocks = nblk((long long)KI * 32, kPairThreads);
+  const unsigned pblocks = nblk((long long)KI, kPairWarps);
   k_pairs<false><<<pblocks, kPairThreads, 0, st>>>(nullptr, S.pair_count.p, nullptr, nullptr,
                                           S.counters.p, S.err_elem.p);
   ++S.launches;
@@ -2110,18 +2224,20 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
         k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
                                                            S.pair_outer.p);
         S.launches += 2;
-        scan64(S, S.gcount.p, true, np, S.goff.p, st);
-        ngunits = read_ll(S.goff.p + np, st);
-        S.gpair.ensure(ngunits + 1);
-        S.gq.ensure(ngunits + 1);
-        S.gmom.ensure(15 * (size_t)ngunits + 1);
-        S.glist.ensure(2 * (size_t)ngunits + 2);
         S.nlist.ensure(4);
         CK(cudaMemsetAsync(S.nlist.p, 0, 4 * sizeof(int), st));
-        k_gunits_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.goff.p, S.gpair.p, S.gq.p,
-                                                     S.partner.p, S.glist.p,
-                                                     S.glist.p + ngunits + 1, S.nlist.p + 2);
-        ++S.launches;
+        if (need_gauss) {
+          scan64(S, S.gcount.p, true, np, S.goff.p, st);
+          ngunits = read_ll(S.goff.p + np, st);
+          S.gpair.ensure(ngunits + 1);
+          S.gq.ensure(ngunits + 1);
+          S.gmom.ensure(15 * (size_t)ngunits + 1);
+          S.glist.ensure(2 * (size_t)ngunits + 2);
+          k_gunits_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.goff.p, S.gpair.p,
+                                                       S.gq.p, S.partner.p, S.glist.p,
+                                                       S.glist.p + ngunits + 1, S.nlist.p + 2);
+          ++S.launches;
+        }
         if (need_mc) {
           scan64(S, S.ucount.p, true, np, S.uoff.p, st);
           nunits = read_ll(S.uoff.p + np, st);
@@ -2138,13 +2254,13 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
         CK(cudaMemcpyAsync(nl, S.nlist.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaEventRecord(S.ev[6], st));
-        if (nl[2] > 0) {
+        if (need_gauss && nl[2] > 0) {
           k_gauss<false><<<nblk(nl[2], kGaussThreads), kGaussThreads, 0, st>>>(
               P0, ngunits, S.glist.p, nl[2], S.gpair.p, S.gq.p, S.pair_outer.p, S.partner.p,
               S.info.p, S.gmom.p, S.counters.p + 1);
           ++S.launches;
         }
-        if (nl[3] > 0) {
+        if (need_gauss && nl[3] > 0) {
           k_gauss<true><<<nblk(nl[3], kGaussThreads), kGaussThreads, 0, st>>>(
               P0, ngunits, S.glist.p + ngunits + 1, nl[3], S.gpair.p, S.gq.p, S.pair_outer.p,
               S.partner.p, S.info.p, S.gmom.p, S.counters.p + 1);
