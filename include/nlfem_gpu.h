@@ -132,6 +132,7 @@ typedef struct {
                               straddle volume 24, Gauss sub-simplex 360/160, MC
                               sub-simplex setup 25, sample 35, hit +62/+12)   */
   uint64_t mc_subsimplices;
+  int64_t shard_pairs;     /* element pairs integrated by this run (its shard)  */
 } nlfem_gpu_stats;
 
 /* One-shot drop-in: host arrays in, host CSR out (upload + device pipeline +
@@ -158,6 +159,30 @@ int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* s
                           char* err, size_t errlen);
 int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* err,
                                size_t errlen);
+/* Multi-GPU building blocks (one process per GPU).
+ * run_shard integrates only interior outer elements [lo, hi) (positions in
+ * ascending interior-id order; pairs and node pattern are built for all), and
+ * leaves the exact fixed-point partial sums on the device; finalize = 1 also
+ * finalizes all rows (single-GPU use).  partials() exposes the device arrays
+ * (V: int64 words, rhsT: doubles, each entry written by one shard only) for a
+ * cross-rank integer sum (e.g. ncclAllReduce int64 / f64).  finalize() then
+ * computes output rows [row_lo, row_hi) and download_rows() copies them out
+ * (row_ptr relative to the block).  The summed result is bit-identical to a
+ * single-GPU run for any sharding. */
+int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
+                                int32_t finalize, nlfem_gpu_stats* stats, char* err,
+                                size_t errlen);
+int nlfem_gpu_session_partials(nlfem_gpu_session* s, void** V, int64_t* nwords, void** rhsT,
+                               int64_t* nrhs);
+int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_lo,
+                               int32_t row_hi, char* err, size_t errlen);
+int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,
+                                    nlfem_gpu_csr* out, char* err, size_t errlen);
+/* Device pointers of the output CSR of the last run (row offsets are int64,
+ * columns int32, values and rhs double), for device-side collectives. */
+int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_idx,
+                              void** values, void** rhs, int32_t* rows, int64_t* nnz);
+
 /* Element-pair list of the last run, for set parity: for each interior outer
  * element (in ascending id order) its partner ids and per-quad-point class
  * codes (5 bits per point).  Arrays sized by *npairs after a

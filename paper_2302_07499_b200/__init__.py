@@ -84,7 +84,8 @@ class Stats(C.Structure):
                 ("mc_samples", C.c_uint64), ("mc_hits", C.c_uint64),
                 ("element_pairs", C.c_int64), ("items", C.c_int64), ("nnz_ext", C.c_int64),
                 ("device_ms", C.c_double), ("phase_ms", C.c_double * 8),
-                ("ledger_flops", C.c_uint64), ("mc_subsimplices", C.c_uint64)]
+                ("ledger_flops", C.c_uint64), ("mc_subsimplices", C.c_uint64),
+                ("shard_pairs", C.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}
@@ -120,6 +121,16 @@ def lib():
     L.nlfem_gpu_session_run.argtypes = [vp, vp, P(Stats), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_download.restype = C.c_int
     L.nlfem_gpu_session_download.argtypes = [vp, P(_Csr), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_run_shard.restype = C.c_int
+    L.nlfem_gpu_session_run_shard.argtypes = [vp, vp, i32, i32, i32, P(Stats), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_partials.restype = C.c_int
+    L.nlfem_gpu_session_partials.argtypes = [vp, P(vp), P(i64), P(vp), P(i64)]
+    L.nlfem_gpu_session_finalize.restype = C.c_int
+    L.nlfem_gpu_session_finalize.argtypes = [vp, vp, i32, i32, C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_download_rows.restype = C.c_int
+    L.nlfem_gpu_session_download_rows.argtypes = [vp, i32, i32, P(_Csr), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_outputs.restype = C.c_int
+    L.nlfem_gpu_session_outputs.argtypes = [vp, P(vp), P(vp), P(vp), P(vp), P(i32), P(i64)]
     L.nlfem_gpu_session_pairs.restype = C.c_int
     L.nlfem_gpu_session_pairs.argtypes = [vp, P(i64), vp, vp, vp, C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_launches.restype = i64
@@ -146,7 +157,9 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
     "nlfem_gpu_session_run", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
-    "nlfem_gpu_fp64_peak",
+    "nlfem_gpu_fp64_peak", "nlfem_gpu_session_run_shard", "nlfem_gpu_session_partials",
+    "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
+    "nlfem_gpu_session_outputs",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
 ]
@@ -362,6 +375,55 @@ class Session:
                                            C.byref(self.stats), err, 1024), err)
         return self.stats
 
+    # -- multi-GPU building blocks ---------------------------
+    @property
+    def interior_count(self) -> int:
+        return int((self.table.region == 0).sum())
+
+    @property
+    def unknowns(self) -> int:
+        return self.table.unknowns
+
+    def run_shard(self, lo: int, hi: int, finalize: bool = False,
+                  stream: int | None = None) -> Stats:
+        """Integrate interior outer elements [lo, hi) only; partial sums stay on device."""
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_run_shard(self._h, C.c_void_p(stream or 0), int(lo),
+                                                 int(hi), int(finalize), C.byref(self.stats),
+                                                 err, 1024), err)
+        return self.stats
+
+    def partials(self):
+        """Device views (V int64 words, rhsT float64) of the exact partial sums."""
+        vp, nv, rp, nr = C.c_void_p(), C.c_int64(), C.c_void_p(), C.c_int64()
+        lib().nlfem_gpu_session_partials(self._h, C.byref(vp), C.byref(nv), C.byref(rp),
+                                         C.byref(nr))
+        return (_CudaView(vp.value or 0, nv.value, "<i8"),
+                _CudaView(rp.value or 0, nr.value, "<f8"))
+
+    def outputs(self):
+        """Device views of the output CSR: (row offsets int64 [rows+1], col_idx,
+        values, rhs)."""
+        ro, ci, va, rh = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        rows, nnz = C.c_int32(), C.c_int64()
+        lib().nlfem_gpu_session_outputs(self._h, C.byref(ro), C.byref(ci), C.byref(va),
+                                        C.byref(rh), C.byref(rows), C.byref(nnz))
+        n, z = rows.value, nnz.value
+        return (_CudaView(ro.value or 0, n + 1, "<i8"), _CudaView(ci.value or 0, z, "<i4"),
+                _CudaView(va.value or 0, z, "<f8"), _CudaView(rh.value or 0, n, "<f8"))
+
+    def finalize(self, row_lo: int, row_hi: int, stream: int | None = None) -> None:
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_finalize(self._h, C.c_void_p(stream or 0), int(row_lo),
+                                                int(row_hi), err, 1024), err)
+
+    def download_rows(self, row_lo: int, row_hi: int) -> dict:
+        csr = _Csr()
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_download_rows(self._h, int(row_lo), int(row_hi),
+                                                     C.byref(csr), err, 1024), err)
+        return _take_csr(csr)
+
     def download(self) -> dict:
         csr = _Csr()
         err = C.create_string_buffer(1024)
@@ -407,6 +469,29 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+class _CudaView:
+    """Zero-copy device array view (__cuda_array_interface__ v3), e.g. for
+    torch.as_tensor(view, device="cuda") in the NCCL reduction."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _take_csr(csr) -> dict:
+    try:
+        n, nnz = csr.rows, csr.nnz
+        return {
+            "row_ptr": np.ctypeslib.as_array(csr.row_ptr, (n + 1,)).copy(),
+            "col_idx": np.ctypeslib.as_array(csr.col_idx, (max(nnz, 1),))[:nnz].copy(),
+            "values": np.ctypeslib.as_array(csr.values, (max(nnz, 1),))[:nnz].copy(),
+            "rhs": np.ctypeslib.as_array(csr.rhs, (max(n, 1),))[:n].copy(),
+        }
+    finally:
+        lib().nlfem_gpu_free_csr(C.byref(csr))
 
 
 def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",

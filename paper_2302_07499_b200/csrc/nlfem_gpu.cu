@@ -1659,11 +1659,11 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
 __global__ void k_finalize(const long long* soff, const int* scols, const long long* mirror,
                            const unsigned long long* V, const long long* ooff,
                            const long long* omap, double* values, const double* rhsT,
-                           double* rhs, const int* dof_node) {
+                           double* rhs, const int* dof_node, int d0, int d1) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= cD.unknowns) return;
-  const int d = warp;
+  const int d = d0 + warp;
+  if (d >= d1) return;
   const int i = dof_node[d];
   const double si = cD.iscale[i];
   // matrix entries of output row d: A_ij = V_ij + V_ji (V_ii carries both halves)
@@ -2062,7 +2062,24 @@ void run_prep(nlfem_gpu_session& S) {
   ++S.launches;
 }
 
-void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
+void run_finalize(nlfem_gpu_session& S, int r0, int r1) {
+  cudaStream_t st = S.stream;
+  S.values.ensure(S.nnz_out);
+  S.rhs.ensure(S.unknowns);
+  if (r1 > r0) {
+    k_finalize<<<nblk((long long)(r1 - r0) * 32, 128), 128, 0, st>>>(
+        S.soff.p, S.scols.p, S.mirror.p, S.V.p, S.ooff.p, S.omap.p, S.values.p, S.rhsT.p,
+        S.rhs.p, S.dof_node.p, r0, r1);
+    ++S.launches;
+  }
+}
+
+// The whole device pipeline.  Outer elements [shard_lo, shard_hi) (positions in
+// the ascending interior list) are integrated; pairs and the node pattern are
+// built for all of them (every rank holds the same pattern, so the fixed-point
+// partial sums of several ranks add up slot by slot).
+void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, int shard_lo,
+             int shard_hi, bool finalize) {
   cudaStream_t st = S.stream;
   Dev& D = S.dev;
   const auto wall0 = std::chrono::steady_clock::now();
@@ -2185,6 +2202,9 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   S.V.ensure(2 * (size_t)S.nnz_s);
   S.rhsT.ensure(4 * (size_t)KI);
   CK(cudaMemsetAsync(S.V.p, 0, 2 * S.nnz_s * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(S.rhsT.p, 0, 4 * (size_t)KI * sizeof(double), st));
+  shard_lo = std::max(0, std::min(shard_lo, KI));
+  shard_hi = std::max(shard_lo, std::min(shard_hi, KI));
   // slot-map capacity: power of two > union of the four rows (<= 4 maxlen)
   int hcap = 64;
   while (hcap <= 4 * std::max(maxlen, 1)) hcap <<= 1;
@@ -2199,18 +2219,18 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   const bool need_gauss = D.strategy != NLFEM_STRATEGY_BARYCENTER;
   float mc_ms = 0;
-  if (KI > 0) {
+  if (shard_hi > shard_lo) {
     // chunks of outer elements sized so the unit buffers stay bounded
     std::vector<long long> poff(KI + 1);
     CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const long long kPairsPerChunk = need_gauss ? (8LL << 20) : (1LL << 40);
-    int ii0 = 0;
-    while (ii0 < KI) {
+    int ii0 = shard_lo;
+    while (ii0 < shard_hi) {
       int ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), poff[ii0] + kPairsPerChunk) -
                       poff.begin()) - 1;
-      ii1 = std::min(std::max(ii1, ii0 + 1), KI);
+      ii1 = std::min(std::max(ii1, ii0 + 1), shard_hi);
       const long long P0 = poff[ii0], np = poff[ii1] - P0;
       long long nunits = 0, ngunits = 0;
       if (need_gauss) {
@@ -2303,14 +2323,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
   CK(cudaEventRecord(S.ev[4], st));
 
   // ---- K6: finalize
-  S.values.ensure(S.nnz_out);
-  S.rhs.ensure(U);
-  if (U > 0) {
-    k_finalize<<<nblk((long long)U * 32, 128), 128, 0, st>>>(
-        S.soff.p, S.scols.p, S.mirror.p, S.V.p, S.ooff.p, S.omap.p, S.values.p, S.rhsT.p,
-        S.rhs.p, S.dof_node.p);
-    ++S.launches;
-  }
+  if (finalize) run_finalize(S, 0, U);
   CK(cudaEventRecord(S.ev[5], st));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
@@ -2337,6 +2350,14 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats) {
     stats->mc_samples = S.mc_samples;
     stats->mc_hits = S.mc_hits;
     stats->element_pairs = S.npairs;
+    {
+      long long a = 0, b = 0;
+      if (KI > 0) {
+        CK(cudaMemcpy(&a, S.pair_off.p + shard_lo, sizeof(long long), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&b, S.pair_off.p + shard_hi, sizeof(long long), cudaMemcpyDeviceToHost));
+      }
+      stats->shard_pairs = b - a;
+    }
     stats->items = (long long)S.items;
     stats->nnz_ext = S.nnz_s;
     stats->ledger_flops = S.ledger;
@@ -2411,7 +2432,75 @@ int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* d
 
 int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* stats, char* err,
                           size_t errlen) {
-  return guard(err, errlen, [&] { run_all(*s, static_cast<cudaStream_t>(stream), stats); });
+  return guard(err, errlen,
+               [&] { run_all(*s, static_cast<cudaStream_t>(stream), stats, 0, s->KI, true); });
+}
+
+int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
+                                int32_t finalize, nlfem_gpu_stats* stats, char* err,
+                                size_t errlen) {
+  return guard(err, errlen, [&] {
+    run_all(*s, static_cast<cudaStream_t>(stream), stats, lo, hi, finalize != 0);
+  });
+}
+
+int nlfem_gpu_session_partials(nlfem_gpu_session* s, void** V, int64_t* nwords, void** rhsT,
+                               int64_t* nrhs) {
+  *V = s->V.p;
+  *nwords = 2 * s->nnz_s;
+  *rhsT = s->rhsT.p;
+  *nrhs = 4 * (int64_t)s->KI;
+  return 0;
+}
+
+int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_idx,
+                              void** values, void** rhs, int32_t* rows, int64_t* nnz) {
+  *row_off = s->ooff.p;
+  *col_idx = s->ocols.p;
+  *values = s->values.p;
+  *rhs = s->rhs.p;
+  *rows = s->unknowns;
+  *nnz = s->nnz_out;
+  return 0;
+}
+
+int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_lo,
+                               int32_t row_hi, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    if (user) {
+      CK(cudaEventRecord(s->ev[7], user));
+      CK(cudaStreamWaitEvent(s->stream, s->ev[7], 0));
+    }
+    run_finalize(*s, std::max(0, row_lo), std::min(row_hi, s->unknowns));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,
+                                    nlfem_gpu_csr* out, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    const int r0 = std::max(0, row_lo), r1 = std::max(r0, std::min(row_hi, s->unknowns));
+    const int n = r1 - r0;
+    std::vector<long long> off(n + 1);
+    CK(cudaMemcpy(off.data(), s->ooff.p + r0, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost));
+    const long long nnz = off[n] - off[0];
+    out->rows = n;
+    out->nnz = nnz;
+    out->row_ptr = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (n + 1)));
+    out->col_idx = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<long long>(nnz, 1)));
+    out->values = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(nnz, 1)));
+    out->rhs = static_cast<double*>(std::malloc(sizeof(double) * std::max(n, 1)));
+    if (!out->row_ptr || !out->col_idx || !out->values || !out->rhs)
+      throw Fail{NLFEM_GPU_ENOMEM, "out of host memory"};
+    for (int i = 0; i <= n; ++i) out->row_ptr[i] = (int32_t)(off[i] - off[0]);
+    if (nnz) {
+      CK(cudaMemcpy(out->col_idx, s->ocols.p + off[0], sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(out->values, s->values.p + off[0], sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+    }
+    if (n) CK(cudaMemcpy(out->rhs, s->rhs.p + r0, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  });
 }
 
 int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* err,
