@@ -1887,15 +1887,17 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     throw Fail{NLFEM_GPU_ENODEVICE, "no CUDA device available (the GPU path has no CPU fallback)"};
   if (cfg->device >= 0) CK(cudaSetDevice(cfg->device));
   CK(cudaGetDevice(&S.device));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, S.device));
-  if (prop.major < 10)
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, S.device));
+  if (major < 10)
     throw Fail{NLFEM_GPU_ENODEVICE, "device is not sm_100 class (built for sm_100a only)"};
-  CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
-  for (int i = 0; i < 8; ++i) {
-    cudaEvent_t e;
-    CK(cudaEventCreate(&e));
-    S.ev.push_back(e);
+  if (!S.stream) {  // a reused workspace keeps its stream, events and buffers
+    CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 8; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      S.ev.push_back(e);
+    }
   }
   S.K = m->elem_count;
   S.J = m->node_count;
@@ -2550,17 +2552,25 @@ void nlfem_gpu_session_destroy(nlfem_gpu_session* s) {
   delete s;
 }
 
+// The one-shot entry keeps one workspace per device (stream, events, device
+// buffers; grow-only) across calls, so repeated assemblies do not pay for
+// cudaMalloc / cudaFree.  Like the reference's assemble, it is meant to be
+// called from one host thread at a time.
 int nlfem_gpu_assemble(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
                        const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
                        const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
                        nlfem_gpu_csr* out, nlfem_gpu_stats* stats, char* err, size_t errlen) {
   const auto t0 = std::chrono::steady_clock::now();
-  nlfem_gpu_session* s = nullptr;
-  int rc = nlfem_gpu_session_create(mesh, dofs, kernel, f, g, cfg, &s, err, errlen);
+  static std::vector<nlfem_gpu_session*> workspaces;
+  int dev = cfg ? cfg->device : -1;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  if ((int)workspaces.size() <= dev) workspaces.resize(dev + 1, nullptr);
+  if (!workspaces[dev]) workspaces[dev] = new nlfem_gpu_session;
+  nlfem_gpu_session* s = workspaces[dev];
+  int rc = guard(err, errlen, [&] { session_init(*s, mesh, dofs, kernel, f, g, cfg); });
   if (rc) return rc;
   rc = nlfem_gpu_session_run(s, nullptr, stats, err, errlen);
   if (!rc) rc = nlfem_gpu_session_download(s, out, err, errlen);
-  nlfem_gpu_session_destroy(s);
   if (!rc && stats)
     stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return rc;
