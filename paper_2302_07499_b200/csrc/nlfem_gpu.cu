@@ -435,30 +435,35 @@ struct CandStage {
 // grid rows of the union of their reach boxes once; a candidate T' survives if
 // its bounding sphere can reach B(delta) of some quadrature point of one of the
 // four T (a conservative superset of the reference's BFS superset,
-// assembly.cpp:569-613); survivors are staged in shared memory.  Each warp then
-// classifies its own survivors with one lane per (candidate, quadrature point)
-// -- the reference's exact per-(T,q,T') predicates -- and ORs the four 5-bit
-// codes.  Pair order is the stream order, identical in the count and fill pass.
-template <bool FILL>
-__global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair_off,
-                                                        int* pair_count, int* partner,
-                                                        unsigned* info,
+// assembly.cpp:569-613).
+//   MODE 0: count each warp's survivors (no classification);
+//   MODE 1: stage survivors in shared memory; each warp classifies its own with
+//           one lane per (candidate, quadrature point) -- the reference's exact
+//           per-(T,q,T') predicates -- ORs the four 5-bit codes and writes
+//           (T', code) into its survivor slots (code 0 = no piece), in stream
+//           order; k_pairs_compact then keeps the nonzero ones.
+template <int MODE>
+__global__ void __launch_bounds__(kPairThreads, 4) k_pairs(int ii_base, int ii_end,
+                                                        const long long* cand_off,
+                                                        long long cand_base, int* cand_count,
+                                                        int* cpartner, unsigned* cinfo,
+                                                        int* pair_count,
                                                         unsigned long long* item_count,
                                                         int* err_elem) {
   __shared__ CandStage sg;
-  __shared__ int nst, xb[6];
+  __shared__ int nst, xb[6], scnt[kPairWarps];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int warp = blockIdx.x * kPairWarps + wl;  // outer element index
-  const bool active = warp < cD.KI;
+  const int warp = ii_base + blockIdx.x * kPairWarps + wl;  // outer element index
+  const bool active = warp < ii_end;
   OuterT o;
   if (active) outer_setup(cD.interior[warp], o);
   else o.R = -1;
   const double reach = o.R + cD.rmax;
-  // union of the reach boxes (cell indices)
   if (threadIdx.x == 0) {
     xb[0] = xb[2] = xb[4] = 1 << 30;
     xb[1] = xb[3] = xb[5] = -1;
   }
+  if (threadIdx.x < kPairWarps) scnt[threadIdx.x] = 0;
   __syncthreads();
   if (active && lane == 0) {
     atomicMin(xb + 0, cell_of(o.c.x - reach, cD.gox, cD.ginv, cD.gx));
@@ -470,7 +475,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
   }
   __syncthreads();
   const int x0 = xb[0], x1 = xb[1], y0 = xb[2], y1 = xb[3], z0 = xb[4], z1 = xb[5];
-  // the four outer centers and radii for the union screen (broadcast via smem)
   __shared__ double oc[kPairWarps][4];
   if (lane == 0) {
     oc[wl][0] = o.c.x;
@@ -479,13 +483,11 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
     oc[wl][3] = active ? o.R : -1.0;
   }
   __syncthreads();
-  const long long out = (FILL && active) ? pair_off[warp] : 0;
-  int cnt = 0;
+  const long long out = (MODE == 1 && active) ? cand_off[warp] - cand_base : 0;
+  int cnt = 0, npair = 0;
   unsigned items = 0;
 
-  // classify the staged chunk for this warp's T
   auto classify_chunk = [&]() {
-    // indices of staged candidates that pass this warp's screen
     int nm = 0;
     for (int base = 0; base < nst; base += 32) {
       const int k = base + lane;
@@ -507,24 +509,20 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
         const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
         const Vd xq = quad_point(o.v, q);
         code = classify_item(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]) << (5 * q);
-        if (!FILL) {
-          items += code != 0;
-          const int4 nb = cD.nbr[Tp];
-          if ((nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) && facet_too_close(v, nb, xq))
-            atomicMin(err_elem, Tp);
-        }
+        items += code != 0;
+        const int4 nb = cD.nbr[Tp];
+        if ((nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) && facet_too_close(v, nb, xq))
+          atomicMin(err_elem, Tp);
       }
       code |= __shfl_xor_sync(FULLMASK, code, 1);
       code |= __shfl_xor_sync(FULLMASK, code, 2);
-      const bool keep = (lane & 3) == 0 && code != 0;
-      const unsigned bal = __ballot_sync(FULLMASK, keep);
-      if (FILL && keep) {
-        const long long pos = out + cnt + __popc(bal & ((1u << lane) - 1));
-        partner[pos] = Tp;
-        info[pos] = code;
+      if ((lane & 3) == 0 && t < nm) {
+        cpartner[out + cnt + t] = Tp;
+        cinfo[out + cnt + t] = code;
       }
-      cnt += __popc(bal);
+      npair += __popc(__ballot_sync(FULLMASK, (lane & 3) == 0 && code != 0));
     }
+    cnt += nm;
   };
 
   if (threadIdx.x == 0) nst = 0;
@@ -549,7 +547,15 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
               pm |= 1u << w;
           }
         }
-        // stage survivors (block-wide compaction)
+        if (MODE == 0) {
+#pragma unroll
+          for (int w = 0; w < kPairWarps; ++w) {
+            const int c = __popc(__ballot_sync(FULLMASK, (pm >> w) & 1));
+            if (lane == 0 && c) atomicAdd(scnt + w, c);
+          }
+          continue;
+        }
+        // stage survivors (block-wide compaction, stream order)
         const unsigned bal = __ballot_sync(FULLMASK, pm != 0);
         __shared__ int wcount[kPairWarps], wbase[kPairWarps];
         if (lane == 0) wcount[wl] = __popc(bal);
@@ -564,7 +570,6 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
         __syncthreads();
         const int tot = wbase[kPairWarps - 1] + wcount[kPairWarps - 1];
         if (tot > kCandChunk) {
-          // chunk full: classify what is staged, then restart the stage
           classify_chunk();
           __syncthreads();
           if (threadIdx.x == 0) {
@@ -594,13 +599,38 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(const long long* pair
       }
     }
   }
+  if (MODE == 0) {
+    __syncthreads();
+    if (active && lane == 0) cand_count[warp] = scnt[wl];
+    return;
+  }
   classify_chunk();
-  if (!FILL) {
-    for (int sh = 16; sh > 0; sh >>= 1) items += __shfl_xor_sync(FULLMASK, items, sh);
-    if (active && lane == 0) {
-      pair_count[warp] = cnt;
-      atomicAdd(item_count, (unsigned long long)items);
+  for (int sh = 16; sh > 0; sh >>= 1) items += __shfl_xor_sync(FULLMASK, items, sh);
+  if (active && lane == 0) {
+    pair_count[warp] = npair;
+    atomicAdd(item_count, (unsigned long long)items);
+  }
+}
+
+// keep the survivors with a nonzero code, in order: warp per outer element
+__global__ void k_pairs_compact(int ii0, int ii1, const long long* cand_off, long long cand_base,
+                                const int* cpartner, const unsigned* cinfo,
+                                const long long* pair_off, int* partner, unsigned* info) {
+  const int ii = ii0 + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (ii >= ii1) return;
+  const long long a = cand_off[ii] - cand_base, b = cand_off[ii + 1] - cand_base;
+  long long o = pair_off[ii];
+  for (long long k = a; k < b; k += 32) {
+    const long long j = k + lane;
+    const unsigned c = j < b ? cinfo[j] : 0;
+    const unsigned bal = __ballot_sync(FULLMASK, c != 0);
+    if (c) {
+      const long long pos = o + __popc(bal & ((1u << lane) - 1));
+      partner[pos] = cpartner[j];
+      info[pos] = c;
     }
+    o += __popc(bal);
   }
 }
 
@@ -1771,7 +1801,9 @@ struct nlfem_gpu_session {
   DBuf<int> cell_start, ni_off;
   DBuf<double> scale, iscale;
   // pairs
-  DBuf<int> pair_count, partner, err_elem, ovf;
+  DBuf<int> pair_count, partner, err_elem, ovf, cand_count, cpartner;
+  DBuf<long long> cand_off;
+  DBuf<unsigned> cinfo;
   DBuf<unsigned> info;
   DBuf<long long> pair_off;
   DBuf<unsigned long long> counters;
@@ -1844,6 +1876,11 @@ long long read_ll(const long long* d, cudaStream_t st) {
   CK(cudaMemcpyAsync(&h, d, sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return h;
+}
+
+__global__ void k_add_offset(long long* a, long long n, long long off) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] += off;
 }
 
 __global__ void k_ll_to_int(long long n, const long long* a, int* b) {
@@ -2106,23 +2143,80 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   CK(cudaMemcpyAsync(S.err_elem.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
   CK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), st));
-  const unsigned pblocks = nblk((long long)KI, kPairWarps);
-  k_pairs<false><<<pblocks, kPairThreads, 0, st>>>(nullptr, S.pair_count.p, nullptr, nullptr,
-                                          S.counters.p, S.err_elem.p);
-  ++S.launches;
+  // pass 0: survivors per outer element (cheap superset count)
+  S.cand_count.ensure(KI + 1);
+  S.cand_off.ensure(KI + 1);
+  if (KI > 0) {
+    k_pairs<0><<<nblk((long long)KI, kPairWarps), kPairThreads, 0, st>>>(
+        0, KI, nullptr, 0, S.cand_count.p, nullptr, nullptr, nullptr, nullptr, nullptr);
+    ++S.launches;
+  }
+  scan64(S, S.cand_count.p, true, KI, S.cand_off.p, st);
+  std::vector<long long> coff(KI + 1, 0);
+  CK(cudaMemcpyAsync(coff.data(), S.cand_off.p, sizeof(long long) * (KI + 1),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // pass 1 + compaction, in chunks of outer elements bounded by survivors
+  const long long kCandBudget = 1LL << 30;  // 8 GiB of (partner, code) slots
+  long long cap = std::max<long long>(1, (long long)(0.8 * coff[KI]));
+  S.partner.ensure(cap);
+  S.info.ensure(cap);
+  S.pair_off.ensure(KI + 1);
+  long long total = 0;
+  int c0 = 0;
+  while (c0 < KI) {
+    int c1 = (int)(std::upper_bound(coff.begin() + c0 + 1, coff.end(), coff[c0] + kCandBudget) -
+                   coff.begin()) - 1;
+    c1 = std::min(std::max(c1, c0 + 1), KI);
+    const long long nc = coff[c1] - coff[c0];
+    S.cpartner.ensure(nc + 1);
+    S.cinfo.ensure(nc + 1);
+    k_pairs<1><<<nblk((long long)(c1 - c0), kPairWarps), kPairThreads, 0, st>>>(
+        c0, c1, S.cand_off.p, coff[c0], nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
+        S.counters.p, S.err_elem.p);
+    ++S.launches;
+    // pair offsets of this chunk continue the running total
+    scan64(S, S.pair_count.p + c0, true, c1 - c0, S.pair_off.p + c0, st);
+    const long long nch = read_ll(S.pair_off.p + c1, st);
+    if (total) {
+      k_add_offset<<<nblk(c1 - c0 + 1, 256), 256, 0, st>>>(S.pair_off.p + c0, c1 - c0 + 1, total);
+      ++S.launches;
+    }
+    if (total + nch > cap) {  // grow, keeping what is compacted
+      cap = (long long)((total + nch) * 1.25) + 1;
+      DBuf<int> np_;
+      DBuf<unsigned> ni_;
+      np_.ensure(cap);
+      ni_.ensure(cap);
+      if (total) {
+        CK(cudaMemcpyAsync(np_.p, S.partner.p, total * sizeof(int), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ni_.p, S.info.p, total * sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+      }
+      CK(cudaStreamSynchronize(st));
+      std::swap(S.partner.p, np_.p);
+      std::swap(S.partner.n, np_.n);
+      std::swap(S.info.p, ni_.p);
+      std::swap(S.info.n, ni_.n);
+    }
+    k_pairs_compact<<<nblk((long long)(c1 - c0) * 32, 256), 256, 0, st>>>(
+        c0, c1, S.cand_off.p, coff[c0], S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p,
+        S.info.p);
+    ++S.launches;
+    total += nch;
+    c0 = c1;
+  }
+  S.npairs = total;
+  {
+    const long long z = 0;
+    if (KI == 0) CK(cudaMemcpyAsync(S.pair_off.p, &z, sizeof(long long), cudaMemcpyHostToDevice, st));
+  }
   int err_elem = big;
   CK(cudaMemcpyAsync(&err_elem, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  scan64(S, S.pair_count.p, true, KI, S.pair_off.p, st);
+  CK(cudaStreamSynchronize(st));
   if (err_elem != big)
     throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
                "BallExitsMesh: ball reaches past an unglued facet of element " +
                    std::to_string(err_elem)};
-  S.npairs = read_ll(S.pair_off.p + KI, st);
-  S.partner.ensure(S.npairs);
-  S.info.ensure(S.npairs);
-  k_pairs<true><<<pblocks, kPairThreads, 0, st>>>(S.pair_off.p, nullptr, S.partner.p, S.info.p, nullptr,
-                                         nullptr);
-  ++S.launches;
   CK(cudaEventRecord(S.ev[2], st));
 
   // ---- K5: pattern
