@@ -946,6 +946,30 @@ __device__ __forceinline__ int reserve2(int* counters, int kind, int n) {
   return kind ? base_b + ib - b : base_a + ia - a;
 }
 
+// Warp-aggregated reservation in one of four lists (counters[0..3]).
+__device__ __forceinline__ int reserve4(int* counters, int kind, int n) {
+  const int lane = threadIdx.x & 31;
+  int own[4], incl[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) own[k] = incl[k] = (kind == k) ? n : 0;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = __shfl_up_sync(FULLMASK, incl[k], off);
+      if (lane >= off) incl[k] += t;
+    }
+  int base = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int b = 0;
+    if (lane == 31 && incl[k]) b = atomicAdd(counters + k, incl[k]);
+    b = __shfl_sync(FULLMASK, b, 31);
+    if (kind == k) base = b + incl[k] - own[k];
+  }
+  return base;
+}
+
 __global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount,
                               int* gcount, int mc_units) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -987,27 +1011,38 @@ __global__ void k_gunits_fill(long long p0, long long np, const unsigned* info,
 // are also listed per parent kind (interior / constraint) so each Monte Carlo
 // launch runs one code path (list order is irrelevant: every unit writes only
 // its own slot)
+// Monte Carlo units: one per sub-simplex slot of a cap item (the reference's
+// straddle_outer pieces, upper bound 3 or 1 before the volume floor).  Items
+// are listed by their first unit id in four lists -- (interior, constraint)
+// parent x (1, 3) slots -- so each k_mc launch runs one uniform code path.
 __global__ void k_units_fill(long long p0, long long np, const unsigned* info,
                              const long long* uoff, int* upair, unsigned char* uqs,
-                             const int* partner, int* list_int, int* list_con, int* nlist) {
+                             const int* partner, int* lists, long long lstride, int* nlist) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool act = i < np;
+  const unsigned code = act ? info[p0 + i] : 0;
+  const bool cons = act && cD.region[partner[p0 + i]] != 0;
   long long u = act ? uoff[i] : 0;
-  const int nu = act ? (int)(uoff[i + 1] - u) : 0;
-  const bool cons = act && nu > 0 && cD.region[partner[p0 + i]] != 0;
-  const int base = reserve2(nlist, cons ? 1 : 0, nu);
-  if (!act) return;
-  const unsigned code = info[p0 + i];
-  {
-    int* lst = cons ? list_con : list_int;
-    for (int k = 0; k < nu; ++k) lst[base + k] = (int)(u + k);
+  // items of this pair, in q order
+  int n1 = 0, n3 = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const unsigned c = (code >> (5 * q)) & 31;
+    if (c == kOutCap) ++n1;
+    else if (c & kStraddle) (outer_units((int)(c & 15)) == 3 ? n3 : n1) += 1;
   }
+  const int kind1 = cons ? 2 : 0, kind3 = cons ? 3 : 1;
+  int b1 = reserve4(nlist, kind1, n1);
+  int b3 = reserve4(nlist, kind3, n3);
+  if (!act) return;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
     int n = 0;
     if (c == kOutCap) n = 1;
     else if (c & kStraddle) n = outer_units((int)(c & 15));
+    if (n == 1) lists[kind1 * lstride + b1++] = (int)u;
+    if (n == 3) lists[kind3 * lstride + b3++] = (int)u;
     for (int sb = 0; sb < n; ++sb, ++u) {
       upair[u] = (int)i;
       uqs[u] = (unsigned char)(q | (sb << 2));
@@ -1129,26 +1164,27 @@ __device__ __forceinline__ void poly2_taylor(const Poly& P, Vd x, double& g0, do
 }
 
 #ifndef NLFEM_MC_MINBLOCKS
-#define NLFEM_MC_MINBLOCKS 6
+#define NLFEM_MC_MINBLOCKS 5
 #endif
 // CONS: constraint parent (accumulates sum g(y) instead of basis moments).
 // G2: g has total degree <= 2, so sum_hits g(x_q + r) follows exactly from the
 // hit count, sum r and sum r r^T -- the same branch-free moments as interior
 // parents -- instead of one polynomial evaluation per hit.
-template <bool CONS, bool G2>
+template <bool CONS, bool G2, int NU>
 __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nunits,
                                                       const int* list, int nlist,
                                                       const int* upair, const unsigned char* uqs,
                                                       const int* pair_outer, const int* partner,
                                                       const unsigned* info, double* mom,
                                                       unsigned long long* mc_stats) {
+  // one thread per cap item: the straddle_outer decomposition is computed once
+  // and each kept piece (unit u0 + j) gets its M samples
   const int li = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long draws = 0, hits = 0, led = 0;
   if (li < nlist) {
-    const long long u = list[li];
-    double S0 = 0, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
-    const int pi = upair[u];
-    const int q = uqs[u] & 3, sub = uqs[u] >> 2;
+    const long long u0 = list[li];
+    const int pi = upair[u0];
+    const int q = uqs[u0] & 3;
     const long long p = p0 + pi;
     const int T = cD.interior[pair_outer[pi]];
     const int Tp = partner[p];
@@ -1158,37 +1194,45 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     const Vd xq = quad_point(vT, q);
     Vd vP[4];
     load_verts(Tp, vP);
-    PickPiece pk;
-    pk.want = sub;
-    if (c == kOutCap) {
-      if (sub == 0) {
-        pk.a = vP[0];
-        pk.b = vP[1];
-        pk.c = vP[2];
-        pk.d = vP[3];
-        pk.vol = tet_volume(vP[0], vP[1], vP[2], vP[3]);
-        pk.found = true;
-      }
-    } else {
-      // the sub-th kept piece of straddle_outer
-      const Straddle st = outer_straddle(vP, (int)(c & 15), xq, cD.delta);
-      const double tau = cD.tau[Tp];
-      for (int k = 0; k < st.n; ++k) {
-        Vd a, b, cc, d;
-        straddle_piece(st, k, a, b, cc, d);
-        const double vol = tet_volume(a, b, cc, d);
-        if (vol > tau) pk(a, b, cc, d, vol);
-      }
+    Straddle st;
+    int npieces;
+    if (c == kOutCap) {  // whole element (reference assembly.cpp:754-759)
+      st.A0 = vP[0]; st.A1 = vP[1]; st.A2 = vP[2]; st.B0 = vP[3];
+      st.B1 = vP[3]; st.B2 = vP[3];
+      st.n = 1;
+      npieces = 1;
+    } else {  // straddle_outer (reference ball_approx.cpp:257-298)
+      st = outer_straddle(vP, (int)(c & 15), xq, cD.delta);
+      npieces = st.n;
       const int m = __popc(c & 15);
-      if (sub == 0) led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
+      led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
     }
-    if (pk.found) {
-      const int M = cD.mc;
-      const double w = pk.vol / M;
+    const double tau = c == kOutCap ? -1.0 : cD.tau[Tp];
+    const int M = cD.mc;
+    const double dd = cD.dd;
+    const uint32_t k0 = (uint32_t)(cD.seed & 0xffffffffu), k1 = (uint32_t)(cD.seed >> 32);
+    double g0 = 0, gr[3] = {0, 0, 0}, H[6] = {0, 0, 0, 0, 0, 0};
+    if (CONS && G2) poly2_taylor(cD.g, xq, g0, gr, H);
+    int kept = 0;
+#pragma unroll 1
+    for (int k = 0; k < NU; ++k) {
+      Vd pa, pb, pc, pd;
+      double vol = 0;
+      bool use = k < npieces;
+      if (use) {
+        straddle_piece(st, k, pa, pb, pc, pd);
+        vol = tet_volume(pa, pb, pc, pd);
+        use = vol > tau;  // push_piece volume floor (ball_approx.cpp:141)
+      }
+      if (!use) continue;
+      const long long u = u0 + kept;
+      const uint32_t c2 = (uint32_t)q | ((uint32_t)kept << 2);
+      ++kept;
+      const double w = vol / M;
       nlfem_mc_frame fr;
       {
-        const double a0[3] = {pk.a.x, pk.a.y, pk.a.z}, a1[3] = {pk.b.x, pk.b.y, pk.b.z},
-                     a2[3] = {pk.c.x, pk.c.y, pk.c.z}, a3[3] = {pk.d.x, pk.d.y, pk.d.z},
+        const double a0[3] = {pa.x, pa.y, pa.z}, a1[3] = {pb.x, pb.y, pb.z},
+                     a2[3] = {pc.x, pc.y, pc.z}, a3[3] = {pd.x, pd.y, pd.z},
                      x[3] = {xq.x, xq.y, xq.z};
         nlfem_mc_make_frame(a0, a1, a2, a3, x, &fr);
       }
@@ -1199,9 +1243,6 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         fs.e1[a] = fr.e1[a] * 0x1p-32;
         fs.e2[a] = fr.e2[a] * 0x1p-32;
       }
-      const double dd = cD.dd;
-      const uint32_t k0 = (uint32_t)(cD.seed & 0xffffffffu), k1 = (uint32_t)(cD.seed >> 32);
-      const uint32_t c2 = (uint32_t)q | ((uint32_t)sub << 2);
       unsigned nh = 0;
       // interior: sums of r and r r^T over hits, r = y - x_q; constraint: sum g(y)
       double t1x = 0, t1y = 0, t1z = 0, t2[6] = {0, 0, 0, 0, 0, 0}, ng = 0;
@@ -1212,12 +1253,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         if (CONS && !G2) {
           if (hit) ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
         } else {
-#ifdef NLFEM_MC_DMUL
-          const double h = hit ? 1.0 : 0.0;
-          const double hx = h * rx, hy = h * ry, hz = h * rz;
-#else
           const double hx = hit ? rx : 0.0, hy = hit ? ry : 0.0, hz = hit ? rz : 0.0;
-#endif
           t1x += hx;
           t1y += hy;
           t1z += hz;
@@ -1241,11 +1277,9 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         sample(B[2], B[3], Cw[0], !tail || 4 * j + 2 < M);
         sample(Cw[1], Cw[2], Cw[3], !tail || 4 * j + 3 < M);
       }
-      S0 = w * nh;
+      double S0 = w * nh, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
       if (CONS && G2) {
         // sum over hits of g(x_q + r) = n g + grad g . sum r + 1/2 sum H_ab r_a r_b
-        double g0, gr[3], H[6];
-        poly2_taylor(cD.g, xq, g0, gr, H);
         const double n = (double)nh;
         const double quad = 0.5 * (H[0] * t2[0] + H[3] * t2[3] + H[5] * t2[5]) +
                             H[1] * t2[1] + H[2] * t2[2] + H[4] * t2[4];
@@ -1266,17 +1300,21 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         m2[4] = w * (t2[4] + c0y * t1z + c0z * t1y + n * c0y * c0z);
         m2[5] = w * (t2[5] + 2.0 * c0z * t1z + n * c0z * c0z);
       }
-      draws = (unsigned long long)M;
-      hits = nh;
+      draws += (unsigned long long)M;
+      hits += nh;
       led += 25ull + 35ull * (unsigned long long)M + (CONS ? 12ull : 62ull) * nh;
-    }
-    mom[u] = S0;
-    mom[nunits + u] = m1x;
-    mom[2 * nunits + u] = m1y;
-    mom[3 * nunits + u] = m1z;
+      mom[u] = S0;
+      mom[nunits + u] = m1x;
+      mom[2 * nunits + u] = m1y;
+      mom[3 * nunits + u] = m1z;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) mom[(4 + k) * nunits + u] = m2[k];
-    mom[10 * nunits + u] = sg;
+      for (int kk = 0; kk < 6; ++kk) mom[(4 + kk) * nunits + u] = m2[kk];
+      mom[10 * nunits + u] = sg;
+    }
+    // unit slots of dropped pieces stay zero
+    for (int j = kept; j < NU; ++j)
+#pragma unroll
+      for (int kk = 0; kk < 11; ++kk) mom[kk * nunits + u0 + j] = 0.0;
   }
   // statistics
   for (int sh = 16; sh > 0; sh >>= 1) {
@@ -1290,7 +1328,6 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     atomicAdd(mc_stats + 2, led);
   }
 }
-
 
 // Gauss rule on the inner sub-simplices of one straddling item (reference
 // AsmSink::sub + accumulate_point, assembly.cpp:332-381): thread per item.
@@ -1401,10 +1438,9 @@ struct SlotMap {
 
 // Combine: CTA per outer element T, thread per element pair.  Whole elements
 // are closed form here; straddle items (Gauss units) and caps (Monte Carlo
-// units) come precomputed.  The T x T' block of every pair is pre-reduced in
-// shared memory (exact two-word fixed point, integer atomics) over the CTA
-// and flushed once per outer element; the T' x T' block goes straight to the
-// node pattern.
+// units) come precomputed.  A shared-memory map from node id to its slots in the
+// four T-node rows of the node pattern locates the T x T' block entries; both
+// blocks are added as two-word fixed point with integer atomics.
 #ifndef NLFEM_INT_THREADS
 #define NLFEM_INT_THREADS 256
 #endif
@@ -1413,15 +1449,6 @@ struct SlotMap {
 #endif
 constexpr int kIntThreads = NLFEM_INT_THREADS;
 
-__device__ __forceinline__ void smem_fixed(unsigned long long* acc, int slot, double v,
-                                           double scale) {
-  const double x = v * scale;
-  const long long hi = __double2ll_rn(x);
-  const long long lo = __double2ll_rn((x - (double)hi) * 0x1p40);
-  if (hi != 0) atomicAdd(acc + 2 * slot, (unsigned long long)hi);
-  if (lo != 0) atomicAdd(acc + 2 * slot + 1, (unsigned long long)lo);
-}
-
 __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
     int ii0, const long long* pair_off, const int* partner, const unsigned* info,
     const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
@@ -1429,13 +1456,11 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
     const long long* goff, const double* gmom, long long ngunits, long long pbase,
     unsigned long long* stats, int hcap, int rowcap) {
   extern __shared__ unsigned long long sml[];
-  unsigned long long* xacc = sml;  // [4][rowcap][2]
   SlotMap mp;
-  mp.key = reinterpret_cast<int*>(sml + 8 * (size_t)rowcap);
+  mp.key = reinterpret_cast<int*>(sml);
   mp.val = reinterpret_cast<short4*>(mp.key + hcap);
   mp.mask = hcap - 1;
   __shared__ long long rbase[4];
-  __shared__ int rlen[4];
   __shared__ double red[kIntThreads / 32][8];
 
   const int ii = ii0 + blockIdx.x;
@@ -1449,11 +1474,7 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
     mp.key[h] = -1;
     mp.val[h] = make_short4(-1, -1, -1, -1);
   }
-  for (int k = threadIdx.x; k < 8 * rowcap; k += blockDim.x) xacc[k] = 0;
-  if (threadIdx.x < 4) {
-    rbase[threadIdx.x] = soff[NT[threadIdx.x]];
-    rlen[threadIdx.x] = (int)(soff[NT[threadIdx.x] + 1] - soff[NT[threadIdx.x]]);
-  }
+  if (threadIdx.x < 4) rbase[threadIdx.x] = soff[NT[threadIdx.x]];
   __syncthreads();
   for (int a = 0; a < 4; ++a) {
     const long long r0 = soff[NT[a]], r1 = soff[NT[a] + 1];
@@ -1615,7 +1636,7 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const double x = -C * wq * X[a][b];
-          smem_fixed(xacc, a * rowcap + sla[a], NT[a] == NP[b] ? 2.0 * x : x, sc[a]);
+          red_fixed(V, rbase[a] + sla[a], NT[a] == NP[b] ? 2.0 * x : x, sc[a]);
         }
       }
       // T' x T' block C w sum_q S2_q at (M_b, M_c), row min(M_b, M_c)
@@ -1664,7 +1685,7 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
         for (int r = 0; r < 4; ++r)
           if (NT[r] == lo) ra = r;
         const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
-        smem_fixed(xacc, ra * rowcap + v[ra], tot[k], sc[ra]);
+        red_fixed(V, rbase[ra] + v[ra], tot[k], sc[ra]);
       }
     // load vector: f term (reference assembly.cpp:703-709) + constraint terms
     for (int a = 0; a < 4; ++a) {
@@ -1673,14 +1694,6 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
       rhsT[4 * (long long)ii + a] = r + tot[10 + a];
     }
   }
-  __syncthreads();
-  // flush the four pre-reduced rows (exact integer sums) to the node pattern
-  for (int a = 0; a < 4; ++a)
-    for (int k = threadIdx.x; k < rlen[a]; k += blockDim.x) {
-      const unsigned long long hi = xacc[2 * (a * rowcap + k)], lo = xacc[2 * (a * rowcap + k) + 1];
-      if (hi) atomicAdd(V + 2 * (rbase[a] + k), hi);
-      if (lo) atomicAdd(V + 2 * (rbase[a] + k) + 1, lo);
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -2307,8 +2320,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   if (maxlen >= 32768)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
   const int rowcap = std::max(maxlen, 1);
-  const size_t ismem = 8 * (size_t)rowcap * sizeof(unsigned long long) +
-                       (size_t)hcap * (sizeof(int) + sizeof(short4));
+  const size_t ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
   if (ismem > 220 * 1024)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
   CK(cudaFuncSetAttribute(k_integrate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
@@ -2340,8 +2352,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
                                                            S.pair_outer.p);
         S.launches += 2;
-        S.nlist.ensure(4);
-        CK(cudaMemsetAsync(S.nlist.p, 0, 4 * sizeof(int), st));
+        S.nlist.ensure(8);
+        CK(cudaMemsetAsync(S.nlist.p, 0, 8 * sizeof(int), st));
         if (need_gauss) {
           scan64(S, S.gcount.p, true, np, S.goff.p, st);
           ngunits = read_ll(S.goff.p + np, st);
@@ -2360,14 +2372,14 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
           S.upair.ensure(nunits + 1);
           S.uqs.ensure(nunits + 1);
           S.mom.ensure(11 * (size_t)nunits + 1);
-          S.ulist.ensure(2 * (size_t)nunits + 2);
+          S.ulist.ensure(4 * (size_t)(nunits + 1));
           k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p,
                                                       S.uqs.p, S.partner.p, S.ulist.p,
-                                                      S.ulist.p + nunits + 1, S.nlist.p);
+                                                      nunits + 1, S.nlist.p + 4);
           ++S.launches;
         }
-        int nl[4] = {0, 0, 0, 0};
-        CK(cudaMemcpyAsync(nl, S.nlist.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        int nl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaEventRecord(S.ev[6], st));
         if (need_gauss && nl[2] > 0) {
@@ -2382,22 +2394,26 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
               S.partner.p, S.info.p, S.gmom.p, S.counters.p + 1);
           ++S.launches;
         }
-        if (nl[0] > 0) {
-          k_mc<false, false><<<nblk(nl[0], kMcThreads), kMcThreads, 0, st>>>(
-              P0, nunits, S.ulist.p, nl[0], S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
-              S.info.p, S.mom.p, S.counters.p + 1);
-          ++S.launches;
-        }
-        if (nl[1] > 0) {
-          if (S.g_deg <= 2)
-            k_mc<true, true><<<nblk(nl[1], kMcThreads), kMcThreads, 0, st>>>(
-                P0, nunits, S.ulist.p + nunits + 1, nl[1], S.upair.p, S.uqs.p, S.pair_outer.p,
-                S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
-          else
-            k_mc<true, false><<<nblk(nl[1], kMcThreads), kMcThreads, 0, st>>>(
-                P0, nunits, S.ulist.p + nunits + 1, nl[1], S.upair.p, S.uqs.p, S.pair_outer.p,
-                S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
-          ++S.launches;
+        if (need_mc) {
+          const long long ls = nunits + 1;
+          const int* L0 = S.ulist.p;
+          auto launch = [&](auto kern, int kind) {
+            const int n = nl[4 + kind];
+            if (n <= 0) return;
+            kern<<<nblk(n, kMcThreads), kMcThreads, 0, st>>>(
+                P0, nunits, L0 + kind * ls, n, S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
+                S.info.p, S.mom.p, S.counters.p + 1);
+            ++S.launches;
+          };
+          launch(k_mc<false, false, 3>, 1);
+          launch(k_mc<false, false, 1>, 0);
+          if (S.g_deg <= 2) {
+            launch(k_mc<true, true, 3>, 3);
+            launch(k_mc<true, true, 1>, 2);
+          } else {
+            launch(k_mc<true, false, 3>, 3);
+            launch(k_mc<true, false, 1>, 2);
+          }
         }
         CK(cudaEventRecord(S.ev[7], st));
       }
