@@ -748,11 +748,12 @@ __global__ void k_col_count(long long n, const int* cols, int* cnt) {
   if (k < n) atomicAdd(cnt + cols[k], 1);
 }
 
+// warp per row: lanes scatter the row's entries into the transposed rows
 __global__ void k_transpose_fill(int J, const long long* roff, const int* rcols,
                                  const long long* toff, int* cursor, int* tcols) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= J) return;
-  for (long long k = roff[i]; k < roff[i + 1]; ++k) {
+  for (long long k = roff[i] + (threadIdx.x & 31); k < roff[i + 1]; k += 32) {
     const int j = rcols[k];
     tcols[toff[j] + atomicAdd(cursor + j, 1)] = i;
   }
@@ -777,33 +778,83 @@ __global__ void __launch_bounds__(256) k_sort_rows(int J, const long long* off, 
   }
 }
 
-// S(i) = R(i) ∪ R^T(i), both sorted
-template <bool FILL>
-__global__ void k_union(int J, const long long* roff, const int* rcols, const long long* toff,
-                        const int* tcols, int* slen, const long long* soff, int* scols,
-                        int* maxlen) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= J) return;
-  long long a = roff[i];
-  const long long ae = roff[i + 1];
-  long long b = toff[i];
-  const long long be = toff[i + 1];
-  long long o = FILL ? soff[i] : 0;
-  int n = 0;
-  while (a < ae || b < be) {
-    int x;
-    if (b >= be || (a < ae && rcols[a] < tcols[b])) x = rcols[a++];
-    else if (a >= ae || tcols[b] < rcols[a]) x = tcols[b++];
-    else {
-      x = rcols[a++];
-      ++b;
-    }
-    if (FILL) scols[o + n] = x;
-    ++n;
+__device__ __forceinline__ int lower_bound_int(const int* a, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
   }
-  if (!FILL) {
-    slen[i] = n;
-    atomicMax(maxlen, n);
+  return lo;
+}
+
+// S(i) = R(i) ∪ R^T(i), both sorted.  CTA per row: flag the R^T entries absent
+// from R, exclusive-scan the flags in shared memory; then every entry knows its
+// merged position from one binary search (R[a] -> a + #new R^T below it,
+// new R^T[b] -> #R below it + #new R^T before b).
+constexpr int kUnionThreads = 128;
+template <bool FILL>
+__global__ void __launch_bounds__(kUnionThreads) k_union(int J, const long long* roff,
+                                                         const int* rcols, const long long* toff,
+                                                         const int* tcols, int* slen,
+                                                         const long long* soff, int* scols,
+                                                         int* maxlen) {
+  __shared__ int pre[kRowMax + 1];
+  __shared__ int wtot[kUnionThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int i = blockIdx.x; i < J; i += gridDim.x) {
+    const long long a0 = roff[i], b0 = toff[i];
+    const int na = (int)(roff[i + 1] - a0), nb = (int)(toff[i + 1] - b0);
+    if (nb > kRowMax) continue;  // flagged by k_sort_rows
+    const int* R = rcols + a0;
+    const int* RT = tcols + b0;
+    const int c = (nb + kUnionThreads - 1) / kUnionThreads;
+    const int lo = min(t * c, nb), hi = min(lo + c, nb);
+    int cnt = 0;
+    for (int b = lo; b < hi; ++b) {
+      const int x = RT[b];
+      const int l = lower_bound_int(R, na, x);
+      const int f = (l < na && R[l] == x) ? 0 : 1;
+      pre[b] = f;
+      cnt += f;
+    }
+    int inc = cnt;
+    for (int sh = 1; sh < 32; sh <<= 1) {
+      const int y = __shfl_up_sync(FULLMASK, inc, sh);
+      if (lane >= sh) inc += y;
+    }
+    if (lane == 31) wtot[wid] = inc;
+    __syncthreads();
+    int run = inc - cnt, total = 0;
+    for (int w = 0; w < kUnionThreads / 32; ++w) {
+      if (w < wid) run += wtot[w];
+      total += wtot[w];
+    }
+    for (int b = lo; b < hi; ++b) {
+      const int f = pre[b];
+      pre[b] = run;
+      run += f;
+    }
+    if (t == 0) pre[nb] = total;
+    __syncthreads();
+    if (!FILL) {
+      if (t == 0) {
+        slen[i] = na + total;
+        atomicMax(maxlen, na + total);
+      }
+    } else {
+      const long long o = soff[i];
+      for (int a = t; a < na; a += kUnionThreads) {
+        const int x = R[a];
+        scols[o + a + pre[lower_bound_int(RT, nb, x)]] = x;
+      }
+      for (int b = t; b < nb; b += kUnionThreads)
+        if (pre[b + 1] != pre[b]) {
+          const int x = RT[b];
+          scols[o + lower_bound_int(R, na, x) + pre[b]] = x;
+        }
+    }
+    __syncthreads();
   }
 }
 
@@ -818,13 +869,13 @@ __device__ __forceinline__ long long find_slot(const long long* soff, const int*
   return (lo <= hi && scols[lo] == j) ? lo : -1;
 }
 
+// warp per row
 __global__ void k_mirror(int J, const long long* soff, const int* scols, long long* mirror,
                          int* ovf) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= J) return;
-  for (long long k = soff[i]; k < soff[i + 1]; ++k) {
-    const int j = scols[k];
-    const long long m = find_slot(soff, scols, j, i);
+  for (long long k = soff[i] + (threadIdx.x & 31); k < soff[i + 1]; k += 32) {
+    const long long m = find_slot(soff, scols, scols[k], i);
     if (m < 0) *ovf = 2;
     mirror[k] = m;
   }
@@ -848,25 +899,29 @@ __global__ void k_edge_slots(const long long* soff, const int* scols, long long*
     }
 }
 
-// output pattern: rows = unknown nodes (dof order), columns = unknown nodes
+// output pattern: rows = unknown nodes (dof order), columns = unknown nodes;
+// warp per row, ballot compaction keeps the column order
 template <bool FILL>
 __global__ void k_outpat(const long long* soff, const int* scols, int* olen,
                          const long long* ooff, int* ocols, long long* omap, const int* dof_node) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (d >= cD.unknowns) return;
   const int i = dof_node[d];
   int n = 0;
   const long long o = FILL ? ooff[d] : 0;
-  for (long long k = soff[i]; k < soff[i + 1]; ++k) {
-    const int dj = cD.dof[scols[k]];
-    if (dj < 0) continue;
-    if (FILL) {
-      ocols[o + n] = dj;
-      omap[o + n] = k;
+  for (long long base = soff[i]; base < soff[i + 1]; base += 32) {
+    const long long k = base + lane;
+    const int dj = k < soff[i + 1] ? cD.dof[scols[k]] : -1;
+    const unsigned m = __ballot_sync(FULLMASK, dj >= 0);
+    if (FILL && dj >= 0) {
+      const long long pos = o + n + __popc(m & ((1u << lane) - 1));
+      ocols[pos] = dj;
+      omap[pos] = k;
     }
-    ++n;
+    n += __popc(m);
   }
-  if (!FILL) olen[d] = n;
+  if (!FILL && lane == 0) olen[d] = n;
 }
 
 // ---------------------------------------------------------------------------
@@ -1106,24 +1161,6 @@ __device__ __forceinline__ bool mc_point_fast(uint32_t w0, uint32_t w1, uint32_t
   rz = fma(u2, f.e2[2], fma(u1, f.e1[2], fma(u0, f.e0[2], f.p[2])));
   return fma(rz, rz, fma(ry, ry, rx * rx)) < dd;
 }
-
-struct PickPiece {  // selects the want-th kept piece
-  int want, seen = 0;
-  bool found = false;
-  Vd a, b, c, d;
-  double vol;
-  __device__ __forceinline__ void operator()(Vd A, Vd B, Vd C, Vd D, double v) {
-    if (seen == want) {
-      a = A;
-      b = B;
-      c = C;
-      d = D;
-      vol = v;
-      found = true;
-    }
-    ++seen;
-  }
-};
 
 // Monte Carlo: one thread per unit = one sub-simplex of one cap item, M samples
 // of the mode-P stream (include/nlfem_mc_stream.h).  Writes the weighted
@@ -1441,15 +1478,12 @@ struct SlotMap {
 // units) come precomputed.  A shared-memory map from node id to its slots in the
 // four T-node rows of the node pattern locates the T x T' block entries; both
 // blocks are added as two-word fixed point with integer atomics.
-#ifndef NLFEM_INT_THREADS
-#define NLFEM_INT_THREADS 256
-#endif
 #ifndef NLFEM_INT_MINBLOCKS
 #define NLFEM_INT_MINBLOCKS 2
 #endif
-constexpr int kIntThreads = NLFEM_INT_THREADS;
 
-__global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
+template <int NTHR>
+__global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 * NLFEM_INT_MINBLOCKS)) k_integrate(
     int ii0, const long long* pair_off, const int* partner, const unsigned* info,
     const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
     double* rhsT, const long long* uoff, const double* mom, long long nunits,
@@ -1461,7 +1495,7 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
   mp.val = reinterpret_cast<short4*>(mp.key + hcap);
   mp.mask = hcap - 1;
   __shared__ long long rbase[4];
-  __shared__ double red[kIntThreads / 32][8];
+  __shared__ double red[NTHR / 32][8];
 
   const int ii = ii0 + blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1669,7 +1703,7 @@ __global__ void __launch_bounds__(kIntThreads, NLFEM_INT_MINBLOCKS) k_integrate(
     double acc[8];
     for (int k = 0; k < 8; ++k) {
       acc[k] = 0;
-      for (int w = 0; w < kIntThreads / 32; ++w) acc[k] += red[w][k];
+      for (int w = 0; w < NTHR / 32; ++w) acc[k] += red[w][k];
     }
     double tot[14];
     for (int k = 0; k < 14; ++k) tot[k] = 0;
@@ -2258,7 +2292,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   scan64(S, S.tcnt.p, true, J, S.toff.p, st);
   S.cursor.ensure(J);
   CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
-  k_transpose_fill<<<nblk(J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.cursor.p,
+  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.cursor.p,
                                                  S.tcols.p);
   CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(kRowMax * sizeof(int))));
@@ -2269,18 +2303,18 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   S.soff.ensure(J + 1);
   CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
   int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
-  k_union<false><<<nblk(J, 128), 128, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+  k_union<false><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
                                                S.slen.p, nullptr, nullptr, d_maxlen);
   ++S.launches;
   scan64(S, S.slen.p, true, J, S.soff.p, st);
   S.nnz_s = read_ll(S.soff.p + J, st);
   S.scols.ensure(S.nnz_s);
-  k_union<true><<<nblk(J, 128), 128, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+  k_union<true><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
                                               nullptr, S.soff.p, S.scols.p, nullptr);
   int maxlen = 0;
   CK(cudaMemcpyAsync(&maxlen, d_maxlen, sizeof(int), cudaMemcpyDeviceToHost, st));
   S.mirror.ensure(S.nnz_s);
-  k_mirror<<<nblk(J, 128), 128, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
+  k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
   S.eslot.ensure(10 * (size_t)KI);
   k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p);
   S.launches += 3;
@@ -2288,14 +2322,14 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const int U = S.unknowns;
   S.olen.ensure(U);
   S.ooff.ensure(U + 1);
-  k_outpat<false><<<nblk(U, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr, nullptr,
+  k_outpat<false><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr, nullptr,
                                                 nullptr, S.dof_node.p);
   ++S.launches;
   scan64(S, S.olen.p, true, U, S.ooff.p, st);
   S.nnz_out = read_ll(S.ooff.p + U, st);
   S.ocols.ensure(S.nnz_out);
   S.omap.ensure(S.nnz_out);
-  k_outpat<true><<<nblk(U, 128), 128, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p, S.ocols.p,
+  k_outpat<true><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p, S.ocols.p,
                                                S.omap.p, S.dof_node.p);
   ++S.launches;
   int ovf = 0;
@@ -2323,7 +2357,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const size_t ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
   if (ismem > 220 * 1024)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
-  CK(cudaFuncSetAttribute(k_integrate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
+  CK(cudaFuncSetAttribute(k_integrate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
+  CK(cudaFuncSetAttribute(k_integrate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   const bool need_gauss = D.strategy != NLFEM_STRATEGY_BARYCENTER;
   float mc_ms = 0;
@@ -2417,10 +2452,18 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         }
         CK(cudaEventRecord(S.ev[7], st));
       }
-      k_integrate<<<ii1 - ii0, kIntThreads, ismem, st>>>(
-          ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
-          S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
-          need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
+      // block size from the mean number of element pairs per outer element
+      const long long ppe = (poff[ii1] - poff[ii0]) / std::max(1, ii1 - ii0);
+      if (ppe < 768)
+        k_integrate<128><<<ii1 - ii0, 128, ismem, st>>>(
+            ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
+            S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
+            need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
+      else
+        k_integrate<256><<<ii1 - ii0, 256, ismem, st>>>(
+            ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
+            S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
+            need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
       ++S.launches;
       if (need_gauss) {
         CK(cudaEventSynchronize(S.ev[7]));
