@@ -1149,18 +1149,41 @@ __device__ __forceinline__ double u32_plus_half(uint32_t w) {
 // nlfem_mc_point with the frame pre-scaled by 2^-32 (E' = 2^-32 E): since
 // u E = (w + 1/2) 2^-32 E = (w + 1/2) E' exactly, fma(u, E, p) == fma(w + 1/2, E', p)
 // bit for bit, so decisions and r equal include/nlfem_mc_stream.h's.
-__device__ __forceinline__ bool mc_point_fast(uint32_t w0, uint32_t w1, uint32_t w2,
-                                              const nlfem_mc_frame& f, double dd, double& rx,
-                                              double& ry, double& rz) {
-  const uint32_t lo = min(w0, w1), hi = max(w0, w1);
-  const uint32_t s0 = min(lo, w2), t = max(lo, w2);
-  const uint32_t s1 = min(hi, t), s2 = max(hi, t);
+__device__ __forceinline__ double mc_point_r2(uint32_t w0, uint32_t w1, uint32_t w2,
+                                               const nlfem_mc_frame& f, double& rx, double& ry,
+                                               double& rz) {
+  // sorted words: 3-input min/max (VIMNMX3) and the median from the sum, exact
+  // in u32 wrap-around arithmetic
+  const uint32_t s0 = min(min(w0, w1), w2), s2 = max(max(w0, w1), w2);
+  const uint32_t s1 = w0 + w1 + w2 - s0 - s2;
   const double u0 = u32_plus_half(s0), u1 = u32_plus_half(s1), u2 = u32_plus_half(s2);
   rx = fma(u2, f.e2[0], fma(u1, f.e1[0], fma(u0, f.e0[0], f.p[0])));
   ry = fma(u2, f.e2[1], fma(u1, f.e1[1], fma(u0, f.e0[1], f.p[1])));
   rz = fma(u2, f.e2[2], fma(u1, f.e1[2], fma(u0, f.e0[2], f.p[2])));
-  return fma(rz, rz, fma(ry, ry, rx * rx)) < dd;
+  return fma(rz, rz, fma(ry, ry, rx * rx));
 }
+
+// hit test r2 < dd and, on a hit, n += 1, t1 += r, t2 += r r^T (upper, 6).
+// A plain branch: ptxas lowers predicated FP64 ops to FSEL pairs, which cost
+// more than the (almost always warp-uniform-taken) branch.
+struct HitMoments {
+  unsigned n = 0;
+  double t1x = 0, t1y = 0, t1z = 0, t2[6] = {0, 0, 0, 0, 0, 0};
+  __device__ __forceinline__ void add(double r2, double dd, double rx, double ry, double rz) {
+    if (r2 < dd) {
+      ++n;
+      t1x += rx;
+      t1y += ry;
+      t1z += rz;
+      t2[0] = fma(rx, rx, t2[0]);
+      t2[1] = fma(rx, ry, t2[1]);
+      t2[2] = fma(rx, rz, t2[2]);
+      t2[3] = fma(ry, ry, t2[3]);
+      t2[4] = fma(ry, rz, t2[4]);
+      t2[5] = fma(rz, rz, t2[5]);
+    }
+  }
+};
 
 // Monte Carlo: one thread per unit = one sub-simplex of one cap item, M samples
 // of the mode-P stream (include/nlfem_mc_stream.h).  Writes the weighted
@@ -1201,7 +1224,7 @@ __device__ __forceinline__ void poly2_taylor(const Poly& P, Vd x, double& g0, do
 }
 
 #ifndef NLFEM_MC_MINBLOCKS
-#define NLFEM_MC_MINBLOCKS 5
+#define NLFEM_MC_MINBLOCKS 4
 #endif
 // CONS: constraint parent (accumulates sum g(y) instead of basis moments).
 // G2: g has total degree <= 2, so sum_hits g(x_q + r) follows exactly from the
@@ -1244,6 +1267,19 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       const int m = __popc(c & 15);
       led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
     }
+    // three-piece items: park the six straddle points in shared memory (column
+    // per thread) so the sampling loop does not carry them in registers
+    __shared__ double sP[NU == 3 ? 18 : 1][kMcThreads];
+    if (NU == 3) {
+      const Vd P6[6] = {st.A0, st.A1, st.A2, st.B0, st.B1, st.B2};
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        sP[3 * k][threadIdx.x] = P6[k].x;
+        sP[3 * k + 1][threadIdx.x] = P6[k].y;
+        sP[3 * k + 2][threadIdx.x] = P6[k].z;
+      }
+    }
+    const Vd v0P = vP[0];
     const double tau = c == kOutCap ? -1.0 : cD.tau[Tp];
     const int M = cD.mc;
     const double dd = cD.dd;
@@ -1257,7 +1293,16 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       double vol = 0;
       bool use = k < npieces;
       if (use) {
-        straddle_piece(st, k, pa, pb, pc, pd);
+        if (NU == 3) {
+          Vd* pv[4] = {&pa, &pb, &pc, &pd};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 3 * (k + j);
+            *pv[j] = {sP[r][threadIdx.x], sP[r + 1][threadIdx.x], sP[r + 2][threadIdx.x]};
+          }
+        } else {
+          straddle_piece(st, k, pa, pb, pc, pd);
+        }
         vol = tet_volume(pa, pb, pc, pd);
         use = vol > tau;  // push_piece volume floor (ball_approx.cpp:141)
       }
@@ -1280,40 +1325,44 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         fs.e1[a] = fr.e1[a] * 0x1p-32;
         fs.e2[a] = fr.e2[a] * 0x1p-32;
       }
-      unsigned nh = 0;
       // interior: sums of r and r r^T over hits, r = y - x_q; constraint: sum g(y)
-      double t1x = 0, t1y = 0, t1z = 0, t2[6] = {0, 0, 0, 0, 0, 0}, ng = 0;
-      auto sample = [&](uint32_t a, uint32_t b, uint32_t cc, bool valid) {
+      HitMoments hm;
+      unsigned ngh = 0;
+      double ng = 0;
+      auto sample = [&](uint32_t a, uint32_t b, uint32_t cc, double ddv) {
         double rx, ry, rz;
-        const bool hit = mc_point_fast(a, b, cc, fs, dd, rx, ry, rz) && valid;
-        nh += hit;
+        const double r2 = mc_point_r2(a, b, cc, fs, rx, ry, rz);
         if (CONS && !G2) {
-          if (hit) ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
+          if (r2 < ddv) {
+            ++ngh;
+            ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
+          }
         } else {
-          const double hx = hit ? rx : 0.0, hy = hit ? ry : 0.0, hz = hit ? rz : 0.0;
-          t1x += hx;
-          t1y += hy;
-          t1z += hz;
-          t2[0] = fma(hx, rx, t2[0]);
-          t2[1] = fma(hx, ry, t2[1]);
-          t2[2] = fma(hx, rz, t2[2]);
-          t2[3] = fma(hy, ry, t2[3]);
-          t2[4] = fma(hy, rz, t2[4]);
-          t2[5] = fma(hz, rz, t2[5]);
+          hm.add(r2, ddv, rx, ry, rz);
         }
       };
-      const int nb = (M + 3) >> 2, full = M >> 2;
+      const int full = M >> 2;
 #pragma unroll 1
-      for (int j = 0; j < nb; ++j) {
+      for (int j = 0; j < full; ++j) {
         // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
         uint32_t A[4], B[4], Cw[4];
         philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, k0, k1, A, B, Cw);
-        const bool tail = j >= full;
-        sample(A[0], A[1], A[2], true);
-        sample(A[3], B[0], B[1], !tail || 4 * j + 1 < M);
-        sample(B[2], B[3], Cw[0], !tail || 4 * j + 2 < M);
-        sample(Cw[1], Cw[2], Cw[3], !tail || 4 * j + 3 < M);
+        sample(A[0], A[1], A[2], dd);
+        sample(A[3], B[0], B[1], dd);
+        sample(B[2], B[3], Cw[0], dd);
+        sample(Cw[1], Cw[2], Cw[3], dd);
       }
+      if (M & 3) {  // partial last block: samples past M are drawn but never hit
+        uint32_t A[4], B[4], Cw[4];
+        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)full, k0, k1, A, B, Cw);
+        const int rem = M & 3;
+        sample(A[0], A[1], A[2], dd);
+        sample(A[3], B[0], B[1], rem > 1 ? dd : -1.0);
+        sample(B[2], B[3], Cw[0], rem > 2 ? dd : -1.0);
+      }
+      const unsigned nh = (CONS && !G2) ? ngh : hm.n;
+      const double t1x = hm.t1x, t1y = hm.t1y, t1z = hm.t1z;
+      const double* t2 = hm.t2;
       double S0 = w * nh, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
       if (CONS && G2) {
         // sum over hits of g(x_q + r) = n g + grad g . sum r + 1/2 sum H_ab r_a r_b
@@ -1325,7 +1374,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         sg = w * ng;
       } else {
         // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
-        const double c0x = xq.x - vP[0].x, c0y = xq.y - vP[0].y, c0z = xq.z - vP[0].z;
+        const double c0x = xq.x - v0P.x, c0y = xq.y - v0P.y, c0z = xq.z - v0P.z;
         const double n = (double)nh;
         m1x = w * (t1x + n * c0x);
         m1y = w * (t1y + n * c0y);
