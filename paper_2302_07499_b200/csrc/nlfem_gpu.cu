@@ -1185,10 +1185,11 @@ struct HitMoments {
   }
 };
 
-// Monte Carlo: one thread per unit = one sub-simplex of one cap item, M samples
-// of the mode-P stream (include/nlfem_mc_stream.h).  Writes the weighted
-// Cartesian moments about v0(T'): S0, sum w r, sum w r r^T (6), and sum w g(y)
-// for constraint parents, SoA [11][nunits].
+// Monte Carlo: one thread per cap item; each kept sub-simplex (piece) gets M
+// samples of the mode-P stream (include/nlfem_mc_stream.h).  Writes one record
+// per item, at the item's first unit slot, SoA [10][nunits]: the weighted
+// S0, then sum w g(y) for constraint parents, or the Cartesian moments about
+// v0(T') sum w r' (3) and sum w r' r'^T (6) for interior parents.
 constexpr int kMcThreads = 128;
 
 // value, gradient and Hessian at x of a polynomial of total degree <= 2
@@ -1280,6 +1281,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       }
     }
     const Vd v0P = vP[0];
+    __shared__ double sAcc[CONS ? 2 : 10][kMcThreads];
     const double tau = c == kOutCap ? -1.0 : cD.tau[Tp];
     const int M = cD.mc;
     const double dd = cD.dd;
@@ -1389,18 +1391,25 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       draws += (unsigned long long)M;
       hits += nh;
       led += 25ull + 35ull * (unsigned long long)M + (CONS ? 12ull : 62ull) * nh;
-      mom[u] = S0;
-      mom[nunits + u] = m1x;
-      mom[2 * nunits + u] = m1y;
-      mom[3 * nunits + u] = m1z;
+      // item totals over its kept pieces, summed in piece order from 0 (the
+      // order the per-piece values were once added in by the combine)
+      const double vals[10] = {S0, CONS ? sg : m1x, m1y, m1z, m2[0], m2[1], m2[2], m2[3], m2[4], m2[5]};
+      constexpr int nv = CONS ? 2 : 10;
 #pragma unroll
-      for (int kk = 0; kk < 6; ++kk) mom[(4 + kk) * nunits + u] = m2[kk];
-      mom[10 * nunits + u] = sg;
+      for (int kk = 0; kk < nv; ++kk) {
+        if (NU == 1) sAcc[kk][threadIdx.x] = vals[kk];
+        else sAcc[kk][threadIdx.x] = (u == u0 ? 0.0 : sAcc[kk][threadIdx.x]) + vals[kk];
+      }
     }
-    // unit slots of dropped pieces stay zero
-    for (int j = kept; j < NU; ++j)
+    // one record per item at its first unit slot: S0, then sum g (constraint
+    // parents) or sum r' and sum r' r'^T (6) about v0(T')
+    constexpr int nv = CONS ? 2 : 10;
+    if (kept == 0) {
 #pragma unroll
-      for (int kk = 0; kk < 11; ++kk) mom[kk * nunits + u0 + j] = 0.0;
+      for (int kk = 0; kk < nv; ++kk) sAcc[kk][threadIdx.x] = 0.0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < nv; ++kk) mom[(long long)kk * nunits + u0] = sAcc[kk][threadIdx.x];
   }
   // statistics
   for (int sh = 16; sh > 0; sh >>= 1) {
@@ -1641,20 +1650,19 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
       }
       // Monte Carlo units of this item, in sub-simplex order
       if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
+        // the item's record (k_mc sums its pieces) sits at its first unit slot
         const int nu = c == kOutCap ? 1 : outer_units((int)(c & 15));
-        double n0 = 0, g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll 1
-        for (int sb = 0; sb < nu; ++sb, ++u) {
-          n0 += mom[u];
-          if (constr) {
-            g0 += mom[10 * nunits + u];
-          } else {
+        double g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
+        const double n0 = mom[u];
+        if (constr) {
+          g0 = mom[nunits + u];
+        } else {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) m1[k] += mom[(1 + k) * nunits + u];
+          for (int k = 0; k < 3; ++k) m1[k] = mom[(1 + k) * nunits + u];
 #pragma unroll
-            for (int k = 0; k < 6; ++k) m2[k] += mom[(4 + k) * nunits + u];
-          }
+          for (int k = 0; k < 6; ++k) m2[k] = mom[(4 + k) * nunits + u];
         }
+        u += nu;
         S0 += n0;
         if (constr) {
           Sg += g0;
@@ -1748,33 +1756,34 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
   for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
   if (lane == 0 && led) atomicAdd(stats + 2, led);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // threads 0..9: the ten D_T entries (a <= b); threads 10..13: rhs of node a
+  const int t = threadIdx.x;
+  if (t < 14) {
     double acc[8];
+#pragma unroll
     for (int k = 0; k < 8; ++k) {
       acc[k] = 0;
       for (int w = 0; w < NTHR / 32; ++w) acc[k] += red[w][k];
     }
-    double tot[14];
-    for (int k = 0; k < 14; ++k) tot[k] = 0;
-    for (int a = 0; a < 4; ++a) tot[10 + a] = 2.0 * C * wq * acc[4 + a];
-    for (int q = 0; q < 4; ++q)
-      for (int a = 0; a < 4; ++a)
-        for (int b = a; b < 4; ++b) tot[s2i(a, b)] += C * wq * acc[q] * qbary(q, a) * qbary(q, b);
-    int k = 0;
-    for (int a = 0; a < 4; ++a)
-      for (int b = a; b < 4; ++b, ++k) {
-        const int lo = min(NT[a], NT[b]), hi = max(NT[a], NT[b]);
-        int ra = 0;
-        for (int r = 0; r < 4; ++r)
-          if (NT[r] == lo) ra = r;
-        const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
-        red_fixed(V, rbase[ra] + v[ra], tot[k], sc[ra]);
-      }
-    // load vector: f term (reference assembly.cpp:703-709) + constraint terms
-    for (int a = 0; a < 4; ++a) {
+    if (t < 10) {
+      const int a = t < 4 ? 0 : (t < 7 ? 1 : (t < 9 ? 2 : 3));
+      const int b = a + t - (a == 0 ? 0 : (a == 1 ? 4 : (a == 2 ? 7 : 9)));
+      double tot = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tot += C * wq * acc[q] * qbary(q, a) * qbary(q, b);
+      const int lo = min(NT[a], NT[b]), hi = max(NT[a], NT[b]);
+      int ra = 0;
+      for (int r = 0; r < 4; ++r)
+        if (NT[r] == lo) ra = r;
+      const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
+      red_fixed(V, rbase[ra] + v[ra], tot, sc[ra]);
+    } else {
+      // load vector: f term (reference assembly.cpp:703-709) + constraint terms
+      const int a = t - 10;
       double r = 0;
       for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, quad_point(vT, q));
-      rhsT[4 * (long long)ii + a] = r + tot[10 + a];
+      const double ca = a == 0 ? acc[4] : (a == 1 ? acc[5] : (a == 2 ? acc[6] : acc[7]));
+      rhsT[4 * (long long)ii + a] = r + 2.0 * C * wq * ca;
     }
   }
 }
@@ -2455,7 +2464,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
           nunits = read_ll(S.uoff.p + np, st);
           S.upair.ensure(nunits + 1);
           S.uqs.ensure(nunits + 1);
-          S.mom.ensure(11 * (size_t)nunits + 1);
+          S.mom.ensure(10 * (size_t)nunits + 1);
           S.ulist.ensure(4 * (size_t)(nunits + 1));
           k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p,
                                                       S.uqs.p, S.partner.p, S.ulist.p,
