@@ -24,13 +24,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "geom.cuh"
@@ -1187,10 +1190,12 @@ struct HitMoments {
 
 // Monte Carlo: one thread per cap item; each kept sub-simplex (piece) gets M
 // samples of the mode-P stream (include/nlfem_mc_stream.h).  Writes one record
-// per item, at the item's first unit slot, SoA [10][nunits]: the weighted
+// per item, at the item's first unit slot (record of kMomStride doubles): the weighted
 // S0, then sum w g(y) for constraint parents, or the Cartesian moments about
 // v0(T') sum w r' (3) and sum w r' r'^T (6) for interior parents.
 constexpr int kMcThreads = 128;
+constexpr long long kMomStride = 10;   // doubles per MC item record (80 B)
+constexpr long long kGmomStride = 16;  // doubles per Gauss unit record (128 B)
 
 // value, gradient and Hessian at x of a polynomial of total degree <= 2
 // (only such g take the moment path in k_mc<true, true>)
@@ -1408,8 +1413,10 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
 #pragma unroll
       for (int kk = 0; kk < nv; ++kk) sAcc[kk][threadIdx.x] = 0.0;
     }
+    double2* rec = reinterpret_cast<double2*>(mom + kMomStride * u0);
 #pragma unroll
-    for (int kk = 0; kk < nv; ++kk) mom[(long long)kk * nunits + u0] = sAcc[kk][threadIdx.x];
+    for (int kk = 0; kk < nv; kk += 2)
+      rec[kk / 2] = make_double2(sAcc[kk][threadIdx.x], sAcc[kk + 1][threadIdx.x]);
   }
   // statistics
   for (int sh = 16; sh > 0; sh >>= 1) {
@@ -1505,14 +1512,17 @@ __global__ void __launch_bounds__(kGaussThreads, 4) k_gauss(long long p0, long l
     const int m = __popc(mask);
     led = 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
           (unsigned long long)kept * (CONS ? 160 : 360);
-    gmom[u] = S0;
+    // one 128-byte record per unit: S0, then Sg (constraint) or S1 (4), S2 (10)
+    double2* rec = reinterpret_cast<double2*>(gmom + kGmomStride * u);
     if (CONS) {
-      gmom[n + u] = Sg;
+      rec[0] = make_double2(S0, Sg);
     } else {
+      rec[0] = make_double2(S0, S1[0]);
+      rec[1] = make_double2(S1[1], S1[2]);
+      rec[2] = make_double2(S1[3], S2[0]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) gmom[(1 + i) * n + u] = S1[i];
-#pragma unroll
-      for (int k = 0; k < 10; ++k) gmom[(5 + k) * n + u] = S2[k];
+      for (int k = 0; k < 4; ++k) rec[3 + k] = make_double2(S2[1 + 2 * k], S2[2 + 2 * k]);
+      rec[7] = make_double2(S2[9], 0.0);
     }
   }
   for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
@@ -1637,14 +1647,25 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
           }
         }
       } else if (c & kStraddle) {
-        S0 = gmom[gu];
+        const double2* rec = reinterpret_cast<const double2*>(gmom + kGmomStride * gu);
+        const double2 r0 = rec[0];
+        S0 = r0.x;
         if (constr) {
-          Sg = gmom[ngunits + gu];
+          Sg = r0.y;
         } else {
+          const double2 r1 = rec[1], r2 = rec[2], r7 = rec[7];
+          S1[0] = r0.y;
+          S1[1] = r1.x;
+          S1[2] = r1.y;
+          S1[3] = r2.x;
+          S2[0] += r2.y;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) S1[i] = gmom[(1 + i) * ngunits + gu];
-#pragma unroll
-          for (int k = 0; k < 10; ++k) S2[k] += gmom[(5 + k) * ngunits + gu];
+          for (int k = 0; k < 4; ++k) {
+            const double2 r = rec[3 + k];
+            S2[1 + 2 * k] += r.x;
+            S2[2 + 2 * k] += r.y;
+          }
+          S2[9] += r7.x;
         }
         ++gu;
       }
@@ -1653,14 +1674,22 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
         // the item's record (k_mc sums its pieces) sits at its first unit slot
         const int nu = c == kOutCap ? 1 : outer_units((int)(c & 15));
         double g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
-        const double n0 = mom[u];
+        const double2* rec = reinterpret_cast<const double2*>(mom + kMomStride * u);
+        const double2 r0 = rec[0];
+        const double n0 = r0.x;
         if (constr) {
-          g0 = mom[nunits + u];
+          g0 = r0.y;
         } else {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) m1[k] = mom[(1 + k) * nunits + u];
-#pragma unroll
-          for (int k = 0; k < 6; ++k) m2[k] = mom[(4 + k) * nunits + u];
+          const double2 r1 = rec[1], r2 = rec[2], r3 = rec[3], r4 = rec[4];
+          m1[0] = r0.y;
+          m1[1] = r1.x;
+          m1[2] = r1.y;
+          m2[0] = r2.x;
+          m2[1] = r2.y;
+          m2[2] = r3.x;
+          m2[3] = r3.y;
+          m2[4] = r4.x;
+          m2[5] = r4.y;
         }
         u += nu;
         S0 += n0;
@@ -1902,7 +1931,7 @@ struct nlfem_gpu_session {
   DBuf<double4> erec;
   // grid / incidence
   DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
-  DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp;
+  DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp, scan_tmp2;
   DBuf<int> cell_start, ni_off;
   DBuf<double> scale, iscale;
   // pairs
@@ -1930,24 +1959,27 @@ struct nlfem_gpu_session {
   DBuf<double> rhsT, values, rhs;
   // results of the last run
   long long npairs = 0, nnz_s = 0, nnz_out = 0;
-  long long launches = 0;
+  std::atomic<long long> launches{0};
   unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0;
   cudaStream_t stream = nullptr;
-  std::vector<cudaEvent_t> ev;
+  // the node pattern is built on a second, higher-priority stream from its own
+  // host thread, concurrently with the units / Monte Carlo work on `stream`
+  cudaStream_t stream2 = nullptr;
+  std::vector<cudaEvent_t> ev;  // 0..7 phases on stream; 8, 9 pattern on stream2
 };
 
 namespace {
 
 // exclusive scan of n counts into out[0..n], out[n] = total; the block sums
 // of every recursion level live in persistent session scratch (no allocation)
-void scan64_level(nlfem_gpu_session& S, const void* in, bool in_is_int, long long n,
-                  long long* out, cudaStream_t st, size_t scratch_off) {
+void scan64_level(nlfem_gpu_session& S, long long* scratch, const void* in, bool in_is_int,
+                  long long n, long long* out, cudaStream_t st, size_t scratch_off) {
   const long long nb = (n + kScanBlock - 1) / kScanBlock;
   if (n <= 0) {
     CK(cudaMemsetAsync(out, 0, sizeof(long long), st));
     return;
   }
-  long long* sums = S.scan_tmp.p + scratch_off;
+  long long* sums = scratch + scratch_off;
   long long* sums_scan = sums + nb + 1;
   if (in_is_int)
     k_scan_block<int><<<(unsigned)nb, kScanBlock, 0, st>>>((const int*)in, out, sums, n);
@@ -1955,7 +1987,7 @@ void scan64_level(nlfem_gpu_session& S, const void* in, bool in_is_int, long lon
     k_scan_block<long long><<<(unsigned)nb, kScanBlock, 0, st>>>((const long long*)in, out, sums, n);
   ++S.launches;
   if (nb > 1) {
-    scan64_level(S, sums, false, nb, sums_scan, st, scratch_off + 2 * (size_t)(nb + 1));
+    scan64_level(S, scratch, sums, false, nb, sums_scan, st, scratch_off + 2 * (size_t)(nb + 1));
     k_scan_add<<<(unsigned)nb, kScanBlock, 0, st>>>(out, sums_scan, n);
     ++S.launches;
     CK(cudaMemcpyAsync(out + n, sums_scan + nb, sizeof(long long), cudaMemcpyDeviceToDevice, st));
@@ -1969,11 +2001,12 @@ void scan64(nlfem_gpu_session& S, const void* in, bool in_is_int, long long n, l
   size_t need = 0;
   for (long long m = n; m > 1; m = (m + kScanBlock - 1) / kScanBlock)
     need += 2 * (size_t)((m + kScanBlock - 1) / kScanBlock + 1);
-  if (S.scan_tmp.n < need + 16) {
+  DBuf<long long>& tmp = (st == S.stream2) ? S.scan_tmp2 : S.scan_tmp;  // scratch per stream
+  if (tmp.n < need + 16) {
     CK(cudaStreamSynchronize(st));  // buffer may be in use by queued work
-    S.scan_tmp.ensure(need + 16);
+    tmp.ensure(need + 16);
   }
-  scan64_level(S, in, in_is_int, n, out, st, 0);
+  scan64_level(S, tmp.p, in, in_is_int, n, out, st, 0);
 }
 
 long long read_ll(const long long* d, cudaStream_t st) {
@@ -2033,9 +2066,12 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, S.device));
   if (major < 10)
     throw Fail{NLFEM_GPU_ENODEVICE, "device is not sm_100 class (built for sm_100a only)"};
-  if (!S.stream) {  // a reused workspace keeps its stream, events and buffers
+  if (!S.stream) {  // a reused workspace keeps its streams, events and buffers
     CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 8; ++i) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&S.stream2, cudaStreamNonBlocking, hi));
+    for (int i = 0; i < 10; ++i) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       S.ev.push_back(e);
@@ -2218,6 +2254,84 @@ void run_finalize(nlfem_gpu_session& S, int r0, int r1) {
   }
 }
 
+// K5: the node pattern S (sorted rows), its mirror / edge slots and the output
+// pattern.  Runs on its own stream; host syncs here block only the caller.
+void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
+  const int KI = S.KI, J = S.J;
+  const size_t rows_smem = (kHE + kHN + kRowMax) * sizeof(int);
+  CK(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  S.rlen.ensure(J);
+  S.roff.ensure(J + 1);
+  const unsigned rgrid = (unsigned)std::min<long long>(J, 148LL * 16);
+  k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
+                                               nullptr, S.ovf.p);
+  ++S.launches;
+  scan64(S, S.rlen.p, true, J, S.roff.p, st);
+  const long long nR = read_ll(S.roff.p + J, st);
+  S.rcols.ensure(nR);
+  k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
+                                              S.rcols.p, S.ovf.p);
+  ++S.launches;
+  // transpose
+  S.tcnt.ensure(J);
+  S.toff.ensure(J + 1);
+  S.tcols.ensure(nR);
+  CK(cudaMemsetAsync(S.tcnt.p, 0, J * sizeof(int), st));
+  k_col_count<<<nblk(nR, 256), 256, 0, st>>>(nR, S.rcols.p, S.tcnt.p);
+  ++S.launches;
+  scan64(S, S.tcnt.p, true, J, S.toff.p, st);
+  S.cursor.ensure(J);
+  CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
+  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.cursor.p,
+                                                 S.tcols.p);
+  CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(kRowMax * sizeof(int))));
+  k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p);
+  S.launches += 2;
+  // union
+  S.slen.ensure(J);
+  S.soff.ensure(J + 1);
+  CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
+  int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
+  k_union<false><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+                                               S.slen.p, nullptr, nullptr, d_maxlen);
+  ++S.launches;
+  scan64(S, S.slen.p, true, J, S.soff.p, st);
+  S.nnz_s = read_ll(S.soff.p + J, st);
+  S.scols.ensure(S.nnz_s);
+  k_union<true><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+                                              nullptr, S.soff.p, S.scols.p, nullptr);
+  maxlen = 0;
+  CK(cudaMemcpyAsync(&maxlen, d_maxlen, sizeof(int), cudaMemcpyDeviceToHost, st));
+  S.mirror.ensure(S.nnz_s);
+  k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
+  S.eslot.ensure(10 * (size_t)KI);
+  k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p);
+  S.launches += 3;
+  // output pattern
+  const int U = S.unknowns;
+  S.olen.ensure(U);
+  S.ooff.ensure(U + 1);
+  k_outpat<false><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr, nullptr,
+                                                nullptr, S.dof_node.p);
+  ++S.launches;
+  scan64(S, S.olen.p, true, U, S.ooff.p, st);
+  S.nnz_out = read_ll(S.ooff.p + U, st);
+  S.ocols.ensure(S.nnz_out);
+  S.omap.ensure(S.nnz_out);
+  k_outpat<true><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p, S.ocols.p,
+                                               S.omap.p, S.dof_node.p);
+  ++S.launches;
+  int ovf = 0;
+  CK(cudaMemcpyAsync(&ovf, S.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ovf)
+    throw Fail{NLFEM_GPU_BAD_CONFIG,
+               "BadConfig: interaction neighbourhood too large for the pattern kernels (code " +
+                   std::to_string(ovf) + ")"};
+}
+
 // The whole device pipeline.  Outer elements [shard_lo, shard_hi) (positions in
 // the ascending interior list) are integrated; pairs and the node pattern are
 // built for all of them (every rank holds the same pattern, so the fixed-point
@@ -2324,99 +2438,62 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
                    std::to_string(err_elem)};
   CK(cudaEventRecord(S.ev[2], st));
 
-  // ---- K5: pattern
-  const size_t rows_smem = (kHE + kHN + kRowMax) * sizeof(int);
-  CK(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
-  CK(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
-  S.rlen.ensure(J);
-  S.roff.ensure(J + 1);
-  const unsigned rgrid = (unsigned)std::min<long long>(J, 148LL * 16);
-  k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
-                                               nullptr, S.ovf.p);
-  ++S.launches;
-  scan64(S, S.rlen.p, true, J, S.roff.p, st);
-  const long long nR = read_ll(S.roff.p + J, st);
-  S.rcols.ensure(nR);
-  k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
-                                              S.rcols.p, S.ovf.p);
-  ++S.launches;
-  // transpose
-  S.tcnt.ensure(J);
-  S.toff.ensure(J + 1);
-  S.tcols.ensure(nR);
-  CK(cudaMemsetAsync(S.tcnt.p, 0, J * sizeof(int), st));
-  k_col_count<<<nblk(nR, 256), 256, 0, st>>>(nR, S.rcols.p, S.tcnt.p);
-  ++S.launches;
-  scan64(S, S.tcnt.p, true, J, S.toff.p, st);
-  S.cursor.ensure(J);
-  CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
-  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.cursor.p,
-                                                 S.tcols.p);
-  CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(kRowMax * sizeof(int))));
-  k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p);
-  S.launches += 2;
-  // union
-  S.slen.ensure(J);
-  S.soff.ensure(J + 1);
-  CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
-  int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
-  k_union<false><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
-                                               S.slen.p, nullptr, nullptr, d_maxlen);
-  ++S.launches;
-  scan64(S, S.slen.p, true, J, S.soff.p, st);
-  S.nnz_s = read_ll(S.soff.p + J, st);
-  S.scols.ensure(S.nnz_s);
-  k_union<true><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
-                                              nullptr, S.soff.p, S.scols.p, nullptr);
+  // ---- K5: pattern, on stream2 from its own host thread (overlaps the units)
+  CK(cudaStreamWaitEvent(S.stream2, S.ev[2], 0));
   int maxlen = 0;
-  CK(cudaMemcpyAsync(&maxlen, d_maxlen, sizeof(int), cudaMemcpyDeviceToHost, st));
-  S.mirror.ensure(S.nnz_s);
-  k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
-  S.eslot.ensure(10 * (size_t)KI);
-  k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p);
-  S.launches += 3;
-  // output pattern
-  const int U = S.unknowns;
-  S.olen.ensure(U);
-  S.ooff.ensure(U + 1);
-  k_outpat<false><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr, nullptr,
-                                                nullptr, S.dof_node.p);
-  ++S.launches;
-  scan64(S, S.olen.p, true, U, S.ooff.p, st);
-  S.nnz_out = read_ll(S.ooff.p + U, st);
-  S.ocols.ensure(S.nnz_out);
-  S.omap.ensure(S.nnz_out);
-  k_outpat<true><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p, S.ocols.p,
-                                               S.omap.p, S.dof_node.p);
-  ++S.launches;
-  int ovf = 0;
-  CK(cudaMemcpyAsync(&ovf, S.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (ovf)
-    throw Fail{NLFEM_GPU_BAD_CONFIG,
-               "BadConfig: interaction neighbourhood too large for the pattern kernels (code " +
-                   std::to_string(ovf) + ")"};
-  CK(cudaEventRecord(S.ev[3], st));
+  std::exception_ptr pattern_error;
+  std::thread pattern_thread([&S, &maxlen, &pattern_error]() {
+    try {
+      CK(cudaSetDevice(S.device));
+      CK(cudaEventRecord(S.ev[8], S.stream2));
+      run_pattern(S, S.stream2, maxlen);
+      CK(cudaEventRecord(S.ev[9], S.stream2));
+    } catch (...) {
+      pattern_error = std::current_exception();
+    }
+  });
+  struct Joiner {  // joins on every exit path (exceptions included)
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{pattern_thread};
+  bool pattern_ready = false;
+  auto wait_pattern = [&]() {
+    if (pattern_ready) return;
+    pattern_thread.join();
+    if (pattern_error) std::rethrow_exception(pattern_error);
+    CK(cudaStreamWaitEvent(st, S.ev[9], 0));
+    pattern_ready = true;
+  };
 
   // ---- K3/K4: integrate + scatter
-  S.V.ensure(2 * (size_t)S.nnz_s);
+  CK(cudaEventRecord(S.ev[3], st));
   S.rhsT.ensure(4 * (size_t)KI);
-  CK(cudaMemsetAsync(S.V.p, 0, 2 * S.nnz_s * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(S.rhsT.p, 0, 4 * (size_t)KI * sizeof(double), st));
   shard_lo = std::max(0, std::min(shard_lo, KI));
   shard_hi = std::max(shard_lo, std::min(shard_hi, KI));
-  // slot-map capacity: power of two > union of the four rows (<= 4 maxlen)
-  int hcap = 64;
-  while (hcap <= 4 * std::max(maxlen, 1)) hcap <<= 1;
-  if (maxlen >= 32768)
-    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
-  const int rowcap = std::max(maxlen, 1);
-  const size_t ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
-  if (ismem > 220 * 1024)
-    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
-  CK(cudaFuncSetAttribute(k_integrate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
-  CK(cudaFuncSetAttribute(k_integrate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
+  // combine set-up once the pattern is known: accumulators and the slot-map
+  // capacity, a power of two > union of the four rows (<= 4 maxlen)
+  int hcap = 64, rowcap = 1;
+  size_t ismem = 0;
+  bool combine_ready = false;
+  auto setup_combine = [&]() {
+    if (combine_ready) return;
+    combine_ready = true;
+    wait_pattern();
+    S.V.ensure(2 * (size_t)S.nnz_s);
+    CK(cudaMemsetAsync(S.V.p, 0, 2 * S.nnz_s * sizeof(unsigned long long), st));
+    while (hcap <= 4 * std::max(maxlen, 1)) hcap <<= 1;
+    if (maxlen >= 32768)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
+    rowcap = std::max(maxlen, 1);
+    ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
+    if (ismem > 220 * 1024)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
+    CK(cudaFuncSetAttribute(k_integrate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
+    CK(cudaFuncSetAttribute(k_integrate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
+  };
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   const bool need_gauss = D.strategy != NLFEM_STRATEGY_BARYCENTER;
   float mc_ms = 0;
@@ -2452,7 +2529,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
           ngunits = read_ll(S.goff.p + np, st);
           S.gpair.ensure(ngunits + 1);
           S.gq.ensure(ngunits + 1);
-          S.gmom.ensure(15 * (size_t)ngunits + 1);
+          S.gmom.ensure(kGmomStride * (size_t)(ngunits + 1));
           S.glist.ensure(2 * (size_t)ngunits + 2);
           k_gunits_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.goff.p, S.gpair.p,
                                                        S.gq.p, S.partner.p, S.glist.p,
@@ -2464,7 +2541,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
           nunits = read_ll(S.uoff.p + np, st);
           S.upair.ensure(nunits + 1);
           S.uqs.ensure(nunits + 1);
-          S.mom.ensure(10 * (size_t)nunits + 1);
+          S.mom.ensure(kMomStride * (size_t)(nunits + 1));
           S.ulist.ensure(4 * (size_t)(nunits + 1));
           k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p,
                                                       S.uqs.p, S.partner.p, S.ulist.p,
@@ -2510,6 +2587,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         }
         CK(cudaEventRecord(S.ev[7], st));
       }
+      setup_combine();
       // block size from the mean number of element pairs per outer element
       const long long ppe = (poff[ii1] - poff[ii0]) / std::max(1, ii1 - ii0);
       if (ppe < 768)
@@ -2533,10 +2611,11 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     }
   }
   S.mc_ms = mc_ms;
+  setup_combine();  // empty shard: the pattern is still needed by finalize
   CK(cudaEventRecord(S.ev[4], st));
 
   // ---- K6: finalize
-  if (finalize) run_finalize(S, 0, U);
+  if (finalize) run_finalize(S, 0, S.unknowns);
   CK(cudaEventRecord(S.ev[5], st));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
@@ -2555,6 +2634,9 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     std::memset(stats, 0, sizeof(*stats));
     float ms[6];
     for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], S.ev[i], S.ev[i + 1]));
+    // pattern: its own stream, overlapping the integrate phase (which is timed
+    // from the end of the pairs phase)
+    CK(cudaEventElapsedTime(&ms[2], S.ev[8], S.ev[9]));
     CK(cudaEventElapsedTime(&ms[5], S.ev[0], S.ev[5]));
     for (int i = 0; i < 5; ++i) stats->phase_ms[i] = ms[i];
     stats->device_ms = ms[5];
@@ -2754,12 +2836,13 @@ int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* oute
   });
 }
 
-int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s) { return s ? s->launches : 0; }
+int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s) { return s ? s->launches.load() : 0; }
 
 void nlfem_gpu_session_destroy(nlfem_gpu_session* s) {
   if (!s) return;
   for (auto e : s->ev) cudaEventDestroy(e);
   if (s->stream) cudaStreamDestroy(s->stream);
+  if (s->stream2) cudaStreamDestroy(s->stream2);
   delete s;
 }
 
