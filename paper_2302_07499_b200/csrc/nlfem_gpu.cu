@@ -2352,7 +2352,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   CK(cudaEventRecord(S.ev[1], st));
 
   // ---- K1: pairs (count, scan, fill)
-  const int KI = S.KI, J = S.J;
+  const int KI = S.KI;
   S.pair_count.ensure(KI);
   S.pair_off.ensure(KI + 1);
   S.err_elem.ensure(1);
