@@ -1965,7 +1965,10 @@ struct nlfem_gpu_session {
   // the node pattern is built on a second, higher-priority stream from its own
   // host thread, concurrently with the units / Monte Carlo work on `stream`
   cudaStream_t stream2 = nullptr;
-  std::vector<cudaEvent_t> ev;  // 0..7 phases on stream; 8, 9 pattern on stream2
+  // Gauss units and the one-piece Monte Carlo lists run on stream3, beside the
+  // three-piece Monte Carlo lists on `stream`
+  cudaStream_t stream3 = nullptr;
+  std::vector<cudaEvent_t> ev;  // 0..7 phases on stream; 8, 9 pattern on stream2; 10, 11 fork/join
 };
 
 namespace {
@@ -2071,7 +2074,8 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&S.stream2, cudaStreamNonBlocking, hi));
-    for (int i = 0; i < 10; ++i) {
+    CK(cudaStreamCreateWithFlags(&S.stream3, cudaStreamNonBlocking));
+    for (int i = 0; i < 12; ++i) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       S.ev.push_back(e);
@@ -2552,14 +2556,17 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaEventRecord(S.ev[6], st));
+        cudaStream_t s3 = S.stream3;
+        CK(cudaEventRecord(S.ev[10], st));  // fork
+        CK(cudaStreamWaitEvent(s3, S.ev[10], 0));
         if (need_gauss && nl[2] > 0) {
-          k_gauss<false><<<nblk(nl[2], kGaussThreads), kGaussThreads, 0, st>>>(
+          k_gauss<false><<<nblk(nl[2], kGaussThreads), kGaussThreads, 0, s3>>>(
               P0, ngunits, S.glist.p, nl[2], S.gpair.p, S.gq.p, S.pair_outer.p, S.partner.p,
               S.info.p, S.gmom.p, S.counters.p + 1);
           ++S.launches;
         }
         if (need_gauss && nl[3] > 0) {
-          k_gauss<true><<<nblk(nl[3], kGaussThreads), kGaussThreads, 0, st>>>(
+          k_gauss<true><<<nblk(nl[3], kGaussThreads), kGaussThreads, 0, s3>>>(
               P0, ngunits, S.glist.p + ngunits + 1, nl[3], S.gpair.p, S.gq.p, S.pair_outer.p,
               S.partner.p, S.info.p, S.gmom.p, S.counters.p + 1);
           ++S.launches;
@@ -2567,24 +2574,26 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         if (need_mc) {
           const long long ls = nunits + 1;
           const int* L0 = S.ulist.p;
-          auto launch = [&](auto kern, int kind) {
+          auto launch = [&](auto kern, int kind, cudaStream_t s) {
             const int n = nl[4 + kind];
             if (n <= 0) return;
-            kern<<<nblk(n, kMcThreads), kMcThreads, 0, st>>>(
+            kern<<<nblk(n, kMcThreads), kMcThreads, 0, s>>>(
                 P0, nunits, L0 + kind * ls, n, S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
                 S.info.p, S.mom.p, S.counters.p + 1);
             ++S.launches;
           };
-          launch(k_mc<false, false, 3>, 1);
-          launch(k_mc<false, false, 1>, 0);
+          launch(k_mc<false, false, 3>, 1, st);
+          launch(k_mc<false, false, 1>, 0, s3);
           if (S.g_deg <= 2) {
-            launch(k_mc<true, true, 3>, 3);
-            launch(k_mc<true, true, 1>, 2);
+            launch(k_mc<true, true, 3>, 3, st);
+            launch(k_mc<true, true, 1>, 2, s3);
           } else {
-            launch(k_mc<true, false, 3>, 3);
-            launch(k_mc<true, false, 1>, 2);
+            launch(k_mc<true, false, 3>, 3, st);
+            launch(k_mc<true, false, 1>, 2, s3);
           }
         }
+        CK(cudaEventRecord(S.ev[11], s3));  // join
+        CK(cudaStreamWaitEvent(st, S.ev[11], 0));
         CK(cudaEventRecord(S.ev[7], st));
       }
       setup_combine();
@@ -2843,6 +2852,7 @@ void nlfem_gpu_session_destroy(nlfem_gpu_session* s) {
   for (auto e : s->ev) cudaEventDestroy(e);
   if (s->stream) cudaStreamDestroy(s->stream);
   if (s->stream2) cudaStreamDestroy(s->stream2);
+  if (s->stream3) cudaStreamDestroy(s->stream3);
   delete s;
 }
 
