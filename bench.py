@@ -278,7 +278,12 @@ def main():
     pairs = int(st.element_pairs)  # all element pairs of the workload (every rank builds them)
     value = pairs * args.steps / (t_total * 1e-3)
 
-    # end to end: one-shot C-ABI call with host arrays (upload + run + download)
+    # end to end: one-shot C-ABI call with host arrays (upload + run + download).
+    # The device-resident session is released first: at C4 its buffers alone
+    # take ~70 GB and the one-shot call keeps its own workspace.
+    sess.close()
+    del flush
+    torch.cuda.empty_cache()
     e2e = None
     if not args.no_e2e:
         h2d = table.nbytes() + 8 * 8 * (len(sess.fterms) + len(sess.uterms))

@@ -297,11 +297,8 @@ __device__ __forceinline__ int count_kept(const Straddle& st, double tau) {
   return n;
 }
 
-// Does a nocaps straddler emit at least one inner sub-simplex (volume > tau)?
-// Cheap certificate first: the inner polytope contains a tet of volume
-// >= (depth/diam)^(4-m) vol(T'), depth = delta - |v - x_q| of the deepest
-// inside vertex, and its <= 3 pieces sum to the polytope; otherwise run the
-// exact straddle_inner.
+// Exact piece tests: does straddle_inner (nocaps) or straddle_inner +
+// straddle_outer (fullcaps) keep at least one sub-simplex above the volume floor?
 __device__ __noinline__ bool inner_pieces_exact(const Vd* v, int mask, Vd xq, double tau) {
   return count_kept(inner_straddle(v, mask, xq, cD.delta), tau) > 0;
 }
@@ -311,48 +308,68 @@ __device__ __noinline__ bool any_pieces_exact(const Vd* v, int mask, Vd xq, doub
              count_kept(outer_straddle(v, mask, xq, cD.delta), tau) > 0;
 }
 
-// Does a nocaps straddler emit at least one inner sub-simplex (volume > tau)?
-// Certificate: the inner polytope contains a tet of volume >= (depth/diam)^(4-m)
-// vol(T'), depth = delta - |v - x_q| of the deepest inside vertex, and its <= 3
-// kept pieces tile the polytope, so some piece exceeds tau once
-// depth > rho = diam * max((8 tau / vol)^(1/3), 1e-6) (the largest of the m-wise
-// thresholds).  Tested on squared distances with a factor-2 margin; otherwise
-// run the exact decomposition.
-__device__ __forceinline__ bool inner_pieces_exist(const Vd v[4], int mask, Vd xq,
-                                                   const double d2[4], double cert2,
-                                                   double tau) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if ((mask >> i & 1) && d2[i] < cert2) return true;
-  return inner_pieces_exact(v, mask, xq, tau);
-}
-
+// Nocaps certificate (used by classify_cheap): the inner polytope contains a
+// tet of volume >= (depth/diam)^(4-m) vol(T'), depth = delta - |v - x_q| of the
+// deepest inside vertex, and its <= 3 kept pieces tile the polytope, so some
+// piece exceeds tau once depth > rho = diam * max((8 tau / vol)^(1/3), 1e-6)
+// (the largest of the m-wise thresholds).  Tested on squared distances with a
+// factor-2 margin; otherwise the exact decomposition decides.
 __device__ __forceinline__ double cert_threshold2(double diam, double vol, double tau) {
   const double rho = diam * fmax(cbrt(8.0 * tau / vol), 1e-6);
   const double t = cD.delta - 2.0 * rho;
   return t > 0 ? t * t * (1.0 - 1e-12) : 0.0;
 }
 
-__device__ __forceinline__ bool any_pieces_fullcaps(const Vd v[4], int mask, Vd xq, double vol,
-                                                    double tau) {
-  if (vol > 64.0 * tau) return true;  // inner + outer polytopes cover T'
-  return any_pieces_exact(v, mask, xq, tau);
+
+// distance_point_simplex(xq, v) < delta, decided from the facets that can hold
+// the closest point: for xq outside T' the closest point lies on a facet whose
+// plane separates xq (lambda_f < 0), so the minimum over facets with
+// lambda_f < 1e-6 (a margin far above rounding) is the true distance up to
+// rounding.  Conclusive when it is 1e-9 delta away from delta; otherwise the
+// reference expression decides.
+__device__ __noinline__ bool outside_cap_hits(Vd xq, const Vd* v, double delta) {
+  const Vd e1 = vsub(v[1], v[0]), e2 = vsub(v[2], v[0]), e3 = vsub(v[3], v[0]);
+  const Vd b = vsub(xq, v[0]);
+  const double det = vdot(e1, vcross(e2, e3));
+  const double l1 = vdot(b, vcross(e2, e3)) / det;
+  const double l2 = vdot(e1, vcross(b, e3)) / det;
+  const double l3 = vdot(e1, vcross(e2, b)) / det;
+  const double l0 = 1.0 - l1 - l2 - l3;
+  if (!(l0 < 0) && !(l1 < 0) && !(l2 < 0) && !(l3 < 0)) return true;  // inside: 0 < delta
+  const double lam[4] = {l0, l1, l2, l3};
+  double d = INFINITY;
+  for (int f = 0; f < 4; ++f)
+    if (lam[f] < 1e-6) d = fmin(d, facet_distance(v, f, xq));
+  if (d < delta * (1.0 - 1e-9)) return true;
+  if (d > delta * (1.0 + 1e-9)) return false;
+  return distance_point_simplex(xq, v) < delta;
 }
 
-__device__ __noinline__ double dist_point_tet(Vd xq, const Vd* v) {
-  return distance_point_simplex(xq, v);
-}
-
+// BallExitsMesh probe: an unglued facet of T' closer than delta - slack to xq.
+// The facet's plane distance bounds its triangle distance from below; facets
+// whose plane is farther than the threshold (1e-9 relative margin) are skipped.
 __device__ __noinline__ bool facet_too_close(const Vd* v, int4 nb, Vd xq) {
   const int nbv[4] = {nb.x, nb.y, nb.z, nb.w};
-  for (int f = 0; f < 4; ++f)
-    if (nbv[f] < 0 && facet_distance(v, f, xq) < cD.delta - cD.slack) return true;
+  const double thr = cD.delta - cD.slack;
+  for (int f = 0; f < 4; ++f) {
+    if (nbv[f] >= 0) continue;
+    const Vd a = v[f == 0 ? 1 : 0], bb = v[f <= 1 ? 2 : 1], c = v[f <= 2 ? 3 : 2];
+    const Vd n = vcross(vsub(bb, a), vsub(c, a));
+    const double h = vdot(n, vsub(xq, a));
+    if (h * h > thr * thr * vnorm2(n) * (1.0 + 1e-9)) continue;
+    if (facet_distance(v, f, xq) < thr) return true;
+  }
   return false;
 }
 
-// The reference's per-(T,q,T') decision (assembly.cpp:722-759).
-__device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, const Vd v[4],
-                                                  double cert2, double vol, double tau) {
+// The reference's per-(T,q,T') decision (assembly.cpp:722-759), split in two:
+// classify_cheap settles every item that the screens, certificates and
+// classify_simplex decide, and returns kDefer | mask for the few that need an
+// exact geometric evaluation (classify_deferred), so a warp can queue those and
+// work them with all lanes.
+constexpr unsigned kDefer = 0x80u;
+__device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, const Vd v[4],
+                                                   double cert2, double vol, double tau) {
   const double delta = cD.delta;
   // The reference compares gap = sqrt(|c - x_q|^2) against thresholds.  A
   // squared comparison with a 1e-12 relative margin decides the same way
@@ -399,11 +416,23 @@ __device__ __forceinline__ unsigned classify_item(Vd xq, Vd cen, double rad, con
     // the barycenter lies in T': gap < delta (with margin) certifies that the
     // computed distance_point_simplex is < delta; otherwise evaluate it
     if (g2 < delta * delta * (1.0 - 1e-11)) return kOutCap;
-    return dist_point_tet(xq, v) < delta ? kOutCap : kNone;
+    return kDefer;
   }
+  if (cD.strategy == NLFEM_STRATEGY_NOCAPS) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if ((mask >> i & 1) && d2[i] < cert2) return kStraddle | mask;
+    return kDefer | mask;
+  }
+  if (vol > 64.0 * tau) return kStraddle | mask;  // inner + outer polytopes cover T'
+  return kDefer | mask;
+}
+
+__device__ __forceinline__ unsigned classify_deferred(Vd xq, const Vd v[4], int mask, double tau) {
+  if (mask == 0) return outside_cap_hits(xq, v, cD.delta) ? kOutCap : kNone;
   if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
-    return inner_pieces_exist(v, mask, xq, d2, cert2, tau) ? (kStraddle | mask) : kNone;
-  return any_pieces_fullcaps(v, mask, xq, vol, tau) ? (kStraddle | mask) : kNone;
+    return inner_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
+  return any_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
 }
 
 struct OuterT {
@@ -490,6 +519,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(int ii_base, int ii_e
   int cnt = 0, npair = 0;
   unsigned items = 0;
 
+  // per warp: the 4 x 5-bit code of each of its candidates, and the queue of
+  // deferred items (bits 0-3 mask, 4 classify, 5 facet probe, 6-7 q, 8-14 index)
+  __shared__ unsigned wcode[kPairWarps][kCandChunk];
+  __shared__ unsigned short wdef[kPairWarps][4 * kCandChunk];
   auto classify_chunk = [&]() {
     int nm = 0;
     for (int base = 0; base < nst; base += 32) {
@@ -500,31 +533,60 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(int ii_base, int ii_e
       nm += __popc(bal);
     }
     __syncwarp();
+    // pass 1: lane = (candidate, quadrature point), cheap decisions
+    int nd = 0;
     for (int base = 0; base < nm; base += 8) {
       const int t = base + (lane >> 2), q = lane & 3;
-      unsigned code = 0;
-      int Tp = -1;
+      unsigned code = 0, ent = 0;
       if (t < nm) {
         const int k = sg.mine[wl][t];
-        Tp = sg.id[k];
         const double4 a = sg.rec[k][0], b = sg.rec[k][1], e = sg.rec[k][2], d = sg.rec[k][3];
         const Vd cp = {a.x, a.y, a.z};
         const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
         const Vd xq = quad_point(o.v, q);
-        code = classify_item(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]) << (5 * q);
-        items += code != 0;
-        const int4 nb = cD.nbr[Tp];
-        if ((nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) && facet_too_close(v, nb, xq))
-          atomicMin(err_elem, Tp);
+        const unsigned c = classify_cheap(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]);
+        if (c & kDefer) ent = 16u | (c & 15u);
+        else code = c << (5 * q);
+        const int4 nb = cD.nbr[sg.id[k]];
+        if (nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) ent |= 32u;
+        if (ent) ent |= ((unsigned)q << 6) | ((unsigned)t << 8);
       }
       code |= __shfl_xor_sync(FULLMASK, code, 1);
       code |= __shfl_xor_sync(FULLMASK, code, 2);
-      if ((lane & 3) == 0 && t < nm) {
-        cpartner[out + cnt + t] = Tp;
-        cinfo[out + cnt + t] = code;
-      }
-      npair += __popc(__ballot_sync(FULLMASK, (lane & 3) == 0 && code != 0));
+      if ((lane & 3) == 0 && t < nm) wcode[wl][t] = code;
+      const unsigned bal = __ballot_sync(FULLMASK, ent != 0);
+      if (ent) wdef[wl][nd + __popc(bal & ((1u << lane) - 1))] = (unsigned short)ent;
+      nd += __popc(bal);
     }
+    __syncwarp();
+    // pass 2: the deferred items, all lanes busy
+    for (int i = lane; i < nd; i += 32) {
+      const unsigned ent = wdef[wl][i];
+      const int t = (int)(ent >> 8), q = (int)((ent >> 6) & 3);
+      const int k = sg.mine[wl][t];
+      const double4 b = sg.rec[k][1], e = sg.rec[k][2], d = sg.rec[k][3];
+      const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
+      const Vd xq = quad_point(o.v, q);
+      if (ent & 16u) {
+        const unsigned c = classify_deferred(xq, v, (int)(ent & 15u), sg.tau[k]);
+        if (c) atomicOr(&wcode[wl][t], c << (5 * q));
+      }
+      if (ent & 32u) {
+        const int Tp = sg.id[k];
+        if (facet_too_close(v, cD.nbr[Tp], xq)) atomicMin(err_elem, Tp);
+      }
+    }
+    __syncwarp();
+    // write (T', code) into the survivor slots, in stream order
+    for (int t = lane; t < nm; t += 32) {
+      const unsigned code = wcode[wl][t];
+      cpartner[out + cnt + t] = sg.id[sg.mine[wl][t]];
+      cinfo[out + cnt + t] = code;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) items += ((code >> (5 * q)) & 31u) != 0;
+      npair += code != 0;
+    }
+    __syncwarp();
     cnt += nm;
   };
 
@@ -608,7 +670,10 @@ __global__ void __launch_bounds__(kPairThreads, 4) k_pairs(int ii_base, int ii_e
     return;
   }
   classify_chunk();
-  for (int sh = 16; sh > 0; sh >>= 1) items += __shfl_xor_sync(FULLMASK, items, sh);
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    items += __shfl_xor_sync(FULLMASK, items, sh);
+    npair += __shfl_xor_sync(FULLMASK, npair, sh);
+  }
   if (active && lane == 0) {
     pair_count[warp] = npair;
     atomicAdd(item_count, (unsigned long long)items);
