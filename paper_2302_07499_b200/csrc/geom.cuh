@@ -280,6 +280,28 @@ __device__ __forceinline__ void orient_warped(Straddle& s) {
   }
 }
 
+// position of the r-th set bit (r = 0..3) of a 4-bit mask: a 2-bit table
+// lookup (__fns is emulated with a loop on sm_100)
+__host__ __device__ constexpr unsigned long long nth_bit_table(int half) {
+  unsigned long long t = 0;
+  for (int m = 8 * half; m < 8 * half + 8; ++m)
+    for (int r = 0; r < 4; ++r) {
+      int cnt = 0, pos = 0;
+      for (int b = 0; b < 4; ++b)
+        if (m >> b & 1) {
+          if (cnt == r) pos = b;
+          ++cnt;
+        }
+      t |= (unsigned long long)pos << (2 * ((m - 8 * half) * 4 + r));
+    }
+  return t;
+}
+constexpr unsigned long long kNthBit0 = nth_bit_table(0), kNthBit1 = nth_bit_table(1);
+__device__ __forceinline__ int nth_bit4(unsigned mask, int r) {
+  const unsigned long long t = mask < 8 ? kNthBit0 : kNthBit1;
+  return (int)((t >> (2 * (((mask & 7u) << 2) | (unsigned)r))) & 3u);
+}
+
 // crossing_points (reference geometry.cpp:39-50) in one loop: crossing k is
 // edge (k-th inside slot -> j-th outside slot), k = i_rank * (4 - m) + j
 struct Crossings {
@@ -300,7 +322,7 @@ __device__ __forceinline__ void crossings4(const Vd v[4], int mask, Vd c, double
 #pragma unroll 1
   for (int k = 0; k < n; ++k) {
     const int ir = k / mo, orr = k - ir * mo;
-    const int i = (int)__fns(inm, 0, ir + 1), o = (int)__fns(outm, 0, orr + 1);
+    const int i = nth_bit4(inm, ir), o = nth_bit4(outm, orr);
     const Vd a = pick(v, i), b = pick(v, o);
     const double t = edge_crossing(a, b, c, r);
     const Vd p = vadd(a, vscale(t, vsub(b, a)));
@@ -326,7 +348,7 @@ __device__ __forceinline__ void set_cross(Straddle& s, int p, const Crossings& X
   s.lt[p] = X.t[k];
 }
 
-__device__ __forceinline__ int nth_slot(int mask, int n) { return (int)__fns((unsigned)mask, 0, n + 1); }
+__device__ __forceinline__ int nth_slot(int mask, int n) { return nth_bit4((unsigned)mask, n); }
 
 // detail::straddle_inner (reference ball_approx.cpp:195-255)
 __device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c, double r) {

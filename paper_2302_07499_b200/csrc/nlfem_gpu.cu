@@ -1594,6 +1594,9 @@ __global__ void __launch_bounds__(kGaussThreads, 4) k_gauss(long long p0, long l
   if ((threadIdx.x & 31) == 0 && led) atomicAdd(stats + 2, led);
 }
 
+// load-vector partials: one slot per (interior element, combine warp, node)
+constexpr int kRhsWarps = 8;
+
 // shared-memory map: node id -> slots of (N_a, node) in the four staged rows
 struct SlotMap {
   int* key;
@@ -1622,13 +1625,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     double* rhsT, const long long* uoff, const double* mom, long long nunits,
     const long long* goff, const double* gmom, long long ngunits, long long pbase,
     unsigned long long* stats, int hcap, int rowcap) {
+  static_assert(NTHR / 32 <= kRhsWarps, "one rhsT slot per combine warp");
   extern __shared__ unsigned long long sml[];
   SlotMap mp;
   mp.key = reinterpret_cast<int*>(sml);
   mp.val = reinterpret_cast<short4*>(mp.key + hcap);
   mp.mask = hcap - 1;
   __shared__ long long rbase[4];
-  __shared__ double red[NTHR / 32][8];
 
   const int ii = ii0 + blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1836,49 +1839,42 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     }
   }
 
-  // ---- per outer element: D_T block and rhs (fixed-order CTA reduction)
+  // ---- per outer element, per warp (no CTA barrier: a warp that is done
+  // leaves): the warp's share of the D_T block as fixed-point REDs (order-free)
+  // and of the load vector into its own rhsT slot, which k_finalize adds up
+  // in warp order
+#pragma unroll
   for (int q = 0; q < 4; ++q) {
     s0w[q] = wsum(s0w[q]);
     sgc[q] = wsum(sgc[q]);
   }
-  if (lane == 0) {
-    for (int q = 0; q < 4; ++q) {
-      red[wid][q] = s0w[q];
-      red[wid][4 + q] = sgc[q];
-    }
-  }
   for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
   if (lane == 0 && led) atomicAdd(stats + 2, led);
-  __syncthreads();
-  // threads 0..9: the ten D_T entries (a <= b); threads 10..13: rhs of node a
-  const int t = threadIdx.x;
-  if (t < 14) {
-    double acc[8];
+  if (lane < 10) {
+    // lanes 0..9: the ten D_T entries (a <= b)
+    const int t = lane;
+    const int a = t < 4 ? 0 : (t < 7 ? 1 : (t < 9 ? 2 : 3));
+    const int b = a + t - (a == 0 ? 0 : (a == 1 ? 4 : (a == 2 ? 7 : 9)));
+    double tot = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      acc[k] = 0;
-      for (int w = 0; w < NTHR / 32; ++w) acc[k] += red[w][k];
-    }
-    if (t < 10) {
-      const int a = t < 4 ? 0 : (t < 7 ? 1 : (t < 9 ? 2 : 3));
-      const int b = a + t - (a == 0 ? 0 : (a == 1 ? 4 : (a == 2 ? 7 : 9)));
-      double tot = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) tot += C * wq * acc[q] * qbary(q, a) * qbary(q, b);
+    for (int q = 0; q < 4; ++q) tot += C * wq * s0w[q] * qbary(q, a) * qbary(q, b);
+    if (tot != 0.0) {
       const int lo = min(NT[a], NT[b]), hi = max(NT[a], NT[b]);
       int ra = 0;
       for (int r = 0; r < 4; ++r)
         if (NT[r] == lo) ra = r;
       const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
       red_fixed(V, rbase[ra] + v[ra], tot, sc[ra]);
-    } else {
-      // load vector: f term (reference assembly.cpp:703-709) + constraint terms
-      const int a = t - 10;
-      double r = 0;
-      for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, quad_point(vT, q));
-      const double ca = a == 0 ? acc[4] : (a == 1 ? acc[5] : (a == 2 ? acc[6] : acc[7]));
-      rhsT[4 * (long long)ii + a] = r + 2.0 * C * wq * ca;
     }
+  } else if (lane < 14) {
+    // lanes 10..13: load vector of node a -- f term (reference
+    // assembly.cpp:703-709, warp 0 only) + this warp's constraint terms
+    const int a = lane - 10;
+    double r = 0;
+    if (wid == 0)
+      for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, quad_point(vT, q));
+    const double ca = a == 0 ? sgc[0] : (a == 1 ? sgc[1] : (a == 2 ? sgc[2] : sgc[3]));
+    rhsT[((long long)ii * kRhsWarps + wid) * 4 + a] = r + 2.0 * C * wq * ca;
   }
 }
 
@@ -1931,10 +1927,12 @@ __global__ void k_finalize(const long long* soff, const int* scols, const long l
       const int lo = cD.ipos[T];
       const int4 w = cD.verts[T];
       const int a = w.x == i ? 0 : (w.y == i ? 1 : (w.z == i ? 2 : 3));
-      double s, e;
-      two_sum(rs, rhsT[4 * (long long)lo + a], s, e);
-      rs = s;
-      re += e;
+      for (int w = 0; w < kRhsWarps; ++w) {
+        double s, e;
+        two_sum(rs, rhsT[((long long)lo * kRhsWarps + w) * 4 + a], s, e);
+        rs = s;
+        re += e;
+      }
     }
     double s, e;
     two_sum(rs, -fs, s, e);
@@ -2538,8 +2536,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
 
   // ---- K3/K4: integrate + scatter
   CK(cudaEventRecord(S.ev[3], st));
-  S.rhsT.ensure(4 * (size_t)KI);
-  CK(cudaMemsetAsync(S.rhsT.p, 0, 4 * (size_t)KI * sizeof(double), st));
+  S.rhsT.ensure(4 * kRhsWarps * (size_t)KI);
+  CK(cudaMemsetAsync(S.rhsT.p, 0, 4 * kRhsWarps * (size_t)KI * sizeof(double), st));
   shard_lo = std::max(0, std::min(shard_lo, KI));
   shard_hi = std::max(shard_lo, std::min(shard_hi, KI));
   // combine set-up once the pattern is known: accumulators and the slot-map
@@ -2662,8 +2660,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         CK(cudaEventRecord(S.ev[7], st));
       }
       setup_combine();
-      // block size from the mean number of element pairs per outer element
-      const long long ppe = (poff[ii1] - poff[ii0]) / std::max(1, ii1 - ii0);
+      // block size from the whole mesh's mean number of pairs per outer element
+      // (the same for every shard and chunk: the per-warp partial sums, and so
+      // the last bits of the result, must not depend on the sharding)
+      const long long ppe = S.npairs / std::max(1, KI);
       if (ppe < 768)
         k_integrate<128><<<ii1 - ii0, 128, ismem, st>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
@@ -2818,7 +2818,7 @@ int nlfem_gpu_session_partials(nlfem_gpu_session* s, void** V, int64_t* nwords, 
   *V = s->V.p;
   *nwords = 2 * s->nnz_s;
   *rhsT = s->rhsT.p;
-  *nrhs = 4 * (int64_t)s->KI;
+  *nrhs = 4 * kRhsWarps * (int64_t)s->KI;
   return 0;
 }
 
