@@ -350,10 +350,9 @@ __device__ __forceinline__ void set_cross(Straddle& s, int p, const Crossings& X
 
 __device__ __forceinline__ int nth_slot(int mask, int n) { return nth_bit4((unsigned)mask, n); }
 
-// detail::straddle_inner (reference ball_approx.cpp:195-255)
-__device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c, double r) {
-  Crossings X;
-  crossings4(v, mask, c, r, X);
+// detail::straddle_inner (reference ball_approx.cpp:195-255), from the item's
+// crossings (shared with straddle_outer: both start from crossing_points)
+__device__ __forceinline__ Straddle inner_straddle_x(const Vd v[4], int mask, const Crossings& X) {
   const int m = __popc(mask);
   const int s0 = nth_slot(mask, 0), s1 = nth_slot(mask, m > 1 ? 1 : 0),
             s2 = nth_slot(mask, m > 2 ? 2 : 0);
@@ -380,9 +379,7 @@ __device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c
 }
 
 // detail::straddle_outer (reference ball_approx.cpp:257-298)
-__device__ __forceinline__ Straddle outer_straddle(const Vd v[4], int mask, Vd c, double r) {
-  Crossings X;
-  crossings4(v, mask, c, r, X);
+__device__ __forceinline__ Straddle outer_straddle_x(const Vd v[4], int mask, const Crossings& X) {
   const int m = __popc(mask), om = ~mask & 15;
   const int t0 = nth_slot(om, 0), t1 = nth_slot(om, m < 3 ? 1 : 0), t2 = nth_slot(om, m < 2 ? 2 : 0);
   const Vd o0 = pick(v, t0), o1 = pick(v, t1), o2 = pick(v, t2);
@@ -405,6 +402,18 @@ __device__ __forceinline__ Straddle outer_straddle(const Vd v[4], int mask, Vd c
     s.n = 1;
   }
   return s;
+}
+
+__device__ __forceinline__ Straddle inner_straddle(const Vd v[4], int mask, Vd c, double r) {
+  Crossings X;
+  crossings4(v, mask, c, r, X);
+  return inner_straddle_x(v, mask, X);
+}
+
+__device__ __forceinline__ Straddle outer_straddle(const Vd v[4], int mask, Vd c, double r) {
+  Crossings X;
+  crossings4(v, mask, c, r, X);
+  return outer_straddle_x(v, mask, X);
 }
 
 // piece k (0..n-1) of the decomposition

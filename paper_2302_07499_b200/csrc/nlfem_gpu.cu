@@ -93,6 +93,7 @@ struct Dev {
   int K, J, KI, unknowns;
   int strategy, mc;
   unsigned long long seed;
+  uint32_t rkey[20];  // Philox4x32-10 round keys (k0 + r W0, k1 + r W1), r = 0..9
   double C, delta, slack, inside_cut, dd;
   // element data
   const double4* erec;  // [4K]: (c, r), (v0, v1.x), (v1.yz, v2.xy), (v2.z, v3)
@@ -1183,8 +1184,7 @@ __global__ void k_pair_outer(int ii0, int ii1, const long long* pair_off, long l
 // Philox4x32-10 on three counters in lockstep (independent chains -> ILP 3);
 // same function as nlfem_philox4x32_10 applied to each counter.
 __device__ __forceinline__ void philox3(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t j3,
-                                        uint32_t k0, uint32_t k1, uint32_t A[4], uint32_t B[4],
-                                        uint32_t Cw[4]) {
+                                        uint32_t A[4], uint32_t B[4], uint32_t Cw[4]) {
   uint32_t a0 = c0, a1 = c1, a2 = c2, a3 = j3;
   uint32_t b0 = c0, b1 = c1, b2 = c2, b3 = j3 + 1;
   uint32_t d0 = c0, d1 = c1, d2 = c2, d3 = j3 + 2;
@@ -1196,7 +1196,8 @@ __device__ __forceinline__ void philox3(uint32_t c0, uint32_t c1, uint32_t c2, u
     const unsigned long long pb2 = (unsigned long long)NLFEM_PHILOX_M1 * b2;
     const unsigned long long pd0 = (unsigned long long)NLFEM_PHILOX_M0 * d0;
     const unsigned long long pd2 = (unsigned long long)NLFEM_PHILOX_M1 * d2;
-    const uint32_t kk0 = k0 + (uint32_t)r * NLFEM_PHILOX_W0, kk1 = k1 + (uint32_t)r * NLFEM_PHILOX_W1;
+    // round keys from constant memory: LOP3 reads them as c[][] operands
+    const uint32_t kk0 = cD.rkey[2 * r], kk1 = cD.rkey[2 * r + 1];
     a0 = (uint32_t)(pa2 >> 32) ^ a1 ^ kk0; a1 = (uint32_t)pa2;
     a2 = (uint32_t)(pa0 >> 32) ^ a3 ^ kk1; a3 = (uint32_t)pa0;
     b0 = (uint32_t)(pb2 >> 32) ^ b1 ^ kk0; b1 = (uint32_t)pb2;
@@ -1253,14 +1254,138 @@ struct HitMoments {
   }
 };
 
+constexpr long long kMomStride = 10;   // doubles per MC item record (80 B)
+constexpr long long kGmomStride = 16;  // doubles per Gauss unit record (128 B)
+
+// Gauss rule on the inner sub-simplices of one straddling item (reference
+// AsmSink::sub + accumulate_point, assembly.cpp:332-381), from the item's
+// crossings.  Writes one 128-byte record: S0, then Sg (constraint parent) or
+// S1 (4), S2 (10, upper triangle) (interior parent).  Returns the FLOP ledger.
+template <bool CONS>
+__device__ __forceinline__ unsigned long long gauss_item(const Vd vP[4], int mask, double tau,
+                                                         const Crossings& X, double* out) {
+  const Straddle st = inner_straddle_x(vP, mask, X);
+  double S0 = 0, Sg = 0, S1[4] = {0, 0, 0, 0}, S2[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int kept = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= st.n) break;
+    Vd pa, pb, pc, pd;
+    straddle_piece(st, k, pa, pb, pc, pd);
+    const double vol = tet_volume(pa, pb, pc, pd);
+    if (!(vol > tau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
+    ++kept;
+    S0 += vol;
+    if (CONS) {
+      // degree-2 Gauss points with g (reference AsmSink::sub, assembly.cpp:372-381)
+      const Vd pv[4] = {pa, pb, pc, pd};
+#pragma unroll
+      for (int g = 0; g < 4; ++g) Sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), Sg);
+    } else {
+      // The reference integrates lambda and lambda lambda^T with the degree-2
+      // rule, which is exact for them; the same values follow in closed form
+      // from the barycentric coordinates L_j of the piece's vertices in T'
+      // (parent vertex e_a; crossing at t on edge a->b: (1-t) e_a + t e_b):
+      //   int lambda = vol/4 sum_j L_j,
+      //   int lambda lambda^T = vol/20 (sum_j L_j L_j^T + (sum_j L_j)(sum_j L_j)^T).
+      double L[4][4], sl[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int a = st.la[k + j], b = st.lb[k + j];
+        const double t = st.lt[k + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          L[j][i] = (i == a ? 1.0 - t : 0.0) + (i == b ? t : 0.0);
+          sl[i] += L[j][i];
+        }
+      }
+      const double v4 = vol * 0.25, v20 = vol / 20.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        S1[i] = fma(v4, sl[i], S1[i]);
+#pragma unroll
+        for (int jj = i; jj < 4; ++jj) {
+          double mm = sl[i] * sl[jj];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mm = fma(L[j][i], L[j][jj], mm);
+          S2[s2i(i, jj)] = fma(v20, mm, S2[s2i(i, jj)]);
+        }
+      }
+    }
+  }
+  double2* rec = reinterpret_cast<double2*>(out);
+  if (CONS) {
+    rec[0] = make_double2(S0, Sg);
+  } else {
+    rec[0] = make_double2(S0, S1[0]);
+    rec[1] = make_double2(S1[1], S1[2]);
+    rec[2] = make_double2(S1[3], S2[0]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rec[3 + k] = make_double2(S2[1 + 2 * k], S2[2 + 2 * k]);
+    rec[7] = make_double2(S2[9], 0.0);
+  }
+  const int m = __popc(mask);
+  return 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
+         (unsigned long long)kept * (CONS ? 160 : 360);
+}
+
+// Inner pieces of a straddling item for fullcaps, in the Monte Carlo record's
+// form: S0 = sum vol, and (interior parent) the exact Cartesian moments about
+// v0(T') of the pieces -- int r' = vol/4 sum_j p'_j, int r' r'^T =
+// vol/20 (sum_j p'_j p'_j^T + (sum p')(sum p')^T) with p' = p - v0(T') -- which
+// the combine maps through the barycentric Jacobian like the cap moments
+// (the reference's degree-2 rule integrates lambda, lambda lambda^T exactly);
+// (constraint parent) sum vol/4 g at the degree-2 points.  Returns the ledger.
+template <bool CONS>
+__device__ __forceinline__ unsigned long long inner_moments(const Vd* vP, int mask, double tau,
+                                                         const Crossings& X, double* out) {
+  const Straddle st = inner_straddle_x(vP, mask, X);
+  int kept = 0;
+  for (int k = 0; k < st.n; ++k) {
+    Vd pa, pb, pc, pd;
+    straddle_piece(st, k, pa, pb, pc, pd);
+    const double vol = tet_volume(pa, pb, pc, pd);
+    if (!(vol > tau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
+    ++kept;
+    out[0] += vol;
+    if (CONS) {
+      const Vd pv[4] = {pa, pb, pc, pd};
+      double sg = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), sg);
+      out[1] += sg;
+    } else {
+      const Vd q[4] = {vsub(pa, vP[0]), vsub(pb, vP[0]), vsub(pc, vP[0]), vsub(pd, vP[0])};
+      const Vd sp = vadd(vadd(q[0], q[1]), vadd(q[2], q[3]));
+      const double v4 = vol * 0.25, v20 = vol / 20.0;
+      out[1] += v4 * sp.x;
+      out[2] += v4 * sp.y;
+      out[3] += v4 * sp.z;
+      double m2[6] = {sp.x * sp.x, sp.x * sp.y, sp.x * sp.z, sp.y * sp.y, sp.y * sp.z, sp.z * sp.z};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        m2[0] = fma(q[j].x, q[j].x, m2[0]);
+        m2[1] = fma(q[j].x, q[j].y, m2[1]);
+        m2[2] = fma(q[j].x, q[j].z, m2[2]);
+        m2[3] = fma(q[j].y, q[j].y, m2[3]);
+        m2[4] = fma(q[j].y, q[j].z, m2[4]);
+        m2[5] = fma(q[j].z, q[j].z, m2[5]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 6; ++kk) out[4 + kk] += v20 * m2[kk];
+    }
+  }
+  const int m = __popc(mask);
+  return 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
+         (unsigned long long)kept * (CONS ? 160 : 360);
+}
+
 // Monte Carlo: one thread per cap item; each kept sub-simplex (piece) gets M
 // samples of the mode-P stream (include/nlfem_mc_stream.h).  Writes one record
 // per item, at the item's first unit slot (record of kMomStride doubles): the weighted
 // S0, then sum w g(y) for constraint parents, or the Cartesian moments about
 // v0(T') sum w r' (3) and sum w r' r'^T (6) for interior parents.
 constexpr int kMcThreads = 128;
-constexpr long long kMomStride = 10;   // doubles per MC item record (80 B)
-constexpr long long kGmomStride = 16;  // doubles per Gauss unit record (128 B)
 
 // value, gradient and Hessian at x of a polynomial of total degree <= 2
 // (only such g take the moment path in k_mc<true, true>)
@@ -1309,7 +1434,8 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
                                                       const unsigned* info, double* mom,
                                                       unsigned long long* mc_stats) {
   // one thread per cap item: the straddle_outer decomposition is computed once
-  // and each kept piece (unit u0 + j) gets its M samples
+  // and each kept piece (unit u0 + j) gets its M samples; a straddling item
+  // first does its inner pieces' Gauss unit from the same crossings
   const int li = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long draws = 0, hits = 0, led = 0;
   if (li < nlist) {
@@ -1327,13 +1453,22 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     load_verts(Tp, vP);
     Straddle st;
     int npieces;
+    double seed[CONS ? 2 : 10];
+#pragma unroll
+    for (int kk = 0; kk < (CONS ? 2 : 10); ++kk) seed[kk] = 0.0;
     if (c == kOutCap) {  // whole element (reference assembly.cpp:754-759)
       st.A0 = vP[0]; st.A1 = vP[1]; st.A2 = vP[2]; st.B0 = vP[3];
       st.B1 = vP[3]; st.B2 = vP[3];
       st.n = 1;
       npieces = 1;
-    } else {  // straddle_outer (reference ball_approx.cpp:257-298)
-      st = outer_straddle(vP, (int)(c & 15), xq, cD.delta);
+    } else {  // straddle_inner + straddle_outer (reference ball_approx.cpp:195-298)
+      const int mask = (int)(c & 15);
+      Crossings X;
+      crossings4(vP, mask, xq, cD.delta, X);
+      // the inner pieces (Gauss rule, reference AsmSink::sub, assembly.cpp:332-381)
+      // seed the item's record in the Monte Carlo units' own form
+      led += inner_moments<CONS>(vP, mask, cD.tau[Tp], X, seed);
+      st = outer_straddle_x(vP, mask, X);
       npieces = st.n;
       const int m = __popc(c & 15);
       led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
@@ -1352,10 +1487,11 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     }
     const Vd v0P = vP[0];
     __shared__ double sAcc[CONS ? 2 : 10][kMcThreads];
+#pragma unroll
+    for (int kk = 0; kk < (CONS ? 2 : 10); ++kk) sAcc[kk][threadIdx.x] = seed[kk];
     const double tau = c == kOutCap ? -1.0 : cD.tau[Tp];
     const int M = cD.mc;
     const double dd = cD.dd;
-    const uint32_t k0 = (uint32_t)(cD.seed & 0xffffffffu), k1 = (uint32_t)(cD.seed >> 32);
     double g0 = 0, gr[3] = {0, 0, 0}, H[6] = {0, 0, 0, 0, 0, 0};
     if (CONS && G2) poly2_taylor(cD.g, xq, g0, gr, H);
     int kept = 0;
@@ -1379,7 +1515,6 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         use = vol > tau;  // push_piece volume floor (ball_approx.cpp:141)
       }
       if (!use) continue;
-      const long long u = u0 + kept;
       const uint32_t c2 = (uint32_t)q | ((uint32_t)kept << 2);
       ++kept;
       const double w = vol / M;
@@ -1418,7 +1553,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       for (int j = 0; j < full; ++j) {
         // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
         uint32_t A[4], B[4], Cw[4];
-        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, k0, k1, A, B, Cw);
+        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, A, B, Cw);
         sample(A[0], A[1], A[2], dd);
         sample(A[3], B[0], B[1], dd);
         sample(B[2], B[3], Cw[0], dd);
@@ -1426,7 +1561,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       }
       if (M & 3) {  // partial last block: samples past M are drawn but never hit
         uint32_t A[4], B[4], Cw[4];
-        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)full, k0, k1, A, B, Cw);
+        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)full, A, B, Cw);
         const int rem = M & 3;
         sample(A[0], A[1], A[2], dd);
         sample(A[3], B[0], B[1], rem > 1 ? dd : -1.0);
@@ -1461,23 +1596,15 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       draws += (unsigned long long)M;
       hits += nh;
       led += 25ull + 35ull * (unsigned long long)M + (CONS ? 12ull : 62ull) * nh;
-      // item totals over its kept pieces, summed in piece order from 0 (the
-      // order the per-piece values were once added in by the combine)
+      // item totals: inner pieces, then the kept outer pieces in piece order
       const double vals[10] = {S0, CONS ? sg : m1x, m1y, m1z, m2[0], m2[1], m2[2], m2[3], m2[4], m2[5]};
       constexpr int nv = CONS ? 2 : 10;
 #pragma unroll
-      for (int kk = 0; kk < nv; ++kk) {
-        if (NU == 1) sAcc[kk][threadIdx.x] = vals[kk];
-        else sAcc[kk][threadIdx.x] = (u == u0 ? 0.0 : sAcc[kk][threadIdx.x]) + vals[kk];
-      }
+      for (int kk = 0; kk < nv; ++kk) sAcc[kk][threadIdx.x] += vals[kk];
     }
     // one record per item at its first unit slot: S0, then sum g (constraint
-    // parents) or sum r' and sum r' r'^T (6) about v0(T')
+    // parents) or sum r' and sum r' r'^T (6) about v0(T'), inner pieces included
     constexpr int nv = CONS ? 2 : 10;
-    if (kept == 0) {
-#pragma unroll
-      for (int kk = 0; kk < nv; ++kk) sAcc[kk][threadIdx.x] = 0.0;
-    }
     double2* rec = reinterpret_cast<double2*>(mom + kMomStride * u0);
 #pragma unroll
     for (int kk = 0; kk < nv; kk += 2)
@@ -1496,10 +1623,8 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
   }
 }
 
-// Gauss rule on the inner sub-simplices of one straddling item (reference
-// AsmSink::sub + accumulate_point, assembly.cpp:332-381): thread per item.
-// Output SoA [15][n]: S0, S1[4], S2[10] (upper triangle) for interior parents;
-// S0, Sg for constraint parents (slots 0, 1).
+// nocaps: thread per straddling item (fullcaps does these inside k_mc, which
+// shares the item's crossings with the outer decomposition)
 constexpr int kGaussThreads = 128;
 
 template <bool CONS>
@@ -1524,71 +1649,9 @@ __global__ void __launch_bounds__(kGaussThreads, 4) k_gauss(long long p0, long l
     load_verts(T, vT);
     load_verts(Tp, vP);
     const Vd xq = quad_point(vT, q);
-    const Straddle st = inner_straddle(vP, mask, xq, cD.delta);
-    const double tau = cD.tau[Tp];
-    double S0 = 0, Sg = 0, S1[4] = {0, 0, 0, 0}, S2[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    int kept = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (k >= st.n) break;
-      Vd pa, pb, pc, pd;
-      straddle_piece(st, k, pa, pb, pc, pd);
-      const double vol = tet_volume(pa, pb, pc, pd);
-      if (!(vol > tau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
-      ++kept;
-      S0 += vol;
-      if (CONS) {
-        // degree-2 Gauss points with g (reference AsmSink::sub, assembly.cpp:372-381)
-        const Vd pv[4] = {pa, pb, pc, pd};
-#pragma unroll
-        for (int g = 0; g < 4; ++g) Sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), Sg);
-      } else {
-        // The reference integrates lambda and lambda lambda^T with the degree-2
-        // rule, which is exact for them; the same values follow in closed form
-        // from the barycentric coordinates L_j of the piece's vertices in T'
-        // (parent vertex e_a; crossing at t on edge a->b: (1-t) e_a + t e_b):
-        //   int lambda = vol/4 sum_j L_j,
-        //   int lambda lambda^T = vol/20 (sum_j L_j L_j^T + (sum_j L_j)(sum_j L_j)^T).
-        double L[4][4], sl[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int a = st.la[k + j], b = st.lb[k + j];
-          const double t = st.lt[k + j];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            L[j][i] = (i == a ? 1.0 - t : 0.0) + (i == b ? t : 0.0);
-            sl[i] += L[j][i];
-          }
-        }
-        const double v4 = vol * 0.25, v20 = vol / 20.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          S1[i] = fma(v4, sl[i], S1[i]);
-#pragma unroll
-          for (int jj = i; jj < 4; ++jj) {
-            double mm = sl[i] * sl[jj];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) mm = fma(L[j][i], L[j][jj], mm);
-            S2[s2i(i, jj)] = fma(v20, mm, S2[s2i(i, jj)]);
-          }
-        }
-      }
-    }
-    const int m = __popc(mask);
-    led = 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
-          (unsigned long long)kept * (CONS ? 160 : 360);
-    // one 128-byte record per unit: S0, then Sg (constraint) or S1 (4), S2 (10)
-    double2* rec = reinterpret_cast<double2*>(gmom + kGmomStride * u);
-    if (CONS) {
-      rec[0] = make_double2(S0, Sg);
-    } else {
-      rec[0] = make_double2(S0, S1[0]);
-      rec[1] = make_double2(S1[1], S1[2]);
-      rec[2] = make_double2(S1[3], S2[0]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) rec[3 + k] = make_double2(S2[1 + 2 * k], S2[2 + 2 * k]);
-      rec[7] = make_double2(S2[9], 0.0);
-    }
+    Crossings X;
+    crossings4(vP, mask, xq, cD.delta, X);
+    led = gauss_item<CONS>(vP, mask, cD.tau[Tp], X, gmom + kGmomStride * u);
   }
   for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
   if ((threadIdx.x & 31) == 0 && led) atomicAdd(stats + 2, led);
@@ -1714,7 +1777,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
             for (int cc = b; cc < 4; ++cc) S2[s2i(b, cc)] += off * (b == cc ? 2.0 : 1.0);
           }
         }
-      } else if (c & kStraddle) {
+      } else if ((c & kStraddle) && gmom != nullptr) {
+        // nocaps: the item's Gauss record (fullcaps folds the inner pieces
+        // into the item's Monte Carlo record)
         const double2* rec = reinterpret_cast<const double2*>(gmom + kGmomStride * gu);
         const double2 r0 = rec[0];
         S0 = r0.x;
@@ -2198,6 +2263,10 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.strategy = cfg->strategy;
   D.mc = cfg->mc_samples;
   D.seed = cfg->seed;
+  for (int r = 0; r < 10; ++r) {
+    D.rkey[2 * r] = (uint32_t)(cfg->seed & 0xffffffffu) + (uint32_t)r * NLFEM_PHILOX_W0;
+    D.rkey[2 * r + 1] = (uint32_t)(cfg->seed >> 32) + (uint32_t)r * NLFEM_PHILOX_W1;
+  }
   D.C = k->C;
   D.delta = k->delta;
   D.slack = 1e-10 * k->delta;                           // eps_geo (core.hpp:83)
@@ -2561,8 +2630,11 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     CK(cudaFuncSetAttribute(k_integrate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
     CK(cudaFuncSetAttribute(k_integrate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
   };
+  // units phase: nocaps -> Gauss records (k_gauss); fullcaps -> one record per
+  // cap item (k_mc, inner pieces included); barycenter -> none
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
-  const bool need_gauss = D.strategy != NLFEM_STRATEGY_BARYCENTER;
+  const bool need_units = D.strategy != NLFEM_STRATEGY_BARYCENTER;
+  const bool need_gauss = D.strategy == NLFEM_STRATEGY_NOCAPS;
   float mc_ms = 0;
   if (shard_hi > shard_lo) {
     // chunks of outer elements sized so the unit buffers stay bounded
@@ -2570,7 +2642,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const long long kPairsPerChunk = need_gauss ? (8LL << 20) : (1LL << 40);
+    const long long kPairsPerChunk = need_units ? (8LL << 20) : (1LL << 40);
     int ii0 = shard_lo;
     while (ii0 < shard_hi) {
       int ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), poff[ii0] + kPairsPerChunk) -
@@ -2578,7 +2650,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
       ii1 = std::min(std::max(ii1, ii0 + 1), shard_hi);
       const long long P0 = poff[ii0], np = poff[ii1] - P0;
       long long nunits = 0, ngunits = 0;
-      if (need_gauss) {
+      if (need_units) {
         S.ucount.ensure(np + 1);
         S.gcount.ensure(np + 1);
         S.uoff.ensure(np + 1);
@@ -2675,7 +2747,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
             S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
             need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
       ++S.launches;
-      if (need_gauss) {
+      if (need_units) {
         CK(cudaEventSynchronize(S.ev[7]));
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, S.ev[6], S.ev[7]));
