@@ -2044,6 +2044,41 @@ struct DBuf {
   }
 };
 
+// pinned host staging buffer (grow-only): host<->device copies run from
+// page-locked memory at full PCIe/C2C rate and asynchronously
+struct HostStage {
+  char* p = nullptr;
+  size_t cap = 0, off = 0;
+  void reset(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      CK(cudaMallocHost(reinterpret_cast<void**>(&p), bytes));
+      cap = bytes;
+    }
+    off = 0;
+  }
+  char* take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    if (off + bytes > cap) throw Fail{NLFEM_GPU_ENOMEM, "host staging buffer overflow"};
+    char* r = p + off;
+    off += bytes;
+    return r;
+  }
+  template <class T>
+  void up(DBuf<T>& d, const T* h, size_t m, cudaStream_t s) {
+    d.ensure(m);
+    if (!m) return;
+    char* b = take(m * sizeof(T));
+    std::memcpy(b, h, m * sizeof(T));
+    CK(cudaMemcpyAsync(d.p, b, m * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  ~HostStage() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
 }  // namespace
 
 struct nlfem_gpu_session {
@@ -2085,6 +2120,8 @@ struct nlfem_gpu_session {
   // values
   DBuf<unsigned long long> V;
   DBuf<double> rhsT, values, rhs;
+  DBuf<int> rowptr32;
+  HostStage stage;
   // results of the last run
   long long npairs = 0, nnz_s = 0, nnz_out = 0;
   std::atomic<long long> launches{0};
@@ -2215,16 +2252,6 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   if (dofs->node_count != m->node_count)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: dof map does not match the mesh"};
   cudaStream_t st = S.stream;
-  S.node.upload(m->node_xyz, 3 * (size_t)S.J, st);
-  S.center.upload(m->center, 3 * (size_t)S.K, st);
-  S.radius.upload(m->radius, S.K, st);
-  S.vol.upload(m->volume, S.K, st);
-  S.diam.upload(m->diam, S.K, st);
-  S.inv.upload(m->inv_edges, 9 * (size_t)S.K, st);
-  S.verts.upload(reinterpret_cast<const int4*>(m->verts), S.K, st);
-  S.nbr.upload(reinterpret_cast<const int4*>(m->neighbor), S.K, st);
-  S.region.upload(m->region, S.K, st);
-  S.dof.upload(dofs->dof_of_node, S.J, st);
   // host-side per-element volume floor tau = 1e-14 * diam^3 (reference core.hpp:85)
   std::vector<double> tau(S.K);
   double rmax = 0, dmax = 0;
@@ -2243,17 +2270,29 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     if (!m->region[t]) S.h_interior.push_back(t);
   }
   S.KI = (int)S.h_interior.size();
-  {
-    std::vector<int> ipos(S.K, -1);
-    for (int i = 0; i < S.KI; ++i) ipos[S.h_interior[i]] = i;
-    S.ipos.upload(ipos.data(), S.K, st);
-  }
-  S.tau.upload(tau.data(), S.K, st);
-  S.interior.upload(S.h_interior.data(), S.KI, st);
+  std::vector<int> ipos(S.K, -1);
+  for (int i = 0; i < S.KI; ++i) ipos[S.h_interior[i]] = i;
   S.h_dof_node.assign(S.unknowns, 0);
   for (int v = 0; v < S.J; ++v)
     if (dofs->dof_of_node[v] >= 0) S.h_dof_node[dofs->dof_of_node[v]] = v;
-  S.dof_node.upload(S.h_dof_node.data(), S.unknowns, st);
+  // all inputs through the pinned staging buffer, asynchronously
+  const size_t K = (size_t)S.K, Jn = (size_t)S.J;
+  S.stage.reset(K * (3 * 8 + 8 + 8 + 8 + 72 + 16 + 16 + 1 + 4 + 8) + Jn * (24 + 4) +
+                4 * (size_t)S.KI + 4 * (size_t)S.unknowns + 16 * 256);
+  S.stage.up(S.node, m->node_xyz, 3 * Jn, st);
+  S.stage.up(S.center, m->center, 3 * K, st);
+  S.stage.up(S.radius, m->radius, K, st);
+  S.stage.up(S.vol, m->volume, K, st);
+  S.stage.up(S.diam, m->diam, K, st);
+  S.stage.up(S.inv, m->inv_edges, 9 * K, st);
+  S.stage.up(S.verts, reinterpret_cast<const int4*>(m->verts), K, st);
+  S.stage.up(S.nbr, reinterpret_cast<const int4*>(m->neighbor), K, st);
+  S.stage.up(S.region, m->region, K, st);
+  S.stage.up(S.dof, dofs->dof_of_node, Jn, st);
+  S.stage.up(S.ipos, ipos.data(), K, st);
+  S.stage.up(S.tau, tau.data(), K, st);
+  S.stage.up(S.interior, S.h_interior.data(), (size_t)S.KI, st);
+  S.stage.up(S.dof_node, S.h_dof_node.data(), (size_t)S.unknowns, st);
 
   Dev& D = S.dev;
   D.K = S.K;
@@ -2958,12 +2997,28 @@ int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* e
       throw Fail{NLFEM_GPU_ENOMEM, "out of host memory"};
     if (s->nnz_out > (long long)0x7fffffff)
       throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: nnz exceeds int32 row pointers"};
-    std::vector<long long> off(U + 1);
-    CK(cudaMemcpy(off.data(), s->ooff.p, sizeof(long long) * (U + 1), cudaMemcpyDeviceToHost));
-    for (int i = 0; i <= U; ++i) out->row_ptr[i] = (int32_t)off[i];
-    CK(cudaMemcpy(out->col_idx, s->ocols.p, sizeof(int32_t) * s->nnz_out, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(out->values, s->values.p, sizeof(double) * s->nnz_out, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(out->rhs, s->rhs.p, sizeof(double) * U, cudaMemcpyDeviceToHost));
+    // int32 row pointers on the device, then every array through the pinned
+    // staging buffer with one synchronisation
+    cudaStream_t st = s->stream;
+    const long long nnz = s->nnz_out;
+    s->rowptr32.ensure(U + 1);
+    k_ll_to_int<<<nblk(U + 1, 256), 256, 0, st>>>(U + 1, s->ooff.p, s->rowptr32.p);
+    s->stage.reset(4 * (size_t)(U + 1) + 12 * (size_t)nnz + 8 * (size_t)U + 4 * 256);
+    char* hr = s->stage.take(4 * (size_t)(U + 1));
+    char* hc = s->stage.take(4 * (size_t)nnz);
+    char* hv = s->stage.take(8 * (size_t)nnz);
+    char* hb = s->stage.take(8 * (size_t)U);
+    CK(cudaMemcpyAsync(hr, s->rowptr32.p, 4 * (size_t)(U + 1), cudaMemcpyDeviceToHost, st));
+    if (nnz) {
+      CK(cudaMemcpyAsync(hc, s->ocols.p, 4 * (size_t)nnz, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv, s->values.p, 8 * (size_t)nnz, cudaMemcpyDeviceToHost, st));
+    }
+    if (U) CK(cudaMemcpyAsync(hb, s->rhs.p, 8 * (size_t)U, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(out->row_ptr, hr, 4 * (size_t)(U + 1));
+    std::memcpy(out->col_idx, hc, 4 * (size_t)nnz);
+    std::memcpy(out->values, hv, 8 * (size_t)nnz);
+    std::memcpy(out->rhs, hb, 8 * (size_t)U);
   });
 }
 
