@@ -476,7 +476,10 @@ struct CandStage {
 //           (T', code) into its survivor slots (code 0 = no piece), in stream
 //           order; k_pairs_compact then keeps the nonzero ones.
 template <int MODE>
-__global__ void __launch_bounds__(kPairThreads, 4) k_pairs(int ii_base, int ii_end,
+#ifndef NLFEM_PAIRS_MINBLOCKS
+#define NLFEM_PAIRS_MINBLOCKS 6
+#endif
+__global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(int ii_base, int ii_end,
                                                         const long long* cand_off,
                                                         long long cand_base, int* cand_count,
                                                         int* cpartner, unsigned* cinfo,
