@@ -94,6 +94,7 @@ struct Dev {
   int strategy, mc;
   unsigned long long seed;
   uint32_t rkey[20];  // Philox4x32-10 round keys (k0 + r W0, k1 + r W1), r = 0..9
+  double inv_mc;      // 1 / mc when mc is a power of two (vol * inv_mc == vol / mc), else 0
   double C, delta, slack, inside_cut, dd;
   // element data
   const double4* erec;  // [4K]: (c, r), (v0, v1.x), (v1.yz, v2.xy), (v2.z, v3)
@@ -1036,16 +1037,21 @@ __device__ __forceinline__ int s2i(int b, int c) { return b * 4 - (b * (b - 1)) 
 
 __device__ __forceinline__ int interior_pos(int T) { return cD.ipos[T]; }
 
-// number of Monte Carlo units (sub-simplices, before the volume floor) of a pair
-__device__ __forceinline__ int pair_units(unsigned code) {
+// Monte Carlo (cap) items of a pair: whole-element caps and straddlers
+__device__ __forceinline__ int pair_cap_items(unsigned code) {
   int n = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
-    if (c == kOutCap) n += 1;
-    else if (c & kStraddle) n += outer_units((int)(c & 15));
+    n += (c == kOutCap || (c & kStraddle)) ? 1 : 0;
   }
   return n;
+}
+
+// case of a cap item: 0 = whole element T' (outside cap), m = 1..3 inside
+// vertices of a straddler (k_mc is specialised on it)
+__device__ __forceinline__ int cap_case(unsigned c) {
+  return c == kOutCap ? 0 : __popc(c & 15u);
 }
 
 // Warp-aggregated reservation in one of two lists: every lane asks for n
@@ -1073,12 +1079,13 @@ __device__ __forceinline__ int reserve2(int* counters, int kind, int n) {
   return kind ? base_b + ib - b : base_a + ia - a;
 }
 
-// Warp-aggregated reservation in one of four lists (counters[0..3]).
-__device__ __forceinline__ int reserve4(int* counters, int kind, int n) {
+// warp-aggregated reservation in four lists at once: every lane asks for n[k]
+// slots in list k and gets its first slot in base[k]
+__device__ __forceinline__ void reserve4v(int* counters, const int n[4], int base[4]) {
   const int lane = threadIdx.x & 31;
-  int own[4], incl[4];
+  int incl[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) own[k] = incl[k] = (kind == k) ? n : 0;
+  for (int k = 0; k < 4; ++k) incl[k] = n[k];
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1)
 #pragma unroll
@@ -1086,15 +1093,13 @@ __device__ __forceinline__ int reserve4(int* counters, int kind, int n) {
       const int t = __shfl_up_sync(FULLMASK, incl[k], off);
       if (lane >= off) incl[k] += t;
     }
-  int base = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     int b = 0;
     if (lane == 31 && incl[k]) b = atomicAdd(counters + k, incl[k]);
     b = __shfl_sync(FULLMASK, b, 31);
-    if (kind == k) base = b + incl[k] - own[k];
+    base[k] = b + incl[k] - n[k];
   }
-  return base;
 }
 
 __global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount,
@@ -1102,7 +1107,7 @@ __global__ void k_units_count(long long p0, long long np, const unsigned* info, 
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= np) return;
   const unsigned code = info[p0 + i];
-  ucount[i] = mc_units ? pair_units(code) : 0;
+  ucount[i] = mc_units ? pair_cap_items(code) : 0;
   int g = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) g += ((code >> (5 * q)) & kStraddle) != 0;
@@ -1142,6 +1147,8 @@ __global__ void k_gunits_fill(long long p0, long long np, const unsigned* info,
 // straddle_outer pieces, upper bound 3 or 1 before the volume floor).  Items
 // are listed by their first unit id in four lists -- (interior, constraint)
 // parent x (1, 3) slots -- so each k_mc launch runs one uniform code path.
+// cap items (one record slot each, in pair then q order) into eight lists by
+// parent kind (interior / constraint) and cap_case
 __global__ void k_units_fill(long long p0, long long np, const unsigned* info,
                              const long long* uoff, int* upair, unsigned char* uqs,
                              const int* partner, int* lists, long long lstride, int* nlist) {
@@ -1149,31 +1156,31 @@ __global__ void k_units_fill(long long p0, long long np, const unsigned* info,
   const bool act = i < np;
   const unsigned code = act ? info[p0 + i] : 0;
   const bool cons = act && cD.region[partner[p0 + i]] != 0;
-  long long u = act ? uoff[i] : 0;
-  // items of this pair, in q order
-  int n1 = 0, n3 = 0;
+  int n[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
-    if (c == kOutCap) ++n1;
-    else if (c & kStraddle) (outer_units((int)(c & 15)) == 3 ? n3 : n1) += 1;
+    if (c == kOutCap || (c & kStraddle)) ++n[cap_case(c)];
   }
-  const int kind1 = cons ? 2 : 0, kind3 = cons ? 3 : 1;
-  int b1 = reserve4(nlist, kind1, n1);
-  int b3 = reserve4(nlist, kind3, n3);
+  const int z[4] = {0, 0, 0, 0};
+  int bi[4], bc[4];
+  reserve4v(nlist, cons ? z : n, bi);
+  reserve4v(nlist + 4, cons ? n : z, bc);
   if (!act) return;
+  long long u = uoff[i];
+  int* L = lists + (cons ? 4 : 0) * lstride;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
-    int n = 0;
-    if (c == kOutCap) n = 1;
-    else if (c & kStraddle) n = outer_units((int)(c & 15));
-    if (n == 1) lists[kind1 * lstride + b1++] = (int)u;
-    if (n == 3) lists[kind3 * lstride + b3++] = (int)u;
-    for (int sb = 0; sb < n; ++sb, ++u) {
-      upair[u] = (int)i;
-      uqs[u] = (unsigned char)(q | (sb << 2));
-    }
+    if (!(c == kOutCap || (c & kStraddle))) continue;
+    const int k = cap_case(c);
+    const int slot = (cons ? bc[k] : bi[k]);
+    if (cons) ++bc[k];
+    else ++bi[k];
+    L[k * lstride + slot] = (int)u;
+    upair[u] = (int)i;
+    uqs[u] = (unsigned char)q;
+    ++u;
   }
 }
 
@@ -1332,57 +1339,6 @@ __device__ __forceinline__ unsigned long long gauss_item(const Vd vP[4], int mas
          (unsigned long long)kept * (CONS ? 160 : 360);
 }
 
-// Inner pieces of a straddling item for fullcaps, in the Monte Carlo record's
-// form: S0 = sum vol, and (interior parent) the exact Cartesian moments about
-// v0(T') of the pieces -- int r' = vol/4 sum_j p'_j, int r' r'^T =
-// vol/20 (sum_j p'_j p'_j^T + (sum p')(sum p')^T) with p' = p - v0(T') -- which
-// the combine maps through the barycentric Jacobian like the cap moments
-// (the reference's degree-2 rule integrates lambda, lambda lambda^T exactly);
-// (constraint parent) sum vol/4 g at the degree-2 points.  Returns the ledger.
-template <bool CONS>
-__device__ __forceinline__ unsigned long long inner_moments(const Vd* vP, int mask, double tau,
-                                                         const Crossings& X, double* out) {
-  const Straddle st = inner_straddle_x(vP, mask, X);
-  int kept = 0;
-  for (int k = 0; k < st.n; ++k) {
-    Vd pa, pb, pc, pd;
-    straddle_piece(st, k, pa, pb, pc, pd);
-    const double vol = tet_volume(pa, pb, pc, pd);
-    if (!(vol > tau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
-    ++kept;
-    out[0] += vol;
-    if (CONS) {
-      const Vd pv[4] = {pa, pb, pc, pd};
-      double sg = 0;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), sg);
-      out[1] += sg;
-    } else {
-      const Vd q[4] = {vsub(pa, vP[0]), vsub(pb, vP[0]), vsub(pc, vP[0]), vsub(pd, vP[0])};
-      const Vd sp = vadd(vadd(q[0], q[1]), vadd(q[2], q[3]));
-      const double v4 = vol * 0.25, v20 = vol / 20.0;
-      out[1] += v4 * sp.x;
-      out[2] += v4 * sp.y;
-      out[3] += v4 * sp.z;
-      double m2[6] = {sp.x * sp.x, sp.x * sp.y, sp.x * sp.z, sp.y * sp.y, sp.y * sp.z, sp.z * sp.z};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        m2[0] = fma(q[j].x, q[j].x, m2[0]);
-        m2[1] = fma(q[j].x, q[j].y, m2[1]);
-        m2[2] = fma(q[j].x, q[j].z, m2[2]);
-        m2[3] = fma(q[j].y, q[j].y, m2[3]);
-        m2[4] = fma(q[j].y, q[j].z, m2[4]);
-        m2[5] = fma(q[j].z, q[j].z, m2[5]);
-      }
-#pragma unroll
-      for (int kk = 0; kk < 6; ++kk) out[4 + kk] += v20 * m2[kk];
-    }
-  }
-  const int m = __popc(mask);
-  return 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
-         (unsigned long long)kept * (CONS ? 160 : 360);
-}
-
 // Monte Carlo: one thread per cap item; each kept sub-simplex (piece) gets M
 // samples of the mode-P stream (include/nlfem_mc_stream.h).  Writes one record
 // per item, at the item's first unit slot (record of kMomStride doubles): the weighted
@@ -1425,26 +1381,136 @@ __device__ __forceinline__ void poly2_taylor(const Poly& P, Vd x, double& g0, do
 #ifndef NLFEM_MC_MINBLOCKS
 #define NLFEM_MC_MINBLOCKS 4
 #endif
+
+// |det(b - a, c - a, d - a)|: six times tet_volume(a, b, c, d) before its
+// division (reference ball_approx.cpp:144-146 divides by 6 after fabs)
+__device__ __forceinline__ double tet_det6(Vd a, Vd b, Vd c, Vd d) {
+  return fabs(vdot(vcross(vsub(b, a), vsub(c, a)), vsub(d, a)));
+}
+
+// A prism A0 A1 A2 | B0 B1 B2 and the volumes of its split
+// (A0A1A2B0, A1A2B0B1, A2B0B1B2) (reference ball_approx.cpp:150-155)
+struct Prism {
+  Vd A0, A1, A2, B0, B1, B2;
+  double v[3];
+};
+
+__device__ __forceinline__ void prism_volumes(Prism& P) {
+  P.v[0] = tet_det6(P.A0, P.A1, P.A2, P.B0) / 6.0;
+  P.v[1] = tet_det6(P.A1, P.A2, P.B0, P.B1) / 6.0;
+  P.v[2] = tet_det6(P.A2, P.B0, P.B1, P.B2) / 6.0;
+}
+
+// split_warped_prism (reference ball_approx.cpp:160-175): the orientation
+// whose three volumes sum larger (vb > va swaps A1/A2 and B1/B2).  Decided
+// from the undivided determinants when they differ by more than 1e-12
+// (far above the few-ulp difference the /6 and the sums can make);
+// otherwise from the reference's exact expressions.  The chosen
+// orientation's volumes are the split's piece volumes, bit for bit.
+__device__ __forceinline__ void warped_prism(Prism& P) {
+  const double a0 = tet_det6(P.A0, P.A1, P.A2, P.B0), a1 = tet_det6(P.A1, P.A2, P.B0, P.B1),
+               a2 = tet_det6(P.A2, P.B0, P.B1, P.B2);
+  const double b0 = tet_det6(P.A0, P.A2, P.A1, P.B0), b1 = tet_det6(P.A2, P.A1, P.B0, P.B2),
+               b2 = tet_det6(P.A1, P.B0, P.B2, P.B1);
+  const double sa = a0 + a1 + a2, sb = b0 + b1 + b2;
+  bool swap;
+  if (sb > sa * (1.0 + 1e-12)) swap = true;
+  else if (sb < sa * (1.0 - 1e-12)) swap = false;
+  else swap = (b0 / 6.0 + b1 / 6.0) + b2 / 6.0 > (a0 / 6.0 + a1 / 6.0) + a2 / 6.0;
+  if (swap) {
+    const Vd t = P.A1;
+    P.A1 = P.A2;
+    P.A2 = t;
+    const Vd u = P.B1;
+    P.B1 = P.B2;
+    P.B2 = u;
+    P.v[0] = b0 / 6.0;
+    P.v[1] = b1 / 6.0;
+    P.v[2] = b2 / 6.0;
+  } else {
+    P.v[0] = a0 / 6.0;
+    P.v[1] = a1 / 6.0;
+    P.v[2] = a2 / 6.0;
+  }
+}
+
+// vertex `slot` of element t from its 128-byte element record
+__device__ __forceinline__ Vd elem_vertex(int t, int slot) {
+  const double* e = reinterpret_cast<const double*>(cD.erec + 4 * (long long)t);
+  return {e[4 + 3 * slot], e[5 + 3 * slot], e[6 + 3 * slot]};
+}
+
+// One inner piece (Gauss rule, reference AsmSink::sub, assembly.cpp:332-381) of
+// a fullcaps straddler, added to the item's record in the Monte Carlo form:
+// S0 += vol and (interior parent) the exact Cartesian moments about v0(T'),
+// int r' = vol/4 sum_j p'_j, int r' r'^T = vol/20 (sum_j p'_j p'_j^T + s s^T),
+// s = sum_j p'_j (the reference's degree-2 rule is exact for lambda and
+// lambda lambda^T, which the combine recovers through the barycentric
+// Jacobian); (constraint parent) sum_g vol/4 g at the degree-2 points.
+template <bool CONS>
+__device__ __forceinline__ void inner_piece(Vd a, Vd b, Vd c, Vd d, double vol, double tau,
+                                            Vd v0, double* acc, int& kept) {
+  if (!(vol > tau)) return;  // push_piece volume floor (ball_approx.cpp:141)
+  ++kept;
+  acc[0] += vol;
+  if (CONS) {
+    const Vd pv[4] = {a, b, c, d};
+    double sg = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), sg);
+    acc[1] += sg;
+  } else {
+    const Vd q[4] = {vsub(a, v0), vsub(b, v0), vsub(c, v0), vsub(d, v0)};
+    const Vd sp = vadd(vadd(q[0], q[1]), vadd(q[2], q[3]));
+    const double v4 = vol * 0.25, v20 = vol / 20.0;
+    acc[1] += v4 * sp.x;
+    acc[2] += v4 * sp.y;
+    acc[3] += v4 * sp.z;
+    double m2[6] = {sp.x * sp.x, sp.x * sp.y, sp.x * sp.z, sp.y * sp.y, sp.y * sp.z, sp.z * sp.z};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      m2[0] = fma(q[j].x, q[j].x, m2[0]);
+      m2[1] = fma(q[j].x, q[j].y, m2[1]);
+      m2[2] = fma(q[j].x, q[j].z, m2[2]);
+      m2[3] = fma(q[j].y, q[j].y, m2[3]);
+      m2[4] = fma(q[j].y, q[j].z, m2[4]);
+      m2[5] = fma(q[j].z, q[j].z, m2[5]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 6; ++kk) acc[4 + kk] += v20 * m2[kk];
+  }
+}
+
 // CONS: constraint parent (accumulates sum g(y) instead of basis moments).
 // G2: g has total degree <= 2, so sum_hits g(x_q + r) follows exactly from the
 // hit count, sum r and sum r r^T -- the same branch-free moments as interior
 // parents -- instead of one polynomial evaluation per hit.
-template <bool CONS, bool G2, int NU>
-__global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nunits,
+// CASE: 0 = whole element T' (one outer piece); m = 1, 2, 3 inside vertices of a
+// straddler -- straddle_inner + straddle_outer (reference ball_approx.cpp:
+// 195-298) with every index static: T''s vertices are loaded in crossing order
+// (inside slots ascending, then outside slots ascending), crossing k = (i, o)
+// at k = i (4 - m) + o.  Outer pieces: m = 1 prism {q0 q1 q2 | w1 w2 w3},
+// m = 2 warped prism {w2 q0 q2 | w3 q1 q3}, m = 3 tet (w3 q0 q1 q2); inner
+// pieces: m = 1 tet (w0 q0 q1 q2), m = 2 warped prism {w0 q0 q1 | w1 q2 q3},
+// m = 3 prism {w0 w1 w2 | q0 q1 q2}.
+template <bool CONS, bool G2, int CASE>
+__global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nitems,
                                                       const int* list, int nlist,
                                                       const int* upair, const unsigned char* uqs,
                                                       const int* pair_outer, const int* partner,
                                                       const unsigned* info, double* mom,
                                                       unsigned long long* mc_stats) {
-  // one thread per cap item: the straddle_outer decomposition is computed once
-  // and each kept piece (unit u0 + j) gets its M samples; a straddling item
-  // first does its inner pieces' Gauss unit from the same crossings
+  constexpr int NOUT = (CASE == 1 || CASE == 2) ? 3 : 1;  // outer pieces
+  constexpr int NV = CONS ? 2 : 10;                       // record doubles
+  __shared__ double sP[NOUT == 3 ? 18 : 1][kMcThreads];  // outer prism points
+  __shared__ double sV[NOUT == 3 ? 3 : 1][kMcThreads];   // outer piece volumes
+  __shared__ double sAcc[NV][kMcThreads];
   const int li = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long draws = 0, hits = 0, led = 0;
   if (li < nlist) {
-    const long long u0 = list[li];
-    const int pi = upair[u0];
-    const int q = uqs[u0] & 3;
+    const long long u = list[li];
+    const int pi = upair[u];
+    const int q = uqs[u];
     const long long p = p0 + pi;
     const int T = cD.interior[pair_outer[pi]];
     const int Tp = partner[p];
@@ -1452,75 +1518,111 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     Vd vT[4];
     load_verts(T, vT);
     const Vd xq = quad_point(vT, q);
-    Vd vP[4];
-    load_verts(Tp, vP);
-    Straddle st;
-    int npieces;
-    double seed[CONS ? 2 : 10];
+    const Vd v0P = elem_vertex(Tp, 0);
+    const double tau = cD.tau[Tp];
+    double acc[NV];
 #pragma unroll
-    for (int kk = 0; kk < (CONS ? 2 : 10); ++kk) seed[kk] = 0.0;
-    if (c == kOutCap) {  // whole element (reference assembly.cpp:754-759)
-      st.A0 = vP[0]; st.A1 = vP[1]; st.A2 = vP[2]; st.B0 = vP[3];
-      st.B1 = vP[3]; st.B2 = vP[3];
-      st.n = 1;
-      npieces = 1;
-    } else {  // straddle_inner + straddle_outer (reference ball_approx.cpp:195-298)
-      const int mask = (int)(c & 15);
-      Crossings X;
-      crossings4(vP, mask, xq, cD.delta, X);
-      // the inner pieces (Gauss rule, reference AsmSink::sub, assembly.cpp:332-381)
-      // seed the item's record in the Monte Carlo units' own form
-      led += inner_moments<CONS>(vP, mask, cD.tau[Tp], X, seed);
-      st = outer_straddle_x(vP, mask, X);
-      npieces = st.n;
-      const int m = __popc(c & 15);
-      led += 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 3 : 1));
-    }
-    // three-piece items: park the six straddle points in shared memory (column
-    // per thread) so the sampling loop does not carry them in registers
-    __shared__ double sP[NU == 3 ? 18 : 1][kMcThreads];
-    if (NU == 3) {
-      const Vd P6[6] = {st.A0, st.A1, st.A2, st.B0, st.B1, st.B2};
+    for (int kk = 0; kk < NV; ++kk) acc[kk] = 0.0;
+    Vd pa, pb, pc, pd;  // the single outer piece (NOUT == 1)
+    double vol1 = 0;
+    if constexpr (CASE == 0) {  // whole element (reference assembly.cpp:754-759): no volume floor
+      pa = v0P;
+      pb = elem_vertex(Tp, 1);
+      pc = elem_vertex(Tp, 2);
+      pd = elem_vertex(Tp, 3);
+      vol1 = tet_det6(pa, pb, pc, pd) / 6.0;
+    } else {
+      constexpr int m = CASE, mo = 4 - CASE;
+      const unsigned mask = c & 15u, om = ~mask & 15u;
+      Vd w[4];
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        sP[3 * k][threadIdx.x] = P6[k].x;
-        sP[3 * k + 1][threadIdx.x] = P6[k].y;
-        sP[3 * k + 2][threadIdx.x] = P6[k].z;
+      for (int j = 0; j < 4; ++j)
+        w[j] = elem_vertex(Tp, j < m ? nth_bit4(mask, j) : nth_bit4(om, j - m));
+      // crossing_points (reference geometry.cpp:39-50)
+      Vd X[m * mo];
+#pragma unroll
+      for (int i = 0; i < m; ++i)
+#pragma unroll
+        for (int o = 0; o < mo; ++o) {
+          const Vd a = w[i], b = w[m + o];
+          const double t = edge_crossing(a, b, xq, cD.delta);
+          X[i * mo + o] = vadd(a, vscale(t, vsub(b, a)));
+        }
+      int kin = 0;
+      if constexpr (CASE == 1) {
+        inner_piece<CONS>(w[0], X[0], X[1], X[2], tet_det6(w[0], X[0], X[1], X[2]) / 6.0, tau,
+                          v0P, acc, kin);
+        Prism P{X[0], X[1], X[2], w[1], w[2], w[3], {0, 0, 0}};
+        prism_volumes(P);
+        const Vd P6[6] = {P.A0, P.A1, P.A2, P.B0, P.B1, P.B2};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          sP[3 * k][threadIdx.x] = P6[k].x;
+          sP[3 * k + 1][threadIdx.x] = P6[k].y;
+          sP[3 * k + 2][threadIdx.x] = P6[k].z;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sV[k][threadIdx.x] = P.v[k];
+      } else if constexpr (CASE == 2) {
+        {
+          Prism I{w[0], X[0], X[1], w[1], X[2], X[3], {0, 0, 0}};
+          warped_prism(I);
+          inner_piece<CONS>(I.A0, I.A1, I.A2, I.B0, I.v[0], tau, v0P, acc, kin);
+          inner_piece<CONS>(I.A1, I.A2, I.B0, I.B1, I.v[1], tau, v0P, acc, kin);
+          inner_piece<CONS>(I.A2, I.B0, I.B1, I.B2, I.v[2], tau, v0P, acc, kin);
+        }
+        Prism P{w[2], X[0], X[2], w[3], X[1], X[3], {0, 0, 0}};
+        warped_prism(P);
+        const Vd P6[6] = {P.A0, P.A1, P.A2, P.B0, P.B1, P.B2};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          sP[3 * k][threadIdx.x] = P6[k].x;
+          sP[3 * k + 1][threadIdx.x] = P6[k].y;
+          sP[3 * k + 2][threadIdx.x] = P6[k].z;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sV[k][threadIdx.x] = P.v[k];
+      } else {  // CASE == 3
+        {
+          Prism I{w[0], w[1], w[2], X[0], X[1], X[2], {0, 0, 0}};
+          prism_volumes(I);
+          inner_piece<CONS>(I.A0, I.A1, I.A2, I.B0, I.v[0], tau, v0P, acc, kin);
+          inner_piece<CONS>(I.A1, I.A2, I.B0, I.B1, I.v[1], tau, v0P, acc, kin);
+          inner_piece<CONS>(I.A2, I.B0, I.B1, I.B2, I.v[2], tau, v0P, acc, kin);
+        }
+        pa = w[3];
+        pb = X[0];
+        pc = X[1];
+        pd = X[2];
+        vol1 = tet_det6(pa, pb, pc, pd) / 6.0;
       }
+      // ledger: straddle_inner + straddle_outer crossings and volumes, Gauss pieces
+      led += 2ull * 38ull * (m * mo) + 24ull * (m == 2 ? 18 : 4) +
+             (unsigned long long)kin * (CONS ? 160 : 360);
     }
-    const Vd v0P = vP[0];
-    __shared__ double sAcc[CONS ? 2 : 10][kMcThreads];
 #pragma unroll
-    for (int kk = 0; kk < (CONS ? 2 : 10); ++kk) sAcc[kk][threadIdx.x] = seed[kk];
-    const double tau = c == kOutCap ? -1.0 : cD.tau[Tp];
+    for (int kk = 0; kk < NV; ++kk) sAcc[kk][threadIdx.x] = acc[kk];
     const int M = cD.mc;
     const double dd = cD.dd;
+    const double otau = CASE == 0 ? -1.0 : tau;
     double g0 = 0, gr[3] = {0, 0, 0}, H[6] = {0, 0, 0, 0, 0, 0};
     if (CONS && G2) poly2_taylor(cD.g, xq, g0, gr, H);
     int kept = 0;
 #pragma unroll 1
-    for (int k = 0; k < NU; ++k) {
-      Vd pa, pb, pc, pd;
-      double vol = 0;
-      bool use = k < npieces;
-      if (use) {
-        if (NU == 3) {
-          Vd* pv[4] = {&pa, &pb, &pc, &pd};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = 3 * (k + j);
-            *pv[j] = {sP[r][threadIdx.x], sP[r + 1][threadIdx.x], sP[r + 2][threadIdx.x]};
-          }
-        } else {
-          straddle_piece(st, k, pa, pb, pc, pd);
-        }
-        vol = tet_volume(pa, pb, pc, pd);
-        use = vol > tau;  // push_piece volume floor (ball_approx.cpp:141)
+    for (int k = 0; k < NOUT; ++k) {
+      double vol = vol1;
+      if (NOUT == 3) {  // prism piece k = points k .. k+3
+        const int r = 3 * k;
+        pa = {sP[r][threadIdx.x], sP[r + 1][threadIdx.x], sP[r + 2][threadIdx.x]};
+        pb = {sP[r + 3][threadIdx.x], sP[r + 4][threadIdx.x], sP[r + 5][threadIdx.x]};
+        pc = {sP[r + 6][threadIdx.x], sP[r + 7][threadIdx.x], sP[r + 8][threadIdx.x]};
+        pd = {sP[r + 9][threadIdx.x], sP[r + 10][threadIdx.x], sP[r + 11][threadIdx.x]};
+        vol = sV[k][threadIdx.x];
       }
-      if (!use) continue;
+      if (!(vol > otau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
       const uint32_t c2 = (uint32_t)q | ((uint32_t)kept << 2);
       ++kept;
-      const double w = vol / M;
+      const double w = cD.inv_mc > 0 ? vol * cD.inv_mc : vol / M;  // vol / M
       nlfem_mc_frame fr;
       {
         const double a0[3] = {pa.x, pa.y, pa.z}, a1[3] = {pb.x, pb.y, pb.z},
@@ -1573,44 +1675,42 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       const unsigned nh = (CONS && !G2) ? ngh : hm.n;
       const double t1x = hm.t1x, t1y = hm.t1y, t1z = hm.t1z;
       const double* t2 = hm.t2;
-      double S0 = w * nh, m1x = 0, m1y = 0, m1z = 0, m2[6] = {0, 0, 0, 0, 0, 0}, sg = 0;
+      double vals[NV];
+      vals[0] = w * nh;
       if (CONS && G2) {
         // sum over hits of g(x_q + r) = n g + grad g . sum r + 1/2 sum H_ab r_a r_b
         const double n = (double)nh;
         const double quad = 0.5 * (H[0] * t2[0] + H[3] * t2[3] + H[5] * t2[5]) +
                             H[1] * t2[1] + H[2] * t2[2] + H[4] * t2[4];
-        sg = w * (n * g0 + gr[0] * t1x + gr[1] * t1y + gr[2] * t1z + quad);
+        vals[1] = w * (n * g0 + gr[0] * t1x + gr[1] * t1y + gr[2] * t1z + quad);
       } else if (CONS) {
-        sg = w * ng;
+        vals[1] = w * ng;
       } else {
         // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
         const double c0x = xq.x - v0P.x, c0y = xq.y - v0P.y, c0z = xq.z - v0P.z;
         const double n = (double)nh;
-        m1x = w * (t1x + n * c0x);
-        m1y = w * (t1y + n * c0y);
-        m1z = w * (t1z + n * c0z);
-        m2[0] = w * (t2[0] + 2.0 * c0x * t1x + n * c0x * c0x);
-        m2[1] = w * (t2[1] + c0x * t1y + c0y * t1x + n * c0x * c0y);
-        m2[2] = w * (t2[2] + c0x * t1z + c0z * t1x + n * c0x * c0z);
-        m2[3] = w * (t2[3] + 2.0 * c0y * t1y + n * c0y * c0y);
-        m2[4] = w * (t2[4] + c0y * t1z + c0z * t1y + n * c0y * c0z);
-        m2[5] = w * (t2[5] + 2.0 * c0z * t1z + n * c0z * c0z);
+        vals[1] = w * (t1x + n * c0x);
+        vals[2 % NV] = w * (t1y + n * c0y);
+        vals[3 % NV] = w * (t1z + n * c0z);
+        vals[4 % NV] = w * (t2[0] + 2.0 * c0x * t1x + n * c0x * c0x);
+        vals[5 % NV] = w * (t2[1] + c0x * t1y + c0y * t1x + n * c0x * c0y);
+        vals[6 % NV] = w * (t2[2] + c0x * t1z + c0z * t1x + n * c0x * c0z);
+        vals[7 % NV] = w * (t2[3] + 2.0 * c0y * t1y + n * c0y * c0y);
+        vals[8 % NV] = w * (t2[4] + c0y * t1z + c0z * t1y + n * c0y * c0z);
+        vals[9 % NV] = w * (t2[5] + 2.0 * c0z * t1z + n * c0z * c0z);
       }
       draws += (unsigned long long)M;
       hits += nh;
       led += 25ull + 35ull * (unsigned long long)M + (CONS ? 12ull : 62ull) * nh;
       // item totals: inner pieces, then the kept outer pieces in piece order
-      const double vals[10] = {S0, CONS ? sg : m1x, m1y, m1z, m2[0], m2[1], m2[2], m2[3], m2[4], m2[5]};
-      constexpr int nv = CONS ? 2 : 10;
 #pragma unroll
-      for (int kk = 0; kk < nv; ++kk) sAcc[kk][threadIdx.x] += vals[kk];
+      for (int kk = 0; kk < NV; ++kk) sAcc[kk][threadIdx.x] += vals[kk];
     }
-    // one record per item at its first unit slot: S0, then sum g (constraint
-    // parents) or sum r' and sum r' r'^T (6) about v0(T'), inner pieces included
-    constexpr int nv = CONS ? 2 : 10;
-    double2* rec = reinterpret_cast<double2*>(mom + kMomStride * u0);
+    // one record per cap item: S0, then sum g (constraint parents) or sum r'
+    // and sum r' r'^T (6) about v0(T') (interior parents), inner pieces included
+    double2* rec = reinterpret_cast<double2*>(mom + kMomStride * u);
 #pragma unroll
-    for (int kk = 0; kk < nv; kk += 2)
+    for (int kk = 0; kk < NV; kk += 2)
       rec[kk / 2] = make_double2(sAcc[kk][threadIdx.x], sAcc[kk + 1][threadIdx.x]);
   }
   // statistics
@@ -1807,8 +1907,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
       }
       // Monte Carlo units of this item, in sub-simplex order
       if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
-        // the item's record (k_mc sums its pieces) sits at its first unit slot
-        const int nu = c == kOutCap ? 1 : outer_units((int)(c & 15));
+        // the cap item's record (k_mc: inner + outer pieces)
         double g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
         const double2* rec = reinterpret_cast<const double2*>(mom + kMomStride * u);
         const double2 r0 = rec[0];
@@ -1827,7 +1926,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
           m2[4] = r4.x;
           m2[5] = r4.y;
         }
-        u += nu;
+        ++u;
         S0 += n0;
         if (constr) {
           Sg += g0;
@@ -2305,6 +2404,9 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.strategy = cfg->strategy;
   D.mc = cfg->mc_samples;
   D.seed = cfg->seed;
+  D.inv_mc = (cfg->mc_samples > 0 && (cfg->mc_samples & (cfg->mc_samples - 1)) == 0)
+                 ? std::ldexp(1.0, -(int)std::log2((double)cfg->mc_samples))
+                 : 0.0;
   for (int r = 0; r < 10; ++r) {
     D.rkey[2 * r] = (uint32_t)(cfg->seed & 0xffffffffu) + (uint32_t)r * NLFEM_PHILOX_W0;
     D.rkey[2 * r + 1] = (uint32_t)(cfg->seed >> 32) + (uint32_t)r * NLFEM_PHILOX_W1;
@@ -2703,8 +2805,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
                                                            S.pair_outer.p);
         S.launches += 2;
-        S.nlist.ensure(8);
-        CK(cudaMemsetAsync(S.nlist.p, 0, 8 * sizeof(int), st));
+        S.nlist.ensure(16);
+        CK(cudaMemsetAsync(S.nlist.p, 0, 16 * sizeof(int), st));
         if (need_gauss) {
           scan64(S, S.gcount.p, true, np, S.goff.p, st);
           ngunits = read_ll(S.goff.p + np, st);
@@ -2723,14 +2825,14 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
           S.upair.ensure(nunits + 1);
           S.uqs.ensure(nunits + 1);
           S.mom.ensure(kMomStride * (size_t)(nunits + 1));
-          S.ulist.ensure(4 * (size_t)(nunits + 1));
+          S.ulist.ensure(8 * (size_t)(nunits + 1));
           k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p,
                                                       S.uqs.p, S.partner.p, S.ulist.p,
                                                       nunits + 1, S.nlist.p + 4);
           ++S.launches;
         }
-        int nl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        int nl[16] = {0};
+        CK(cudaMemcpyAsync(nl, S.nlist.p, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaEventRecord(S.ev[6], st));
         cudaStream_t s3 = S.stream3;
@@ -2759,14 +2861,22 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
                 S.info.p, S.mom.p, S.counters.p + 1);
             ++S.launches;
           };
-          launch(k_mc<false, false, 3>, 1, st);
-          launch(k_mc<false, false, 1>, 0, s3);
+          // lists 0..3: interior parents by cap case, 4..7: constraint parents;
+          // the big straddle lists on `stream`, the rest beside them on s3
+          launch(k_mc<false, false, 2>, 2, st);
+          launch(k_mc<false, false, 1>, 1, st);
+          launch(k_mc<false, false, 3>, 3, s3);
+          launch(k_mc<false, false, 0>, 0, s3);
           if (S.g_deg <= 2) {
-            launch(k_mc<true, true, 3>, 3, st);
-            launch(k_mc<true, true, 1>, 2, s3);
+            launch(k_mc<true, true, 2>, 6, st);
+            launch(k_mc<true, true, 1>, 5, st);
+            launch(k_mc<true, true, 3>, 7, s3);
+            launch(k_mc<true, true, 0>, 4, s3);
           } else {
-            launch(k_mc<true, false, 3>, 3, st);
-            launch(k_mc<true, false, 1>, 2, s3);
+            launch(k_mc<true, false, 2>, 6, st);
+            launch(k_mc<true, false, 1>, 5, st);
+            launch(k_mc<true, false, 3>, 7, s3);
+            launch(k_mc<true, false, 0>, 4, s3);
           }
         }
         CK(cudaEventRecord(S.ev[11], s3));  // join
