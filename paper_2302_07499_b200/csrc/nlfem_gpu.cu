@@ -1054,30 +1054,6 @@ __device__ __forceinline__ int cap_case(unsigned c) {
   return c == kOutCap ? 0 : __popc(c & 15u);
 }
 
-// Warp-aggregated reservation in one of two lists: every lane asks for n
-// slots in list `kind` (0/1); one atomic per warp and list.  Whole warps must
-// call it (inactive lanes pass n = 0).
-__device__ __forceinline__ int reserve2(int* counters, int kind, int n) {
-  const int lane = threadIdx.x & 31;
-  int a = kind ? 0 : n, b = kind ? n : 0;
-  int ia = a, ib = b;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int ta = __shfl_up_sync(FULLMASK, ia, off), tb = __shfl_up_sync(FULLMASK, ib, off);
-    if (lane >= off) {
-      ia += ta;
-      ib += tb;
-    }
-  }
-  int base_a = 0, base_b = 0;
-  if (lane == 31) {
-    if (ia) base_a = atomicAdd(counters, ia);
-    if (ib) base_b = atomicAdd(counters + 1, ib);
-  }
-  base_a = __shfl_sync(FULLMASK, base_a, 31);
-  base_b = __shfl_sync(FULLMASK, base_b, 31);
-  return kind ? base_b + ib - b : base_a + ia - a;
-}
 
 // warp-aggregated reservation in four lists at once: every lane asks for n[k]
 // slots in list k and gets its first slot in base[k]
@@ -1102,42 +1078,12 @@ __device__ __forceinline__ void reserve4v(int* counters, const int n[4], int bas
   }
 }
 
-__global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount,
-                              int* gcount, int mc_units) {
+__global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= np) return;
-  const unsigned code = info[p0 + i];
-  ucount[i] = mc_units ? pair_cap_items(code) : 0;
-  int g = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) g += ((code >> (5 * q)) & kStraddle) != 0;
-  gcount[i] = g;
+  ucount[i] = pair_cap_items(info[p0 + i]);
 }
 
-// Gauss units: one per straddling (T, q, T') item; same list split by parent kind
-__global__ void k_gunits_fill(long long p0, long long np, const unsigned* info,
-                              const long long* goff, int* gpair, unsigned char* gq,
-                              const int* partner, int* list_int, int* list_con, int* nlist) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool act = i < np;
-  long long u = act ? goff[i] : 0;
-  const int nu = act ? (int)(goff[i + 1] - u) : 0;
-  const bool cons = act && nu > 0 && cD.region[partner[p0 + i]] != 0;
-  const int base = reserve2(nlist, cons ? 1 : 0, nu);
-  if (!act || nu == 0) return;
-  const unsigned code = info[p0 + i];
-  int* lst = cons ? list_con : list_int;
-  int k = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if ((code >> (5 * q)) & kStraddle) {
-      gpair[u] = (int)i;
-      gq[u] = (unsigned char)q;
-      lst[base + k] = (int)u;
-      ++u;
-      ++k;
-    }
-}
 
 // unit descriptors: pair index (chunk-relative) and (q | sub << 2); unit ids
 // are also listed per parent kind (interior / constraint) so each Monte Carlo
@@ -1184,11 +1130,13 @@ __global__ void k_units_fill(long long p0, long long np, const unsigned* info,
   }
 }
 
+// outer element of every pair of the chunk: warp per outer element
 __global__ void k_pair_outer(int ii0, int ii1, const long long* pair_off, long long P0,
                              int* pair_outer) {
-  const int ii = ii0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int ii = ii0 + (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (ii >= ii1) return;
-  for (long long p = pair_off[ii]; p < pair_off[ii + 1]; ++p) pair_outer[p - P0] = ii;
+  for (long long p = pair_off[ii] + (threadIdx.x & 31); p < pair_off[ii + 1]; p += 32)
+    pair_outer[p - P0] = ii;
 }
 
 // Philox4x32-10 on three counters in lockstep (independent chains -> ILP 3);
@@ -1265,79 +1213,6 @@ struct HitMoments {
 };
 
 constexpr long long kMomStride = 10;   // doubles per MC item record (80 B)
-constexpr long long kGmomStride = 16;  // doubles per Gauss unit record (128 B)
-
-// Gauss rule on the inner sub-simplices of one straddling item (reference
-// AsmSink::sub + accumulate_point, assembly.cpp:332-381), from the item's
-// crossings.  Writes one 128-byte record: S0, then Sg (constraint parent) or
-// S1 (4), S2 (10, upper triangle) (interior parent).  Returns the FLOP ledger.
-template <bool CONS>
-__device__ __forceinline__ unsigned long long gauss_item(const Vd vP[4], int mask, double tau,
-                                                         const Crossings& X, double* out) {
-  const Straddle st = inner_straddle_x(vP, mask, X);
-  double S0 = 0, Sg = 0, S1[4] = {0, 0, 0, 0}, S2[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  int kept = 0;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (k >= st.n) break;
-    Vd pa, pb, pc, pd;
-    straddle_piece(st, k, pa, pb, pc, pd);
-    const double vol = tet_volume(pa, pb, pc, pd);
-    if (!(vol > tau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
-    ++kept;
-    S0 += vol;
-    if (CONS) {
-      // degree-2 Gauss points with g (reference AsmSink::sub, assembly.cpp:372-381)
-      const Vd pv[4] = {pa, pb, pc, pd};
-#pragma unroll
-      for (int g = 0; g < 4; ++g) Sg = fma(vol * 0.25, poly_eval(cD.g, quad_point(pv, g)), Sg);
-    } else {
-      // The reference integrates lambda and lambda lambda^T with the degree-2
-      // rule, which is exact for them; the same values follow in closed form
-      // from the barycentric coordinates L_j of the piece's vertices in T'
-      // (parent vertex e_a; crossing at t on edge a->b: (1-t) e_a + t e_b):
-      //   int lambda = vol/4 sum_j L_j,
-      //   int lambda lambda^T = vol/20 (sum_j L_j L_j^T + (sum_j L_j)(sum_j L_j)^T).
-      double L[4][4], sl[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int a = st.la[k + j], b = st.lb[k + j];
-        const double t = st.lt[k + j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          L[j][i] = (i == a ? 1.0 - t : 0.0) + (i == b ? t : 0.0);
-          sl[i] += L[j][i];
-        }
-      }
-      const double v4 = vol * 0.25, v20 = vol / 20.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        S1[i] = fma(v4, sl[i], S1[i]);
-#pragma unroll
-        for (int jj = i; jj < 4; ++jj) {
-          double mm = sl[i] * sl[jj];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) mm = fma(L[j][i], L[j][jj], mm);
-          S2[s2i(i, jj)] = fma(v20, mm, S2[s2i(i, jj)]);
-        }
-      }
-    }
-  }
-  double2* rec = reinterpret_cast<double2*>(out);
-  if (CONS) {
-    rec[0] = make_double2(S0, Sg);
-  } else {
-    rec[0] = make_double2(S0, S1[0]);
-    rec[1] = make_double2(S1[1], S1[2]);
-    rec[2] = make_double2(S1[3], S2[0]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) rec[3 + k] = make_double2(S2[1 + 2 * k], S2[2 + 2 * k]);
-    rec[7] = make_double2(S2[9], 0.0);
-  }
-  const int m = __popc(mask);
-  return 38ull * (m * (4 - m)) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3)) +
-         (unsigned long long)kept * (CONS ? 160 : 360);
-}
 
 // Monte Carlo: one thread per cap item; each kept sub-simplex (piece) gets M
 // samples of the mode-P stream (include/nlfem_mc_stream.h).  Writes one record
@@ -1493,17 +1368,19 @@ __device__ __forceinline__ void inner_piece(Vd a, Vd b, Vd c, Vd d, double vol, 
 // m = 2 warped prism {w2 q0 q2 | w3 q1 q3}, m = 3 tet (w3 q0 q1 q2); inner
 // pieces: m = 1 tet (w0 q0 q1 q2), m = 2 warped prism {w0 q0 q1 | w1 q2 q3},
 // m = 3 prism {w0 w1 w2 | q0 q1 q2}.
-template <bool CONS, bool G2, int CASE>
+// OUTER = false (nocaps): the inner pieces only, no Monte Carlo.
+template <bool CONS, bool G2, int CASE, bool OUTER = true>
 __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nitems,
                                                       const int* list, int nlist,
                                                       const int* upair, const unsigned char* uqs,
                                                       const int* pair_outer, const int* partner,
                                                       const unsigned* info, double* mom,
                                                       unsigned long long* mc_stats) {
-  constexpr int NOUT = (CASE == 1 || CASE == 2) ? 3 : 1;  // outer pieces
+  constexpr int NOUT = !OUTER ? 0 : ((CASE == 1 || CASE == 2) ? 3 : 1);  // outer pieces
   constexpr int NV = CONS ? 2 : 10;                       // record doubles
   __shared__ double sP[NOUT == 3 ? 18 : 1][kMcThreads];  // outer prism points
   __shared__ double sV[NOUT == 3 ? 3 : 1][kMcThreads];   // outer piece volumes
+  static_assert(OUTER || CASE != 0, "nocaps has no whole-element caps");
   __shared__ double sAcc[NV][kMcThreads];
   const int li = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long draws = 0, hits = 0, led = 0;
@@ -1552,17 +1429,19 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
       if constexpr (CASE == 1) {
         inner_piece<CONS>(w[0], X[0], X[1], X[2], tet_det6(w[0], X[0], X[1], X[2]) / 6.0, tau,
                           v0P, acc, kin);
-        Prism P{X[0], X[1], X[2], w[1], w[2], w[3], {0, 0, 0}};
-        prism_volumes(P);
-        const Vd P6[6] = {P.A0, P.A1, P.A2, P.B0, P.B1, P.B2};
+        if constexpr (OUTER) {
+          Prism P{X[0], X[1], X[2], w[1], w[2], w[3], {0, 0, 0}};
+          prism_volumes(P);
+          const Vd P6[6] = {P.A0, P.A1, P.A2, P.B0, P.B1, P.B2};
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          sP[3 * k][threadIdx.x] = P6[k].x;
-          sP[3 * k + 1][threadIdx.x] = P6[k].y;
-          sP[3 * k + 2][threadIdx.x] = P6[k].z;
+          for (int k = 0; k < 6; ++k) {
+            sP[3 * k][threadIdx.x] = P6[k].x;
+            sP[3 * k + 1][threadIdx.x] = P6[k].y;
+            sP[3 * k + 2][threadIdx.x] = P6[k].z;
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) sV[k][threadIdx.x] = P.v[k];
         }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sV[k][threadIdx.x] = P.v[k];
       } else if constexpr (CASE == 2) {
         {
           Prism I{w[0], X[0], X[1], w[1], X[2], X[3], {0, 0, 0}};
@@ -1571,17 +1450,19 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
           inner_piece<CONS>(I.A1, I.A2, I.B0, I.B1, I.v[1], tau, v0P, acc, kin);
           inner_piece<CONS>(I.A2, I.B0, I.B1, I.B2, I.v[2], tau, v0P, acc, kin);
         }
-        Prism P{w[2], X[0], X[2], w[3], X[1], X[3], {0, 0, 0}};
-        warped_prism(P);
-        const Vd P6[6] = {P.A0, P.A1, P.A2, P.B0, P.B1, P.B2};
+        if constexpr (OUTER) {
+          Prism P{w[2], X[0], X[2], w[3], X[1], X[3], {0, 0, 0}};
+          warped_prism(P);
+          const Vd P6[6] = {P.A0, P.A1, P.A2, P.B0, P.B1, P.B2};
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          sP[3 * k][threadIdx.x] = P6[k].x;
-          sP[3 * k + 1][threadIdx.x] = P6[k].y;
-          sP[3 * k + 2][threadIdx.x] = P6[k].z;
+          for (int k = 0; k < 6; ++k) {
+            sP[3 * k][threadIdx.x] = P6[k].x;
+            sP[3 * k + 1][threadIdx.x] = P6[k].y;
+            sP[3 * k + 2][threadIdx.x] = P6[k].z;
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) sV[k][threadIdx.x] = P.v[k];
         }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sV[k][threadIdx.x] = P.v[k];
       } else {  // CASE == 3
         {
           Prism I{w[0], w[1], w[2], X[0], X[1], X[2], {0, 0, 0}};
@@ -1596,9 +1477,12 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         pd = X[2];
         vol1 = tet_det6(pa, pb, pc, pd) / 6.0;
       }
-      // ledger: straddle_inner + straddle_outer crossings and volumes, Gauss pieces
-      led += 2ull * 38ull * (m * mo) + 24ull * (m == 2 ? 18 : 4) +
-             (unsigned long long)kin * (CONS ? 160 : 360);
+      // ledger: straddle_inner (+ straddle_outer) crossings and volumes, Gauss pieces
+      if (OUTER)
+        led += 2ull * 38ull * (m * mo) + 24ull * (m == 2 ? 18 : 4);
+      else
+        led += 38ull * (m * mo) + 24ull * (m == 2 ? 9 : (m == 1 ? 1 : 3));
+      led += (unsigned long long)kin * (CONS ? 160 : 360);
     }
 #pragma unroll
     for (int kk = 0; kk < NV; ++kk) sAcc[kk][threadIdx.x] = acc[kk];
@@ -1606,7 +1490,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     const double dd = cD.dd;
     const double otau = CASE == 0 ? -1.0 : tau;
     double g0 = 0, gr[3] = {0, 0, 0}, H[6] = {0, 0, 0, 0, 0, 0};
-    if (CONS && G2) poly2_taylor(cD.g, xq, g0, gr, H);
+    if (OUTER && CONS && G2) poly2_taylor(cD.g, xq, g0, gr, H);
     int kept = 0;
 #pragma unroll 1
     for (int k = 0; k < NOUT; ++k) {
@@ -1726,40 +1610,6 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
   }
 }
 
-// nocaps: thread per straddling item (fullcaps does these inside k_mc, which
-// shares the item's crossings with the outer decomposition)
-constexpr int kGaussThreads = 128;
-
-template <bool CONS>
-__global__ void __launch_bounds__(kGaussThreads, 4) k_gauss(long long p0, long long n,
-                                                            const int* list, int nlist,
-                                                            const int* gpair,
-                                                            const unsigned char* gq,
-                                                            const int* pair_outer,
-                                                            const int* partner,
-                                                            const unsigned* info, double* gmom,
-                                                            unsigned long long* stats) {
-  const int li = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long led = 0;
-  if (li < nlist) {
-    const long long u = list[li];
-    const int pi = gpair[u], q = gq[u];
-    const long long p = p0 + pi;
-    const int T = cD.interior[pair_outer[pi]];
-    const int Tp = partner[p];
-    const int mask = (int)((info[p] >> (5 * q)) & 15);
-    Vd vT[4], vP[4];
-    load_verts(T, vT);
-    load_verts(Tp, vP);
-    const Vd xq = quad_point(vT, q);
-    Crossings X;
-    crossings4(vP, mask, xq, cD.delta, X);
-    led = gauss_item<CONS>(vP, mask, cD.tau[Tp], X, gmom + kGmomStride * u);
-  }
-  for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
-  if ((threadIdx.x & 31) == 0 && led) atomicAdd(stats + 2, led);
-}
-
 // load-vector partials: one slot per (interior element, combine warp, node)
 constexpr int kRhsWarps = 8;
 
@@ -1788,8 +1638,7 @@ template <int NTHR>
 __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 * NLFEM_INT_MINBLOCKS)) k_integrate(
     int ii0, const long long* pair_off, const int* partner, const unsigned* info,
     const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
-    double* rhsT, const long long* uoff, const double* mom, long long nunits,
-    const long long* goff, const double* gmom, long long ngunits, long long pbase,
+    double* rhsT, const long long* uoff, const double* mom, long long pbase,
     unsigned long long* stats, int hcap, int rowcap) {
   static_assert(NTHR / 32 <= kRhsWarps, "one rhsT slot per combine warp");
   extern __shared__ unsigned long long sml[];
@@ -1853,8 +1702,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     const bool constr = cD.region[Tp] != 0;
     const double volP = cD.vol[Tp];
     const double* invP = cD.inv + 9 * (long long)Tp;
-    long long u = (mom != nullptr) ? uoff[p - pbase] : 0;
-    long long gu = (gmom != nullptr) ? goff[p - pbase] : 0;
+    long long u = (mom != nullptr) ? uoff[p - pbase] : 0;  // first record of the pair
 
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
@@ -1880,34 +1728,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
             for (int cc = b; cc < 4; ++cc) S2[s2i(b, cc)] += off * (b == cc ? 2.0 : 1.0);
           }
         }
-      } else if ((c & kStraddle) && gmom != nullptr) {
-        // nocaps: the item's Gauss record (fullcaps folds the inner pieces
-        // into the item's Monte Carlo record)
-        const double2* rec = reinterpret_cast<const double2*>(gmom + kGmomStride * gu);
-        const double2 r0 = rec[0];
-        S0 = r0.x;
-        if (constr) {
-          Sg = r0.y;
-        } else {
-          const double2 r1 = rec[1], r2 = rec[2], r7 = rec[7];
-          S1[0] = r0.y;
-          S1[1] = r1.x;
-          S1[2] = r1.y;
-          S1[3] = r2.x;
-          S2[0] += r2.y;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double2 r = rec[3 + k];
-            S2[1 + 2 * k] += r.x;
-            S2[2 + 2 * k] += r.y;
-          }
-          S2[9] += r7.x;
-        }
-        ++gu;
       }
-      // Monte Carlo units of this item, in sub-simplex order
+      // straddling / cap item: its record (k_mc: inner pieces, + outer pieces by
+      // Monte Carlo for fullcaps), Cartesian moments about v0(T')
       if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
-        // the cap item's record (k_mc: inner + outer pieces)
         double g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
         const double2* rec = reinterpret_cast<const double2*>(mom + kMomStride * u);
         const double2 r0 = rec[0];
@@ -2210,10 +2034,7 @@ struct nlfem_gpu_session {
   DBuf<int> rlen, rcols, tcnt, tcols, slen, scols, olen, ocols;
   DBuf<long long> roff, toff, soff, mirror, eslot, ooff, omap;
   // Monte Carlo units (per chunk)
-  DBuf<int> ucount, gcount, pair_outer, upair, ulist, nlist, gpair, glist;
-  DBuf<long long> goff;
-  DBuf<unsigned char> gq;
-  DBuf<double> gmom;
+  DBuf<int> ucount, pair_outer, upair, ulist, nlist;
   DBuf<long long> uoff;
   DBuf<unsigned char> uqs;
   DBuf<double> mom;
@@ -2776,9 +2597,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   };
   // units phase: nocaps -> Gauss records (k_gauss); fullcaps -> one record per
   // cap item (k_mc, inner pieces included); barycenter -> none
+  // units phase: one record per straddling / cap item -- inner pieces (nocaps,
+  // fullcaps) and outer pieces by Monte Carlo (fullcaps); none for barycenter
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   const bool need_units = D.strategy != NLFEM_STRATEGY_BARYCENTER;
-  const bool need_gauss = D.strategy == NLFEM_STRATEGY_NOCAPS;
   float mc_ms = 0;
   if (shard_hi > shard_lo) {
     // chunks of outer elements sized so the unit buffers stay bounded
@@ -2793,76 +2615,45 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
                       poff.begin()) - 1;
       ii1 = std::min(std::max(ii1, ii0 + 1), shard_hi);
       const long long P0 = poff[ii0], np = poff[ii1] - P0;
-      long long nunits = 0, ngunits = 0;
+      long long nitems = 0;
       if (need_units) {
         S.ucount.ensure(np + 1);
-        S.gcount.ensure(np + 1);
         S.uoff.ensure(np + 1);
-        S.goff.ensure(np + 1);
         S.pair_outer.ensure(np + 1);
-        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.ucount.p, S.gcount.p,
-                                                     need_mc ? 1 : 0);
-        k_pair_outer<<<nblk(ii1 - ii0, 128), 128, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
-                                                           S.pair_outer.p);
+        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.ucount.p);
+        k_pair_outer<<<nblk(32LL * (ii1 - ii0), 256), 256, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
+                                                                    S.pair_outer.p);
         S.launches += 2;
-        S.nlist.ensure(16);
-        CK(cudaMemsetAsync(S.nlist.p, 0, 16 * sizeof(int), st));
-        if (need_gauss) {
-          scan64(S, S.gcount.p, true, np, S.goff.p, st);
-          ngunits = read_ll(S.goff.p + np, st);
-          S.gpair.ensure(ngunits + 1);
-          S.gq.ensure(ngunits + 1);
-          S.gmom.ensure(kGmomStride * (size_t)(ngunits + 1));
-          S.glist.ensure(2 * (size_t)ngunits + 2);
-          k_gunits_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.goff.p, S.gpair.p,
-                                                       S.gq.p, S.partner.p, S.glist.p,
-                                                       S.glist.p + ngunits + 1, S.nlist.p + 2);
-          ++S.launches;
-        }
-        if (need_mc) {
-          scan64(S, S.ucount.p, true, np, S.uoff.p, st);
-          nunits = read_ll(S.uoff.p + np, st);
-          S.upair.ensure(nunits + 1);
-          S.uqs.ensure(nunits + 1);
-          S.mom.ensure(kMomStride * (size_t)(nunits + 1));
-          S.ulist.ensure(8 * (size_t)(nunits + 1));
-          k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p,
-                                                      S.uqs.p, S.partner.p, S.ulist.p,
-                                                      nunits + 1, S.nlist.p + 4);
-          ++S.launches;
-        }
-        int nl[16] = {0};
-        CK(cudaMemcpyAsync(nl, S.nlist.p, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        S.nlist.ensure(8);
+        CK(cudaMemsetAsync(S.nlist.p, 0, 8 * sizeof(int), st));
+        scan64(S, S.ucount.p, true, np, S.uoff.p, st);
+        nitems = read_ll(S.uoff.p + np, st);
+        S.upair.ensure(nitems + 1);
+        S.uqs.ensure(nitems + 1);
+        S.mom.ensure(kMomStride * (size_t)(nitems + 1));
+        S.ulist.ensure(8 * (size_t)(nitems + 1));
+        k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p, S.uqs.p,
+                                                    S.partner.p, S.ulist.p, nitems + 1, S.nlist.p);
+        ++S.launches;
+        int nl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaEventRecord(S.ev[6], st));
         cudaStream_t s3 = S.stream3;
         CK(cudaEventRecord(S.ev[10], st));  // fork
         CK(cudaStreamWaitEvent(s3, S.ev[10], 0));
-        if (need_gauss && nl[2] > 0) {
-          k_gauss<false><<<nblk(nl[2], kGaussThreads), kGaussThreads, 0, s3>>>(
-              P0, ngunits, S.glist.p, nl[2], S.gpair.p, S.gq.p, S.pair_outer.p, S.partner.p,
-              S.info.p, S.gmom.p, S.counters.p + 1);
+        const long long ls = nitems + 1;
+        auto launch = [&](auto kern, int kind, cudaStream_t s) {
+          const int n = nl[kind];
+          if (n <= 0) return;
+          kern<<<nblk(n, kMcThreads), kMcThreads, 0, s>>>(
+              P0, nitems, S.ulist.p + kind * ls, n, S.upair.p, S.uqs.p, S.pair_outer.p,
+              S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
           ++S.launches;
-        }
-        if (need_gauss && nl[3] > 0) {
-          k_gauss<true><<<nblk(nl[3], kGaussThreads), kGaussThreads, 0, s3>>>(
-              P0, ngunits, S.glist.p + ngunits + 1, nl[3], S.gpair.p, S.gq.p, S.pair_outer.p,
-              S.partner.p, S.info.p, S.gmom.p, S.counters.p + 1);
-          ++S.launches;
-        }
+        };
+        // lists 0..3: interior parents by cap case, 4..7: constraint parents;
+        // the big straddle lists on `stream`, the rest beside them on s3
         if (need_mc) {
-          const long long ls = nunits + 1;
-          const int* L0 = S.ulist.p;
-          auto launch = [&](auto kern, int kind, cudaStream_t s) {
-            const int n = nl[4 + kind];
-            if (n <= 0) return;
-            kern<<<nblk(n, kMcThreads), kMcThreads, 0, s>>>(
-                P0, nunits, L0 + kind * ls, n, S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
-                S.info.p, S.mom.p, S.counters.p + 1);
-            ++S.launches;
-          };
-          // lists 0..3: interior parents by cap case, 4..7: constraint parents;
-          // the big straddle lists on `stream`, the rest beside them on s3
           launch(k_mc<false, false, 2>, 2, st);
           launch(k_mc<false, false, 1>, 1, st);
           launch(k_mc<false, false, 3>, 3, s3);
@@ -2878,6 +2669,13 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
             launch(k_mc<true, false, 3>, 7, s3);
             launch(k_mc<true, false, 0>, 4, s3);
           }
+        } else {  // nocaps: inner pieces only
+          launch(k_mc<false, false, 2, false>, 2, st);
+          launch(k_mc<false, false, 1, false>, 1, st);
+          launch(k_mc<false, false, 3, false>, 3, s3);
+          launch(k_mc<true, false, 2, false>, 6, st);
+          launch(k_mc<true, false, 1, false>, 5, st);
+          launch(k_mc<true, false, 3, false>, 7, s3);
         }
         CK(cudaEventRecord(S.ev[11], s3));  // join
         CK(cudaStreamWaitEvent(st, S.ev[11], 0));
@@ -2891,13 +2689,13 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
       if (ppe < 768)
         k_integrate<128><<<ii1 - ii0, 128, ismem, st>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
-            S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
-            need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
+            S.rhsT.p, S.uoff.p, need_units ? S.mom.p : nullptr, P0, S.counters.p + 1, hcap,
+            rowcap);
       else
         k_integrate<256><<<ii1 - ii0, 256, ismem, st>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
-            S.rhsT.p, S.uoff.p, need_mc ? S.mom.p : nullptr, nunits, S.goff.p,
-            need_gauss ? S.gmom.p : nullptr, ngunits, P0, S.counters.p + 1, hcap, rowcap);
+            S.rhsT.p, S.uoff.p, need_units ? S.mom.p : nullptr, P0, S.counters.p + 1, hcap,
+            rowcap);
       ++S.launches;
       if (need_units) {
         CK(cudaEventSynchronize(S.ev[7]));
