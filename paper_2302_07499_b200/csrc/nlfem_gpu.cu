@@ -98,6 +98,7 @@ struct Dev {
   double C, delta, slack, inside_cut, dd;
   // element data
   const double4* erec;  // [4K]: (c, r), (v0, v1.x), (v1.yz, v2.xy), (v2.z, v3)
+  const double* gbar;   // [K] constraint elements: sum_k vol/4 g(x_k) (whole-element Sg)
   const int4* verts;
   const int4* nbr;
   const double* vol;
@@ -186,6 +187,21 @@ __global__ void k_erec(int K, const double* node, const int4* verts, const doubl
   erec[4 * t + 1] = make_double4(a[0], a[1], a[2], b[0]);
   erec[4 * t + 2] = make_double4(b[1], b[2], c[0], c[1]);
   erec[4 * t + 3] = make_double4(c[2], d[0], d[1], d[2]);
+}
+
+// whole constraint element: measure times g average with the degree-2 rule
+// (reference assembly.cpp:350-359), the same for every (T, q) that meets it
+__global__ void k_gbar(int K, double* gbar) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  double Sg = 0;
+  if (cD.region[t] != 0) {
+    Vd v[4];
+    load_verts(t, v);
+    const double volP = cD.vol[t];
+    for (int k = 0; k < 4; ++k) Sg += volP * 0.25 * poly_eval(cD.g, quad_point(v, k));
+  }
+  gbar[t] = Sg;
 }
 
 __device__ __forceinline__ int cell_of(double c, double o, double inv, int n) {
@@ -1713,11 +1729,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
         led += constr ? 133 : 39;
         S0 = volP;
         if (constr) {
-          // constraint parent: measure and g average (reference assembly.cpp:350-359)
-          Vd vP[4];
-          load_verts(Tp, vP);
-#pragma unroll 1
-          for (int k = 0; k < 4; ++k) Sg += volP * 0.25 * poly_eval(cD.g, quad_point(vP, k));
+          // constraint parent: measure and g average (reference assembly.cpp:350-359),
+          // per element from prep (same expression)
+          Sg = cD.gbar[Tp];
         } else {
           // exact basis moments of a whole element (reference assembly.cpp:361-369)
           const double s1 = volP / 4, off = volP / 20.0;
@@ -2018,6 +2032,7 @@ struct nlfem_gpu_session {
   DBuf<uint8_t> region;
   DBuf<int> interior, ipos, dof, dof_node;
   DBuf<double4> erec;
+  DBuf<double> gbar;
   // grid / incidence
   DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
   DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp, scan_tmp2;
@@ -2255,7 +2270,9 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.gz = std::max(1, (int)std::floor((hi[2] - lo[2]) / hg) + 1);
   D.rmax = rmax;
   S.erec.ensure(4 * (size_t)S.K);
+  S.gbar.ensure(S.K);
   D.erec = S.erec.p;
+  D.gbar = S.gbar.p;
   D.verts = S.verts.p;
   D.nbr = S.nbr.p;
   D.vol = S.vol.p;
@@ -2281,7 +2298,8 @@ void run_prep(nlfem_gpu_session& S) {
   const long long ncell = (long long)D.gx * D.gy * D.gz;
   CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
   k_erec<<<nblk(K, 256), 256, 0, st>>>(K, S.node.p, S.verts.p, S.center.p, S.radius.p, S.erec.p);
-  ++S.launches;
+  k_gbar<<<nblk(K, 256), 256, 0, st>>>(K, S.gbar.p);
+  S.launches += 2;
   // grid
   S.cell_key.ensure(K);
   S.cell_cnt.ensure(ncell);
