@@ -10,7 +10,9 @@
  *
  * Plain pointers and sizes only; no C++ or torch types cross this boundary.
  * Inputs are borrowed for the duration of a call.  Output arrays are owned by
- * the library and released with nlfem_gpu_free_csr().  Every entry point
+ * the library and released with nlfem_gpu_free_csr() (whole-system downloads
+ * live in one page-locked block from a process-wide pool, so the download is a
+ * straight DMA; freeing returns the block to the pool).  Every entry point
  * returns 0 on success or an nlfem_gpu_status code, with a message in `err`.
  * There is no CPU fallback: without a usable sm_100 device the calls fail
  * with NLFEM_GPU_ENODEVICE.

@@ -428,17 +428,7 @@ class Session:
         csr = _Csr()
         err = C.create_string_buffer(1024)
         _check(lib().nlfem_gpu_session_download(self._h, C.byref(csr), err, 1024), err)
-        try:
-            n, nnz = csr.rows, csr.nnz
-            out = {
-                "row_ptr": np.ctypeslib.as_array(csr.row_ptr, (n + 1,)).copy(),
-                "col_idx": np.ctypeslib.as_array(csr.col_idx, (max(nnz, 1),))[:nnz].copy(),
-                "values": np.ctypeslib.as_array(csr.values, (max(nnz, 1),))[:nnz].copy(),
-                "rhs": np.ctypeslib.as_array(csr.rhs, (max(n, 1),))[:n].copy(),
-            }
-        finally:
-            lib().nlfem_gpu_free_csr(C.byref(csr))
-        return out
+        return _take_csr(csr)
 
     def pairs(self) -> dict:
         """Element-pair list of the last run (set parity): offsets per interior
@@ -481,17 +471,39 @@ class _CudaView:
                                          "strides": None}
 
 
+class _CsrOwner:
+    """Keeps a library-owned CSR (page-locked block) alive while any of the
+    numpy arrays viewing it exists; returns it to the library afterwards."""
+
+    def __init__(self, csr):
+        self.csr = csr
+
+    def __del__(self):
+        try:
+            lib().nlfem_gpu_free_csr(C.byref(self.csr))
+        except Exception:
+            pass
+
+
+def _view(owner, ptr, ctype, n, dtype):
+    addr = C.cast(ptr, C.c_void_p).value
+    if not addr or n == 0:
+        return np.zeros(0, dtype)
+    buf = (ctype * n).from_address(addr)
+    buf._owner = owner  # the array's base holds the owner
+    return np.frombuffer(buf, dtype)
+
+
 def _take_csr(csr) -> dict:
-    try:
-        n, nnz = csr.rows, csr.nnz
-        return {
-            "row_ptr": np.ctypeslib.as_array(csr.row_ptr, (n + 1,)).copy(),
-            "col_idx": np.ctypeslib.as_array(csr.col_idx, (max(nnz, 1),))[:nnz].copy(),
-            "values": np.ctypeslib.as_array(csr.values, (max(nnz, 1),))[:nnz].copy(),
-            "rhs": np.ctypeslib.as_array(csr.rhs, (max(n, 1),))[:n].copy(),
-        }
-    finally:
-        lib().nlfem_gpu_free_csr(C.byref(csr))
+    """Zero-copy numpy views of a library-owned CSR (freed with the last view)."""
+    owner = _CsrOwner(csr)
+    n, nnz = csr.rows, csr.nnz
+    return {
+        "row_ptr": _view(owner, csr.row_ptr, C.c_int32, n + 1, np.int32),
+        "col_idx": _view(owner, csr.col_idx, C.c_int32, nnz, np.int32),
+        "values": _view(owner, csr.values, C.c_double, nnz, np.float64),
+        "rhs": _view(owner, csr.rhs, C.c_double, n, np.float64),
+    }
 
 
 def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
@@ -524,17 +536,7 @@ def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
                               C.byref(fp), C.byref(gp), C.byref(cfg), C.byref(csr), C.byref(st),
                               err, 1024)
     _check(rc, err)
-    try:
-        n, nnz = csr.rows, csr.nnz
-        out = {
-            "row_ptr": np.ctypeslib.as_array(csr.row_ptr, (n + 1,)).copy(),
-            "col_idx": np.ctypeslib.as_array(csr.col_idx, (max(nnz, 1),))[:nnz].copy(),
-            "values": np.ctypeslib.as_array(csr.values, (max(nnz, 1),))[:nnz].copy(),
-            "rhs": np.ctypeslib.as_array(csr.rhs, (max(n, 1),))[:n].copy(),
-        }
-    finally:
-        L.nlfem_gpu_free_csr(C.byref(csr))
-    return out, st.as_dict()
+    return _take_csr(csr), st.as_dict()
 
 
 def assemble_system(coords, cells, region, delta, strategy="nocaps", normalization="mass",

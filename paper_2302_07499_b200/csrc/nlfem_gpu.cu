@@ -32,6 +32,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -2019,6 +2020,43 @@ struct HostStage {
   }
 };
 
+// Process-wide pool of page-locked host blocks for the CSR arrays the library
+// returns: the download is a straight DMA into the caller's result (no
+// staging copy); nlfem_gpu_free_csr hands the block back for the next call.
+struct PinnedPool {
+  struct Blk {
+    char* p;
+    size_t n;
+    bool used;
+  };
+  std::mutex mu;
+  std::vector<Blk> blks;
+  char* acquire(size_t n) {
+    std::lock_guard<std::mutex> g(mu);
+    Blk* best = nullptr;
+    for (auto& b : blks)
+      if (!b.used && b.n >= n && (!best || b.n < best->n)) best = &b;
+    if (best) {
+      best->used = true;
+      return best->p;
+    }
+    char* p = nullptr;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&p), std::max<size_t>(n, 256)));
+    blks.push_back({p, std::max<size_t>(n, 256), true});
+    return p;
+  }
+  bool release(const void* p) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& b : blks)
+      if (b.p == p) {
+        b.used = false;
+        return true;
+      }
+    return false;
+  }
+};
+PinnedPool g_result_pool;
+
 }  // namespace
 
 struct nlfem_gpu_session {
@@ -2916,38 +2954,30 @@ int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* e
                                size_t errlen) {
   return guard(err, errlen, [&] {
     const int U = s->unknowns;
-    out->rows = U;
-    out->nnz = s->nnz_out;
-    out->row_ptr = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (U + 1)));
-    out->col_idx = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<long long>(s->nnz_out, 1)));
-    out->values = static_cast<double*>(std::malloc(sizeof(double) * std::max<long long>(s->nnz_out, 1)));
-    out->rhs = static_cast<double*>(std::malloc(sizeof(double) * std::max(U, 1)));
-    if (!out->row_ptr || !out->col_idx || !out->values || !out->rhs)
-      throw Fail{NLFEM_GPU_ENOMEM, "out of host memory"};
-    if (s->nnz_out > (long long)0x7fffffff)
-      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: nnz exceeds int32 row pointers"};
-    // int32 row pointers on the device, then every array through the pinned
-    // staging buffer with one synchronisation
-    cudaStream_t st = s->stream;
     const long long nnz = s->nnz_out;
+    if (nnz > (long long)0x7fffffff)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: nnz exceeds int32 row pointers"};
+    // one page-locked block from the result pool: row_ptr | col_idx | values | rhs
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t br = al(4 * (size_t)(U + 1)), bc = al(4 * (size_t)nnz), bv = al(8 * (size_t)nnz);
+    char* blk = g_result_pool.acquire(br + bc + bv + 8 * (size_t)std::max(U, 1));
+    out->rows = U;
+    out->nnz = nnz;
+    out->row_ptr = reinterpret_cast<int32_t*>(blk);
+    out->col_idx = reinterpret_cast<int32_t*>(blk + br);
+    out->values = reinterpret_cast<double*>(blk + br + bc);
+    out->rhs = reinterpret_cast<double*>(blk + br + bc + bv);
+    // int32 row pointers on the device, then straight DMA into the result
+    cudaStream_t st = s->stream;
     s->rowptr32.ensure(U + 1);
     k_ll_to_int<<<nblk(U + 1, 256), 256, 0, st>>>(U + 1, s->ooff.p, s->rowptr32.p);
-    s->stage.reset(4 * (size_t)(U + 1) + 12 * (size_t)nnz + 8 * (size_t)U + 4 * 256);
-    char* hr = s->stage.take(4 * (size_t)(U + 1));
-    char* hc = s->stage.take(4 * (size_t)nnz);
-    char* hv = s->stage.take(8 * (size_t)nnz);
-    char* hb = s->stage.take(8 * (size_t)U);
-    CK(cudaMemcpyAsync(hr, s->rowptr32.p, 4 * (size_t)(U + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->row_ptr, s->rowptr32.p, 4 * (size_t)(U + 1), cudaMemcpyDeviceToHost, st));
     if (nnz) {
-      CK(cudaMemcpyAsync(hc, s->ocols.p, 4 * (size_t)nnz, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(hv, s->values.p, 8 * (size_t)nnz, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(out->col_idx, s->ocols.p, 4 * (size_t)nnz, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(out->values, s->values.p, 8 * (size_t)nnz, cudaMemcpyDeviceToHost, st));
     }
-    if (U) CK(cudaMemcpyAsync(hb, s->rhs.p, 8 * (size_t)U, cudaMemcpyDeviceToHost, st));
+    if (U) CK(cudaMemcpyAsync(out->rhs, s->rhs.p, 8 * (size_t)U, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    std::memcpy(out->row_ptr, hr, 4 * (size_t)(U + 1));
-    std::memcpy(out->col_idx, hc, 4 * (size_t)nnz);
-    std::memcpy(out->values, hv, 8 * (size_t)nnz);
-    std::memcpy(out->rhs, hb, 8 * (size_t)U);
   });
 }
 
@@ -3003,10 +3033,12 @@ int nlfem_gpu_assemble(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
 
 void nlfem_gpu_free_csr(nlfem_gpu_csr* csr) {
   if (!csr) return;
-  std::free(csr->row_ptr);
-  std::free(csr->col_idx);
-  std::free(csr->values);
-  std::free(csr->rhs);
+  if (!csr->row_ptr || !g_result_pool.release(csr->row_ptr)) {  // pooled block, else malloc'd
+    std::free(csr->row_ptr);
+    std::free(csr->col_idx);
+    std::free(csr->values);
+    std::free(csr->rhs);
+  }
   csr->row_ptr = csr->col_idx = nullptr;
   csr->values = csr->rhs = nullptr;
 }
