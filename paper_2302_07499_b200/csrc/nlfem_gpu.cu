@@ -1274,6 +1274,10 @@ __device__ __forceinline__ void poly2_taylor(const Poly& P, Vd x, double& g0, do
 #ifndef NLFEM_MC_MINBLOCKS
 #define NLFEM_MC_MINBLOCKS 4
 #endif
+#ifndef NLFEM_MC_UNROLL
+#define NLFEM_MC_UNROLL 1
+#endif
+constexpr int kMcUnroll = NLFEM_MC_UNROLL;  // Philox blocks in flight per thread
 
 // |det(b - a, c - a, d - a)|: six times tet_volume(a, b, c, d) before its
 // division (reference ball_approx.cpp:144-146 divides by 6 after fabs)
@@ -1556,7 +1560,7 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         }
       };
       const int full = M >> 2;
-#pragma unroll 1
+#pragma unroll kMcUnroll
       for (int j = 0; j < full; ++j) {
         // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
         uint32_t A[4], B[4], Cw[4];
