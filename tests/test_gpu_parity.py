@@ -221,3 +221,37 @@ def test_fullcaps_custom_g_against_oracle(gterms):
     assert row_rel_err(out, o) <= TOL_MC
     assert rhs_rel_err(out, o) <= TOL_MC
     assert (st["mc_samples"], st["mc_hits"]) == (o["mc_samples"], o["mc_hits"])
+
+
+@pytest.mark.parametrize("mc", [5, 7, 10, 64])
+def test_fullcaps_partial_blocks_and_weights_against_oracle(mc):
+    # M % 4 != 0 exercises the partial last Philox block; M not a power of two
+    # takes the vol / M division, M = 64 the exact vol * 2^-6 multiply.
+    m = P.generate_mesh(3, 4, 0.3)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    out, st = P.assemble(t, 0.3, "fullcaps", "moment2", U2, seed=SEED, mc_samples=mc)
+    o = _oracle(t, 0.3, "fullcaps", mc)
+    assert same_pattern(out, o)
+    assert row_rel_err(out, o) <= TOL_MC
+    assert rhs_rel_err(out, o) <= TOL_MC
+    # same stream -> the same draws and bit-identical accept decisions
+    assert st["mc_samples"] == o["mc_samples"]
+    assert st["mc_hits"] == o["mc_hits"]
+
+
+def test_results_are_independent_pooled_blocks():
+    # two results held at once live in different pinned blocks; freeing one
+    # (dropping its arrays) leaves the other intact and reusable
+    m = P.generate_mesh(3, 4, 0.3)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    a, _ = P.assemble(t, 0.3, "nocaps", "moment2", U2)
+    keep = {k: v.copy() for k, v in a.items()}
+    b, _ = P.assemble(t, 0.3, "barycenter", "moment2", U2)
+    assert a["values"].ctypes.data != b["values"].ctypes.data
+    for k in keep:
+        assert np.array_equal(a[k], keep[k])
+    del b
+    c, _ = P.assemble(t, 0.3, "nocaps", "moment2", U2)
+    for k in keep:
+        assert np.array_equal(a[k], keep[k])
+        assert np.array_equal(c[k], keep[k])
