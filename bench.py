@@ -189,10 +189,13 @@ def run_reference_arm(args, cfg_name, cfg):
     value = cb["pairs"] * len(cb["times"]) / tot
     line = {
         "impl": "reference", "metric": "element-pair integrals/s", "value": value,
-        "unit": "element-pair integrals/s", "n_gpus": 0, "steps": args.steps,
+        "unit": "element-pair integrals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(cb["times"]),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": describe(cfg_name, cfg)["text"]},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": describe(cfg_name, cfg)["text"], "name": cfg_name,
+                   "element_pairs": int(cb["pairs"]),
+                   "parallelism": f"reference assemble() on {cb['cores']} host threads (rank 0)"},
         "cpu_baseline": {"value": value, "unit": "element-pair integrals/s", "cores": cb["cores"],
                          "kind": cb["kind"], "sample": cb["sample"]},
         "e2e": {"value": value, "unit": "element-pair integrals/s", "h2d_bytes_per_step": 0,
