@@ -1073,28 +1073,6 @@ __device__ __forceinline__ int cap_case(unsigned c) {
 }
 
 
-// warp-aggregated reservation in four lists at once: every lane asks for n[k]
-// slots in list k and gets its first slot in base[k]
-__device__ __forceinline__ void reserve4v(int* counters, const int n[4], int base[4]) {
-  const int lane = threadIdx.x & 31;
-  int incl[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) incl[k] = n[k];
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int t = __shfl_up_sync(FULLMASK, incl[k], off);
-      if (lane >= off) incl[k] += t;
-    }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    int b = 0;
-    if (lane == 31 && incl[k]) b = atomicAdd(counters + k, incl[k]);
-    b = __shfl_sync(FULLMASK, b, 31);
-    base[k] = b + incl[k] - n[k];
-  }
-}
 
 __global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1112,36 +1090,61 @@ __global__ void k_units_count(long long p0, long long np, const unsigned* info, 
 // are listed by their first unit id in four lists -- (interior, constraint)
 // parent x (1, 3) slots -- so each k_mc launch runs one uniform code path.
 // cap items (one record slot each, in pair then q order) into eight lists by
-// parent kind (interior / constraint) and cap_case
-__global__ void k_units_fill(long long p0, long long np, const unsigned* info,
-                             const long long* uoff, int* upair, unsigned char* uqs,
-                             const int* partner, int* lists, long long lstride, int* nlist) {
+// parent kind (interior / constraint) and cap_case.  Reservation: per-lane
+// counts packed 8 bits per list into one 64-bit word (a warp adds at most 128
+// per field), one warp scan, then a block prefix and one global atomic per
+// list and block.
+constexpr int kFillThreads = 256;
+__global__ void __launch_bounds__(kFillThreads) k_units_fill(long long p0, long long np,
+                                                             const unsigned* info,
+                                                             const long long* uoff, int* upair,
+                                                             unsigned char* uqs,
+                                                             const int* partner, int* lists,
+                                                             long long lstride, int* nlist) {
+  constexpr int W = kFillThreads / 32;
+  __shared__ unsigned long long wtot[W];
+  __shared__ int bbase[8][W];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool act = i < np;
   const unsigned code = act ? info[p0 + i] : 0;
-  const bool cons = act && cD.region[partner[p0 + i]] != 0;
-  int n[4] = {0, 0, 0, 0};
+  const int kind0 = (act && cD.region[partner[p0 + i]] != 0) ? 4 : 0;
+  unsigned long long packed = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
-    if (c == kOutCap || (c & kStraddle)) ++n[cap_case(c)];
+    if (c == kOutCap || (c & kStraddle)) packed += 1ull << (8 * (kind0 + cap_case(c)));
   }
-  const int z[4] = {0, 0, 0, 0};
-  int bi[4], bc[4];
-  reserve4v(nlist, cons ? z : n, bi);
-  reserve4v(nlist + 4, cons ? n : z, bc);
+  unsigned long long incl = packed;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long t = __shfl_up_sync(FULLMASK, incl, off);
+    if (lane >= off) incl += t;
+  }
+  if (lane == 31) wtot[wl] = incl;
+  __syncthreads();
+  if (threadIdx.x < 8) {  // list k: warp offsets within the block, one global atomic
+    const int k = threadIdx.x;
+    int run = 0;
+    for (int w = 0; w < W; ++w) {
+      bbase[k][w] = run;
+      run += (int)((wtot[w] >> (8 * k)) & 0xff);
+    }
+    const int g = run ? atomicAdd(nlist + k, run) : 0;
+    for (int w = 0; w < W; ++w) bbase[k][w] += g;
+  }
+  __syncthreads();
   if (!act) return;
+  unsigned long long excl = incl - packed;  // bumped per item: same-list items are consecutive
   long long u = uoff[i];
-  int* L = lists + (cons ? 4 : 0) * lstride;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
     if (!(c == kOutCap || (c & kStraddle))) continue;
-    const int k = cap_case(c);
-    const int slot = (cons ? bc[k] : bi[k]);
-    if (cons) ++bc[k];
-    else ++bi[k];
-    L[k * lstride + slot] = (int)u;
+    const int k = kind0 + cap_case(c);
+    const int slot = bbase[k][wl] + (int)((excl >> (8 * k)) & 0xff);
+    excl += 1ull << (8 * k);
+    lists[k * lstride + slot] = (int)u;
     upair[u] = (int)i;
     uqs[u] = (unsigned char)q;
     ++u;
@@ -1393,7 +1396,7 @@ __device__ __forceinline__ void inner_piece(Vd a, Vd b, Vd c, Vd d, double vol, 
 // OUTER = false (nocaps): the inner pieces only, no Monte Carlo.
 template <bool CONS, bool G2, int CASE, bool OUTER = true>
 __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nitems,
-                                                      const int* list, int nlist,
+                                                      const int* list, const int* nlistp,
                                                       const int* upair, const unsigned char* uqs,
                                                       const int* pair_outer, const int* partner,
                                                       const unsigned* info, double* mom,
@@ -1404,9 +1407,20 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
   __shared__ double sV[NOUT == 3 ? 3 : 1][kMcThreads];   // outer piece volumes
   static_assert(OUTER || CASE != 0, "nocaps has no whole-element caps");
   __shared__ double sAcc[NV][kMcThreads];
-  const int li = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long draws = 0, hits = 0, led = 0;
-  if (li < nlist) {
+  // warps fetch 32 list entries at a time from a per-list cursor (dynamic
+  // balance for items of uneven cost); the list length is read on the device,
+  // so there is no host round trip between the list fill and this launch
+  const int nlist = nlistp[0];
+  int* cursor = const_cast<int*>(nlistp) + 8;
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cursor, 32);
+    base = __shfl_sync(FULLMASK, base, 0);
+    if (base >= nlist) break;
+    const int li = base + lane;
+    if (li >= nlist) continue;
     const long long u = list[li];
     const int pi = upair[u];
     const int q = uqs[u];
@@ -2368,7 +2382,7 @@ void run_prep(nlfem_gpu_session& S) {
   k_ninc_count<<<nblk(K, 256), 256, 0, st>>>(K, S.ni_cnt.p);
   ++S.launches;
   scan64(S, S.ni_cnt.p, true, J, S.ni_off64.p, st);
-  const long long nin = read_ll(S.ni_off64.p + J, st);
+  const long long nin = 4LL * S.KI;  // every interior element has 4 nodes: no read-back
   S.ni_el.ensure(nin);
   CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
   k_ninc_fill<<<nblk(K, 256), 256, 0, st>>>(K, S.ni_off64.p, S.cursor.p, S.ni_el.p);
@@ -2685,31 +2699,44 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         k_pair_outer<<<nblk(32LL * (ii1 - ii0), 256), 256, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
                                                                     S.pair_outer.p);
         S.launches += 2;
-        S.nlist.ensure(8);
-        CK(cudaMemsetAsync(S.nlist.p, 0, 8 * sizeof(int), st));
+        S.nlist.ensure(16);  // 8 list lengths, 8 work cursors
+        CK(cudaMemsetAsync(S.nlist.p, 0, 16 * sizeof(int), st));
         scan64(S, S.ucount.p, true, np, S.uoff.p, st);
-        nitems = read_ll(S.uoff.p + np, st);
+        // buffers by the upper bound (4 items per pair): no count read-back
+        nitems = 4 * np;
         S.upair.ensure(nitems + 1);
         S.uqs.ensure(nitems + 1);
         S.mom.ensure(kMomStride * (size_t)(nitems + 1));
         S.ulist.ensure(8 * (size_t)(nitems + 1));
-        k_units_fill<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.uoff.p, S.upair.p, S.uqs.p,
-                                                    S.partner.p, S.ulist.p, nitems + 1, S.nlist.p);
+        k_units_fill<<<nblk(np, kFillThreads), kFillThreads, 0, st>>>(
+            P0, np, S.info.p, S.uoff.p, S.upair.p, S.uqs.p, S.partner.p, S.ulist.p, nitems + 1,
+            S.nlist.p);
         ++S.launches;
-        int nl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
         CK(cudaEventRecord(S.ev[6], st));
         cudaStream_t s3 = S.stream3;
         CK(cudaEventRecord(S.ev[10], st));  // fork
         CK(cudaStreamWaitEvent(s3, S.ev[10], 0));
         const long long ls = nitems + 1;
+#ifndef NLFEM_MC_PERSIST
+#define NLFEM_MC_PERSIST 1
+#endif
+#if NLFEM_MC_PERSIST
+        // list lengths stay on the device: launches of two waves of resident CTAs
+        int nl[8];
+        for (int k = 0; k < 8; ++k)
+          nl[k] = (int)std::min<long long>(nitems, 148LL * NLFEM_MC_MINBLOCKS * 2 * kMcThreads);
+#else
+        // list lengths to the host (one round trip) for exactly sized grids, so
+        // the CTAs retire as the lists drain and the pattern stream keeps SMs
+        int nl[8];
+        CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+#endif
         auto launch = [&](auto kern, int kind, cudaStream_t s) {
-          const int n = nl[kind];
-          if (n <= 0) return;
-          kern<<<nblk(n, kMcThreads), kMcThreads, 0, s>>>(
-              P0, nitems, S.ulist.p + kind * ls, n, S.upair.p, S.uqs.p, S.pair_outer.p,
-              S.partner.p, S.info.p, S.mom.p, S.counters.p + 1);
+          if (nl[kind] <= 0) return;
+          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(P0, nitems, S.ulist.p + kind * ls, S.nlist.p + kind,
+                                             S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
+                                             S.info.p, S.mom.p, S.counters.p + 1);
           ++S.launches;
         };
         // lists 0..3: interior parents by cap case, 4..7: constraint parents;
