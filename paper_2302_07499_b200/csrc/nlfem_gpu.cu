@@ -2553,65 +2553,81 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   CK(cudaStreamSynchronize(st));
   // pass 1 + compaction, in chunks of outer elements bounded by survivors
   const long long kCandBudget = 1LL << 30;  // 8 GiB of (partner, code) slots
-  long long cap = std::max<long long>(1, (long long)(0.8 * coff[KI]));
-  S.partner.ensure(cap);
-  S.info.ensure(cap);
   S.pair_off.ensure(KI + 1);
-  long long total = 0;
-  int c0 = 0;
-  while (c0 < KI) {
-    int c1 = (int)(std::upper_bound(coff.begin() + c0 + 1, coff.end(), coff[c0] + kCandBudget) -
-                   coff.begin()) - 1;
-    c1 = std::min(std::max(c1, c0 + 1), KI);
-    const long long nc = coff[c1] - coff[c0];
+  if (coff[KI] <= kCandBudget) {
+    // one chunk: pairs <= survivors bounds the pair arrays, so the pair total
+    // need not come back to the host here (it arrives with the pair offsets
+    // the integration phase reads anyway)
+    const long long nc = coff[KI];
+    S.partner.ensure(std::max<long long>(1, nc));
+    S.info.ensure(std::max<long long>(1, nc));
     S.cpartner.ensure(nc + 1);
     S.cinfo.ensure(nc + 1);
-    k_pairs<1><<<nblk((long long)(c1 - c0), kPairWarps), kPairThreads, 0, st>>>(
-        c0, c1, S.cand_off.p, coff[c0], nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
-        S.counters.p, S.err_elem.p);
-    ++S.launches;
-    // pair offsets of this chunk continue the running total
-    scan64(S, S.pair_count.p + c0, true, c1 - c0, S.pair_off.p + c0, st);
-    const long long nch = read_ll(S.pair_off.p + c1, st);
-    if (total) {
-      k_add_offset<<<nblk(c1 - c0 + 1, 256), 256, 0, st>>>(S.pair_off.p + c0, c1 - c0 + 1, total);
+    if (KI > 0) {
+      k_pairs<1><<<nblk((long long)KI, kPairWarps), kPairThreads, 0, st>>>(
+          0, KI, S.cand_off.p, 0, nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p, S.counters.p,
+          S.err_elem.p);
+      scan64(S, S.pair_count.p, true, KI, S.pair_off.p, st);
+      k_pairs_compact<<<nblk((long long)KI * 32, 256), 256, 0, st>>>(
+          0, KI, S.cand_off.p, 0, S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p, S.info.p);
+      S.launches += 2;
+    }
+  } else {
+    long long cap = std::max<long long>(1, (long long)(0.8 * coff[KI]));
+    S.partner.ensure(cap);
+    S.info.ensure(cap);
+    long long total = 0;
+    int c0 = 0;
+    while (c0 < KI) {
+      int c1 = (int)(std::upper_bound(coff.begin() + c0 + 1, coff.end(), coff[c0] + kCandBudget) -
+                     coff.begin()) - 1;
+      c1 = std::min(std::max(c1, c0 + 1), KI);
+      const long long nc = coff[c1] - coff[c0];
+      S.cpartner.ensure(nc + 1);
+      S.cinfo.ensure(nc + 1);
+      k_pairs<1><<<nblk((long long)(c1 - c0), kPairWarps), kPairThreads, 0, st>>>(
+          c0, c1, S.cand_off.p, coff[c0], nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
+          S.counters.p, S.err_elem.p);
       ++S.launches;
-    }
-    if (total + nch > cap) {  // grow, keeping what is compacted
-      cap = (long long)((total + nch) * 1.25) + 1;
-      DBuf<int> np_;
-      DBuf<unsigned> ni_;
-      np_.ensure(cap);
-      ni_.ensure(cap);
+      // pair offsets of this chunk continue the running total
+      scan64(S, S.pair_count.p + c0, true, c1 - c0, S.pair_off.p + c0, st);
+      const long long nch = read_ll(S.pair_off.p + c1, st);
       if (total) {
-        CK(cudaMemcpyAsync(np_.p, S.partner.p, total * sizeof(int), cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemcpyAsync(ni_.p, S.info.p, total * sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+        k_add_offset<<<nblk(c1 - c0 + 1, 256), 256, 0, st>>>(S.pair_off.p + c0, c1 - c0 + 1, total);
+        ++S.launches;
       }
-      CK(cudaStreamSynchronize(st));
-      std::swap(S.partner.p, np_.p);
-      std::swap(S.partner.n, np_.n);
-      std::swap(S.info.p, ni_.p);
-      std::swap(S.info.n, ni_.n);
+      if (total + nch > cap) {  // grow, keeping what is compacted
+        cap = (long long)((total + nch) * 1.25) + 1;
+        DBuf<int> np_;
+        DBuf<unsigned> ni_;
+        np_.ensure(cap);
+        ni_.ensure(cap);
+        if (total) {
+          CK(cudaMemcpyAsync(np_.p, S.partner.p, total * sizeof(int), cudaMemcpyDeviceToDevice, st));
+          CK(cudaMemcpyAsync(ni_.p, S.info.p, total * sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+        }
+        CK(cudaStreamSynchronize(st));
+        std::swap(S.partner.p, np_.p);
+        std::swap(S.partner.n, np_.n);
+        std::swap(S.info.p, ni_.p);
+        std::swap(S.info.n, ni_.n);
+      }
+      k_pairs_compact<<<nblk((long long)(c1 - c0) * 32, 256), 256, 0, st>>>(
+          c0, c1, S.cand_off.p, coff[c0], S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p,
+          S.info.p);
+      ++S.launches;
+      total += nch;
+      c0 = c1;
     }
-    k_pairs_compact<<<nblk((long long)(c1 - c0) * 32, 256), 256, 0, st>>>(
-        c0, c1, S.cand_off.p, coff[c0], S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p,
-        S.info.p);
-    ++S.launches;
-    total += nch;
-    c0 = c1;
   }
-  S.npairs = total;
   {
     const long long z = 0;
     if (KI == 0) CK(cudaMemcpyAsync(S.pair_off.p, &z, sizeof(long long), cudaMemcpyHostToDevice, st));
   }
-  int err_elem = big;
-  CK(cudaMemcpyAsync(&err_elem, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (err_elem != big)
-    throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
-               "BallExitsMesh: ball reaches past an unglued facet of element " +
-                   std::to_string(err_elem)};
+  // the pair offsets (hence the total) and the BallExitsMesh flag come back in
+  // one round trip, after the pattern work has been handed to its stream
+  std::vector<long long> poff(KI + 1, 0);
+  int err_elem_h = big;
   CK(cudaEventRecord(S.ev[2], st));
 
   // ---- K5: pattern, on stream2 from its own host thread (overlaps the units)
@@ -2677,12 +2693,17 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   const bool need_units = D.strategy != NLFEM_STRATEGY_BARYCENTER;
   float mc_ms = 0;
+  CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&err_elem_h, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err_elem_h != big)
+    throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
+               "BallExitsMesh: ball reaches past an unglued facet of element " +
+                   std::to_string(err_elem_h)};
+  S.npairs = poff[KI];
   if (shard_hi > shard_lo) {
     // chunks of outer elements sized so the unit buffers stay bounded
-    std::vector<long long> poff(KI + 1);
-    CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
     const long long kPairsPerChunk = need_units ? (8LL << 20) : (1LL << 40);
     int ii0 = shard_lo;
     while (ii0 < shard_hi) {
