@@ -1579,10 +1579,22 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
         // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
         uint32_t A[4], B[4], Cw[4];
         philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, A, B, Cw);
-        sample(A[0], A[1], A[2], dd);
-        sample(A[3], B[0], B[1], dd);
-        sample(B[2], B[3], Cw[0], dd);
-        sample(Cw[1], Cw[2], Cw[3], dd);
+        if (CONS && !G2) {
+          sample(A[0], A[1], A[2], dd);
+          sample(A[3], B[0], B[1], dd);
+          sample(B[2], B[3], Cw[0], dd);
+          sample(Cw[1], Cw[2], Cw[3], dd);
+        } else {
+          // the four points and |r|^2 first (four independent FP64 chains),
+          // then the hit updates
+          double rx[4], ry[4], rz[4], r2[4];
+          r2[0] = mc_point_r2(A[0], A[1], A[2], fs, rx[0], ry[0], rz[0]);
+          r2[1] = mc_point_r2(A[3], B[0], B[1], fs, rx[1], ry[1], rz[1]);
+          r2[2] = mc_point_r2(B[2], B[3], Cw[0], fs, rx[2], ry[2], rz[2]);
+          r2[3] = mc_point_r2(Cw[1], Cw[2], Cw[3], fs, rx[3], ry[3], rz[3]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) hm.add(r2[i], dd, rx[i], ry[i], rz[i]);
+        }
       }
       if (M & 3) {  // partial last block: samples past M are drawn but never hit
         uint32_t A[4], B[4], Cw[4];
