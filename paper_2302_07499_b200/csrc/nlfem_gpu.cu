@@ -168,6 +168,40 @@ __global__ void k_scan_block(const Tin* in, long long* out, long long* sums, lon
   if (threadIdx.x == kScanBlock - 1) sums[blockIdx.x] = s[threadIdx.x];
 }
 
+// single-CTA exclusive scan for small n (one launch, total written to out[n]):
+// thread t scans its contiguous slice, warp and block prefixes of the slice sums
+constexpr int kScan1Threads = 1024;
+constexpr long long kScan1Max = 64 * 1024;
+template <class Tin>
+__global__ void __launch_bounds__(kScan1Threads) k_scan_one(const Tin* in, long long* out,
+                                                            long long n) {
+  __shared__ long long wsum[kScan1Threads / 32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const long long per = (n + kScan1Threads - 1) / kScan1Threads;
+  const long long lo = min(n, (long long)t * per), hi = min(n, lo + per);
+  long long acc = 0;
+  for (long long i = lo; i < hi; ++i) acc += (long long)in[i];
+  long long inc = acc;
+  for (int sh = 1; sh < 32; sh <<= 1) {
+    const long long y = __shfl_up_sync(FULLMASK, inc, sh);
+    if (lane >= sh) inc += y;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  long long wbase = 0, total = 0;
+  for (int w = 0; w < kScan1Threads / 32; ++w) {
+    wbase += w < wid ? wsum[w] : 0;
+    total += wsum[w];
+  }
+  long long run = wbase + inc - acc;
+  for (long long i = lo; i < hi; ++i) {
+    const long long v = (long long)in[i];
+    out[i] = run;
+    run += v;
+  }
+  if (t == 0) out[n] = total;
+}
+
 __global__ void k_scan_add(long long* out, const long long* offs, long long n) {
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   if (i < n) out[i] += offs[blockIdx.x];
@@ -2173,6 +2207,14 @@ void scan64_level(nlfem_gpu_session& S, long long* scratch, const void* in, bool
 
 void scan64(nlfem_gpu_session& S, const void* in, bool in_is_int, long long n, long long* out,
             cudaStream_t st) {
+  if (n > 0 && n <= kScan1Max) {
+    if (in_is_int)
+      k_scan_one<int><<<1, kScan1Threads, 0, st>>>((const int*)in, out, n);
+    else
+      k_scan_one<long long><<<1, kScan1Threads, 0, st>>>((const long long*)in, out, n);
+    ++S.launches;
+    return;
+  }
   size_t need = 0;
   for (long long m = n; m > 1; m = (m + kScanBlock - 1) / kScanBlock)
     need += 2 * (size_t)((m + kScanBlock - 1) / kScanBlock + 1);
