@@ -1065,6 +1065,20 @@ __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot,
   if (lo != 0) atomicAdd(V + 2 * slot + 1, (unsigned long long)lo);
 }
 
+// Entries whose row and column are both unknowns take the high word only
+// (~62 bits of the row bound: errors stay ~1e-13 of the row's largest entry);
+// entries touching a constrained node feed the rhs folding, where
+// cancellation can amplify errors, and keep both words.
+__device__ __forceinline__ void red_fixed_sel(unsigned long long* V, long long slot, double v,
+                                              double scale, bool two) {
+  if (!two) {
+    const long long hi = __double2ll_rn(v * scale);
+    if (hi != 0) atomicAdd(V + 2 * slot, (unsigned long long)hi);
+    return;
+  }
+  red_fixed(V, slot, v, scale);
+}
+
 __device__ __forceinline__ double fixed_value(const unsigned long long* V, long long slot,
                                               double iscale) {
   const long long hi = (long long)V[2 * slot], lo = (long long)V[2 * slot + 1];
@@ -1763,6 +1777,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
   const double wq = 0.25 * cD.vol[T];  // rule.w[k] * vol (reference assembly.cpp:702)
   const double C = cD.C;
   const double sc[4] = {cD.scale[NT[0]], cD.scale[NT[1]], cD.scale[NT[2]], cD.scale[NT[3]]};
+  const bool conT[4] = {cD.dof[NT[0]] < 0, cD.dof[NT[1]] < 0, cD.dof[NT[2]] < 0,
+                        cD.dof[NT[3]] < 0};
   // per outer element: sum over pairs of S0_q (constraint parents weigh 2,
   // reference assembly.cpp:419) and of sum_q c_{q,a} Sg_q
   double s0w[4] = {0, 0, 0, 0}, sgc[4] = {0, 0, 0, 0};
@@ -1887,6 +1903,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     if (!constr) {
       const int4 wP = cD.verts[Tp];
       const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
+      const bool conP[4] = {cD.dof[NP[0]] < 0, cD.dof[NP[1]] < 0, cD.dof[NP[2]] < 0,
+                            cD.dof[NP[3]] < 0};
       // T x T' cross block -C w X[a][b] at (N_a, M_b): shared-memory rows
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -1895,7 +1913,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const double x = -C * wq * X[a][b];
-          red_fixed(V, rbase[a] + sla[a], NT[a] == NP[b] ? 2.0 * x : x, sc[a]);
+          red_fixed_sel(V, rbase[a] + sla[a], NT[a] == NP[b] ? 2.0 * x : x, sc[a],
+                        conT[a] || conP[b]);
         }
       }
       // T' x T' block C w sum_q S2_q at (M_b, M_c), row min(M_b, M_c)
@@ -1905,7 +1924,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
         for (int cc = b; cc < 4; ++cc) {
           const int k = s2i(b, cc);
-          red_fixed(V, es[k], C * wq * S2[k], cD.scale[min(NP[b], NP[cc])]);
+          red_fixed_sel(V, es[k], C * wq * S2[k], cD.scale[min(NP[b], NP[cc])],
+                        conP[b] || conP[cc]);
         }
     }
   }
