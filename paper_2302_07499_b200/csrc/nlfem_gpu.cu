@@ -101,6 +101,7 @@ struct Dev {
   // element data
   const double4* erec;  // [4K]: (c, r), (v0, v1.x), (v1.yz, v2.xy), (v2.z, v3)
   const double* gbar;   // [K] constraint elements: sum_k vol/4 g(x_k) (whole-element Sg)
+  const double* cert2;  // [K] nocaps certificate threshold (cert_threshold2)
   const int4* verts;
   const int4* nbr;
   const double* vol;
@@ -372,6 +373,12 @@ __device__ __forceinline__ double cert_threshold2(double diam, double vol, doubl
   const double rho = diam * fmax(cbrt(8.0 * tau / vol), 1e-6);
   const double t = cD.delta - 2.0 * rho;
   return t > 0 ? t * t * (1.0 - 1e-12) : 0.0;
+}
+
+// per element: the nocaps certificate threshold (depends on T' only)
+__global__ void k_cert2(int K, double* cert2) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < K) cert2[t] = cert_threshold2(cD.diam[t], cD.vol[t], cD.tau[t]);
 }
 
 
@@ -712,7 +719,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
           sg.rec[k][3] = cD.erec[4 * Tp + 3];
           sg.vol[k] = cD.vol[Tp];
           sg.tau[k] = cD.tau[Tp];
-          sg.cert2[k] = cert_threshold2(cD.diam[Tp], sg.vol[k], sg.tau[k]);
+          sg.cert2[k] = cD.cert2[Tp];
           sg.pass[k] = (unsigned char)pm;
         }
         __syncthreads();
@@ -2155,7 +2162,7 @@ struct nlfem_gpu_session {
   DBuf<uint8_t> region;
   DBuf<int> interior, ipos, dof, dof_node;
   DBuf<double4> erec;
-  DBuf<double> gbar;
+  DBuf<double> gbar, cert2;
   // grid / incidence
   DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
   DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp, scan_tmp2;
@@ -2402,8 +2409,10 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.rmax = rmax;
   S.erec.ensure(4 * (size_t)S.K);
   S.gbar.ensure(S.K);
+  S.cert2.ensure(S.K);
   D.erec = S.erec.p;
   D.gbar = S.gbar.p;
+  D.cert2 = S.cert2.p;
   D.verts = S.verts.p;
   D.nbr = S.nbr.p;
   D.vol = S.vol.p;
@@ -2430,7 +2439,8 @@ void run_prep(nlfem_gpu_session& S) {
   CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
   k_erec<<<nblk(K, 256), 256, 0, st>>>(K, S.node.p, S.verts.p, S.center.p, S.radius.p, S.erec.p);
   k_gbar<<<nblk(K, 256), 256, 0, st>>>(K, S.gbar.p);
-  S.launches += 2;
+  k_cert2<<<nblk(K, 256), 256, 0, st>>>(K, S.cert2.p);
+  S.launches += 3;
   // grid
   S.cell_key.ensure(K);
   S.cell_cnt.ensure(ncell);
