@@ -102,6 +102,7 @@ struct Dev {
   const double4* erec;  // [4K]: (c, r), (v0, v1.x), (v1.yz, v2.xy), (v2.z, v3)
   const double* gbar;   // [K] constraint elements: sum_k vol/4 g(x_k) (whole-element Sg)
   const double* cert2;  // [K] nocaps certificate threshold (cert_threshold2)
+  const unsigned char* bnd;  // [K] 1 if the element has an unglued facet
   const int4* verts;
   const int4* nbr;
   const double* vol;
@@ -375,10 +376,14 @@ __device__ __forceinline__ double cert_threshold2(double diam, double vol, doubl
   return t > 0 ? t * t * (1.0 - 1e-12) : 0.0;
 }
 
-// per element: the nocaps certificate threshold (depends on T' only)
-__global__ void k_cert2(int K, double* cert2) {
+// per element: the nocaps certificate threshold and whether it has an unglued
+// facet (the BallExitsMesh probe applies), both depending on T' only
+__global__ void k_cert2(int K, double* cert2, unsigned char* bnd) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < K) cert2[t] = cert_threshold2(cD.diam[t], cD.vol[t], cD.tau[t]);
+  if (t >= K) return;
+  cert2[t] = cert_threshold2(cD.diam[t], cD.vol[t], cD.tau[t]);
+  const int4 nb = cD.nbr[t];
+  bnd[t] = (nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) ? 1 : 0;
 }
 
 
@@ -521,6 +526,7 @@ struct CandStage {
   double vol[kCandChunk], tau[kCandChunk], cert2[kCandChunk];
   int id[kCandChunk];
   unsigned char pass[kCandChunk];  // bit w: passes warp w's superset screen
+  unsigned char bnd[kCandChunk];   // candidate has an unglued facet
   short mine[kPairWarps][kCandChunk];  // per warp: indices of its candidates
 };
 
@@ -611,8 +617,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
         const unsigned c = classify_cheap(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]);
         if (c & kDefer) ent = 16u | (c & 15u);
         else code = c << (5 * q);
-        const int4 nb = cD.nbr[sg.id[k]];
-        if (nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) ent |= 32u;
+        if (sg.bnd[k]) ent |= 32u;
         if (ent) ent |= ((unsigned)q << 6) | ((unsigned)t << 8);
       }
       code |= __shfl_xor_sync(FULLMASK, code, 1);
@@ -720,6 +725,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
           sg.vol[k] = cD.vol[Tp];
           sg.tau[k] = cD.tau[Tp];
           sg.cert2[k] = cD.cert2[Tp];
+          sg.bnd[k] = cD.bnd[Tp];
           sg.pass[k] = (unsigned char)pm;
         }
         __syncthreads();
@@ -2163,6 +2169,7 @@ struct nlfem_gpu_session {
   DBuf<int> interior, ipos, dof, dof_node;
   DBuf<double4> erec;
   DBuf<double> gbar, cert2;
+  DBuf<unsigned char> bnd;
   // grid / incidence
   DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
   DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp, scan_tmp2;
@@ -2410,9 +2417,11 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   S.erec.ensure(4 * (size_t)S.K);
   S.gbar.ensure(S.K);
   S.cert2.ensure(S.K);
+  S.bnd.ensure(S.K);
   D.erec = S.erec.p;
   D.gbar = S.gbar.p;
   D.cert2 = S.cert2.p;
+  D.bnd = S.bnd.p;
   D.verts = S.verts.p;
   D.nbr = S.nbr.p;
   D.vol = S.vol.p;
@@ -2439,7 +2448,7 @@ void run_prep(nlfem_gpu_session& S) {
   CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
   k_erec<<<nblk(K, 256), 256, 0, st>>>(K, S.node.p, S.verts.p, S.center.p, S.radius.p, S.erec.p);
   k_gbar<<<nblk(K, 256), 256, 0, st>>>(K, S.gbar.p);
-  k_cert2<<<nblk(K, 256), 256, 0, st>>>(K, S.cert2.p);
+  k_cert2<<<nblk(K, 256), 256, 0, st>>>(K, S.cert2.p, S.bnd.p);
   S.launches += 3;
   // grid
   S.cell_key.ensure(K);
