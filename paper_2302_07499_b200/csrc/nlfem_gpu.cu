@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
                                                         unsigned long long* item_count,
                                                         int* err_elem) {
   __shared__ CandStage sg;
-  __shared__ int nst, xb[6], scnt[kPairWarps];
+  __shared__ int xb[6], scnt[kPairWarps];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int warp = ii_base + blockIdx.x * kPairWarps + wl;  // outer element index
   const bool active = warp < ii_end;
@@ -593,11 +593,12 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
   // deferred items (bits 0-3 mask, 4 classify, 5 facet probe, 6-7 q, 8-14 index)
   __shared__ unsigned wcode[kPairWarps][kCandChunk];
   __shared__ unsigned short wdef[kPairWarps][4 * kCandChunk];
+  int nreg = 0;  // candidates staged so far (same value in every thread)
   auto classify_chunk = [&]() {
     int nm = 0;
-    for (int base = 0; base < nst; base += 32) {
+    for (int base = 0; base < nreg; base += 32) {
       const int k = base + lane;
-      const bool mine = k < nst && ((sg.pass[k] >> wl) & 1);
+      const bool mine = k < nreg && ((sg.pass[k] >> wl) & 1);
       const unsigned bal = __ballot_sync(FULLMASK, mine);
       if (mine) sg.mine[wl][nm + __popc(bal & ((1u << lane) - 1))] = (short)k;
       nm += __popc(bal);
@@ -659,8 +660,12 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
     cnt += nm;
   };
 
-  if (threadIdx.x == 0) nst = 0;
-  __syncthreads();
+  // staging: one block barrier per batch of kPairThreads candidates.  The
+  // per-warp survivor counts are double-buffered by batch parity; every thread
+  // derives the warp bases and the running staged count itself; the next
+  // batch's barrier orders this batch's staging writes before any reads.
+  __shared__ int wcount[2][kPairWarps];
+  int par = 0;
   for (int z = z0; z <= z1; ++z) {
     for (int y = y0; y <= y1; ++y) {
       const int row = (z * cD.gy + y) * cD.gx;
@@ -681,7 +686,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
               pm |= 1u << w;
           }
         }
-        if (MODE == 0) {
+        if constexpr (MODE == 0) {
 #pragma unroll
           for (int w = 0; w < kPairWarps; ++w) {
             const int c = __popc(__ballot_sync(FULLMASK, (pm >> w) & 1));
@@ -691,32 +696,23 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
         }
         // stage survivors (block-wide compaction, stream order)
         const unsigned bal = __ballot_sync(FULLMASK, pm != 0);
-        __shared__ int wcount[kPairWarps], wbase[kPairWarps];
-        if (lane == 0) wcount[wl] = __popc(bal);
+        if (lane == 0) wcount[par][wl] = __popc(bal);
         __syncthreads();
-        if (threadIdx.x == 0) {
-          int acc = nst;
-          for (int w = 0; w < kPairWarps; ++w) {
-            wbase[w] = acc;
-            acc += wcount[w];
-          }
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kPairWarps; ++w) {
+          const int c = wcount[par][w];
+          before += w < wl ? c : 0;
+          tot += c;
         }
-        __syncthreads();
-        const int tot = wbase[kPairWarps - 1] + wcount[kPairWarps - 1];
-        if (tot > kCandChunk) {
+        par ^= 1;
+        if (nreg + tot > kCandChunk) {
           classify_chunk();
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int w = 0; w < kPairWarps; ++w) {
-              wbase[w] = acc;
-              acc += wcount[w];
-            }
-          }
-          __syncthreads();
+          __syncthreads();  // every warp is done reading the staged chunk
+          nreg = 0;
         }
         if (pm) {
-          const int k = wbase[wl] + __popc(bal & ((1u << lane) - 1));
+          const int k = nreg + before + __popc(bal & ((1u << lane) - 1));
           sg.id[k] = Tp;
           sg.rec[k][0] = a;
           sg.rec[k][1] = cD.erec[4 * Tp + 1];
@@ -728,9 +724,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
           sg.bnd[k] = cD.bnd[Tp];
           sg.pass[k] = (unsigned char)pm;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) nst = wbase[kPairWarps - 1] + wcount[kPairWarps - 1];
-        __syncthreads();
+        nreg += tot;
       }
     }
   }
@@ -739,6 +733,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
     if (active && lane == 0) cand_count[warp] = scnt[wl];
     return;
   }
+  __syncthreads();  // the last batch's staging before the final chunk
   classify_chunk();
   for (int sh = 16; sh > 0; sh >>= 1) {
     items += __shfl_xor_sync(FULLMASK, items, sh);
