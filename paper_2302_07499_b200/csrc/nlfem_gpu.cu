@@ -1809,6 +1809,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     const double volP = cD.vol[Tp];
     const double* invP = cD.inv + 9 * (long long)Tp;
     long long u = (mom != nullptr) ? uoff[p - pbase] : 0;  // first record of the pair
+    if (mom != nullptr && p + NTHR < p1) {
+      // next pair of this thread: pull its records (<= 4 x 80 B) into L2 now
+      const char* nr = reinterpret_cast<const char*>(mom + kMomStride * uoff[p + NTHR - pbase]);
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nr + 128 * l));
+    }
 
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
