@@ -39,17 +39,6 @@ __device__ __forceinline__ double tet_volume(Vd a, Vd b, Vd c, Vd d) {
   return fabs(vdot(vcross(vsub(b, a), vsub(c, a)), vsub(d, a))) / 6.0;
 }
 
-// classify_simplex inside flags (reference geometry.cpp:8-24): bit i set iff
-// |v_i - c|^2 < (r - 1e-10 r)^2.
-__device__ __forceinline__ int inside_mask(const Vd v[4], Vd c, double r) {
-  const double r_in = r - 1e-10 * r;
-  const double r2 = r_in * r_in;
-  int m = 0;
-  for (int i = 0; i < 4; ++i)
-    if (vnorm2(vsub(v[i], c)) < r2) m |= 1 << i;
-  return m;
-}
-
 // edge_sphere_crossing (reference geometry.cpp:26-37).
 __device__ __forceinline__ double edge_crossing(Vd a, Vd b, Vd c, double r) {
   const Vd d = vsub(b, a);
@@ -62,107 +51,6 @@ __device__ __forceinline__ double edge_crossing(Vd a, Vd b, Vd c, double r) {
   const double sq = sqrt(disc);
   double t = (B <= 0) ? (-B + sq) / A : -C / (B + sq);
   return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
-}
-
-// crossing_points (reference geometry.cpp:39-50): inside slots ascending, then
-// outside slots ascending; at most 4 for a tetrahedron.
-__device__ __forceinline__ int crossing_points(const Vd v[4], int mask, Vd c, double r, Vd q[4]) {
-  int n = 0;
-  for (int i = 0; i < 4; ++i) {
-    if (!(mask >> i & 1)) continue;
-    for (int o = 0; o < 4; ++o) {
-      if (mask >> o & 1) continue;
-      const double t = edge_crossing(v[i], v[o], c, r);
-      q[n++] = vadd(v[i], vscale(t, vsub(v[o], v[i])));
-    }
-  }
-  return n;
-}
-
-struct Tet {
-  Vd v[4];
-};
-
-// push_piece (reference ball_approx.cpp:135-142): keep iff volume > tau.
-__device__ __forceinline__ void push_piece(Tet* out, int& n, Vd a, Vd b, Vd c, Vd d, double tau) {
-  if (tet_volume(a, b, c, d) > tau) {
-    out[n].v[0] = a;
-    out[n].v[1] = b;
-    out[n].v[2] = c;
-    out[n].v[3] = d;
-    ++n;
-  }
-}
-
-// split_prism / split_warped_prism (reference ball_approx.cpp:150-175).
-__device__ __forceinline__ void split_prism(Tet* out, int& n, const Vd A[3], const Vd B[3],
-                                            double tau) {
-  push_piece(out, n, A[0], A[1], A[2], B[0], tau);
-  push_piece(out, n, A[1], A[2], B[0], B[1], tau);
-  push_piece(out, n, A[2], B[0], B[1], B[2], tau);
-}
-
-__device__ __forceinline__ void split_warped_prism(Tet* out, int& n, const Vd A[3],
-                                                   const Vd B[3], double tau) {
-  const double va = tet_volume(A[0], A[1], A[2], B[0]) + tet_volume(A[1], A[2], B[0], B[1]) +
-                    tet_volume(A[2], B[0], B[1], B[2]);
-  const double vb = tet_volume(A[0], A[2], A[1], B[0]) + tet_volume(A[2], A[1], B[0], B[2]) +
-                    tet_volume(A[1], B[0], B[2], B[1]);
-  if (vb > va) {
-    const Vd A2[3] = {A[0], A[2], A[1]};
-    const Vd B2[3] = {B[0], B[2], B[1]};
-    split_prism(out, n, A2, B2, tau);
-  } else {
-    split_prism(out, n, A, B, tau);
-  }
-}
-
-// detail::straddle_inner without sphere points (reference ball_approx.cpp:195-255).
-__device__ __forceinline__ int straddle_inner(const Vd v[4], int mask, Vd c, double r,
-                                              double tau, Tet out[3]) {
-  Vd q[4];
-  crossing_points(v, mask, c, r, q);
-  int in_slot[4], m = 0;
-  for (int i = 0; i < 4; ++i)
-    if (mask >> i & 1) in_slot[m++] = i;
-  int n = 0;
-  if (m == 1) {
-    push_piece(out, n, v[in_slot[0]], q[0], q[1], q[2], tau);
-  } else if (m == 2) {
-    const Vd A[3] = {v[in_slot[0]], q[0], q[1]};
-    const Vd B[3] = {v[in_slot[1]], q[2], q[3]};
-    split_warped_prism(out, n, A, B, tau);
-  } else {
-    const Vd A[3] = {v[in_slot[0]], v[in_slot[1]], v[in_slot[2]]};
-    const Vd B[3] = {q[0], q[1], q[2]};
-    split_prism(out, n, A, B, tau);
-  }
-  return n;
-}
-
-// detail::straddle_outer (reference ball_approx.cpp:257-298).
-__device__ __forceinline__ int straddle_outer(const Vd v[4], int mask, Vd c, double r,
-                                              double tau, Tet out[3]) {
-  Vd q[4];
-  crossing_points(v, mask, c, r, q);
-  int out_slot[4], m = 0, mo = 0;
-  for (int i = 0; i < 4; ++i) {
-    if (mask >> i & 1) ++m;
-    else out_slot[mo++] = i;
-  }
-  int n = 0;
-  if (m == 1) {
-    const Vd A[3] = {q[0], q[1], q[2]};
-    const Vd B[3] = {v[out_slot[0]], v[out_slot[1]], v[out_slot[2]]};
-    split_prism(out, n, A, B, tau);
-  } else if (m == 2) {
-    const Vd A[3] = {v[out_slot[0]], q[0], q[2]};
-    const Vd B[3] = {v[out_slot[1]], q[1], q[3]};
-    split_warped_prism(out, n, A, B, tau);
-  } else {
-    push_piece(out, n, v[out_slot[0]], q[0], q[1], q[2], tau);
-  }
-  return n;
 }
 
 // point_triangle_distance, Ericson's region walk (reference geometry.cpp:98-127).
@@ -233,29 +121,10 @@ __device__ __forceinline__ double facet_distance(const Vd v[4], int slot, Vd p) 
 struct Straddle {
   Vd A0, A1, A2, B0, B1, B2;
   int n;  // 1 (single tet) or 3 (prism split)
-  // barycentric coordinates of the six points in the parent element:
-  // lambda = (1 - t) e_a + t e_b (vertices: a = b, t = 0; crossings: the edge)
-  int la[6], lb[6];
-  double lt[6];
 };
-
-__device__ __forceinline__ Vd crossing_point(Vd a, Vd b, Vd c, double r) {
-  const double t = edge_crossing(a, b, c, r);
-  return vadd(a, vscale(t, vsub(b, a)));
-}
 
 __device__ __forceinline__ Vd pick(const Vd v[4], int i) {
   return i == 0 ? v[0] : (i == 1 ? v[1] : (i == 2 ? v[2] : v[3]));
-}
-
-__device__ __forceinline__ void split_slots(int mask, int in[4], int out[4], int& m) {
-  m = 0;
-  int mo = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (mask >> i & 1) in[m++] = i;
-    else out[mo++] = i;
-  }
 }
 
 __device__ __forceinline__ void orient_warped(Straddle& s) {
@@ -270,13 +139,6 @@ __device__ __forceinline__ void orient_warped(Straddle& s) {
     const Vd u = s.B1;
     s.B1 = s.B2;
     s.B2 = u;
-    int ia = s.la[1], ib = s.lb[1];
-    double it = s.lt[1];
-    s.la[1] = s.la[2]; s.lb[1] = s.lb[2]; s.lt[1] = s.lt[2];
-    s.la[2] = ia; s.lb[2] = ib; s.lt[2] = it;
-    ia = s.la[4]; ib = s.lb[4]; it = s.lt[4];
-    s.la[4] = s.la[5]; s.lb[4] = s.lb[5]; s.lt[4] = s.lt[5];
-    s.la[5] = ia; s.lb[5] = ib; s.lt[5] = it;
   }
 }
 
@@ -306,19 +168,13 @@ __device__ __forceinline__ int nth_bit4(unsigned mask, int r) {
 // edge (k-th inside slot -> j-th outside slot), k = i_rank * (4 - m) + j
 struct Crossings {
   Vd q[4];
-  int a[4], b[4];  // edge (inside slot, outside slot)
-  double t[4];
 };
 
 __device__ __forceinline__ void crossings4(const Vd v[4], int mask, Vd c, double r, Crossings& X) {
   const int m = __popc(mask), mo = 4 - m, n = m * mo;
   const unsigned inm = (unsigned)mask, outm = (unsigned)(~mask & 15);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    X.q[k] = v[0];
-    X.a[k] = X.b[k] = 0;
-    X.t[k] = 0;
-  }
+  for (int k = 0; k < 4; ++k) X.q[k] = v[0];
 #pragma unroll 1
   for (int k = 0; k < n; ++k) {
     const int ir = k / mo, orr = k - ir * mo;
@@ -328,24 +184,8 @@ __device__ __forceinline__ void crossings4(const Vd v[4], int mask, Vd c, double
     const Vd p = vadd(a, vscale(t, vsub(b, a)));
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (k == j) {
-        X.q[j] = p;
-        X.a[j] = i;
-        X.b[j] = o;
-        X.t[j] = t;
-      }
+      if (k == j) X.q[j] = p;
   }
-}
-
-__device__ __forceinline__ void set_vertex(Straddle& s, int p, int slot) {
-  s.la[p] = slot;
-  s.lb[p] = slot;
-  s.lt[p] = 0.0;
-}
-__device__ __forceinline__ void set_cross(Straddle& s, int p, const Crossings& X, int k) {
-  s.la[p] = X.a[k];
-  s.lb[p] = X.b[k];
-  s.lt[p] = X.t[k];
 }
 
 __device__ __forceinline__ int nth_slot(int mask, int n) { return nth_bit4((unsigned)mask, n); }
@@ -360,19 +200,13 @@ __device__ __forceinline__ Straddle inner_straddle_x(const Vd v[4], int mask, co
   Straddle s;
   if (m == 1) {  // tet (a, a->o0, a->o1, a->o2)
     s.A0 = i0; s.A1 = X.q[0]; s.A2 = X.q[1]; s.B0 = X.q[2]; s.B1 = X.q[2]; s.B2 = X.q[2];
-    set_vertex(s, 0, s0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 1);
-    set_cross(s, 3, X, 2); set_cross(s, 4, X, 2); set_cross(s, 5, X, 2);
     s.n = 1;
   } else if (m == 2) {  // warped prism {a, a->o0, a->o1} | {b, b->o0, b->o1}
     s.A0 = i0; s.A1 = X.q[0]; s.A2 = X.q[1]; s.B0 = i1; s.B1 = X.q[2]; s.B2 = X.q[3];
-    set_vertex(s, 0, s0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 1);
-    set_vertex(s, 3, s1); set_cross(s, 4, X, 2); set_cross(s, 5, X, 3);
     s.n = 3;
     orient_warped(s);
   } else {  // frustum {a, b, d} | {a->o, b->o, d->o}
     s.A0 = i0; s.A1 = i1; s.A2 = i2; s.B0 = X.q[0]; s.B1 = X.q[1]; s.B2 = X.q[2];
-    set_vertex(s, 0, s0); set_vertex(s, 1, s1); set_vertex(s, 2, s2);
-    set_cross(s, 3, X, 0); set_cross(s, 4, X, 1); set_cross(s, 5, X, 2);
     s.n = 3;
   }
   return s;
@@ -386,19 +220,13 @@ __device__ __forceinline__ Straddle outer_straddle_x(const Vd v[4], int mask, co
   Straddle s;
   if (m == 1) {  // frustum {a->o0, a->o1, a->o2} | {o0, o1, o2}
     s.A0 = X.q[0]; s.A1 = X.q[1]; s.A2 = X.q[2]; s.B0 = o0; s.B1 = o1; s.B2 = o2;
-    set_cross(s, 0, X, 0); set_cross(s, 1, X, 1); set_cross(s, 2, X, 2);
-    set_vertex(s, 3, t0); set_vertex(s, 4, t1); set_vertex(s, 5, t2);
     s.n = 3;
   } else if (m == 2) {  // warped prism {c, a->c, b->c} | {d, a->d, b->d}
     s.A0 = o0; s.A1 = X.q[0]; s.A2 = X.q[2]; s.B0 = o1; s.B1 = X.q[1]; s.B2 = X.q[3];
-    set_vertex(s, 0, t0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 2);
-    set_vertex(s, 3, t1); set_cross(s, 4, X, 1); set_cross(s, 5, X, 3);
     s.n = 3;
     orient_warped(s);
   } else {  // corner tet (o, a->o, b->o, d->o)
     s.A0 = o0; s.A1 = X.q[0]; s.A2 = X.q[1]; s.B0 = X.q[2]; s.B1 = X.q[2]; s.B2 = X.q[2];
-    set_vertex(s, 0, t0); set_cross(s, 1, X, 0); set_cross(s, 2, X, 1);
-    set_cross(s, 3, X, 2); set_cross(s, 4, X, 2); set_cross(s, 5, X, 2);
     s.n = 1;
   }
   return s;
@@ -425,14 +253,3 @@ __device__ __forceinline__ void straddle_piece(const Straddle& s, int k, Vd& a, 
   d = k == 0 ? s.B0 : (k == 1 ? s.B1 : s.B2);
 }
 
-// barycentric-label indices (into la/lb/lt) of the four vertices of piece k
-__device__ __forceinline__ void straddle_piece_ids(int k, int& p0, int& p1, int& p2, int& p3) {
-  p0 = k;      // A0 | A1 | A2
-  p1 = k + 1;  // A1 | A2 | B0
-  p2 = k + 2;  // A2 | B0 | B1
-  p3 = k + 3;  // B0 | B1 | B2
-}
-
-// number of Monte Carlo sub-simplices straddle_outer can emit (before the
-// volume floor): m=1 prism -> 3, m=2 warped prism -> 3, m=3 corner -> 1
-__device__ __forceinline__ int outer_units(int mask) { return __popc(mask) == 3 ? 1 : 3; }
