@@ -176,6 +176,22 @@ int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, 
                                 size_t errlen);
 int nlfem_gpu_session_partials(nlfem_gpu_session* s, void** V, int64_t* nwords, void** rhsT,
                                int64_t* nrhs);
+/* Sharded element pairs (multi-GPU without redundant pair construction).
+ * pairs_shard builds the element pairs of outer elements [lo, hi) only (after
+ * the mesh preprocessing) and returns their number; pairs_shard_out exposes
+ * device views of the range's per-outer-element pair counts (int32, hi - lo)
+ * and partner ids (int32, in outer order) for an all-gather; pairs_install takes
+ * the gathered counts of ALL outer elements (int32, interior order) and all
+ * partner ids (device pointers, concatenated in outer order) and makes the next
+ * run_shard build the node pattern from them and integrate [lo, hi) with the
+ * codes this rank computed.  Results are bit-identical to an unsharded run. */
+int nlfem_gpu_session_pairs_shard(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
+                                  int64_t* npairs, char* err, size_t errlen);
+int nlfem_gpu_session_pairs_shard_out(nlfem_gpu_session* s, void** counts, void** partners,
+                                      int64_t* npairs);
+int nlfem_gpu_session_pairs_install(nlfem_gpu_session* s, void* stream, const void* counts,
+                                    const void* partners, int64_t npairs_total, char* err,
+                                    size_t errlen);
 int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_lo,
                                int32_t row_hi, char* err, size_t errlen);
 int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,

@@ -125,6 +125,12 @@ def lib():
     L.nlfem_gpu_session_run_shard.argtypes = [vp, vp, i32, i32, i32, P(Stats), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_partials.restype = C.c_int
     L.nlfem_gpu_session_partials.argtypes = [vp, P(vp), P(i64), P(vp), P(i64)]
+    L.nlfem_gpu_session_pairs_shard.restype = C.c_int
+    L.nlfem_gpu_session_pairs_shard.argtypes = [vp, vp, i32, i32, P(i64), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_pairs_shard_out.restype = C.c_int
+    L.nlfem_gpu_session_pairs_shard_out.argtypes = [vp, P(vp), P(vp), P(i64)]
+    L.nlfem_gpu_session_pairs_install.restype = C.c_int
+    L.nlfem_gpu_session_pairs_install.argtypes = [vp, vp, vp, vp, i64, C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_finalize.restype = C.c_int
     L.nlfem_gpu_session_finalize.argtypes = [vp, vp, i32, i32, C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_download_rows.restype = C.c_int
@@ -159,7 +165,8 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
     "nlfem_gpu_fp64_peak", "nlfem_gpu_session_run_shard", "nlfem_gpu_session_partials",
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
-    "nlfem_gpu_session_outputs",
+    "nlfem_gpu_session_outputs", "nlfem_gpu_session_pairs_shard",
+    "nlfem_gpu_session_pairs_shard_out", "nlfem_gpu_session_pairs_install",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
 ]
@@ -392,6 +399,35 @@ class Session:
                                                  int(hi), int(finalize), C.byref(self.stats),
                                                  err, 1024), err)
         return self.stats
+
+    def pairs_shard(self, lo: int, hi: int, stream: int | None = None) -> int:
+        """Build the element pairs of outer elements [lo, hi) only; returns their
+        number (multi-GPU: each rank its own range, see distributed.py)."""
+        n = C.c_int64()
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_pairs_shard(self._h, C.c_void_p(stream or 0), int(lo),
+                                                   int(hi), C.byref(n), err, 1024), err)
+        self._last_shard = (int(lo), int(hi))
+        return n.value
+
+    def pairs_shard_out(self):
+        """Device views of the shard's per-outer-element pair counts (int32) and
+        partner ids (int32, outer order)."""
+        cp, pp, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        lib().nlfem_gpu_session_pairs_shard_out(self._h, C.byref(cp), C.byref(pp), C.byref(n))
+        lo_hi = self._last_shard
+        return (_CudaView(cp.value or 0, lo_hi[1] - lo_hi[0], "<i4"),
+                _CudaView(pp.value or 0, n.value, "<i4"))
+
+    def pairs_install(self, counts, partners, npairs_total: int, stream: int | None = None) -> None:
+        """Install the gathered pair counts of all outer elements and all partner
+        ids (CUDA arrays) for the next run_shard."""
+        def ptr(a):
+            return C.c_void_p(int(a.__cuda_array_interface__["data"][0]))
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_pairs_install(self._h, C.c_void_p(stream or 0),
+                                                     ptr(counts), ptr(partners),
+                                                     int(npairs_total), err, 1024), err)
 
     def partials(self):
         """Device views (V int64 words, rhsT float64) of the exact partial sums."""

@@ -2201,6 +2201,12 @@ struct nlfem_gpu_session {
   HostStage stage;
   // results of the last run
   long long npairs = 0, nnz_s = 0, nnz_out = 0;
+  // sharded pairs (multi-GPU): this rank's K1 range, its pair count, and whether
+  // a gathered pair list of all outer elements is installed for the next run
+  int pairs_lo = 0, pairs_hi = 0;
+  long long shard_npairs = 0;
+  bool pairs_installed = false;
+  DBuf<unsigned> info_own;
   std::atomic<long long> launches{0};
   unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0;
   cudaStream_t stream = nullptr;
@@ -2603,26 +2609,12 @@ void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
                    std::to_string(ovf) + ")"};
 }
 
-// The whole device pipeline.  Outer elements [shard_lo, shard_hi) (positions in
-// the ascending interior list) are integrated; pairs and the node pattern are
-// built for all of them (every rank holds the same pattern, so the fixed-point
-// partial sums of several ranks add up slot by slot).
-void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, int shard_lo,
-             int shard_hi, bool finalize) {
+// K1 over outer elements [lo, hi) (positions in the ascending interior list):
+// pair_count[ii], cand_off[ii], pair_off[ii] are indexed absolutely, offsets are
+// relative to the range start (pair_off[lo] = 0); partner / info hold the
+// range's pairs in outer order.  Resets the counters and the BallExitsMesh flag.
+void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
   cudaStream_t st = S.stream;
-  Dev& D = S.dev;
-  const auto wall0 = std::chrono::steady_clock::now();
-  S.launches = 0;
-  if (user) {
-    // order after work the caller queued on its stream
-    CK(cudaEventRecord(S.ev[7], user));
-    CK(cudaStreamWaitEvent(st, S.ev[7], 0));
-  }
-  CK(cudaEventRecord(S.ev[0], st));
-  run_prep(S);
-  CK(cudaEventRecord(S.ev[1], st));
-
-  // ---- K1: pairs (count, scan, fill)
   const int KI = S.KI;
   S.pair_count.ensure(KI);
   S.pair_off.ensure(KI + 1);
@@ -2636,52 +2628,57 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   // pass 0: survivors per outer element (cheap superset count)
   S.cand_count.ensure(KI + 1);
   S.cand_off.ensure(KI + 1);
-  if (KI > 0) {
-    k_pairs<0><<<nblk((long long)KI, kPairWarps), kPairThreads, 0, st>>>(
-        0, KI, nullptr, 0, S.cand_count.p, nullptr, nullptr, nullptr, nullptr, nullptr);
+  const int n = hi - lo;
+  if (n > 0) {
+    k_pairs<0><<<nblk((long long)n, kPairWarps), kPairThreads, 0, st>>>(
+        lo, hi, nullptr, 0, S.cand_count.p, nullptr, nullptr, nullptr, nullptr, nullptr);
     ++S.launches;
   }
-  scan64(S, S.cand_count.p, true, KI, S.cand_off.p, st);
-  std::vector<long long> coff(KI + 1, 0);
-  CK(cudaMemcpyAsync(coff.data(), S.cand_off.p, sizeof(long long) * (KI + 1),
+  // survivor offsets of the range, relative to its start (cand_off[lo] = 0)
+  scan64(S, S.cand_count.p + lo, true, n, S.cand_off.p + lo, st);
+  std::vector<long long> coffr(n + 1, 0);
+  CK(cudaMemcpyAsync(coffr.data(), S.cand_off.p + lo, sizeof(long long) * (n + 1),
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  // absolute-indexed view: coff[ii] for ii in [lo, hi]
+  auto coff = [&](int ii) { return coffr[ii - lo]; };
   // pass 1 + compaction, in chunks of outer elements bounded by survivors
   const long long kCandBudget = 1LL << 30;  // 8 GiB of (partner, code) slots
   S.pair_off.ensure(KI + 1);
-  if (coff[KI] <= kCandBudget) {
+  if (coff(hi) <= kCandBudget) {
     // one chunk: pairs <= survivors bounds the pair arrays, so the pair total
     // need not come back to the host here (it arrives with the pair offsets
     // the integration phase reads anyway)
-    const long long nc = coff[KI];
+    const long long nc = coff(hi);
     S.partner.ensure(std::max<long long>(1, nc));
     S.info.ensure(std::max<long long>(1, nc));
     S.cpartner.ensure(nc + 1);
     S.cinfo.ensure(nc + 1);
-    if (KI > 0) {
-      k_pairs<1><<<nblk((long long)KI, kPairWarps), kPairThreads, 0, st>>>(
-          0, KI, S.cand_off.p, 0, nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p, S.counters.p,
+    if (n > 0) {
+      k_pairs<1><<<nblk((long long)n, kPairWarps), kPairThreads, 0, st>>>(
+          lo, hi, S.cand_off.p, 0, nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p, S.counters.p,
           S.err_elem.p);
-      scan64(S, S.pair_count.p, true, KI, S.pair_off.p, st);
-      k_pairs_compact<<<nblk((long long)KI * 32, 256), 256, 0, st>>>(
-          0, KI, S.cand_off.p, 0, S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p, S.info.p);
+      scan64(S, S.pair_count.p + lo, true, n, S.pair_off.p + lo, st);
+      k_pairs_compact<<<nblk((long long)n * 32, 256), 256, 0, st>>>(
+          lo, hi, S.cand_off.p, 0, S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p, S.info.p);
       S.launches += 2;
     }
   } else {
-    long long cap = std::max<long long>(1, (long long)(0.8 * coff[KI]));
+    long long cap = std::max<long long>(1, (long long)(0.8 * coff(hi)));
     S.partner.ensure(cap);
     S.info.ensure(cap);
     long long total = 0;
-    int c0 = 0;
-    while (c0 < KI) {
-      int c1 = (int)(std::upper_bound(coff.begin() + c0 + 1, coff.end(), coff[c0] + kCandBudget) -
-                     coff.begin()) - 1;
-      c1 = std::min(std::max(c1, c0 + 1), KI);
-      const long long nc = coff[c1] - coff[c0];
+    int c0 = lo;
+    while (c0 < hi) {
+      int c1 = lo + (int)(std::upper_bound(coffr.begin() + (c0 - lo) + 1, coffr.end(),
+                                           coff(c0) + kCandBudget) -
+                          coffr.begin()) - 1;
+      c1 = std::min(std::max(c1, c0 + 1), hi);
+      const long long nc = coff(c1) - coff(c0);
       S.cpartner.ensure(nc + 1);
       S.cinfo.ensure(nc + 1);
       k_pairs<1><<<nblk((long long)(c1 - c0), kPairWarps), kPairThreads, 0, st>>>(
-          c0, c1, S.cand_off.p, coff[c0], nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
+          c0, c1, S.cand_off.p, coff(c0), nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
           S.counters.p, S.err_elem.p);
       ++S.launches;
       // pair offsets of this chunk continue the running total
@@ -2708,16 +2705,48 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         std::swap(S.info.n, ni_.n);
       }
       k_pairs_compact<<<nblk((long long)(c1 - c0) * 32, 256), 256, 0, st>>>(
-          c0, c1, S.cand_off.p, coff[c0], S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p,
+          c0, c1, S.cand_off.p, coff(c0), S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p,
           S.info.p);
       ++S.launches;
       total += nch;
       c0 = c1;
     }
   }
-  {
+  if (n == 0) {
     const long long z = 0;
-    if (KI == 0) CK(cudaMemcpyAsync(S.pair_off.p, &z, sizeof(long long), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(S.pair_off.p + lo, &z, sizeof(long long), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+}
+
+// The whole device pipeline.  Outer elements [shard_lo, shard_hi) (positions in
+// the ascending interior list) are integrated; pairs and the node pattern are
+// built for all of them (every rank holds the same pattern, so the fixed-point
+// partial sums of several ranks add up slot by slot).
+void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, int shard_lo,
+             int shard_hi, bool finalize) {
+  cudaStream_t st = S.stream;
+  Dev& D = S.dev;
+  const auto wall0 = std::chrono::steady_clock::now();
+  S.launches = 0;
+  if (user) {
+    // order after work the caller queued on its stream
+    CK(cudaEventRecord(S.ev[7], user));
+    CK(cudaStreamWaitEvent(st, S.ev[7], 0));
+  }
+  CK(cudaEventRecord(S.ev[0], st));
+
+  // ---- K1: pairs (count, scan, fill), unless a gathered pair list of all
+  // outer elements has been installed (sharded multi-GPU pairs)
+  const int KI = S.KI;
+  const int big = 0x7fffffff;
+  if (!S.pairs_installed) {
+    run_prep(S);
+    CK(cudaEventRecord(S.ev[1], st));
+    build_pairs(S, 0, KI);
+  } else {
+    CK(cudaEventRecord(S.ev[1], st));
+    S.pairs_installed = false;  // one run per installation
   }
   // the pair offsets (hence the total) and the BallExitsMesh flag come back in
   // one round trip, after the pattern work has been handed to its stream
@@ -3036,6 +3065,85 @@ int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, 
                                 size_t errlen) {
   return guard(err, errlen, [&] {
     run_all(*s, static_cast<cudaStream_t>(stream), stats, lo, hi, finalize != 0);
+  });
+}
+
+int nlfem_gpu_session_pairs_shard(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
+                                  int64_t* npairs, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    nlfem_gpu_session& S = *s;
+    cudaStream_t st = S.stream;
+    if (stream) {
+      CK(cudaEventRecord(S.ev[7], static_cast<cudaStream_t>(stream)));
+      CK(cudaStreamWaitEvent(st, S.ev[7], 0));
+    }
+    lo = std::max(0, std::min(lo, S.KI));
+    hi = std::max(lo, std::min(hi, S.KI));
+    S.launches = 0;
+    S.pairs_installed = false;
+    run_prep(S);
+    build_pairs(S, lo, hi);
+    long long tot = 0;
+    int e = 0;
+    CK(cudaMemcpyAsync(&tot, S.pair_off.p + hi, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&e, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (e != 0x7fffffff)
+      throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
+                 "BallExitsMesh: ball reaches past an unglued facet of element " + std::to_string(e)};
+    S.pairs_lo = lo;
+    S.pairs_hi = hi;
+    S.shard_npairs = tot;
+    if (npairs) *npairs = tot;
+  });
+}
+
+int nlfem_gpu_session_pairs_shard_out(nlfem_gpu_session* s, void** counts, void** partners,
+                                      int64_t* npairs) {
+  *counts = s->pair_count.p + s->pairs_lo;
+  *partners = s->partner.p;
+  *npairs = s->shard_npairs;
+  return 0;
+}
+
+int nlfem_gpu_session_pairs_install(nlfem_gpu_session* s, void* stream, const void* counts,
+                                    const void* partners, int64_t npairs_total, char* err,
+                                    size_t errlen) {
+  return guard(err, errlen, [&] {
+    nlfem_gpu_session& S = *s;
+    cudaStream_t st = S.stream;
+    if (stream) {
+      CK(cudaEventRecord(S.ev[7], static_cast<cudaStream_t>(stream)));
+      CK(cudaStreamWaitEvent(st, S.ev[7], 0));
+    }
+    const int KI = S.KI;
+    // keep this rank's own codes, then the global counts, offsets and partners
+    S.info_own.ensure(S.shard_npairs + 1);
+    if (S.shard_npairs)
+      CK(cudaMemcpyAsync(S.info_own.p, S.info.p, S.shard_npairs * sizeof(unsigned),
+                         cudaMemcpyDeviceToDevice, st));
+    if (counts != S.pair_count.p)
+      CK(cudaMemcpyAsync(S.pair_count.p, counts, (size_t)KI * sizeof(int),
+                         cudaMemcpyDeviceToDevice, st));
+    scan64(S, S.pair_count.p, true, KI, S.pair_off.p, st);
+    long long base = 0, tot = 0;
+    CK(cudaMemcpyAsync(&base, S.pair_off.p + S.pairs_lo, sizeof(long long), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaMemcpyAsync(&tot, S.pair_off.p + KI, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (tot != npairs_total)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: installed pair counts do not add up"};
+    S.partner.ensure(std::max<long long>(1, tot));
+    S.info.ensure(std::max<long long>(1, tot));
+    if (tot && partners != S.partner.p)
+      CK(cudaMemcpyAsync(S.partner.p, partners, tot * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    // codes are needed only for this rank's outer elements; the rest stay zero
+    if (tot) CK(cudaMemsetAsync(S.info.p, 0, tot * sizeof(unsigned), st));
+    if (S.shard_npairs)
+      CK(cudaMemcpyAsync(S.info.p + base, S.info_own.p, S.shard_npairs * sizeof(unsigned),
+                         cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    S.pairs_installed = true;
   });
 }
 

@@ -1,10 +1,13 @@
 """Multi-GPU assembly: one process per GPU (torch.distributed, NCCL over NVLink).
 
 Outer elements are independent units.  Each rank
-  1. builds element pairs and the node pattern (identical on every rank),
-  2. integrates its contiguous range of outer elements (z-slabs on lattice
-     meshes, whose element ids are z-major) into the exact two-word fixed-point
-     partial sums of the pattern,
+  1. builds the element pairs of its contiguous range of outer elements only,
+     all-gathers the 4-byte partner lists and per-element pair counts, and
+     builds the node pattern from the gathered list (identical on every rank:
+     the list is the single-GPU one, concatenated in outer order),
+  2. integrates its range of outer elements (z-slabs on lattice
+     meshes, whose element ids are z-major) into the fixed-point partial sums
+     of the pattern (integer words),
   3. all-reduces the partials (int64 words; per-element rhs partials are written
      by one rank only) -- integer addition is exact and order-free, so the sum is
      bit-identical to a single-GPU run for any number of ranks,
@@ -82,12 +85,55 @@ def allreduce_partials(V, rhsT, group=None) -> None:
     dist.all_reduce(rhsT, group=group)
 
 
+def gather_pairs(session, lo: int, hi: int, group=None, device=None) -> int:
+    """Build this rank's element pairs (outer elements [lo, hi)), all-gather the
+    pair counts and partner ids of every rank (NCCL, padded device tensors) and
+    install the concatenation -- the unsharded pair list -- for the next
+    run_shard.  Returns the total number of element pairs."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    npairs = session.pairs_shard(lo, hi)
+    cview, pview = session.pairs_shard_out()
+    dev = torch.device("cuda") if device is None else torch.device(device)
+    counts = (torch.as_tensor(cview, device=dev) if hi > lo
+              else torch.zeros(0, dtype=torch.int32, device=dev))
+    partners = (torch.as_tensor(pview, device=dev) if npairs > 0
+                else torch.zeros(0, dtype=torch.int32, device=dev))
+    counts, partners = counts.to(torch.int32), partners.to(torch.int32)
+    stream = torch.cuda.current_stream().cuda_stream if dev.type == "cuda" else None
+    if world == 1:
+        session.pairs_install(counts, partners, npairs, stream=stream)
+        return npairs
+    # flat outputs viewed as (world, n): accepted by NCCL and gloo alike
+    meta = torch.tensor([hi - lo, npairs], dtype=torch.int64, device=dev)
+    metas = torch.empty(world * 2, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(metas, meta, group=group)
+    m = metas.view(world, 2).cpu().numpy()
+
+    def gather(t, n_max):
+        pad = torch.zeros(max(int(n_max), 1), dtype=t.dtype, device=dev)
+        pad[: t.numel()] = torch.as_tensor(t, device=dev)
+        out = torch.empty(world * pad.numel(), dtype=t.dtype, device=dev)
+        dist.all_gather_into_tensor(out, pad, group=group)
+        return out.view(world, pad.numel())
+
+    gc = gather(counts, m[:, 0].max())
+    gp = gather(partners, m[:, 1].max())
+    all_counts = torch.cat([gc[r, : int(m[r, 0])] for r in range(world)])
+    all_partners = torch.cat([gp[r, : int(m[r, 1])] for r in range(world)])
+    total = int(m[:, 1].sum())
+    session.pairs_install(all_counts, all_partners, total, stream=stream)
+    return total
+
+
 def assemble_distributed(session, group=None, stream: int | None = None) -> tuple[dict, dict]:
     """Sharded assembly on this rank's GPU; every rank returns the full system."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     lo, hi = shard_range(session.interior_count, rank, world)
+    gather_pairs(session, lo, hi, group)
     st = session.run_shard(lo, hi, finalize=False, stream=stream)
     vv, rv = session.partials()
     V = torch.as_tensor(vv, device="cuda")
@@ -112,6 +158,7 @@ def device_step(session, group=None, stream: int | None = None):
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     lo, hi = shard_range(session.interior_count, rank, world)
+    gather_pairs(session, lo, hi, group)
     st = session.run_shard(lo, hi, finalize=False, stream=stream)
     vv, rv = session.partials()
     V = torch.as_tensor(vv, device="cuda")

@@ -91,3 +91,56 @@ def test_gloo_world2_gather_and_reduce():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for (_, a, b, c) in res for ok in (a, b, c)), res
+
+
+class _FakePairsSession:
+    """Stand-in for Session's sharded-pair API: outer element i has (i % 5) + 1
+    partners with ids 1000 * i + j."""
+
+    def __init__(self, ki):
+        self.ki = ki
+        self.installed = None
+
+    def _lists(self, lo, hi):
+        counts = np.array([(i % 5) + 1 for i in range(lo, hi)], np.int32)
+        partners = np.array([1000 * i + j for i in range(lo, hi) for j in range((i % 5) + 1)],
+                            np.int32)
+        return counts, partners
+
+    def pairs_shard(self, lo, hi):
+        self._c, self._p = self._lists(lo, hi)
+        return len(self._p)
+
+    def pairs_shard_out(self):
+        return self._c, self._p
+
+    def pairs_install(self, counts, partners, total, stream=None):
+        self.installed = (np.asarray(counts).copy(), np.asarray(partners).copy(), total)
+
+
+def _pairs_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ki = 23
+        s = _FakePairsSession(ki)
+        lo, hi = D.shard_range(ki, rank, world)
+        total = D.gather_pairs(s, lo, hi, device="cpu")
+        wc, wp = s._lists(0, ki)
+        c, p, t = s.installed
+        q.put((rank, t == total == len(wp), np.array_equal(c, wc), np.array_equal(p, wp)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_gather_pairs_concatenates_in_outer_order():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pairs_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for (_, a, b, c) in res for ok in (a, b, c)), res

@@ -68,3 +68,53 @@ def test_assemble_distributed_world1_nccl():
         assert st["shard_pairs"] == st["element_pairs"]
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("strat,mc,nshard", [("nocaps", 1, 3), ("fullcaps", 8, 2),
+                                             ("barycenter", 1, 4)])
+def test_sharded_pairs_sum_to_single_gpu_bitwise(strat, mc, nshard):
+    # nshard "ranks" as nshard sessions on one GPU: each builds only its own
+    # outer elements' pairs; the concatenated lists are installed everywhere
+    # (what gather_pairs does over NCCL), each integrates its range, and the
+    # integer partials summed give the unsharded system bit for bit
+    import torch
+    m = P.generate_mesh(3, 6, 0.34, jitter_seed=5)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    ref = P.Session(t, 0.34, strat, "moment2", U2, seed=SEED, mc_samples=mc)
+    ref.run()
+    want = ref.download()
+    KI = ref.interior_count
+    ranks = [P.Session(t, 0.34, strat, "moment2", U2, seed=SEED, mc_samples=mc)
+             for _ in range(nshard)]
+    counts, partners, total = [], [], 0
+    for r, s in enumerate(ranks):
+        lo, hi = D.shard_range(KI, r, nshard)
+        n = s.pairs_shard(lo, hi)
+        cv, pv = s.pairs_shard_out()
+        counts.append(torch.as_tensor(cv, device="cuda").clone())
+        partners.append(torch.as_tensor(pv, device="cuda").clone() if n else
+                        torch.zeros(0, dtype=torch.int32, device="cuda"))
+        total += n
+    allc, allp = torch.cat(counts), torch.cat(partners)
+    assert total == ref.stats.element_pairs
+    Vsum = Rsum = None
+    for r, s in enumerate(ranks):
+        lo, hi = D.shard_range(KI, r, nshard)
+        s.pairs_install(allc, allp, total)
+        st = s.run_shard(lo, hi)
+        assert st.element_pairs == total
+        vv, rv = s.partials()
+        V = torch.as_tensor(vv, device="cuda").cpu().numpy().copy()
+        R = torch.as_tensor(rv, device="cuda").cpu().numpy().copy()
+        with np.errstate(over="ignore"):
+            Vsum = V if Vsum is None else Vsum + V
+        Rsum = R if Rsum is None else Rsum + R
+    s0 = ranks[0]
+    vv, rv = s0.partials()
+    torch.as_tensor(vv, device="cuda").copy_(torch.from_numpy(Vsum))
+    torch.as_tensor(rv, device="cuda").copy_(torch.from_numpy(Rsum))
+    torch.cuda.synchronize()
+    s0.finalize(0, s0.unknowns)
+    got = s0.download_rows(0, s0.unknowns)
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(got[k], want[k]), (strat, k)
