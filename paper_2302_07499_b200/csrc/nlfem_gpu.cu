@@ -821,6 +821,14 @@ __device__ void block_sort(int* a, int n) {
   }
 }
 
+// Pattern pass with speculative capacities: a size-dependent kernel does nothing
+// once a total has exceeded its buffer (ovf = kCapRetry; the host then reruns
+// the pass with exact sizes), or once an error has been flagged.
+constexpr int kCapRetry = 9;
+__global__ void k_cap_check(const long long* total, long long cap, int* ovf) {
+  if (threadIdx.x == 0 && *total > cap) atomicCAS(ovf, 0, kCapRetry);
+}
+
 // R(i) = sorted nodes of interior partners of every interior T containing node i.
 template <bool FILL>
 __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const int* partner,
@@ -831,6 +839,7 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
   int* tabN = sm + kHE;
   int* list = tabN + kHN;
   __shared__ int nlist;
+  if (FILL && *ovf) return;
   for (int i = blockIdx.x; i < cD.J; i += gridDim.x) {
     const int a = cD.ni_off[i], b = cD.ni_off[i + 1];
     if (a == b) {
@@ -876,16 +885,17 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
   }
 }
 
-__global__ void k_col_count(long long n, const int* cols, int* cnt) {
+__global__ void k_col_count(const long long* total, const int* cols, int* cnt, const int* ovf) {
+  if (*ovf) return;
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) atomicAdd(cnt + cols[k], 1);
+  if (k < *total) atomicAdd(cnt + cols[k], 1);
 }
 
 // warp per row: lanes scatter the row's entries into the transposed rows
 __global__ void k_transpose_fill(int J, const long long* roff, const int* rcols,
-                                 const long long* toff, int* cursor, int* tcols) {
+                                 const long long* toff, int* cursor, int* tcols, const int* ovf) {
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (i >= J) return;
+  if (i >= J || *ovf) return;
   for (long long k = roff[i] + (threadIdx.x & 31); k < roff[i + 1]; k += 32) {
     const int j = rcols[k];
     tcols[toff[j] + atomicAdd(cursor + j, 1)] = i;
@@ -895,6 +905,7 @@ __global__ void k_transpose_fill(int J, const long long* roff, const int* rcols,
 __global__ void __launch_bounds__(256) k_sort_rows(int J, const long long* off, int* cols,
                                                    int* ovf) {
   extern __shared__ int sm[];
+  if (*ovf) return;
   for (int i = blockIdx.x; i < J; i += gridDim.x) {
     const long long a = off[i];
     const int n = (int)(off[i + 1] - a);
@@ -931,10 +942,11 @@ __global__ void __launch_bounds__(kUnionThreads) k_union(int J, const long long*
                                                          const int* rcols, const long long* toff,
                                                          const int* tcols, int* slen,
                                                          const long long* soff, int* scols,
-                                                         int* maxlen) {
+                                                         int* maxlen, const int* ovf) {
   __shared__ int pre[kRowMax + 1];
   __shared__ int wtot[kUnionThreads / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  if (*ovf) return;
   for (int i = blockIdx.x; i < J; i += gridDim.x) {
     const long long a0 = roff[i], b0 = toff[i];
     const int na = (int)(roff[i + 1] - a0), nb = (int)(toff[i + 1] - b0);
@@ -1006,7 +1018,7 @@ __device__ __forceinline__ long long find_slot(const long long* soff, const int*
 __global__ void k_mirror(int J, const long long* soff, const int* scols, long long* mirror,
                          int* ovf) {
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (i >= J) return;
+  if (i >= J || *ovf) return;
   for (long long k = soff[i] + (threadIdx.x & 31); k < soff[i + 1]; k += 32) {
     const long long m = find_slot(soff, scols, scols[k], i);
     if (m < 0) *ovf = 2;
@@ -1019,7 +1031,7 @@ __global__ void k_mirror(int J, const long long* soff, const int* scols, long lo
 __global__ void k_edge_slots(const long long* soff, const int* scols, long long* eslot,
                              int* ovf) {
   const int ii = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ii >= cD.KI) return;
+  if (ii >= cD.KI || *ovf) return;
   const int4 w = cD.verts[cD.interior[ii]];
   const int v[4] = {w.x, w.y, w.z, w.w};
   int k = 0;
@@ -1036,10 +1048,11 @@ __global__ void k_edge_slots(const long long* soff, const int* scols, long long*
 // warp per row, ballot compaction keeps the column order
 template <bool FILL>
 __global__ void k_outpat(const long long* soff, const int* scols, int* olen,
-                         const long long* ooff, int* ocols, long long* omap, const int* dof_node) {
+                         const long long* ooff, int* ocols, long long* omap, const int* dof_node,
+                         const int* ovf) {
   const int d = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (d >= cD.unknowns) return;
+  if (d >= cD.unknowns || *ovf) return;
   const int i = dof_node[d];
   int n = 0;
   const long long o = FILL ? ooff[d] : 0;
@@ -2531,13 +2544,19 @@ void run_finalize(nlfem_gpu_session& S, int r0, int r1) {
   }
 }
 
-// K5: the node pattern S (sorted rows), its mirror / edge slots and the output
-// pattern.  Runs on its own stream; host syncs here block only the caller.
-void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
-  const int KI = S.KI, J = S.J;
+// One pass of K5.  spec = true: the buffers keep the capacities of an earlier
+// run and nothing comes back to the host until the end (a single read-back);
+// returns false if a total exceeded its capacity (nothing was written past
+// it) so the caller reruns with spec = false, which reads each size back and
+// allocates exactly.
+bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec) {
+  const int KI = S.KI, J = S.J, U = S.unknowns;
   const size_t rows_smem = (kHE + kHN + kRowMax) * sizeof(int);
   CK(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
   CK(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(kRowMax * sizeof(int))));
+  CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
   S.rlen.ensure(J);
   S.roff.ensure(J + 1);
   const unsigned rgrid = (unsigned)std::min<long long>(J, 148LL * 16);
@@ -2545,68 +2564,101 @@ void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
                                                nullptr, S.ovf.p);
   ++S.launches;
   scan64(S, S.rlen.p, true, J, S.roff.p, st);
-  const long long nR = read_ll(S.roff.p + J, st);
-  S.rcols.ensure(nR);
+  long long capR;
+  if (spec) {
+    capR = (long long)std::min(S.rcols.n, S.tcols.n);
+    k_cap_check<<<1, 32, 0, st>>>(S.roff.p + J, capR, S.ovf.p);
+  } else {
+    capR = read_ll(S.roff.p + J, st);
+    S.rcols.ensure(capR);
+    S.tcols.ensure(capR);
+  }
   k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
                                               S.rcols.p, S.ovf.p);
-  ++S.launches;
   // transpose
   S.tcnt.ensure(J);
   S.toff.ensure(J + 1);
-  S.tcols.ensure(nR);
   CK(cudaMemsetAsync(S.tcnt.p, 0, J * sizeof(int), st));
-  k_col_count<<<nblk(nR, 256), 256, 0, st>>>(nR, S.rcols.p, S.tcnt.p);
-  ++S.launches;
+  k_col_count<<<nblk(std::max<long long>(capR, 1), 256), 256, 0, st>>>(S.roff.p + J, S.rcols.p,
+                                                                      S.tcnt.p, S.ovf.p);
   scan64(S, S.tcnt.p, true, J, S.toff.p, st);
   S.cursor.ensure(J);
   CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
-  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.cursor.p,
-                                                 S.tcols.p);
-  CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(kRowMax * sizeof(int))));
+  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p,
+                                                        S.cursor.p, S.tcols.p, S.ovf.p);
   k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p);
-  S.launches += 2;
+  S.launches += 5;
   // union
   S.slen.ensure(J);
   S.soff.ensure(J + 1);
   CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
   int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
   k_union<false><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
-                                               S.slen.p, nullptr, nullptr, d_maxlen);
+                                                  S.slen.p, nullptr, nullptr, d_maxlen, S.ovf.p);
   ++S.launches;
   scan64(S, S.slen.p, true, J, S.soff.p, st);
-  S.nnz_s = read_ll(S.soff.p + J, st);
-  S.scols.ensure(S.nnz_s);
+  long long capS;
+  if (spec) {
+    capS = (long long)std::min(S.scols.n, S.mirror.n);
+    k_cap_check<<<1, 32, 0, st>>>(S.soff.p + J, capS, S.ovf.p);
+  } else {
+    capS = read_ll(S.soff.p + J, st);
+    S.scols.ensure(capS);
+    S.mirror.ensure(capS);
+  }
   k_union<true><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
-                                              nullptr, S.soff.p, S.scols.p, nullptr);
-  maxlen = 0;
-  CK(cudaMemcpyAsync(&maxlen, d_maxlen, sizeof(int), cudaMemcpyDeviceToHost, st));
-  S.mirror.ensure(S.nnz_s);
+                                                 nullptr, S.soff.p, S.scols.p, nullptr, S.ovf.p);
   k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
   S.eslot.ensure(10 * (size_t)KI);
   k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p);
   S.launches += 3;
   // output pattern
-  const int U = S.unknowns;
   S.olen.ensure(U);
   S.ooff.ensure(U + 1);
-  k_outpat<false><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr, nullptr,
-                                                nullptr, S.dof_node.p);
+  k_outpat<false><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, S.olen.p, nullptr,
+                                                       nullptr, nullptr, S.dof_node.p, S.ovf.p);
   ++S.launches;
   scan64(S, S.olen.p, true, U, S.ooff.p, st);
-  S.nnz_out = read_ll(S.ooff.p + U, st);
-  S.ocols.ensure(S.nnz_out);
-  S.omap.ensure(S.nnz_out);
-  k_outpat<true><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p, S.ocols.p,
-                                               S.omap.p, S.dof_node.p);
+  long long capO;
+  if (spec) {
+    capO = (long long)std::min(S.ocols.n, S.omap.n);
+    k_cap_check<<<1, 32, 0, st>>>(S.ooff.p + U, capO, S.ovf.p);
+  } else {
+    capO = read_ll(S.ooff.p + U, st);
+    S.ocols.ensure(capO);
+    S.omap.ensure(capO);
+  }
+  k_outpat<true><<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, nullptr, S.ooff.p,
+                                                      S.ocols.p, S.omap.p, S.dof_node.p, S.ovf.p);
   ++S.launches;
-  int ovf = 0;
-  CK(cudaMemcpyAsync(&ovf, S.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  // one read-back: flags, sizes, longest row
+  long long sz[3] = {0, 0, 0};
+  int flags[2] = {0, 0};
+  CK(cudaMemcpyAsync(&flags[0], S.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&flags[1], d_maxlen, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&sz[0], S.roff.p + J, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&sz[1], S.soff.p + J, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&sz[2], S.ooff.p + U, sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (ovf)
+  if (flags[0] == kCapRetry) return false;
+  if (flags[0])
     throw Fail{NLFEM_GPU_BAD_CONFIG,
                "BadConfig: interaction neighbourhood too large for the pattern kernels (code " +
-                   std::to_string(ovf) + ")"};
+                   std::to_string(flags[0]) + ")"};
+  S.nnz_s = sz[1];
+  S.nnz_out = sz[2];
+  maxlen = flags[1];
+  return true;
+}
+
+// K5: the node pattern S (sorted rows), its mirror / edge slots and the output
+// pattern.  Runs on its own stream; buffers sized by an earlier run are reused
+// speculatively (no host round trips); otherwise sizes are read back.
+void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
+  const bool spec = S.rcols.n > 1 && S.tcols.n > 1 && S.scols.n > 1 && S.mirror.n > 1 &&
+                    S.ocols.n > 1 && S.omap.n > 1;
+  if (spec && pattern_pass(S, st, maxlen, true)) return;
+  pattern_pass(S, st, maxlen, false);
 }
 
 // K1 over outer elements [lo, hi) (positions in the ascending interior list):
