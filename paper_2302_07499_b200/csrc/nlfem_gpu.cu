@@ -1143,10 +1143,13 @@ __device__ __forceinline__ int cap_case(unsigned c) {
 
 
 
-__global__ void k_units_count(long long p0, long long np, const unsigned* info, int* ucount) {
+// np bounds the chunk's pairs on the host; the actual end (*pend) is read on
+// the device, entries past it count zero
+__global__ void k_units_count(long long p0, long long np, const long long* pend,
+                              const unsigned* info, int* ucount) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= np) return;
-  ucount[i] = pair_cap_items(info[p0 + i]);
+  ucount[i] = (p0 + i < *pend) ? pair_cap_items(info[p0 + i]) : 0;
 }
 
 
@@ -1165,6 +1168,7 @@ __global__ void k_units_count(long long p0, long long np, const unsigned* info, 
 // list and block.
 constexpr int kFillThreads = 256;
 __global__ void __launch_bounds__(kFillThreads) k_units_fill(long long p0, long long np,
+                                                             const long long* pend,
                                                              const unsigned* info,
                                                              const long long* uoff, int* upair,
                                                              unsigned char* uqs,
@@ -1175,7 +1179,7 @@ __global__ void __launch_bounds__(kFillThreads) k_units_fill(long long p0, long 
   __shared__ int bbase[8][W];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool act = i < np;
+  const bool act = i < np && p0 + i < *pend;
   const unsigned code = act ? info[p0 + i] : 0;
   const int kind0 = (act && cD.region[partner[p0 + i]] != 0) ? 4 : 0;
   unsigned long long packed = 0;
@@ -2217,8 +2221,10 @@ struct nlfem_gpu_session {
   // sharded pairs (multi-GPU): this rank's K1 range, its pair count, and whether
   // a gathered pair list of all outer elements is installed for the next run
   int pairs_lo = 0, pairs_hi = 0;
-  long long shard_npairs = 0;
+  long long shard_npairs = 0, installed_base = 0;
   bool pairs_installed = false;
+  long long survivors = 0;   // K1 survivors of the last build_pairs range (bounds its pairs)
+  double delta_over_h = 0;   // delta / cbrt(6 mean element volume)
   DBuf<unsigned> info_own;
   std::atomic<long long> launches{0};
   unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0;
@@ -2435,6 +2441,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.gy = std::max(1, (int)std::floor((hi[1] - lo[1]) / hg) + 1);
   D.gz = std::max(1, (int)std::floor((hi[2] - lo[2]) / hg) + 1);
   D.rmax = rmax;
+  S.delta_over_h = S.K > 0 ? k->delta / std::cbrt(6.0 * volsum / S.K) : 0.0;
   S.erec.ensure(4 * (size_t)S.K);
   S.gbar.ensure(S.K);
   S.cert2.ensure(S.K);
@@ -2694,6 +2701,7 @@ void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
   CK(cudaStreamSynchronize(st));
   // absolute-indexed view: coff[ii] for ii in [lo, hi]
   auto coff = [&](int ii) { return coffr[ii - lo]; };
+  S.survivors = coff(hi);
   // pass 1 + compaction, in chunks of outer elements bounded by survivors
   const long long kCandBudget = 1LL << 30;  // 8 GiB of (partner, code) slots
   S.pair_off.ensure(KI + 1);
@@ -2792,7 +2800,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   // outer elements has been installed (sharded multi-GPU pairs)
   const int KI = S.KI;
   const int big = 0x7fffffff;
-  if (!S.pairs_installed) {
+  const bool installed = S.pairs_installed;
+  if (!installed) {
     run_prep(S);
     CK(cudaEventRecord(S.ev[1], st));
     build_pairs(S, 0, KI);
@@ -2869,30 +2878,52 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   const bool need_units = D.strategy != NLFEM_STRATEGY_BARYCENTER;
   float mc_ms = 0;
-  CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
-                     cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&err_elem_h, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (err_elem_h != big)
-    throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
-               "BallExitsMesh: ball reaches past an unglued facet of element " +
-                   std::to_string(err_elem_h)};
-  S.npairs = poff[KI];
+  // chunks of outer elements sized so the unit buffers stay bounded.  One
+  // chunk needs no host round trip when its first pair and a bound on its
+  // pairs are known on the host: a full run (pairs <= K1 survivors) or a
+  // sharded run on installed pairs (offset and count from the install).
+  const long long kPairsPerChunk = need_units ? (8LL << 20) : (1LL << 40);
+  const bool full_run = !installed && shard_lo == 0 && shard_hi == KI;
+  const bool own_range = installed && shard_lo == S.pairs_lo && shard_hi == S.pairs_hi;
+  const bool fast = (full_run && S.survivors <= kPairsPerChunk) ||
+                    (own_range && S.shard_npairs <= kPairsPerChunk);
+  bool npairs_pending = false;
+  if (fast) {
+    npairs_pending = full_run;  // read at the end with the BallExitsMesh flag
+  } else {
+    CK(cudaMemcpyAsync(poff.data(), S.pair_off.p, sizeof(long long) * (KI + 1),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&err_elem_h, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (err_elem_h != big)
+      throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
+                 "BallExitsMesh: ball reaches past an unglued facet of element " +
+                     std::to_string(err_elem_h)};
+    S.npairs = poff[KI];
+  }
   if (shard_hi > shard_lo) {
-    // chunks of outer elements sized so the unit buffers stay bounded
-    const long long kPairsPerChunk = need_units ? (8LL << 20) : (1LL << 40);
     int ii0 = shard_lo;
     while (ii0 < shard_hi) {
-      int ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), poff[ii0] + kPairsPerChunk) -
-                      poff.begin()) - 1;
-      ii1 = std::min(std::max(ii1, ii0 + 1), shard_hi);
-      const long long P0 = poff[ii0], np = poff[ii1] - P0;
+      int ii1;
+      long long P0, np;
+      if (fast) {
+        ii1 = shard_hi;
+        P0 = full_run ? 0 : S.installed_base;
+        np = full_run ? S.survivors : S.shard_npairs;  // bound on the chunk's pairs
+      } else {
+        ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), poff[ii0] + kPairsPerChunk) -
+                    poff.begin()) - 1;
+        ii1 = std::min(std::max(ii1, ii0 + 1), shard_hi);
+        P0 = poff[ii0];
+        np = poff[ii1] - P0;
+      }
+      const long long* pend = S.pair_off.p + ii1;  // the chunk's actual pair end
       long long nitems = 0;
       if (need_units) {
         S.ucount.ensure(np + 1);
         S.uoff.ensure(np + 1);
         S.pair_outer.ensure(np + 1);
-        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, S.info.p, S.ucount.p);
+        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, pend, S.info.p, S.ucount.p);
         k_pair_outer<<<nblk(32LL * (ii1 - ii0), 256), 256, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
                                                                     S.pair_outer.p);
         S.launches += 2;
@@ -2906,8 +2937,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         S.mom.ensure(kMomStride * (size_t)(nitems + 1));
         S.ulist.ensure(8 * (size_t)(nitems + 1));
         k_units_fill<<<nblk(np, kFillThreads), kFillThreads, 0, st>>>(
-            P0, np, S.info.p, S.uoff.p, S.upair.p, S.uqs.p, S.partner.p, S.ulist.p, nitems + 1,
-            S.nlist.p);
+            P0, np, pend, S.info.p, S.uoff.p, S.upair.p, S.uqs.p, S.partner.p, S.ulist.p,
+            nitems + 1, S.nlist.p);
         ++S.launches;
         CK(cudaEventRecord(S.ev[6], st));
         cudaStream_t s3 = S.stream3;
@@ -2967,11 +2998,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         CK(cudaEventRecord(S.ev[7], st));
       }
       setup_combine();
-      // block size from the whole mesh's mean number of pairs per outer element
-      // (the same for every shard and chunk: the per-warp partial sums, and so
-      // the last bits of the result, must not depend on the sharding)
-      const long long ppe = S.npairs / std::max(1, KI);
-      if (ppe < 768)
+      // block size from delta/h (pairs per outer element grow like (delta/h)^3):
+      // a property of the mesh, the same for every shard and chunk -- the
+      // per-warp partial sums, hence the last bits, must not depend on sharding
+      if (S.delta_over_h < 2.5)
         k_integrate<128><<<ii1 - ii0, 128, ismem, st>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
             S.rhsT.p, S.uoff.p, need_units ? S.mom.p : nullptr, P0, S.counters.p + 1, hcap,
@@ -3002,6 +3032,16 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   CK(cudaStreamSynchronize(st));
   unsigned long long cnt[8];
   CK(cudaMemcpy(cnt, S.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+  if (npairs_pending) {  // deferred from the pairs phase (no round trip there)
+    long long tot = 0;
+    int e = big;
+    CK(cudaMemcpy(&tot, S.pair_off.p + KI, sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&e, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e != big)
+      throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
+                 "BallExitsMesh: ball reaches past an unglued facet of element " + std::to_string(e)};
+    S.npairs = tot;
+  }
   S.items = cnt[0];
   S.mc_samples = cnt[1];
   S.mc_hits = cnt[2];
@@ -3185,6 +3225,8 @@ int nlfem_gpu_session_pairs_install(nlfem_gpu_session* s, void* stream, const vo
     CK(cudaStreamSynchronize(st));
     if (tot != npairs_total)
       throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: installed pair counts do not add up"};
+    S.installed_base = base;
+    S.npairs = tot;
     S.partner.ensure(std::max<long long>(1, tot));
     S.info.ensure(std::max<long long>(1, tot));
     if (tot && partners != S.partner.p)
