@@ -212,52 +212,12 @@ __global__ void k_scan_add(long long* out, const long long* offs, long long n) {
 // ---------------------------------------------------------------------------
 // prep kernels
 
-__global__ void k_erec(int K, const double* node, const int4* verts, const double* center,
-                       const double* radius, double4* erec) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
-  const int4 w = verts[t];
-  const double* a = node + 3 * (long long)w.x;
-  const double* b = node + 3 * (long long)w.y;
-  const double* c = node + 3 * (long long)w.z;
-  const double* d = node + 3 * (long long)w.w;
-  erec[4 * t] = make_double4(center[3 * t], center[3 * t + 1], center[3 * t + 2], radius[t]);
-  erec[4 * t + 1] = make_double4(a[0], a[1], a[2], b[0]);
-  erec[4 * t + 2] = make_double4(b[1], b[2], c[0], c[1]);
-  erec[4 * t + 3] = make_double4(c[2], d[0], d[1], d[2]);
-}
-
-// whole constraint element: measure times g average with the degree-2 rule
-// (reference assembly.cpp:350-359), the same for every (T, q) that meets it
-__global__ void k_gbar(int K, double* gbar) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
-  double Sg = 0;
-  if (cD.region[t] != 0) {
-    Vd v[4];
-    load_verts(t, v);
-    const double volP = cD.vol[t];
-    for (int k = 0; k < 4; ++k) Sg += volP * 0.25 * poly_eval(cD.g, quad_point(v, k));
-  }
-  gbar[t] = Sg;
-}
 
 __device__ __forceinline__ int cell_of(double c, double o, double inv, int n) {
   int k = (int)floor((c - o) * inv);
   return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 
-__global__ void k_cell_count(int K, int* key, int* cnt) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
-  const double4 a = cD.erec[4 * t];
-  const int cx = cell_of(a.x, cD.gox, cD.ginv, cD.gx);
-  const int cy = cell_of(a.y, cD.goy, cD.ginv, cD.gy);
-  const int cz = cell_of(a.z, cD.goz, cD.ginv, cD.gz);
-  const int k = (cz * cD.gy + cy) * cD.gx + cx;
-  key[t] = k;
-  atomicAdd(cnt + k, 1);
-}
 
 __global__ void k_fill_by_key(int n, const int* key, const long long* off, int* cursor, int* out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -285,15 +245,6 @@ __global__ void k_sort_segments(int nseg, const long long* off, int* data) {
 }
 
 // node -> interior-element incidence (count / fill by (node, elem) items)
-__global__ void k_ninc_count(int K, int* cnt) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K || cD.region[t]) return;
-  const int4 w = cD.verts[t];
-  atomicAdd(cnt + w.x, 1);
-  atomicAdd(cnt + w.y, 1);
-  atomicAdd(cnt + w.z, 1);
-  atomicAdd(cnt + w.w, 1);
-}
 
 __global__ void k_ninc_fill(int K, const long long* off, int* cursor, int* out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -304,12 +255,13 @@ __global__ void k_ninc_fill(int K, const long long* off, int* cursor, int* out) 
 }
 
 // per-node patch volume over all elements -> power-of-two fixed-point scale
-__global__ void k_scales(int J, const long long* aoff, const int* ael, double cbound,
+// per row: bound of every contribution (count x largest incident volume, an
+// upper bound of the patch volume that is independent of summation order)
+__global__ void k_scales(int J, const int* acnt, const unsigned long long* avmax, double cbound,
                          double* scale, double* iscale) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= J) return;
-  double patch = 0;
-  for (long long k = aoff[i]; k < aoff[i + 1]; ++k) patch += cD.vol[ael[k]];
+  const double patch = (double)acnt[i] * __longlong_as_double((long long)avmax[i]);
   const double bound = cbound * (patch > 0 ? patch : 1e-300);
   int ex;
   frexp(bound, &ex);  // bound < 2^ex
@@ -317,23 +269,7 @@ __global__ void k_scales(int J, const long long* aoff, const int* ael, double cb
   iscale[i] = ldexp(1.0, ex - 61);
 }
 
-__global__ void k_all_inc_count(int K, int* cnt) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
-  const int4 w = cD.verts[t];
-  atomicAdd(cnt + w.x, 1);
-  atomicAdd(cnt + w.y, 1);
-  atomicAdd(cnt + w.z, 1);
-  atomicAdd(cnt + w.w, 1);
-}
 
-__global__ void k_all_inc_fill(int K, const long long* off, int* cursor, int* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
-  const int4 w = cD.verts[t];
-  const int v[4] = {w.x, w.y, w.z, w.w};
-  for (int i = 0; i < 4; ++i) out[off[v[i]] + atomicAdd(cursor + v[i], 1)] = t;
-}
 
 // ---------------------------------------------------------------------------
 // K1: element pairs
@@ -376,16 +312,52 @@ __device__ __forceinline__ double cert_threshold2(double diam, double vol, doubl
   return t > 0 ? t * t * (1.0 - 1e-12) : 0.0;
 }
 
-// per element: the nocaps certificate threshold and whether it has an unglued
-// facet (the BallExitsMesh probe applies), both depending on T' only
-__global__ void k_cert2(int K, double* cert2, unsigned char* bnd) {
+// Element-wise preparation in one pass: the 128-byte element record, the
+// whole-constraint g average, the nocaps certificate and unglued-facet flag,
+// the grid cell (key and count), and per node the number of interior and of
+// all incident elements and the largest incident volume (row bounds).
+__global__ void k_elem_prep(int K, const double* node, const int4* verts, const double* center,
+                            const double* radius, double4* erec, double* gbar, double* cert2,
+                            unsigned char* bnd, int* cell_key, int* cell_cnt, int* ni_cnt,
+                            int* ai_cnt, unsigned long long* ai_vmax) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= K) return;
-  cert2[t] = cert_threshold2(cD.diam[t], cD.vol[t], cD.tau[t]);
+  const int4 w = verts[t];
+  const double* a = node + 3 * (long long)w.x;
+  const double* b = node + 3 * (long long)w.y;
+  const double* c = node + 3 * (long long)w.z;
+  const double* d = node + 3 * (long long)w.w;
+  const double cx = center[3 * t], cy = center[3 * t + 1], cz = center[3 * t + 2];
+  erec[4 * t] = make_double4(cx, cy, cz, radius[t]);
+  erec[4 * t + 1] = make_double4(a[0], a[1], a[2], b[0]);
+  erec[4 * t + 2] = make_double4(b[1], b[2], c[0], c[1]);
+  erec[4 * t + 3] = make_double4(c[2], d[0], d[1], d[2]);
+  const double vol = cD.vol[t];
+  const bool interior = cD.region[t] == 0;
+  double Sg = 0;
+  if (!interior) {  // whole constraint element (reference assembly.cpp:350-359)
+    const Vd v[4] = {{a[0], a[1], a[2]}, {b[0], b[1], b[2]}, {c[0], c[1], c[2]}, {d[0], d[1], d[2]}};
+    for (int k = 0; k < 4; ++k) Sg += vol * 0.25 * poly_eval(cD.g, quad_point(v, k));
+  }
+  gbar[t] = Sg;
+  cert2[t] = cert_threshold2(cD.diam[t], vol, cD.tau[t]);
   const int4 nb = cD.nbr[t];
   bnd[t] = (nb.x < 0 || nb.y < 0 || nb.z < 0 || nb.w < 0) ? 1 : 0;
+  const int kx = cell_of(cx, cD.gox, cD.ginv, cD.gx);
+  const int ky = cell_of(cy, cD.goy, cD.ginv, cD.gy);
+  const int kz = cell_of(cz, cD.goz, cD.ginv, cD.gz);
+  const int key = (kz * cD.gy + ky) * cD.gx + kx;
+  cell_key[t] = key;
+  atomicAdd(cell_cnt + key, 1);
+  const int vv[4] = {w.x, w.y, w.z, w.w};
+  const unsigned long long vb = (unsigned long long)__double_as_longlong(vol);  // vol > 0
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (interior) atomicAdd(ni_cnt + vv[k], 1);
+    atomicAdd(ai_cnt + vv[k], 1);
+    atomicMax(ai_vmax + vv[k], vb);
+  }
 }
-
 
 // distance_point_simplex(xq, v) < delta, decided from the facets that can hold
 // the closest point: for xq outside T' the closest point lies on a facet whose
@@ -2190,8 +2162,9 @@ struct nlfem_gpu_session {
   DBuf<double> gbar, cert2;
   DBuf<unsigned char> bnd;
   // grid / incidence
-  DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt, ai_el;
-  DBuf<long long> cell_start64, ni_off64, ai_off64, scan_tmp, scan_tmp2;
+  DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt;
+  DBuf<unsigned long long> ai_vmax;
+  DBuf<long long> cell_start64, ni_off64, scan_tmp, scan_tmp2;
   DBuf<int> cell_start, ni_off;
   DBuf<double> scale, iscale;
   // pairs
@@ -2474,20 +2447,26 @@ void run_prep(nlfem_gpu_session& S) {
   const int K = S.K, J = S.J;
   const long long ncell = (long long)D.gx * D.gy * D.gz;
   CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
-  k_erec<<<nblk(K, 256), 256, 0, st>>>(K, S.node.p, S.verts.p, S.center.p, S.radius.p, S.erec.p);
-  k_gbar<<<nblk(K, 256), 256, 0, st>>>(K, S.gbar.p);
-  k_cert2<<<nblk(K, 256), 256, 0, st>>>(K, S.cert2.p, S.bnd.p);
-  S.launches += 3;
-  // grid
   S.cell_key.ensure(K);
   S.cell_cnt.ensure(ncell);
   S.cell_elems.ensure(K);
   S.cursor.ensure(std::max<long long>(ncell, J));
   S.cell_start64.ensure(ncell + 1);
   S.cell_start.ensure(ncell + 1);
+  S.ni_cnt.ensure(J);
+  S.ni_off64.ensure(J + 1);
+  S.ni_off.ensure(J + 1);
+  S.ai_cnt.ensure(J);
+  S.ai_vmax.ensure(J);
   CK(cudaMemsetAsync(S.cell_cnt.p, 0, ncell * sizeof(int), st));
-  k_cell_count<<<nblk(K, 256), 256, 0, st>>>(K, S.cell_key.p, S.cell_cnt.p);
+  CK(cudaMemsetAsync(S.ni_cnt.p, 0, J * sizeof(int), st));
+  CK(cudaMemsetAsync(S.ai_cnt.p, 0, J * sizeof(int), st));
+  CK(cudaMemsetAsync(S.ai_vmax.p, 0, J * sizeof(unsigned long long), st));
+  k_elem_prep<<<nblk(K, 256), 256, 0, st>>>(K, S.node.p, S.verts.p, S.center.p, S.radius.p,
+                                            S.erec.p, S.gbar.p, S.cert2.p, S.bnd.p, S.cell_key.p,
+                                            S.cell_cnt.p, S.ni_cnt.p, S.ai_cnt.p, S.ai_vmax.p);
   ++S.launches;
+  // grid: elements sorted by cell (ids ascending within a cell)
   scan64(S, S.cell_cnt.p, true, ncell, S.cell_start64.p, st);
   CK(cudaMemsetAsync(S.cursor.p, 0, ncell * sizeof(int), st));
   k_fill_by_key<<<nblk(K, 256), 256, 0, st>>>(K, S.cell_key.p, S.cell_start64.p, S.cursor.p,
@@ -2495,13 +2474,7 @@ void run_prep(nlfem_gpu_session& S) {
   k_sort_segments<<<nblk(ncell, 256), 256, 0, st>>>((int)ncell, S.cell_start64.p, S.cell_elems.p);
   k_ll_to_int<<<nblk(ncell + 1, 256), 256, 0, st>>>(ncell + 1, S.cell_start64.p, S.cell_start.p);
   S.launches += 3;
-  // node -> interior elements
-  S.ni_cnt.ensure(J);
-  S.ni_off64.ensure(J + 1);
-  S.ni_off.ensure(J + 1);
-  CK(cudaMemsetAsync(S.ni_cnt.p, 0, J * sizeof(int), st));
-  k_ninc_count<<<nblk(K, 256), 256, 0, st>>>(K, S.ni_cnt.p);
-  ++S.launches;
+  // node -> interior elements (ascending)
   scan64(S, S.ni_cnt.p, true, J, S.ni_off64.p, st);
   const long long nin = 4LL * S.KI;  // every interior element has 4 nodes: no read-back
   S.ni_el.ensure(nin);
@@ -2510,17 +2483,6 @@ void run_prep(nlfem_gpu_session& S) {
   k_sort_segments<<<nblk(J, 256), 256, 0, st>>>(J, S.ni_off64.p, S.ni_el.p);
   k_ll_to_int<<<nblk(J + 1, 256), 256, 0, st>>>(J + 1, S.ni_off64.p, S.ni_off.p);
   S.launches += 3;
-  // node -> all elements (patch volumes for the fixed-point scales)
-  S.ai_cnt.ensure(J);
-  S.ai_off64.ensure(J + 1);
-  CK(cudaMemsetAsync(S.ai_cnt.p, 0, J * sizeof(int), st));
-  k_all_inc_count<<<nblk(K, 256), 256, 0, st>>>(K, S.ai_cnt.p);
-  ++S.launches;
-  scan64(S, S.ai_cnt.p, true, J, S.ai_off64.p, st);
-  S.ai_el.ensure(4 * (size_t)K);
-  CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
-  k_all_inc_fill<<<nblk(K, 256), 256, 0, st>>>(K, S.ai_off64.p, S.cursor.p, S.ai_el.p);
-  ++S.launches;
   S.scale.ensure(J);
   S.iscale.ensure(J);
   D.cell_start = S.cell_start.p;
@@ -2535,7 +2497,7 @@ void run_prep(nlfem_gpu_session& S) {
   // around node i, at most 5 such terms (X, 2X on the diagonal, D_T', 2 D_T)
   const double rr = D.delta + 3 * D.rmax;
   const double cbound = 6.0 * D.C * (4.0 / 3.0 * M_PI * rr * rr * rr);
-  k_scales<<<nblk(J, 256), 256, 0, st>>>(J, S.ai_off64.p, S.ai_el.p, cbound, S.scale.p, S.iscale.p);
+  k_scales<<<nblk(J, 256), 256, 0, st>>>(J, S.ai_cnt.p, S.ai_vmax.p, cbound, S.scale.p, S.iscale.p);
   ++S.launches;
 }
 
