@@ -147,6 +147,26 @@ int nlfem_gpu_assemble(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
 
 void nlfem_gpu_free_csr(nlfem_gpu_csr* csr);
 
+/* Conjugate gradients on the assembled system (reference cg_solve,
+ * proj/include/nlfem/solver.hpp, proj/src/solver.cpp:26-66): unpreconditioned,
+ * x0 = 0, stops at the first iteration with ||r|| <= tol ||b|| or when p.Ap
+ * loses positivity, at most max_iter iterations.  Deterministic (fixed-order
+ * reductions).  _device takes device arrays (row offsets int64, e.g. from
+ * nlfem_gpu_session_outputs) and a device x; nlfem_gpu_cg host arrays. */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double relative_residual;
+} nlfem_gpu_solve_report;
+
+int nlfem_gpu_cg(const nlfem_gpu_csr* sys, const double* b, double tol, int32_t max_iter,
+                 int32_t device, double* x, nlfem_gpu_solve_report* report, char* err,
+                 size_t errlen);
+int nlfem_gpu_cg_device(int32_t rows, const int64_t* row_off, const int32_t* col_idx,
+                        const double* values, const double* b, double tol, int32_t max_iter,
+                        double* x, void* stream, nlfem_gpu_solve_report* report, char* err,
+                        size_t errlen);
+
 /* Device-resident session: the mesh is uploaded once; run() executes the
  * device pipeline with inputs already in HBM and leaves the CSR on the device;
  * download() copies it out.  Not reentrant per session. */

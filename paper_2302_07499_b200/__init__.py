@@ -72,6 +72,11 @@ class _Config(C.Structure):
                 ("sampler", C.c_int32), ("device", C.c_int32)]
 
 
+class _SolveReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32),
+                ("relative_residual", C.c_double)]
+
+
 class _Csr(C.Structure):
     _fields_ = [("rows", C.c_int32), ("nnz", C.c_int64), ("row_ptr", C.POINTER(C.c_int32)),
                 ("col_idx", C.POINTER(C.c_int32)), ("values", C.POINTER(C.c_double)),
@@ -131,6 +136,12 @@ def lib():
     L.nlfem_gpu_session_pairs_shard_out.argtypes = [vp, P(vp), P(vp), P(i64)]
     L.nlfem_gpu_session_pairs_install.restype = C.c_int
     L.nlfem_gpu_session_pairs_install.argtypes = [vp, vp, vp, vp, i64, C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_cg.restype = C.c_int
+    L.nlfem_gpu_cg.argtypes = [P(_Csr), vp, dbl, i32, i32, vp, P(_SolveReport), C.c_char_p,
+                               C.c_size_t]
+    L.nlfem_gpu_cg_device.restype = C.c_int
+    L.nlfem_gpu_cg_device.argtypes = [i32, vp, vp, vp, vp, dbl, i32, vp, vp, P(_SolveReport),
+                                      C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_finalize.restype = C.c_int
     L.nlfem_gpu_session_finalize.argtypes = [vp, vp, i32, i32, C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_download_rows.restype = C.c_int
@@ -167,6 +178,7 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
     "nlfem_gpu_session_outputs", "nlfem_gpu_session_pairs_shard",
     "nlfem_gpu_session_pairs_shard_out", "nlfem_gpu_session_pairs_install",
+    "nlfem_gpu_cg", "nlfem_gpu_cg_device",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
 ]
@@ -429,6 +441,25 @@ class Session:
                                                      ptr(counts), ptr(partners),
                                                      int(npairs_total), err, 1024), err)
 
+    def cg(self, tol: float = 1e-10, max_iterations: int = 10000) -> dict:
+        """Conjugate gradients on the assembled system where it lies in HBM
+        (after run()); returns x (host), iterations, converged,
+        relative_residual."""
+        import torch
+        ro, ci, va, rh = self.outputs()
+        n = rh.__cuda_array_interface__["shape"][0]
+        x = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        rep = _SolveReport()
+        err = C.create_string_buffer(1024)
+
+        def ptr(a):
+            return C.c_void_p(int(a.__cuda_array_interface__["data"][0]))
+        _check(lib().nlfem_gpu_cg_device(int(n), ptr(ro), ptr(ci), ptr(va), ptr(rh), float(tol),
+                                         int(max_iterations), C.c_void_p(x.data_ptr()), None,
+                                         C.byref(rep), err, 1024), err)
+        return {"x": x[:n].cpu().numpy(), "iterations": rep.iterations,
+                "converged": bool(rep.converged), "relative_residual": rep.relative_residual}
+
     def partials(self):
         """Device views (V int64 words, rhsT float64) of the exact partial sums."""
         vp, nv, rp, nr = C.c_void_p(), C.c_int64(), C.c_void_p(), C.c_int64()
@@ -573,6 +604,29 @@ def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
                               err, 1024)
     _check(rc, err)
     return _take_csr(csr), st.as_dict()
+
+
+def cg(row_ptr, col_idx, values, rhs, tol: float = 1e-10, max_iterations: int = 10000,
+       device: int = -1) -> dict:
+    """Mirror of the reference's nlfem.cg (nlfem_module.cpp:228-256): conjugate
+    gradients from zero on the GPU; returns x, iterations, converged,
+    relative_residual."""
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    ci = np.ascontiguousarray(col_idx, np.int32)
+    va = np.ascontiguousarray(values, np.float64)
+    b = np.ascontiguousarray(rhs, np.float64)
+    if len(rp) != len(b) + 1:
+        raise ValueError("row_ptr length must be len(rhs) + 1")
+    csr = _Csr(len(b), len(va), rp.ctypes.data_as(C.POINTER(C.c_int32)),
+               ci.ctypes.data_as(C.POINTER(C.c_int32)), va.ctypes.data_as(C.POINTER(C.c_double)),
+               b.ctypes.data_as(C.POINTER(C.c_double)))
+    x = np.zeros(len(b))
+    rep = _SolveReport()
+    err = C.create_string_buffer(1024)
+    _check(lib().nlfem_gpu_cg(C.byref(csr), _p(b), float(tol), int(max_iterations), int(device),
+                              _p(x), C.byref(rep), err, 1024), err)
+    return {"x": x, "iterations": rep.iterations, "converged": bool(rep.converged),
+            "relative_residual": rep.relative_residual}
 
 
 def assemble_system(coords, cells, region, delta, strategy="nocaps", normalization="mass",
