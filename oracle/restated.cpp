@@ -307,7 +307,7 @@ struct Job {
   int unknowns;
   double C, delta;
   Poly f, g;
-  int strategy;  // 2 barycenter, 3 nocaps, 5 fullcaps
+  int strategy;  // 0 inside, 1 overlap, 2 barycenter, 3 nocaps, 5 fullcaps
   uint64_t seed;
   int M;
   int sampler;  // 0 Philox (P), 1 xoshiro walk order (R)
@@ -669,8 +669,12 @@ Run do_block(const Job& J, int b, std::vector<uint32_t>& stamp, uint32_t& epoch,
         const V ct = m.cen(t);
         const double gap = dist(ct, p);
         if (gap >= m.radius[t] + delta) continue;
-        if (J.strategy == 2) {
+        if (J.strategy == 2) {  // barycenter, assembly.cpp:725-727
           if (gap < delta) A.whole(t);
+          continue;
+        }
+        if (J.strategy == 1) {  // overlap, assembly.cpp:728-733
+          if (gap + m.radius[t] < delta || tet_dist(p, m.tet(t)) < delta) A.whole(t);
           continue;
         }
         if (gap + m.radius[t] < icut) {
@@ -682,6 +686,7 @@ Run do_block(const Job& J, int b, std::vector<uint32_t>& stamp, uint32_t& epoch,
         if (mask == 15) {
           A.whole(t);
         } else if (mask != 0) {
+          if (J.strategy == 0) continue;  // inside: straddlers dropped, assembly.cpp:744
           inner_pieces(st, mask, p, delta, J.tau[t], A.scratch);
           for (const Tet& sb : A.scratch) A.sub(t, sb);
           if (J.strategy == 5) {
@@ -826,8 +831,8 @@ void* oracle_assemble(int K, int Jn, const double* node, const int32_t* verts,
   try {
     if (!(delta > 0)) throw Err(8, "BadConfig: delta must be positive");
     if (M <= 0) throw Err(8, "BadConfig: mc_samples must be positive");
-    if (strategy != 2 && strategy != 3 && strategy != 5)
-      throw Err(102, "oracle restates barycenter, nocaps and fullcaps only");
+    if (strategy < 0 || strategy > 5 || strategy == 4)
+      throw Err(102, "oracle restates inside, overlap, barycenter, nocaps and fullcaps only");
     Job J{Mesh{K, Jn, node, verts, nbr, center, radius, volume, diam, region, inv},
           dof_of_node, unknowns, C, delta, make_poly(fterms, nf), make_poly(gterms, ng),
           strategy, seed, M, sampler, {}, {}, {}};

@@ -30,7 +30,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NLFEM_GPU_LIB") or os.path.join(_HERE, "libnlfem_gpu.so")
 
 STRATEGIES = ["inside", "overlap", "barycenter", "nocaps", "approxcaps", "fullcaps"]
-GPU_STRATEGIES = ("barycenter", "nocaps", "fullcaps")
+GPU_STRATEGIES = ("inside", "overlap", "barycenter", "nocaps", "fullcaps")
 ERROR_NAMES = {1: "BadIndex", 2: "DanglingVertex", 3: "NonManifold", 4: "SeedMismatch",
                5: "BallExitsMesh", 6: "DegenerateHull", 7: "BadMeshFile", 8: "BadConfig",
                100: "NoDevice", 101: "OutOfMemory", 102: "Unsupported"}

@@ -421,6 +421,25 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
     gap = sqrt(g2);
     if (gap >= rad + delta) return kNone;
   }
+  if (cD.strategy == NLFEM_STRATEGY_OVERLAP) {
+    // gap + rad < delta || distance_point_simplex(x_q, T') < delta
+    const double t2 = delta - rad;
+    if (t2 > 0) {
+      if (g2 < t2 * t2 * (1.0 - 1e-12)) return kWhole;
+      if (!(g2 >= t2 * t2 * (1.0 + 1e-12))) {
+        if (gap < 0) gap = sqrt(g2);
+        if (gap + rad < delta) return kWhole;
+      }
+    }
+    // a point of T' (barycenter or vertex) well inside the ball certifies the
+    // computed distance < delta; otherwise evaluate it (classify_deferred)
+    const double c2 = delta * delta * (1.0 - 1e-11);
+    if (g2 < c2) return kWhole;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (vnorm2(vsub(v[i], xq)) < c2) return kWhole;
+    return kDefer;
+  }
   if (cD.strategy == NLFEM_STRATEGY_BARYCENTER) {
     if (g2 < delta * delta * (1.0 - 1e-12)) return kWhole;
     if (g2 >= delta * delta * (1.0 + 1e-12)) return kNone;
@@ -449,6 +468,7 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
     }
   }
   if (mask == 15) return kWhole;
+  if (cD.strategy == NLFEM_STRATEGY_INSIDE) return kNone;  // straddlers dropped
   if (mask == 0) {
     if (cD.strategy != NLFEM_STRATEGY_FULLCAPS) return kNone;
     // the barycenter lies in T': gap < delta (with margin) certifies that the
@@ -467,7 +487,10 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
 }
 
 __device__ __forceinline__ unsigned classify_deferred(Vd xq, const Vd v[4], int mask, double tau) {
-  if (mask == 0) return outside_cap_hits(xq, v, cD.delta) ? kOutCap : kNone;
+  if (mask == 0)
+    return outside_cap_hits(xq, v, cD.delta)
+               ? (cD.strategy == NLFEM_STRATEGY_OVERLAP ? kWhole : kOutCap)
+               : kNone;
   if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
     return inner_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
   return any_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
@@ -2283,10 +2306,10 @@ void check_config(const nlfem_gpu_kernel* k, const nlfem_gpu_config* cfg) {
   if (!(k->delta > 0)) throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: delta must be positive"};
   if (cfg->mc_samples <= 0)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: mc_samples must be positive"};
-  if (cfg->strategy != NLFEM_STRATEGY_BARYCENTER && cfg->strategy != NLFEM_STRATEGY_NOCAPS &&
-      cfg->strategy != NLFEM_STRATEGY_FULLCAPS)
-    throw Fail{NLFEM_GPU_EUNSUPPORTED,
-               "strategy not implemented on the GPU path (barycenter, nocaps, fullcaps only)"};
+  if (cfg->strategy < NLFEM_STRATEGY_INSIDE || cfg->strategy > NLFEM_STRATEGY_FULLCAPS)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown strategy"};
+  if (cfg->strategy == NLFEM_STRATEGY_APPROXCAPS)
+    throw Fail{NLFEM_GPU_EUNSUPPORTED, "strategy approxcaps is not implemented on the GPU path"};
   if (cfg->sampler != NLFEM_SAMPLER_PHILOX)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown sampler"};
 }
@@ -2838,7 +2861,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   // units phase: one record per straddling / cap item -- inner pieces (nocaps,
   // fullcaps) and outer pieces by Monte Carlo (fullcaps); none for barycenter
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
-  const bool need_units = D.strategy != NLFEM_STRATEGY_BARYCENTER;
+  // straddling pieces only under nocaps / fullcaps; the other strategies emit
+  // whole-element items only
+  const bool need_units =
+      D.strategy == NLFEM_STRATEGY_NOCAPS || D.strategy == NLFEM_STRATEGY_FULLCAPS;
   float mc_ms = 0;
   // chunks of outer elements sized so the unit buffers stay bounded.  One
   // chunk needs no host round trip when its first pair and a bound on its

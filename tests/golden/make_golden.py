@@ -3,7 +3,7 @@
 Run here (needs /root/reference compiled by `make -C oracle ref`):
     python tests/golden/make_golden.py
 Each fixture holds a small 3D mesh, the reference's assemble() output for
-barycenter / nocaps / fullcaps (reference xoshiro sampler, seed 1234) with the
+inside / overlap / barycenter / nocaps / fullcaps (reference xoshiro sampler, seed 1234) with the
 moment2 kernel and u = |x|^2, and the per-(T, q) pieces the reference's public
 walk_ball emits for a seeded sample of outer points.  These pin the oracle
 restatement (tests/test_oracle.py) and the GPU sets/pattern (tests/test_gpu_*.py)
@@ -23,6 +23,7 @@ from oracle import ref  # noqa: E402
 
 U = np.array([[1, 2, 0, 0], [1, 0, 2, 0], [1, 0, 0, 2]], float)
 SEED = 1234
+STRATS = ("inside", "overlap", "barycenter", "nocaps", "fullcaps")
 
 
 def lattice(res, delta, jitter=None):
@@ -65,7 +66,7 @@ def main():
                    uterms=U)
         tab = P.table()
         interior = np.nonzero(tab["region"] == 0)[0]
-        for strat in ("barycenter", "nocaps", "fullcaps"):
+        for strat in STRATS:
             s = P.assemble(delta, strat, U, threads=1, seed=SEED, mc_samples=mc)
             for key in ("row_ptr", "col_idx", "values", "rhs"):
                 out[f"{strat}_{key}"] = s[key]
@@ -83,7 +84,7 @@ def main():
             out[f"{strat}_walk"] = np.array(rows, np.int32)
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
         print(name, len(c), "nodes", len(k), "cells",
-              {s: len(out[f"{s}_values"]) for s in ("barycenter", "nocaps", "fullcaps")})
+              {s: len(out[f"{s}_values"]) for s in STRATS})
 
 
 if __name__ == "__main__":
