@@ -234,7 +234,8 @@ def main():
             dist.barrier()
 
     m = P.generate_mesh(3, cfg["res"], cfg["delta"], jitter_seed=cfg["jitter"])
-    table = P.ElementTable(m["coords"], m["cells"], m["region"])
+    # upstream setup (cmap, element table, dof map) on this rank's GPU
+    table = P.ElementTable(m["coords"], m["cells"], m["region"], device=local)
     sess = P.Session(table, cfg["delta"], cfg["strategy"], "moment2", U2, seed=SEED,
                      mc_samples=cfg["mc"], device=local)
     stream = torch.cuda.current_stream()

@@ -167,6 +167,20 @@ int nlfem_gpu_cg_device(int32_t rows, const int64_t* row_off, const int32_t* col
                         double* x, void* stream, nlfem_gpu_solve_report* report, char* err,
                         size_t errlen);
 
+/* The reference's upstream setup on the GPU: build_cmap (cmap.cpp:56-278),
+ * build_element_table (ball_approx.cpp:51-95) and build_dofmap
+ * (assembly.cpp:16-40) from raw (coords, cells, region) host arrays.  Writes
+ * the same arrays as nlfem_host_element_table + nlfem_host_dofmap
+ * (include/nlfem_host.h), bit for bit, and the same error codes and messages
+ * (BAD_INDEX, DANGLING_VERTEX, NON_MANIFOLD, BAD_CONFIG for a degenerate
+ * element).  device < 0: the current device. */
+int nlfem_gpu_element_table(const double* coords, int64_t nnodes, const int32_t* cells,
+                            const uint8_t* region, int64_t ncells, int32_t* verts,
+                            int32_t* neighbor, double* center, double* radius, double* volume,
+                            double* diam, double* inv_edges, int32_t* dof_of_node,
+                            uint8_t* constrained, int32_t* unknowns, int32_t device, char* err,
+                            size_t errlen);
+
 /* Device-resident session: the mesh is uploaded once; run() executes the
  * device pipeline with inputs already in HBM and leaves the CSR on the device;
  * download() copies it out.  Not reentrant per session. */

@@ -142,6 +142,9 @@ def lib():
     L.nlfem_gpu_cg_device.restype = C.c_int
     L.nlfem_gpu_cg_device.argtypes = [i32, vp, vp, vp, vp, dbl, i32, vp, vp, P(_SolveReport),
                                       C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_element_table.restype = C.c_int
+    L.nlfem_gpu_element_table.argtypes = [vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp,
+                                          vp, P(i32), i32, C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_finalize.restype = C.c_int
     L.nlfem_gpu_session_finalize.argtypes = [vp, vp, i32, i32, C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_download_rows.restype = C.c_int
@@ -178,7 +181,7 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
     "nlfem_gpu_session_outputs", "nlfem_gpu_session_pairs_shard",
     "nlfem_gpu_session_pairs_shard_out", "nlfem_gpu_session_pairs_install",
-    "nlfem_gpu_cg", "nlfem_gpu_cg_device",
+    "nlfem_gpu_cg", "nlfem_gpu_cg_device", "nlfem_gpu_element_table",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
 ]
@@ -246,9 +249,11 @@ def _mesh_arrays(coords, cells, region):
 
 
 class ElementTable:
-    """build_cmap + build_element_table + build_dofmap, restated on the host."""
+    """build_cmap + build_element_table + build_dofmap: restated on the host
+    (device=None), or built on GPU `device` (nlfem_gpu_element_table; -1 = the
+    current device) -- the same arrays, bit for bit."""
 
-    def __init__(self, coords, cells, region):
+    def __init__(self, coords, cells, region, device: int | None = None):
         coords, cells, region = _mesh_arrays(coords, cells, region)
         L = lib()
         K, V = cells.shape[0], coords.shape[0]
@@ -261,6 +266,18 @@ class ElementTable:
         self.diam = np.empty(K)
         self.inv_edges = np.empty((K, 9))
         err = C.create_string_buffer(512)
+        if device is not None:
+            self.dof_of_node = np.empty(V, np.int32)
+            self.constrained = np.empty(V, np.uint8)
+            u = C.c_int32(0)
+            _check(L.nlfem_gpu_element_table(
+                _p(coords), V, _p(cells), _p(region), K, _p(self.verts), _p(self.neighbor),
+                _p(self.center), _p(self.radius), _p(self.volume), _p(self.diam),
+                _p(self.inv_edges), _p(self.dof_of_node), _p(self.constrained), C.byref(u),
+                int(device), err, 512), err)
+            self.unknowns = int(u.value)
+            self.node_of_dof = np.nonzero(self.dof_of_node >= 0)[0].astype(np.int32)
+            return
         _check(L.nlfem_host_element_table(
             _p(coords), V, _p(cells), _p(region), K, _p(self.verts), _p(self.neighbor),
             _p(self.center), _p(self.radius), _p(self.volume), _p(self.diam),
