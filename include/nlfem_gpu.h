@@ -41,7 +41,7 @@ enum nlfem_gpu_status {
   NLFEM_GPU_BAD_CONFIG = 8,      /* reference assembly.cpp:620-622 */
   NLFEM_GPU_ENODEVICE = 100,     /* no sm_100 device / CUDA error */
   NLFEM_GPU_ENOMEM = 101,
-  NLFEM_GPU_EUNSUPPORTED = 102   /* strategy approxcaps (not on the GPU path)   */
+  NLFEM_GPU_EUNSUPPORTED = 102   /* reserved: a configuration the GPU path does not support */
 };
 
 /* Strategy ids follow nlfem::Strategy (reference ball_approx.hpp:17-24). */

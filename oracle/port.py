@@ -15,7 +15,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
-STRATEGY = {"inside": 0, "overlap": 1, "barycenter": 2, "nocaps": 3, "fullcaps": 5}
+STRATEGY = {"inside": 0, "overlap": 1, "barycenter": 2, "nocaps": 3, "approxcaps": 4,
+            "fullcaps": 5}
 _lib = None
 
 

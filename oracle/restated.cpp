@@ -176,6 +176,132 @@ void inner_pieces(const Tet& s, int mask, V c, double r, double tau, std::vector
   }
 }
 
+// ---- approxcaps: inner polytope with sphere points, as a convex hull --------------
+// Points (reference ball_approx.cpp:210-229): the inside vertices, the
+// crossings, and per crossing pair sharing an inside or an outside endpoint the
+// radial projection of their midpoint onto the sphere.  Incremental hull with
+// the reference's seeds, eps tests and face order (geometry.cpp:198-298), fan
+// from the centroid of the hull vertices (geometry.cpp:310-328), pieces above
+// the volume floor (ball_approx.cpp:177-192).  Empty on a degenerate hull.
+void approx_pieces(const Tet& s, int mask, V c, double r, double tau, std::vector<Tet>& out) {
+  out.clear();
+  V q[4];
+  const int nq = crossings(s, mask, c, r, q);
+  int qi[4], qo[4];
+  {
+    int k = 0;
+    for (int i = 0; i < 4; ++i) {
+      if (!(mask >> i & 1)) continue;
+      for (int o = 0; o < 4; ++o)
+        if (!(mask >> o & 1)) qi[k] = i, qo[k] = o, ++k;
+    }
+  }
+  std::vector<V> pts;
+  for (int i = 0; i < 4; ++i)
+    if (mask >> i & 1) pts.push_back(s.v[i]);
+  for (int k = 0; k < nq; ++k) pts.push_back(q[k]);
+  for (int i = 0; i < nq; ++i)
+    for (int j = i + 1; j < nq; ++j) {
+      if (qi[i] != qi[j] && qo[i] != qo[j]) continue;
+      const V mid = 0.5 * (q[i] + q[j]) - c;
+      const double len = std::sqrt(n2(mid));
+      if (len <= 0) continue;
+      pts.push_back(c + (r / len) * mid);
+    }
+  const int n = int(pts.size());
+  // hull3d
+  V lo = pts[0], hi = pts[0];
+  for (const V& p : pts) {
+    lo = {std::min(lo.x, p.x), std::min(lo.y, p.y), std::min(lo.z, p.z)};
+    hi = {std::max(hi.x, p.x), std::max(hi.y, p.y), std::max(hi.z, p.z)};
+  }
+  const double scale = std::max(std::sqrt(n2(hi - lo)), 1e-300);
+  const double eps = 1e-12 * scale;
+  int s0 = 0, s1 = -1, s2 = -1, s3 = -1;
+  for (int i = 1; i < n; ++i)
+    if (dist(pts[i], pts[s0]) > eps) {
+      s1 = i;
+      break;
+    }
+  if (s1 < 0) return;
+  const V d01 = pts[s1] - pts[s0];
+  for (int i = 0; i < n; ++i)
+    if (std::sqrt(n2(cross(d01, pts[i] - pts[s0]))) / std::sqrt(n2(d01)) > eps) {
+      s2 = i;
+      break;
+    }
+  if (s2 < 0) return;
+  const V nrm = cross(d01, pts[s2] - pts[s0]);
+  for (int i = 0; i < n; ++i)
+    if (std::abs(dot(nrm, pts[i] - pts[s0])) / std::sqrt(n2(nrm)) > eps) {
+      s3 = i;
+      break;
+    }
+  if (s3 < 0) return;
+  if (dot(nrm, pts[s3] - pts[s0]) > 0) std::swap(s1, s2);
+  using F = std::array<int, 3>;
+  std::vector<F> faces{{s0, s2, s1}, {s0, s1, s3}, {s1, s2, s3}, {s0, s3, s2}};
+  const V inner = 0.25 * (pts[s0] + pts[s1] + pts[s2] + pts[s3]);
+  auto outward = [&](F& f) {
+    const V nn = cross(pts[f[1]] - pts[f[0]], pts[f[2]] - pts[f[0]]);
+    if (dot(nn, inner - pts[f[0]]) > 0) std::swap(f[1], f[2]);
+  };
+  for (auto& f : faces) outward(f);
+  std::vector<char> used(n, 0), vis;
+  used[s0] = used[s1] = used[s2] = used[s3] = 1;
+  for (int pi = 0; pi < n; ++pi) {
+    if (used[pi]) continue;
+    used[pi] = 1;
+    const V p = pts[pi];
+    bool dup = false;
+    for (const F& f : faces)
+      for (int v : f)
+        if (dist(p, pts[v]) <= eps) dup = true;
+    if (dup) continue;
+    vis.assign(faces.size(), 0);
+    bool any = false;
+    for (size_t fi = 0; fi < faces.size(); ++fi) {
+      const F& f = faces[fi];
+      const V nn = cross(pts[f[1]] - pts[f[0]], pts[f[2]] - pts[f[0]]);
+      if (dot(nn, p - pts[f[0]]) > eps * std::sqrt(n2(nn))) vis[fi] = 1, any = true;
+    }
+    if (!any) continue;
+    std::vector<std::array<int, 2>> horizon;
+    for (size_t fi = 0; fi < faces.size(); ++fi) {
+      if (!vis[fi]) continue;
+      for (int e = 0; e < 3; ++e) {
+        const int a = faces[fi][e], b = faces[fi][(e + 1) % 3];
+        bool open = true;
+        for (size_t fj = 0; fj < faces.size() && open; ++fj) {
+          if (vis[fj]) continue;
+          for (int e2 = 0; e2 < 3; ++e2)
+            if (faces[fj][e2] == b && faces[fj][(e2 + 1) % 3] == a) open = false;
+        }
+        if (!open) horizon.push_back({a, b});
+      }
+    }
+    std::vector<F> next;
+    for (size_t fi = 0; fi < faces.size(); ++fi)
+      if (!vis[fi]) next.push_back(faces[fi]);
+    for (auto [a, b] : horizon) {
+      F f{a, b, pi};
+      outward(f);
+      next.push_back(f);
+    }
+    faces.swap(next);
+  }
+  // triangulate_polytope: fan from the centroid of the distinct hull vertices
+  std::vector<int> vs;
+  for (const F& f : faces)
+    for (int i = 0; i < 3; ++i) vs.push_back(f[i]);
+  std::sort(vs.begin(), vs.end());
+  vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+  V cen{};
+  for (int v : vs) cen = cen + pts[v];
+  cen = (1.0 / double(vs.size())) * cen;
+  for (const F& f : faces) keep(out, cen, pts[f[0]], pts[f[1]], pts[f[2]], tau);
+}
+
 void outer_pieces(const Tet& s, int mask, V c, double r, double tau, std::vector<Tet>& out) {
   out.clear();
   V q[4];
@@ -307,7 +433,7 @@ struct Job {
   int unknowns;
   double C, delta;
   Poly f, g;
-  int strategy;  // 0 inside, 1 overlap, 2 barycenter, 3 nocaps, 5 fullcaps
+  int strategy;  // 0 inside, 1 overlap, 2 barycenter, 3 nocaps, 4 approxcaps, 5 fullcaps
   uint64_t seed;
   int M;
   int sampler;  // 0 Philox (P), 1 xoshiro walk order (R)
@@ -687,7 +813,10 @@ Run do_block(const Job& J, int b, std::vector<uint32_t>& stamp, uint32_t& epoch,
           A.whole(t);
         } else if (mask != 0) {
           if (J.strategy == 0) continue;  // inside: straddlers dropped, assembly.cpp:744
-          inner_pieces(st, mask, p, delta, J.tau[t], A.scratch);
+          if (J.strategy == 4)  // approxcaps: straddle_inner with sphere points
+            approx_pieces(st, mask, p, delta, J.tau[t], A.scratch);
+          else
+            inner_pieces(st, mask, p, delta, J.tau[t], A.scratch);
           for (const Tet& sb : A.scratch) A.sub(t, sb);
           if (J.strategy == 5) {
             outer_pieces(st, mask, p, delta, J.tau[t], A.scratch);
@@ -831,8 +960,7 @@ void* oracle_assemble(int K, int Jn, const double* node, const int32_t* verts,
   try {
     if (!(delta > 0)) throw Err(8, "BadConfig: delta must be positive");
     if (M <= 0) throw Err(8, "BadConfig: mc_samples must be positive");
-    if (strategy < 0 || strategy > 5 || strategy == 4)
-      throw Err(102, "oracle restates inside, overlap, barycenter, nocaps and fullcaps only");
+    if (strategy < 0 || strategy > 5) throw Err(8, "BadConfig: unknown strategy");
     Job J{Mesh{K, Jn, node, verts, nbr, center, radius, volume, diam, region, inv},
           dof_of_node, unknowns, C, delta, make_poly(fterms, nf), make_poly(gterms, ng),
           strategy, seed, M, sampler, {}, {}, {}};

@@ -253,3 +253,155 @@ __device__ __forceinline__ void straddle_piece(const Straddle& s, int k, Vd& a, 
   d = k == 0 ? s.B0 : (k == 1 ? s.B1 : s.B2);
 }
 
+
+// ---------------------------------------------------------------------------
+// approxcaps: detail::straddle_inner with sphere_points (reference
+// ball_approx.cpp:210-229): the inside vertices, the crossings, and for every
+// crossing pair sharing an inside or an outside endpoint the radial projection
+// of their midpoint onto the sphere (<= 10 points); their convex hull by the
+// reference's incremental algorithm (geometry.cpp:198-298: seeds, eps tests,
+// horizon order, face order), fanned from the centroid of the hull vertices
+// (geometry.cpp:310-328).  `fn(a, b, c, d, vol)` is called for every fan piece
+// above the volume floor (hull_pieces, ball_approx.cpp:177-192), in the
+// reference's order.  A degenerate hull emits nothing (DegenerateHull is
+// swallowed there).  Returns false if the face table overflowed (cannot happen
+// for <= 10 points: a triangulated hull has <= 2V - 4 = 16 faces).
+constexpr int kHullFaces = 32;
+
+template <class Fn>
+__device__ __forceinline__ bool approx_pieces(const Vd v[4], int mask, Vd c, double r, double tau,
+                                              Fn&& fn) {
+  const int m = __popc(mask), mo = 4 - m, nq = m * mo;
+  Crossings X;
+  crossings4(v, mask, c, r, X);
+  Vd pts[10];
+  int n = 0;
+  for (int i = 0; i < m; ++i) pts[n++] = pick(v, nth_bit4((unsigned)mask, i));
+  for (int k = 0; k < nq; ++k) pts[n++] = X.q[k];
+  // crossing k = (inside rank k / mo, outside rank k % mo)
+  for (int i = 0; i < nq; ++i)
+    for (int j = i + 1; j < nq; ++j) {
+      if (i / mo != j / mo && i % mo != j % mo) continue;
+      const Vd mid = vsub(vscale(0.5, vadd(X.q[i], X.q[j])), c);
+      const double len = sqrt(vnorm2(mid));
+      if (len <= 0) continue;
+      pts[n++] = vadd(c, vscale(r / len, mid));
+    }
+  // hull3d: scale and eps
+  Vd lo = pts[0], hi = pts[0];
+  for (int i = 0; i < n; ++i) {
+    lo = {fmin(lo.x, pts[i].x), fmin(lo.y, pts[i].y), fmin(lo.z, pts[i].z)};
+    hi = {fmax(hi.x, pts[i].x), fmax(hi.y, pts[i].y), fmax(hi.z, pts[i].z)};
+  }
+  const double eps = 1e-12 * fmax(sqrt(vnorm2(vsub(hi, lo))), 1e-300);
+  // affinely independent seed
+  int s0 = 0, s1 = -1, s2 = -1, s3 = -1;
+  for (int i = 1; i < n; ++i)
+    if (vdist(pts[i], pts[s0]) > eps) {
+      s1 = i;
+      break;
+    }
+  if (s1 < 0) return true;
+  const Vd d01 = vsub(pts[s1], pts[s0]);
+  for (int i = 0; i < n; ++i)
+    if (sqrt(vnorm2(vcross(d01, vsub(pts[i], pts[s0])))) / sqrt(vnorm2(d01)) > eps) {
+      s2 = i;
+      break;
+    }
+  if (s2 < 0) return true;
+  const Vd nrm = vcross(d01, vsub(pts[s2], pts[s0]));
+  for (int i = 0; i < n; ++i)
+    if (fabs(vdot(nrm, vsub(pts[i], pts[s0]))) / sqrt(vnorm2(nrm)) > eps) {
+      s3 = i;
+      break;
+    }
+  if (s3 < 0) return true;
+  if (vdot(nrm, vsub(pts[s3], pts[s0])) > 0) {
+    const int t = s1;
+    s1 = s2;
+    s2 = t;
+  }
+  const Vd inner = vscale(0.25, vadd(vadd(vadd(pts[s0], pts[s1]), pts[s2]), pts[s3]));
+  int fa[kHullFaces], fb[kHullFaces], fc[kHullFaces];
+  auto outward = [&](int& a, int& b, int& cc) {
+    const Vd nn = vcross(vsub(pts[b], pts[a]), vsub(pts[cc], pts[a]));
+    if (vdot(nn, vsub(inner, pts[a])) > 0) {
+      const int t = b;
+      b = cc;
+      cc = t;
+    }
+  };
+  int nf = 4;
+  fa[0] = s0, fb[0] = s2, fc[0] = s1;
+  fa[1] = s0, fb[1] = s1, fc[1] = s3;
+  fa[2] = s1, fb[2] = s2, fc[2] = s3;
+  fa[3] = s0, fb[3] = s3, fc[3] = s2;
+  for (int f = 0; f < 4; ++f) outward(fa[f], fb[f], fc[f]);
+  unsigned used = (1u << s0) | (1u << s1) | (1u << s2) | (1u << s3);
+  for (int pi = 0; pi < n; ++pi) {
+    if (used >> pi & 1) continue;
+    used |= 1u << pi;
+    const Vd p = pts[pi];
+    bool dup = false;
+    for (int f = 0; f < nf; ++f)
+      if (vdist(p, pts[fa[f]]) <= eps || vdist(p, pts[fb[f]]) <= eps || vdist(p, pts[fc[f]]) <= eps)
+        dup = true;
+    if (dup) continue;
+    unsigned vis = 0;  // kHullFaces <= 32
+    for (int f = 0; f < nf; ++f) {
+      const Vd nn = vcross(vsub(pts[fb[f]], pts[fa[f]]), vsub(pts[fc[f]], pts[fa[f]]));
+      if (vdot(nn, vsub(p, pts[fa[f]])) > eps * sqrt(vnorm2(nn))) vis |= 1u << f;
+    }
+    if (!vis) continue;
+    // horizon: directed edges of visible faces whose reverse lies in an
+    // invisible face, in (face, edge) order
+    int ha[3 * kHullFaces], hb[3 * kHullFaces], nh = 0;
+    for (int f = 0; f < nf; ++f) {
+      if (!(vis >> f & 1)) continue;
+      const int e3[3] = {fa[f], fb[f], fc[f]};
+      for (int e = 0; e < 3; ++e) {
+        const int a = e3[e], b = e3[e == 2 ? 0 : e + 1];
+        bool open = true;
+        for (int g = 0; g < nf && open; ++g) {
+          if (vis >> g & 1) continue;
+          if ((fa[g] == b && fb[g] == a) || (fb[g] == b && fc[g] == a) || (fc[g] == b && fa[g] == a))
+            open = false;
+        }
+        if (!open) {
+          ha[nh] = a;
+          hb[nh] = b;
+          ++nh;
+        }
+      }
+    }
+    // next = invisible faces in order, then one face per horizon edge
+    int k = 0;
+    for (int f = 0; f < nf; ++f)
+      if (!(vis >> f & 1)) {
+        fa[k] = fa[f], fb[k] = fb[f], fc[k] = fc[f];
+        ++k;
+      }
+    if (k + nh > kHullFaces) return false;
+    for (int h = 0; h < nh; ++h) {
+      int a = ha[h], b = hb[h], cc = pi;
+      outward(a, b, cc);
+      fa[k] = a, fb[k] = b, fc[k] = cc;
+      ++k;
+    }
+    nf = k;
+  }
+  // triangulate_polytope: centroid of the distinct hull vertices, summed in
+  // ascending vertex order, times 1/count
+  unsigned vs = 0;
+  for (int f = 0; f < nf; ++f) vs |= (1u << fa[f]) | (1u << fb[f]) | (1u << fc[f]);
+  Vd cen = {0.0, 0.0, 0.0};
+  for (int i = 0; i < n; ++i)
+    if (vs >> i & 1) cen = vadd(cen, pts[i]);
+  cen = vscale(1.0 / (double)__popc(vs), cen);
+  for (int f = 0; f < nf; ++f) {
+    const Vd a = pts[fa[f]], b = pts[fb[f]], cc = pts[fc[f]];
+    const double vol = tet_volume(cen, a, b, cc);
+    if (vol > tau) fn(cen, a, b, cc, vol);
+  }
+  return true;
+}

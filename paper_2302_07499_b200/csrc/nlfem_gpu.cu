@@ -126,6 +126,7 @@ struct Dev {
   const double* scale;
   const double* iscale;
   Poly f, g;
+  unsigned long long* flags;  // counter 7: approxcaps hull face-table overflow
 };
 
 __constant__ Dev cD;
@@ -298,6 +299,17 @@ __device__ __noinline__ bool inner_pieces_exact(const Vd* v, int mask, Vd xq, do
 __device__ __noinline__ bool any_pieces_exact(const Vd* v, int mask, Vd xq, double tau) {
   return count_kept(inner_straddle(v, mask, xq, cD.delta), tau) +
              count_kept(outer_straddle(v, mask, xq, cD.delta), tau) > 0;
+}
+
+// approxcaps: does the sphere-point hull keep a fan piece above the floor?
+// (a face-table overflow -- impossible for <= 10 points -- is flagged in
+// counter 7 and fails the run)
+__device__ __noinline__ bool approx_pieces_exact(const Vd* v, int mask, Vd xq, double tau) {
+  int kept = 0;
+  const bool ok = approx_pieces(v, mask, xq, cD.delta, tau,
+                                [&](Vd, Vd, Vd, Vd, double) { ++kept; });
+  if (!ok) atomicOr(cD.flags, 1ull);
+  return kept > 0;
 }
 
 // Nocaps certificate (used by classify_cheap): the inner polytope contains a
@@ -476,7 +488,9 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
     if (g2 < delta * delta * (1.0 - 1e-11)) return kOutCap;
     return kDefer;
   }
-  if (cD.strategy == NLFEM_STRATEGY_NOCAPS) {
+  if (cD.strategy == NLFEM_STRATEGY_NOCAPS || cD.strategy == NLFEM_STRATEGY_APPROXCAPS) {
+    // (approxcaps: the hull contains the nocaps polytope, whose certified
+    // volume > 64 tau exceeds its <= 16 fan pieces x tau)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if ((mask >> i & 1) && d2[i] < cert2) return kStraddle | mask;
@@ -493,6 +507,8 @@ __device__ __forceinline__ unsigned classify_deferred(Vd xq, const Vd v[4], int 
                : kNone;
   if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
     return inner_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
+  if (cD.strategy == NLFEM_STRATEGY_APPROXCAPS)
+    return approx_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
   return any_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
 }
 
@@ -1726,6 +1742,53 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
   }
 }
 
+// approxcaps units: one thread per straddling item; the sphere-point hull's
+// fan pieces (approx_pieces, geom.cuh) integrated by the degree-2 rule into the
+// item record exactly as k_mc<..., OUTER = false> does for nocaps pieces
+// (reference straddle_inner(sphere_points = true) + AsmSink::sub,
+// ball_approx.cpp:210-229, assembly.cpp:372-381).
+template <bool CONS>
+__global__ void __launch_bounds__(kMcThreads) k_approx(long long p0, long long nitems,
+                                                       const int* list, const int* nlistp,
+                                                       const int* upair, const unsigned char* uqs,
+                                                       const int* pair_outer, const int* partner,
+                                                       const unsigned* info, double* mom,
+                                                       unsigned long long* mc_stats) {
+  constexpr int NV = CONS ? 2 : 10;
+  unsigned long long led = 0;
+  const int nlist = nlistp[0];
+  for (int li = blockIdx.x * blockDim.x + threadIdx.x; li < nlist; li += gridDim.x * blockDim.x) {
+    const long long u = list[li];
+    const int pi = upair[u];
+    const int q = uqs[u];
+    const long long p = p0 + pi;
+    const int T = cD.interior[pair_outer[pi]];
+    const int Tp = partner[p];
+    const int mask = (int)((info[p] >> (5 * q)) & 15u);
+    Vd vT[4], w[4];
+    load_verts(T, vT);
+    const Vd xq = quad_point(vT, q);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = elem_vertex(Tp, j);
+    const double tau = cD.tau[Tp];
+    double acc[NV];
+#pragma unroll
+    for (int kk = 0; kk < NV; ++kk) acc[kk] = 0.0;
+    int kin = 0;
+    if (!approx_pieces(w, mask, xq, cD.delta, tau, [&](Vd a, Vd b, Vd c, Vd d, double vol) {
+          inner_piece<CONS>(a, b, c, d, vol, tau, w[0], acc, kin);
+        }))
+      atomicOr(cD.flags, 1ull);
+    const int m = __popc(mask);
+    led += 38ull * (m * (4 - m)) + 24ull * kin + (unsigned long long)kin * (CONS ? 160 : 360);
+    double2* rec = reinterpret_cast<double2*>(mom + kMomStride * u);
+#pragma unroll
+    for (int kk = 0; kk < NV; kk += 2) rec[kk / 2] = make_double2(acc[kk], acc[kk + 1]);
+  }
+  for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
+  if ((threadIdx.x & 31) == 0 && led) atomicAdd(mc_stats + 2, led);
+}
+
 // load-vector partials: one slot per (interior element, combine warp, node)
 constexpr int kRhsWarps = 8;
 
@@ -2308,8 +2371,6 @@ void check_config(const nlfem_gpu_kernel* k, const nlfem_gpu_config* cfg) {
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: mc_samples must be positive"};
   if (cfg->strategy < NLFEM_STRATEGY_INSIDE || cfg->strategy > NLFEM_STRATEGY_FULLCAPS)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown strategy"};
-  if (cfg->strategy == NLFEM_STRATEGY_APPROXCAPS)
-    throw Fail{NLFEM_GPU_EUNSUPPORTED, "strategy approxcaps is not implemented on the GPU path"};
   if (cfg->sampler != NLFEM_SAMPLER_PHILOX)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown sampler"};
 }
@@ -2446,6 +2507,8 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.gbar = S.gbar.p;
   D.cert2 = S.cert2.p;
   D.bnd = S.bnd.p;
+  S.counters.ensure(8);
+  D.flags = S.counters.p + 7;
   D.verts = S.verts.p;
   D.nbr = S.nbr.p;
   D.vol = S.vol.p;
@@ -2863,8 +2926,9 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const bool need_mc = D.strategy == NLFEM_STRATEGY_FULLCAPS;
   // straddling pieces only under nocaps / fullcaps; the other strategies emit
   // whole-element items only
-  const bool need_units =
-      D.strategy == NLFEM_STRATEGY_NOCAPS || D.strategy == NLFEM_STRATEGY_FULLCAPS;
+  const bool need_units = D.strategy == NLFEM_STRATEGY_NOCAPS ||
+                          D.strategy == NLFEM_STRATEGY_APPROXCAPS ||
+                          D.strategy == NLFEM_STRATEGY_FULLCAPS;
   float mc_ms = 0;
   // chunks of outer elements sized so the unit buffers stay bounded.  One
   // chunk needs no host round trip when its first pair and a bound on its
@@ -2973,6 +3037,9 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
             launch(k_mc<true, false, 3>, 7, s3);
             launch(k_mc<true, false, 0>, 4, s3);
           }
+        } else if (D.strategy == NLFEM_STRATEGY_APPROXCAPS) {  // sphere-point hulls
+          for (int kind : {1, 2, 3}) launch(k_approx<false>, kind, kind == 3 ? s3 : st);
+          for (int kind : {5, 6, 7}) launch(k_approx<true>, kind, kind == 7 ? s3 : st);
         } else {  // nocaps: inner pieces only
           launch(k_mc<false, false, 2, false>, 2, st);
           launch(k_mc<false, false, 1, false>, 1, st);
@@ -3035,6 +3102,9 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   S.mc_hits = cnt[2];
   S.ledger = cnt[3];
   S.mc_subs = cnt[4];
+  if (cnt[7])
+    throw Fail{NLFEM_GPU_DEGENERATE_HULL,
+               "DegenerateHull: approxcaps hull face table overflow (more than 32 faces)"};
   if (user) {
     CK(cudaEventRecord(S.ev[6], st));
     CK(cudaStreamWaitEvent(user, S.ev[6], 0));
@@ -3117,7 +3187,7 @@ int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen
   });
 }
 
-const char* nlfem_gpu_version(void) { return "nlfem_gpu 0.1 sm_100a (barycenter, nocaps, fullcaps)"; }
+const char* nlfem_gpu_version(void) { return "nlfem_gpu 0.2 sm_100a (inside, overlap, barycenter, nocaps, approxcaps, fullcaps)"; }
 
 int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
                              const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,

@@ -3,7 +3,7 @@
 Run here (needs /root/reference compiled by `make -C oracle ref`):
     python tests/golden/make_golden.py
 Each fixture holds a small 3D mesh, the reference's assemble() output for
-inside / overlap / barycenter / nocaps / fullcaps (reference xoshiro sampler, seed 1234) with the
+inside / overlap / barycenter / nocaps / approxcaps / fullcaps (reference xoshiro sampler, seed 1234) with the
 moment2 kernel and u = |x|^2, and the per-(T, q) pieces the reference's public
 walk_ball emits for a seeded sample of outer points.  These pin the oracle
 restatement (tests/test_oracle.py) and the GPU sets/pattern (tests/test_gpu_*.py)
@@ -23,7 +23,7 @@ from oracle import ref  # noqa: E402
 
 U = np.array([[1, 2, 0, 0], [1, 0, 2, 0], [1, 0, 0, 2]], float)
 SEED = 1234
-STRATS = ("inside", "overlap", "barycenter", "nocaps", "fullcaps")
+STRATS = ("inside", "overlap", "barycenter", "nocaps", "approxcaps", "fullcaps")
 
 
 def lattice(res, delta, jitter=None):

@@ -47,13 +47,6 @@ def _table():
     return P.ElementTable(g["coords"], g["cells"], g["region"])
 
 
-def test_unsupported_strategy_is_an_error():
-    t = _table()
-    with pytest.raises(P.NlfemError) as ei:
-        P.assemble(t, 0.3, "approxcaps", "moment2", U2)
-    assert ei.value.code == 102
-
-
 def test_bad_config_codes():
     t = _table()
     with pytest.raises(P.NlfemError) as ei:

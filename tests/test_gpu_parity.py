@@ -2,7 +2,7 @@
 
 (a) element-pair sets per (T, q) equal the reference's walk_ball pieces, and the
     CSR sparsity pattern is bit-exact;
-(b) overlap / barycenter / nocaps entries within 1e-12 of the reference, row-normwise
+(b) overlap / barycenter / nocaps / approxcaps entries within 1e-12 of the reference, row-normwise
     (|a_ik - b_ik| <= 1e-12 max_k |b_ik|), rhs within 1e-12 max|b|; inside
     within 5e-12 max|A| (the reference's own criterion, its rows cancel);
 (c) fullcaps entries within 1e-11 row-normwise of the CPU oracle drawing the
@@ -43,7 +43,8 @@ def golden(request):
     return request.param, load_golden(request.param)
 
 
-@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "fullcaps"])
+@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "approxcaps",
+                                   "fullcaps"])
 def test_pattern_and_sets(golden, strat):
     name, g = golden
     t = _table(g)
@@ -58,7 +59,7 @@ def test_pattern_and_sets(golden, strat):
         assert got.get(key, set()) == ws, (name, strat, key)
 
 
-@pytest.mark.parametrize("strat", ["overlap", "barycenter", "nocaps"])
+@pytest.mark.parametrize("strat", ["overlap", "barycenter", "nocaps", "approxcaps"])
 def test_deterministic_values_match_reference(golden, strat):
     name, g = golden
     out, st = P.assemble(_table(g), float(g["delta"]), strat, "moment2", U2)
@@ -271,3 +272,17 @@ def test_results_are_independent_pooled_blocks():
     for k in keep:
         assert np.array_equal(a[k], keep[k])
         assert np.array_equal(c[k], keep[k])
+
+
+def test_approxcaps_jittered_matches_oracle():
+    # a jittered mesh beyond the fixtures (general straddle shapes, many
+    # deferred hull decisions in the pairs kernel) against the restated oracle,
+    # which is bit-identical to the reference (tests/test_oracle.py)
+    m = P.generate_mesh(3, 7, 0.3, jitter_seed=5)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    out, st = P.assemble(t, 0.3, "approxcaps", "moment2", U2)
+    o = _oracle(t, 0.3, "approxcaps", 1, sampler="R")
+    assert same_pattern(out, o)
+    assert row_rel_err(out, o) <= TOL_DET
+    assert rhs_rel_err(out, o) <= TOL_DET
+    assert st["element_pairs"] == o["element_pairs"]

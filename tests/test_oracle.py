@@ -35,7 +35,8 @@ def test_philox_known_answers():
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "fullcaps"])
+@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "approxcaps",
+                                   "fullcaps"])
 def test_mode_r_matches_reference_golden(name, strat):
     g = load_golden(name)
     o = _run(_table(g), float(g["delta"]), strat, int(g["mc_samples"]), "R", threads=2)
@@ -49,7 +50,8 @@ def test_mode_r_matches_live_reference():
     m = P.generate_mesh(3, 5, 0.3, jitter_seed=3)
     t = P.ElementTable(m["coords"], m["cells"], m["region"])
     r = ref.Problem(m["coords"], m["cells"], m["region"])
-    for strat, mc in (("inside", 1), ("overlap", 1), ("nocaps", 1), ("fullcaps", 12)):
+    for strat, mc in (("inside", 1), ("overlap", 1), ("nocaps", 1), ("approxcaps", 1),
+                      ("fullcaps", 12)):
         o = _run(t, 0.3, strat, mc, "R")
         s = r.assemble(0.3, strat, U2, threads=3, seed=SEED, mc_samples=mc)
         for k in ("row_ptr", "col_idx", "values", "rhs"):
