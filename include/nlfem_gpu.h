@@ -235,6 +235,27 @@ int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_
 int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_idx,
                               void** values, void** rhs, int32_t* rows, int64_t* nnz);
 
+/* solve_problem + l2_error on the GPU (reference study.cpp:38-99): CG on the
+ * session's assembled system where it lies in HBM (nlfem_gpu_cg_device, x0 = 0),
+ * node values (unknowns from x, constrained nodes g(x_j), study.cpp:64-74),
+ * the L2 error against `exact` with the 14-point degree-5 tetrahedral rule
+ * over interior elements (study.cpp:76-99, quadrature.cpp:42-62) and the
+ * largest nodal error max_j |u_h(x_j) - exact(x_j)|.  Deterministic
+ * (fixed-order reductions).  u_node: optional host array [node_count]. */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double relative_residual;
+  double l2_error;
+  double max_nodal_error;
+  double device_ms; /* CG + node values + error norms, CUDA events */
+} nlfem_gpu_study;
+
+int nlfem_gpu_session_solve(nlfem_gpu_session* s, double tol, int32_t max_iter,
+                            const nlfem_gpu_poly* exact, double* u_node, nlfem_gpu_study* out,
+                            char* err, size_t errlen);
+
+
 /* Element-pair list of the last run, for set parity: for each interior outer
  * element (in ascending id order) its partner ids and per-quad-point class
  * codes (5 bits per point).  Arrays sized by *npairs after a

@@ -77,6 +77,12 @@ class _SolveReport(C.Structure):
                 ("relative_residual", C.c_double)]
 
 
+class _Study(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32),
+                ("relative_residual", C.c_double), ("l2_error", C.c_double),
+                ("max_nodal_error", C.c_double), ("device_ms", C.c_double)]
+
+
 class _Csr(C.Structure):
     _fields_ = [("rows", C.c_int32), ("nnz", C.c_int64), ("row_ptr", C.POINTER(C.c_int32)),
                 ("col_idx", C.POINTER(C.c_int32)), ("values", C.POINTER(C.c_double)),
@@ -142,6 +148,9 @@ def lib():
     L.nlfem_gpu_cg_device.restype = C.c_int
     L.nlfem_gpu_cg_device.argtypes = [i32, vp, vp, vp, vp, dbl, i32, vp, vp, P(_SolveReport),
                                       C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_solve.restype = C.c_int
+    L.nlfem_gpu_session_solve.argtypes = [vp, dbl, i32, P(_Poly), vp, P(_Study), C.c_char_p,
+                                          C.c_size_t]
     L.nlfem_gpu_element_table.restype = C.c_int
     L.nlfem_gpu_element_table.argtypes = [vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp,
                                           vp, P(i32), i32, C.c_char_p, C.c_size_t]
@@ -181,7 +190,7 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
     "nlfem_gpu_session_outputs", "nlfem_gpu_session_pairs_shard",
     "nlfem_gpu_session_pairs_shard_out", "nlfem_gpu_session_pairs_install",
-    "nlfem_gpu_cg", "nlfem_gpu_cg_device", "nlfem_gpu_element_table",
+    "nlfem_gpu_cg", "nlfem_gpu_cg_device", "nlfem_gpu_session_solve", "nlfem_gpu_element_table",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
 ]
@@ -476,6 +485,31 @@ class Session:
                                          C.byref(rep), err, 1024), err)
         return {"x": x[:n].cpu().numpy(), "iterations": rep.iterations,
                 "converged": bool(rep.converged), "relative_residual": rep.relative_residual}
+
+    def solve(self, tol: float = 1e-10, max_iterations: int | None = None, exact_terms=None,
+              node_values: bool = False) -> dict:
+        """solve_problem + l2_error on the GPU (reference study.cpp:38-99) for the
+        system assembled by run(), in place in HBM: CG from zero, node values
+        (constrained nodes from g), the L2 error against `exact_terms` (default:
+        the manufactured solution this session was built from) with the
+        14-point degree-5 rule, and the largest nodal error.  max_iterations
+        defaults to the reference harness's 100 x unknowns."""
+        ex = self.uterms if exact_terms is None else _check_terms(exact_terms)
+        ep, keep = _poly_struct(ex)
+        if max_iterations is None:
+            max_iterations = 100 * max(self.table.unknowns, 1)
+        vals = np.empty(self.table.node_count) if node_values else None
+        rep = _Study()
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_solve(self._h, float(tol), int(max_iterations),
+                                             C.byref(ep), _p(vals) if node_values else None,
+                                             C.byref(rep), err, 1024), err)
+        out = {"iterations": rep.iterations, "converged": bool(rep.converged),
+               "relative_residual": rep.relative_residual, "l2": rep.l2_error,
+               "max_nodal_error": rep.max_nodal_error, "device_ms": rep.device_ms}
+        if node_values:
+            out["node_values"] = vals
+        return out
 
     def partials(self):
         """Device views (V int64 words, rhsT float64) of the exact partial sums."""

@@ -2294,7 +2294,9 @@ struct nlfem_gpu_session {
   // Gauss units and the one-piece Monte Carlo lists run on stream3, beside the
   // three-piece Monte Carlo lists on `stream`
   cudaStream_t stream3 = nullptr;
-  std::vector<cudaEvent_t> ev;  // 0..7 phases on stream; 8, 9 pattern on stream2; 10, 11 fork/join
+  std::vector<cudaEvent_t> ev;  // 0..7 phases on stream; 8, 9 pattern on stream2; 10, 11 fork/join;
+                                // 12, 13 solve
+  DBuf<double> solx, nodev, study_tmp;  // solve: x, node values, reduction scratch
 };
 
 namespace {
@@ -2407,7 +2409,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&S.stream2, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithFlags(&S.stream3, cudaStreamNonBlocking));
-    for (int i = 0; i < 12; ++i) {
+    for (int i = 0; i < 14; ++i) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       S.ev.push_back(e);
@@ -3159,6 +3161,173 @@ int guard(char* err, size_t errlen, const std::function<void()>& fn) {
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// solve_problem + l2_error (reference study.cpp:38-99) on the assembled system
+
+// node values (study.cpp:64-74): unknowns from x, constrained nodes g(x_j);
+// per-block maxima of |u_h(x_j) - exact(x_j)|
+constexpr int kStudyThreads = 256;
+__global__ void __launch_bounds__(kStudyThreads) k_node_values(int J, const double* node,
+                                                               const int* dof, const double* x,
+                                                               Poly g, Poly exact, double* vals,
+                                                               double* bmax) {
+  __shared__ double sm[kStudyThreads / 32];
+  const int j = blockIdx.x * kStudyThreads + threadIdx.x;
+  double e = 0;
+  if (j < J) {
+    const Vd p = {node[3 * j], node[3 * j + 1], node[3 * j + 2]};
+    const int d = dof[j];
+    const double v = d >= 0 ? x[d] : poly_eval(g, p);
+    vals[j] = v;
+    e = fabs(v - poly_eval(exact, p));
+  }
+  for (int sh = 16; sh > 0; sh >>= 1) e = fmax(e, __shfl_xor_sync(FULLMASK, e, sh));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0;
+    for (int w = 0; w < kStudyThreads / 32; ++w) m = fmax(m, sm[w]);
+    bmax[blockIdx.x] = m;
+  }
+}
+
+// degree-5 14-point rule (reference quadrature.cpp:42-62): barycentric rows, weights
+__constant__ double cL2Rule[14][5];
+
+// per-block sums of vol_t w_q (u_h - exact)^2 over interior elements (thread
+// per element, fixed order inside a block: warp tree, then warps in order)
+__global__ void __launch_bounds__(kStudyThreads) k_l2_partial(int KI, const int* interior,
+                                                              const int4* verts, const double* vol,
+                                                              const double* node, const double* vals,
+                                                              Poly exact, double* bsum) {
+  __shared__ double sm[kStudyThreads / 32];
+  const int i = blockIdx.x * kStudyThreads + threadIdx.x;
+  double acc = 0;
+  if (i < KI) {
+    const int t = interior[i];
+    const int4 w = verts[t];
+    const int vv[4] = {w.x, w.y, w.z, w.w};
+    Vd x[4];
+    double u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[k] = {node[3 * vv[k]], node[3 * vv[k] + 1], node[3 * vv[k] + 2]};
+      u[k] = vals[vv[k]];
+    }
+    const double V = vol[t];
+    for (int q = 0; q < 14; ++q) {
+      Vd p = {0.0, 0.0, 0.0};
+      double uh = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double b = cL2Rule[q][k];
+        p = vadd(p, vscale(b, x[k]));
+        uh += b * u[k];
+      }
+      const double d = uh - poly_eval(exact, p);
+      acc += V * cL2Rule[q][4] * d * d;
+    }
+  }
+  for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, sh);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < kStudyThreads / 32; ++w) s += sm[w];
+    bsum[blockIdx.x] = s;
+  }
+}
+
+// one CTA: block sums in a fixed order -> sqrt; block maxima -> max
+__global__ void __launch_bounds__(kStudyThreads) k_study_final(int nb_sum, const double* bsum,
+                                                               int nb_max, const double* bmax,
+                                                               double* res) {
+  __shared__ double ss[kStudyThreads], sx[kStudyThreads];
+  double a = 0, m = 0;
+  for (int i = threadIdx.x; i < nb_sum; i += kStudyThreads) a += bsum[i];
+  for (int i = threadIdx.x; i < nb_max; i += kStudyThreads) m = fmax(m, bmax[i]);
+  ss[threadIdx.x] = a;
+  sx[threadIdx.x] = m;
+  __syncthreads();
+  for (int h = kStudyThreads / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      ss[threadIdx.x] += ss[threadIdx.x + h];
+      sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + h]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    res[0] = sqrt(ss[0]);
+    res[1] = sx[0];
+  }
+}
+
+void session_solve(nlfem_gpu_session& S, double tol, int32_t max_iter, const nlfem_gpu_poly* exact,
+                   double* u_node, nlfem_gpu_study* out) {
+  if (S.nnz_out < 0 || !S.values.p)
+    throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: solve needs an assembled system (run first)"};
+  CK(cudaSetDevice(S.device));
+  static bool rule_set = false;  // per process; the rule is a constant
+  if (!rule_set) {
+    const double a = 0.3108859192633005, wa = 0.1126879257180162;
+    const double b = 0.0927352503108912, wb = 0.0734930431163619;
+    const double c = 0.0455037041256497, d = 0.5 - c, wc = 0.0425460207770812;
+    const double a4 = 1.0 - 3.0 * a, b4 = 1.0 - 3.0 * b;
+    const double rows[14][5] = {{a4, a, a, a, wa}, {a, a4, a, a, wa}, {a, a, a4, a, wa},
+                                {a, a, a, a4, wa}, {b4, b, b, b, wb}, {b, b4, b, b, wb},
+                                {b, b, b4, b, wb}, {b, b, b, b4, wb}, {c, c, d, d, wc},
+                                {c, d, c, d, wc}, {c, d, d, c, wc}, {d, c, c, d, wc},
+                                {d, c, d, c, wc}, {d, d, c, c, wc}};
+    CK(cudaMemcpyToSymbol(cL2Rule, rows, sizeof(rows)));
+    rule_set = true;
+  }
+  Poly ex, g;
+  poly_to_dev(exact, ex);
+  g = S.dev.g;
+  cudaStream_t st = S.stream;
+  CK(cudaEventRecord(S.ev[12], st));
+  S.solx.ensure(std::max(S.unknowns, 1));
+  char cgerr[512] = {0};
+  nlfem_gpu_solve_report rep{};
+  const int rc = nlfem_gpu_cg_device(S.unknowns, reinterpret_cast<const int64_t*>(S.ooff.p), S.ocols.p, S.values.p, S.rhs.p, tol,
+                                     max_iter, S.solx.p, st, &rep, cgerr, sizeof(cgerr));
+  if (rc) throw Fail{rc, cgerr};
+  const int nbJ = std::max(1, (S.J + kStudyThreads - 1) / kStudyThreads);
+  const int nbK = std::max(1, (S.KI + kStudyThreads - 1) / kStudyThreads);
+  S.nodev.ensure(std::max(S.J, 1));
+  S.study_tmp.ensure(nbJ + nbK + 2);
+  double* bmax = S.study_tmp.p;
+  double* bsum = bmax + nbJ;
+  double* res = bsum + nbK;
+  if (S.J > 0)
+    k_node_values<<<nbJ, kStudyThreads, 0, st>>>(S.J, S.node.p, S.dof.p, S.solx.p, g, ex,
+                                                 S.nodev.p, bmax);
+  else
+    CK(cudaMemsetAsync(bmax, 0, sizeof(double), st));
+  if (S.KI > 0)
+    k_l2_partial<<<nbK, kStudyThreads, 0, st>>>(S.KI, S.interior.p, S.verts.p, S.vol.p, S.node.p,
+                                                S.nodev.p, ex, bsum);
+  else
+    CK(cudaMemsetAsync(bsum, 0, sizeof(double), st));
+  k_study_final<<<1, kStudyThreads, 0, st>>>(S.KI > 0 ? nbK : 1, bsum, S.J > 0 ? nbJ : 1, bmax,
+                                             res);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(S.ev[13], st));
+  double h[2];
+  CK(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (u_node && S.J > 0)
+    CK(cudaMemcpyAsync(u_node, S.nodev.p, sizeof(double) * S.J, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, S.ev[12], S.ev[13]));
+  out->iterations = rep.iterations;
+  out->converged = rep.converged;
+  out->relative_residual = rep.relative_residual;
+  out->l2_error = h[0];
+  out->max_nodal_error = h[1];
+  out->device_ms = ms;
+}
+
 extern "C" {
 
 int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen) {
@@ -3306,6 +3475,12 @@ int nlfem_gpu_session_partials(nlfem_gpu_session* s, void** V, int64_t* nwords, 
   *rhsT = s->rhsT.p;
   *nrhs = 4 * kRhsWarps * (int64_t)s->KI;
   return 0;
+}
+
+int nlfem_gpu_session_solve(nlfem_gpu_session* s, double tol, int32_t max_iter,
+                            const nlfem_gpu_poly* exact, double* u_node, nlfem_gpu_study* out,
+                            char* err, size_t errlen) {
+  return guard(err, errlen, [&] { session_solve(*s, tol, max_iter, exact, u_node, out); });
 }
 
 int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_idx,

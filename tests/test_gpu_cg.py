@@ -55,3 +55,42 @@ def test_cg_edge_cases(c1):
     assert capped["iterations"] == 5 and not capped["converged"]
     with pytest.raises(ValueError):
         P.cg(sys["row_ptr"][:-1], sys["col_idx"], sys["values"], sys["rhs"])
+
+
+def test_session_solve_matches_reference_harness(c1):
+    # solve_problem + l2_error on the device (study.cpp:38-99) against the
+    # oracle's restatement of the same harness (CG from zero, node values, the
+    # 14-point L2 rule) on the same assembled system
+    t, sys = c1
+    s = P.Session(t, 0.25, "nocaps", "moment2", U2, seed=SEED)
+    s.run()
+    got = s.solve(tol=1e-12, node_values=True)
+    ref = port.solve_l2(t, sys, U2, tol=1e-12)
+    assert got["converged"] and abs(got["iterations"] - ref["iterations"]) <= 3
+    assert abs(got["l2"] - ref["l2"]) <= 1e-9 * ref["l2"]
+    # node values: unknowns from CG, constrained nodes exactly g
+    nv = got["node_values"]
+    con = t.dof_of_node < 0
+    c = t.coords[con]
+    assert np.array_equal(nv[con], c[:, 0] * c[:, 0] + c[:, 1] * c[:, 1] + c[:, 2] * c[:, 2]) or \
+        np.abs(nv[con] - (c * c).sum(1)).max() <= 1e-15 * (c * c).sum(1).max()
+    exact = (t.coords * t.coords).sum(1)
+    assert got["max_nodal_error"] == pytest.approx(np.abs(nv - exact).max(), rel=1e-12, abs=1e-300)
+    again = s.solve(tol=1e-12)
+    assert again["l2"] == got["l2"] and again["iterations"] == got["iterations"]
+
+
+def test_session_solve_error_matches_reference_golden():
+    # north_star: the solved error against u = |x|^2 within 1% of the reference's
+    # (nocaps deterministic: agrees to CG tolerance; fullcaps: Philox vs the
+    # reference's xoshiro stream, so within 1%)
+    from tests.helpers import load_golden
+    g = load_golden("lat6_d025")
+    t = P.ElementTable(g["coords"], g["cells"], g["region"])
+    for strat, tol in (("nocaps", 1e-6), ("approxcaps", 1e-6), ("fullcaps", 1e-2)):
+        s = P.Session(t, float(g["delta"]), strat, "moment2", U2, seed=SEED,
+                      mc_samples=int(g["mc_samples"]))
+        s.run()
+        r = s.solve(tol=1e-12)
+        want = float(g[f"{strat}_l2"])
+        assert abs(r["l2"] / want - 1) < tol, (strat, r["l2"], want)
