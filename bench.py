@@ -56,6 +56,12 @@ CONFIGS = {
     "P3n": dict(res=24, delta=3 / 24, strategy="nocaps", mc=1, jitter=7),
     "P3f": dict(res=24, delta=3 / 24, strategy="fullcaps", mc=128, jitter=7),
 }
+# dram__bytes_read.sum + dram__bytes_write.sum of the units kernels (all k_mc
+# launches of one step) from the committed ncu --set full capture; None where
+# no capture was taken for that workload
+TRAFFIC = {"C1": 432067584}
+
+
 def describe(name, cfg):
     d = dict(cfg)
     s = (f"{name}: structured N={cfg['res']} cubes/side (6 tets each) + layer, "
@@ -259,7 +265,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    step_ms, k3_ms = [], []
+    step_ms, k3_ms, mc_ms = [], [], []
     st = None
     for _ in range(args.steps):
         flush.fill_(1.0)  # evict L2 between timed steps (inputs are smaller than L2)
@@ -271,6 +277,7 @@ def main():
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         k3_ms.append(st.phase_ms[3])
+        mc_ms.append(st.phase_ms[5])
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
@@ -323,7 +330,18 @@ def main():
 
     peak = P.fp64_peak_tflops(local)
     k3 = float(np.mean(k3_ms))
-    achieved = st.ledger_flops / (k3 * 1e-3) / 1e12
+    kmc = float(np.mean(mc_ms))
+    # dominant kernel: the units kernels (k_mc: inner pieces + Monte Carlo; its
+    # launches run on two streams, timed together by CUDA events around them)
+    units = kmc > 0 and st.ledger_flops_units > 0
+    if units:
+        achieved = st.ledger_flops_units / (kmc * 1e-3) / 1e12
+        rl_kernel, rl_flops, rl_ms = ("k_mc (units phase: inner pieces + Monte Carlo, all "
+                                      "launches of one step)"), st.ledger_flops_units, kmc
+    else:  # barycenter / overlap / inside: whole-element items in the combine only
+        achieved = st.ledger_flops / (k3 * 1e-3) / 1e12
+        rl_kernel, rl_flops, rl_ms = "k_integrate (combine)", st.ledger_flops, k3
+    integ = st.ledger_flops / (k3 * 1e-3) / 1e12
     line = {
         "metric": "element-pair integrals/s", "value": value, "unit": "element-pair integrals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -337,11 +355,16 @@ def main():
                                   "row-block all-gather)" if world > 1 else "single GPU"},
         "fp64_gflops_ledger": st.ledger_flops / (t_total / args.steps * 1e-3) / 1e9,
         "phase_ms": [round(x, 3) for x in st.phase_ms[:6]],
-        "roofline": {"kernel": "k_integrate", "bound": "fp64", "achieved": achieved,
+        "roofline": {"kernel": rl_kernel, "bound": "fp64", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": "nlfem_gpu_fp64_peak() DFMA microbenchmark, this run (burst)",
-                     "ledger_flops_per_launch": int(st.ledger_flops), "launch_ms": k3,
-                     "traffic": None},
+                     "ledger_flops_per_launch": int(rl_flops), "launch_ms": rl_ms,
+                     "traffic": TRAFFIC.get(args.config) if units else None,
+                     "traffic_source": "profiles/r1_c1_kmc_ncu.txt (dram read+write summed over "
+                                       "the step's k_mc launches)" if units else None,
+                     "integration_phase": {"kernels": "k_mc + k_integrate", "ms": k3,
+                                           "ledger_flops": int(st.ledger_flops),
+                                           "achieved": integ, "frac": integ / peak}},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }

@@ -135,6 +135,9 @@ typedef struct {
                               sub-simplex setup 25, sample 35, hit +62/+12)   */
   uint64_t mc_subsimplices;
   int64_t shard_pairs;     /* element pairs integrated by this run (its shard)  */
+  uint64_t ledger_flops_units; /* the part of ledger_flops done by the units
+                              kernels (k_mc / k_approx: inner pieces and Monte
+                              Carlo), whose phase time is phase_ms[5]        */
 } nlfem_gpu_stats;
 
 /* One-shot drop-in: host arrays in, host CSR out (upload + device pipeline +

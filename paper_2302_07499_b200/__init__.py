@@ -96,7 +96,7 @@ class Stats(C.Structure):
                 ("element_pairs", C.c_int64), ("items", C.c_int64), ("nnz_ext", C.c_int64),
                 ("device_ms", C.c_double), ("phase_ms", C.c_double * 8),
                 ("ledger_flops", C.c_uint64), ("mc_subsimplices", C.c_uint64),
-                ("shard_pairs", C.c_int64)]
+                ("shard_pairs", C.c_int64), ("ledger_flops_units", C.c_uint64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}

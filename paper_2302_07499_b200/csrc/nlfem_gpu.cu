@@ -2030,7 +2030,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     sgc[q] = wsum(sgc[q]);
   }
   for (int sh = 16; sh > 0; sh >>= 1) led += __shfl_xor_sync(FULLMASK, led, sh);
-  if (lane == 0 && led) atomicAdd(stats + 2, led);
+  if (lane == 0 && led) atomicAdd(stats + 4, led);  // counter 5: combine ledger
   if (lane < 10) {
     // lanes 0..9: the ten D_T entries (a <= b)
     const int t = lane;
@@ -2286,7 +2286,8 @@ struct nlfem_gpu_session {
   double delta_over_h = 0;   // delta / cbrt(6 mean element volume)
   DBuf<unsigned> info_own;
   std::atomic<long long> launches{0};
-  unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0;
+  unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0,
+                     ledger_units = 0;
   cudaStream_t stream = nullptr;
   // the node pattern is built on a second, higher-priority stream from its own
   // host thread, concurrently with the units / Monte Carlo work on `stream`
@@ -3102,7 +3103,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   S.items = cnt[0];
   S.mc_samples = cnt[1];
   S.mc_hits = cnt[2];
-  S.ledger = cnt[3];
+  S.ledger = cnt[3] + cnt[5];
+  S.ledger_units = cnt[3];
   S.mc_subs = cnt[4];
   if (cnt[7])
     throw Fail{NLFEM_GPU_DEGENERATE_HULL,
@@ -3137,6 +3139,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     stats->items = (long long)S.items;
     stats->nnz_ext = S.nnz_s;
     stats->ledger_flops = S.ledger;
+    stats->ledger_flops_units = S.ledger_units;
     stats->mc_subsimplices = S.mc_subs;
     stats->phase_ms[5] = S.mc_ms;
     stats->seconds =
