@@ -52,6 +52,9 @@ CONFIGS = {
     "C3n": dict(res=48, delta=3 / 48, strategy="nocaps", mc=1, jitter=7),
     "C3f": dict(res=48, delta=3 / 48, strategy="fullcaps", mc=128, jitter=7),
     "C4": dict(res=96, delta=3 / 96, strategy="fullcaps", mc=128, jitter=None),
+    # the other strategies on the config-1 mesh (not BASELINE workloads)
+    "C1n": dict(res=8, delta=0.25, strategy="nocaps", mc=1, jitter=None),
+    "C1a": dict(res=8, delta=0.25, strategy="approxcaps", mc=1, jitter=None),
     # smaller same-delta/h variants for profiling
     "P3n": dict(res=24, delta=3 / 24, strategy="nocaps", mc=1, jitter=7),
     "P3f": dict(res=24, delta=3 / 24, strategy="fullcaps", mc=128, jitter=7),
