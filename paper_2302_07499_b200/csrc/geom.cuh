@@ -266,7 +266,8 @@ __device__ __forceinline__ void straddle_piece(const Straddle& s, int k, Vd& a, 
 // reference's order.  A degenerate hull emits nothing (DegenerateHull is
 // swallowed there).  Returns false if the face table overflowed (cannot happen
 // for <= 10 points: a triangulated hull has <= 2V - 4 = 16 faces).
-constexpr int kHullFaces = 32;
+constexpr int kHullFaces = 32;   // faces after an insertion (a closed hull of <= 10 points has <= 16)
+constexpr int kHullScratch = 48; // faces + new horizon faces during an insertion (<= 16 + 10)
 
 template <class Fn>
 __device__ __forceinline__ bool approx_pieces(const Vd v[4], int mask, Vd c, double r, double tau,
@@ -322,84 +323,81 @@ __device__ __forceinline__ bool approx_pieces(const Vd v[4], int mask, Vd c, dou
     s2 = t;
   }
   const Vd inner = vscale(0.25, vadd(vadd(vadd(pts[s0], pts[s1]), pts[s2]), pts[s3]));
-  int fa[kHullFaces], fb[kHullFaces], fc[kHullFaces];
-  auto outward = [&](int& a, int& b, int& cc) {
+  // faces packed one per word (a | b << 8 | c << 16): the table stays small
+  // enough for L1 (the data-dependent indexing puts it in local memory)
+  auto pack = [](int a, int b, int cc) { return (unsigned)a | ((unsigned)b << 8) | ((unsigned)cc << 16); };
+  auto outward = [&](int a, int b, int cc) {
     const Vd nn = vcross(vsub(pts[b], pts[a]), vsub(pts[cc], pts[a]));
-    if (vdot(nn, vsub(inner, pts[a])) > 0) {
-      const int t = b;
-      b = cc;
-      cc = t;
-    }
+    return vdot(nn, vsub(inner, pts[a])) > 0 ? pack(a, cc, b) : pack(a, b, cc);
   };
+  // faces [0, nf); horizon faces are built at [nf, nf + nh) and moved down
+  unsigned F[kHullScratch];
   int nf = 4;
-  fa[0] = s0, fb[0] = s2, fc[0] = s1;
-  fa[1] = s0, fb[1] = s1, fc[1] = s3;
-  fa[2] = s1, fb[2] = s2, fc[2] = s3;
-  fa[3] = s0, fb[3] = s3, fc[3] = s2;
-  for (int f = 0; f < 4; ++f) outward(fa[f], fb[f], fc[f]);
+  F[0] = outward(s0, s2, s1);
+  F[1] = outward(s0, s1, s3);
+  F[2] = outward(s1, s2, s3);
+  F[3] = outward(s0, s3, s2);
   unsigned used = (1u << s0) | (1u << s1) | (1u << s2) | (1u << s3);
+  unsigned hv = used;  // vertices of the current faces
   for (int pi = 0; pi < n; ++pi) {
     if (used >> pi & 1) continue;
     used |= 1u << pi;
     const Vd p = pts[pi];
+    // duplicate of a face corner (the reference tests every face's corners;
+    // the distinct corners give the same answer)
     bool dup = false;
-    for (int f = 0; f < nf; ++f)
-      if (vdist(p, pts[fa[f]]) <= eps || vdist(p, pts[fb[f]]) <= eps || vdist(p, pts[fc[f]]) <= eps)
-        dup = true;
+    for (int i = 0; i < n; ++i)
+      if ((hv >> i & 1) && vdist(p, pts[i]) <= eps) dup = true;
     if (dup) continue;
     unsigned vis = 0;  // kHullFaces <= 32
     for (int f = 0; f < nf; ++f) {
-      const Vd nn = vcross(vsub(pts[fb[f]], pts[fa[f]]), vsub(pts[fc[f]], pts[fa[f]]));
-      if (vdot(nn, vsub(p, pts[fa[f]])) > eps * sqrt(vnorm2(nn))) vis |= 1u << f;
+      const int a = F[f] & 255, b = (F[f] >> 8) & 255, cc = F[f] >> 16;
+      const Vd nn = vcross(vsub(pts[b], pts[a]), vsub(pts[cc], pts[a]));
+      if (vdot(nn, vsub(p, pts[a])) > eps * sqrt(vnorm2(nn))) vis |= 1u << f;
     }
     if (!vis) continue;
     // horizon: directed edges of visible faces whose reverse lies in an
-    // invisible face, in (face, edge) order
-    int ha[3 * kHullFaces], hb[3 * kHullFaces], nh = 0;
+    // invisible face, in (face, edge) order -> new faces (a, b, pi)
+    int nh = 0;
     for (int f = 0; f < nf; ++f) {
       if (!(vis >> f & 1)) continue;
-      const int e3[3] = {fa[f], fb[f], fc[f]};
+      const int e3[3] = {(int)(F[f] & 255), (int)((F[f] >> 8) & 255), (int)(F[f] >> 16)};
       for (int e = 0; e < 3; ++e) {
         const int a = e3[e], b = e3[e == 2 ? 0 : e + 1];
+        // reverse edge (b, a) as a directed edge of face g: one of its three
+        // rotations starts with b then a
+        const unsigned ba = (unsigned)b | ((unsigned)a << 8);
         bool open = true;
         for (int g = 0; g < nf && open; ++g) {
           if (vis >> g & 1) continue;
-          if ((fa[g] == b && fb[g] == a) || (fb[g] == b && fc[g] == a) || (fc[g] == b && fa[g] == a))
-            open = false;
+          const unsigned w = F[g];
+          const unsigned r1 = (w & 0xffffu), r2 = (w >> 8), r3 = (w >> 16) | ((w & 255u) << 8);
+          if (r1 == ba || r2 == ba || r3 == ba) open = false;
         }
         if (!open) {
-          ha[nh] = a;
-          hb[nh] = b;
-          ++nh;
+          if (nf + nh >= kHullScratch) return false;
+          F[nf + nh++] = outward(a, b, pi);
         }
       }
     }
-    // next = invisible faces in order, then one face per horizon edge
     int k = 0;
     for (int f = 0; f < nf; ++f)
-      if (!(vis >> f & 1)) {
-        fa[k] = fa[f], fb[k] = fb[f], fc[k] = fc[f];
-        ++k;
-      }
+      if (!(vis >> f & 1)) F[k++] = F[f];
     if (k + nh > kHullFaces) return false;
-    for (int h = 0; h < nh; ++h) {
-      int a = ha[h], b = hb[h], cc = pi;
-      outward(a, b, cc);
-      fa[k] = a, fb[k] = b, fc[k] = cc;
-      ++k;
-    }
-    nf = k;
+    for (int h = 0; h < nh; ++h) F[k + h] = F[nf + h];
+    nf = k + nh;
+    hv = 0;
+    for (int f = 0; f < nf; ++f) hv |= (1u << (F[f] & 255)) | (1u << ((F[f] >> 8) & 255)) | (1u << (F[f] >> 16));
   }
   // triangulate_polytope: centroid of the distinct hull vertices, summed in
   // ascending vertex order, times 1/count
-  unsigned vs = 0;
-  for (int f = 0; f < nf; ++f) vs |= (1u << fa[f]) | (1u << fb[f]) | (1u << fc[f]);
+  const unsigned vs = hv;
   Vd cen = {0.0, 0.0, 0.0};
   for (int i = 0; i < n; ++i)
     if (vs >> i & 1) cen = vadd(cen, pts[i]);
   cen = vscale(1.0 / (double)__popc(vs), cen);
   for (int f = 0; f < nf; ++f) {
-    const Vd a = pts[fa[f]], b = pts[fb[f]], cc = pts[fc[f]];
+    const Vd a = pts[F[f] & 255], b = pts[(F[f] >> 8) & 255], cc = pts[F[f] >> 16];
     const double vol = tet_volume(cen, a, b, cc);
     if (vol > tau) fn(cen, a, b, cc, vol);
   }
