@@ -95,10 +95,47 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.rows = []
+        self.source = "nvidia-smi, every 0.2 s"
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        """NVML handle of this process's CUDA device (matched by PCI bus id)."""
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId_v2(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
     def start(self):
+        try:  # in-process NVML, sampled every 5 ms (short timed regions)
+            nv, h = self._nvml_handle()
+            names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown",
+                     0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def nvml_loop():
+                while not self._stop.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        act = ["Active" if bits & b else "Not Active" for b in names]
+                        self.rows.append([str(self.index), str(sm), str(mx), "", hex(bits),
+                                          act[0], act[1], act[2], act[3]])
+                    except Exception:
+                        pass
+                    self._stop.wait(0.005)
+            self._t = threading.Thread(target=nvml_loop, daemon=True)
+            self._t.start()
+            self.source = "nvml, every 5 ms"
+            return
+        except Exception:
+            pass
+
         def loop():
             while not self._stop.is_set():
                 try:
@@ -130,7 +167,7 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "sampler": self.source}
 
 
 def cpu_baseline(cfg_name, cfg, steps=1):
