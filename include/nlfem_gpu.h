@@ -194,6 +194,12 @@ int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* d
                              const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
                              nlfem_gpu_session** out, char* err, size_t errlen);
 /* stream: a cudaStream_t (NULL = the legacy default stream). */
+/* Reload a session with new inputs (same meaning as _create), reusing its
+ * streams and device buffers: the workspace of repeated one-shot calls. */
+int nlfem_gpu_session_reset(nlfem_gpu_session* s, const nlfem_gpu_mesh* mesh,
+                            const nlfem_gpu_dofs* dofs, const nlfem_gpu_kernel* kernel,
+                            const nlfem_gpu_poly* f, const nlfem_gpu_poly* g,
+                            const nlfem_gpu_config* cfg, char* err, size_t errlen);
 int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* stats,
                           char* err, size_t errlen);
 int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* err,

@@ -128,6 +128,9 @@ def lib():
     L.nlfem_gpu_session_create.restype = C.c_int
     L.nlfem_gpu_session_create.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
                                            P(_Config), P(vp), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_reset.restype = C.c_int
+    L.nlfem_gpu_session_reset.argtypes = [vp, P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
+                                          P(_Config), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_run.restype = C.c_int
     L.nlfem_gpu_session_run.argtypes = [vp, vp, P(Stats), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_download.restype = C.c_int
@@ -184,7 +187,7 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
-    "nlfem_gpu_session_run", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
+    "nlfem_gpu_session_run", "nlfem_gpu_session_reset", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
     "nlfem_gpu_fp64_peak", "nlfem_gpu_session_run_shard", "nlfem_gpu_session_partials",
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
@@ -413,6 +416,27 @@ class Session:
                                           C.byref(gp), C.byref(cfg), C.byref(self._h), err,
                                           1024), err)
         self.stats = Stats()
+        self._cfg_args = (normalization, int(seed), int(mc_samples), int(device))
+
+    def reset(self, table: ElementTable, problem_terms=None) -> None:
+        """Reload this session with a new element table (and problem), keeping
+        its strategy, kernel, seed and sample count and reusing its device
+        buffers: the workspace of repeated one-shot calls
+        (nlfem_gpu_session_reset)."""
+        normalization, seed, mc_samples, device = self._cfg_args
+        u = self.uterms if problem_terms is None else _check_terms(problem_terms)
+        self.table = table
+        self.uterms = u
+        self.fterms = forcing_terms(self.delta, u, normalization)
+        m, d = table._structs()
+        k = _Kernel(self.C, self.delta)
+        fp, self._fkeep = _poly_struct(self.fterms)
+        gp, self._gkeep = _poly_struct(u)
+        cfg = _Config(STRATEGIES.index(self.strategy), mc_samples, seed & (2**64 - 1), 0, device)
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_reset(self._h, C.byref(m), C.byref(d), C.byref(k),
+                                             C.byref(fp), C.byref(gp), C.byref(cfg), err, 1024),
+               err)
 
     def run(self, stream: int | None = None) -> Stats:
         err = C.create_string_buffer(1024)

@@ -3376,6 +3376,16 @@ int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* d
   return 0;
 }
 
+int nlfem_gpu_session_reset(nlfem_gpu_session* s, const nlfem_gpu_mesh* mesh,
+                            const nlfem_gpu_dofs* dofs, const nlfem_gpu_kernel* kernel,
+                            const nlfem_gpu_poly* f, const nlfem_gpu_poly* g,
+                            const nlfem_gpu_config* cfg, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    s->pairs_installed = false;
+    session_init(*s, mesh, dofs, kernel, f, g, cfg);
+  });
+}
+
 int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* stats, char* err,
                           size_t errlen) {
   return guard(err, errlen,

@@ -128,23 +128,14 @@ def gather_pairs(session, lo: int, hi: int, group=None, device=None) -> int:
 
 
 def assemble_distributed(session, group=None, stream: int | None = None) -> tuple[dict, dict]:
-    """Sharded assembly on this rank's GPU; every rank returns the full system."""
+    """Sharded assembly on this rank's GPU; every rank returns the full system
+    on the host: device_step (partials all-reduced and row blocks all-gathered
+    in HBM over NCCL), then one device-to-host copy of the gathered CSR."""
     import torch
-    import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    lo, hi = shard_range(session.interior_count, rank, world)
-    gather_pairs(session, lo, hi, group)
-    st = session.run_shard(lo, hi, finalize=False, stream=stream)
-    vv, rv = session.partials()
-    V = torch.as_tensor(vv, device="cuda")
-    R = torch.as_tensor(rv, device="cuda")
-    if world > 1:
-        allreduce_partials(V, R, group)
-    torch.cuda.synchronize()
-    r0, r1 = shard_range(session.unknowns, rank, world)
-    session.finalize(r0, r1)
-    block = session.download_rows(r0, r1)
-    full = allgather_csr(block, group, device=torch.device("cuda")) if world > 1 else block
+    (va, ci, rh), st = device_step(session, group, stream)
+    ro = torch.as_tensor(session.outputs()[0], device="cuda")
+    full = {"row_ptr": ro.to(torch.int32).cpu().numpy(), "col_idx": ci.cpu().numpy(),
+            "values": va.cpu().numpy(), "rhs": rh.cpu().numpy()}
     return full, st.as_dict()
 
 
