@@ -552,7 +552,10 @@ struct CandStage {
 //           per-(T,q,T') predicates -- ORs the four 5-bit codes and writes
 //           (T', code) into its survivor slots (code 0 = no piece), in stream
 //           order; k_pairs_compact then keeps the nonzero ones.
-template <int MODE>
+//   WIDE: one outer element per CTA, its staged survivors split over the four
+//         warps in groups of 8 (small ranges, e.g. one rank's shard: four times
+//         the warps per element, a quarter of the per-CTA latency).
+template <int MODE, bool WIDE = false>
 #ifndef NLFEM_PAIRS_MINBLOCKS
 #define NLFEM_PAIRS_MINBLOCKS 6
 #endif
@@ -566,7 +569,8 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
   __shared__ CandStage sg;
   __shared__ int xb[6], scnt[kPairWarps];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int warp = ii_base + blockIdx.x * kPairWarps + wl;  // outer element index
+  // outer element index
+  const int warp = ii_base + (WIDE ? (int)blockIdx.x : (int)blockIdx.x * kPairWarps + wl);
   const bool active = warp < ii_end;
   OuterT o;
   if (active) outer_setup(cD.interior[warp], o);
@@ -609,7 +613,8 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
     int nm = 0;
     for (int base = 0; base < nreg; base += 32) {
       const int k = base + lane;
-      const bool mine = k < nreg && ((sg.pass[k] >> wl) & 1);
+      const bool mine =
+          k < nreg && (WIDE ? (((k >> 3) & (kPairWarps - 1)) == wl) : ((sg.pass[k] >> wl) & 1));
       const unsigned bal = __ballot_sync(FULLMASK, mine);
       if (mine) sg.mine[wl][nm + __popc(bal & ((1u << lane) - 1))] = (short)k;
       nm += __popc(bal);
@@ -661,14 +666,16 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
     // write (T', code) into the survivor slots, in stream order
     for (int t = lane; t < nm; t += 32) {
       const unsigned code = wcode[wl][t];
-      cpartner[out + cnt + t] = sg.id[sg.mine[wl][t]];
-      cinfo[out + cnt + t] = code;
+      // survivor slot: the warp's t-th, or (WIDE) the element's staged index
+      const long long slot = out + cnt + (WIDE ? sg.mine[wl][t] : t);
+      cpartner[slot] = sg.id[sg.mine[wl][t]];
+      cinfo[slot] = code;
 #pragma unroll
       for (int q = 0; q < 4; ++q) items += ((code >> (5 * q)) & 31u) != 0;
       npair += code != 0;
     }
     __syncwarp();
-    cnt += nm;
+    cnt += WIDE ? nreg : nm;
   };
 
   // staging: one block barrier per batch of kPairThreads candidates.  The
@@ -741,7 +748,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
   }
   if (MODE == 0) {
     __syncthreads();
-    if (active && lane == 0) cand_count[warp] = scnt[wl];
+    if (active && lane == 0 && (!WIDE || wl == 0)) cand_count[warp] = scnt[wl];
     return;
   }
   __syncthreads();  // the last batch's staging before the final chunk
@@ -749,6 +756,16 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
   for (int sh = 16; sh > 0; sh >>= 1) {
     items += __shfl_xor_sync(FULLMASK, items, sh);
     npair += __shfl_xor_sync(FULLMASK, npair, sh);
+  }
+  if (WIDE) {  // the element's pair count over its four warps
+    __shared__ int spair;
+    if (threadIdx.x == 0) spair = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&spair, npair);
+    __syncthreads();
+    if (active && threadIdx.x == 0) pair_count[warp] = spair;
+    if (active && lane == 0) atomicAdd(item_count, (unsigned long long)items);
+    return;
   }
   if (active && lane == 0) {
     pair_count[warp] = npair;
@@ -2723,6 +2740,16 @@ void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
 // pair_count[ii], cand_off[ii], pair_off[ii] are indexed absolutely, offsets are
 // relative to the range start (pair_off[lo] = 0); partner / info hold the
 // range's pairs in outer order.  Resets the counters and the BallExitsMesh flag.
+// ranges of at most this many outer elements take the one-element-per-CTA K1
+// (NLFEM_PAIRS_WIDE_MAX overrides)
+int pairs_wide_max() {
+  static const int v = [] {
+    const char* e = std::getenv("NLFEM_PAIRS_WIDE_MAX");
+    return e ? std::atoi(e) : 1024;
+  }();
+  return v;
+}
+
 void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
   cudaStream_t st = S.stream;
   const int KI = S.KI;
@@ -2766,9 +2793,14 @@ void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
     S.cpartner.ensure(nc + 1);
     S.cinfo.ensure(nc + 1);
     if (n > 0) {
-      k_pairs<1><<<nblk((long long)n, kPairWarps), kPairThreads, 0, st>>>(
-          lo, hi, S.cand_off.p, 0, nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p, S.counters.p,
-          S.err_elem.p);
+      if (n <= pairs_wide_max())
+        k_pairs<1, true><<<n, kPairThreads, 0, st>>>(lo, hi, S.cand_off.p, 0, nullptr,
+                                                     S.cpartner.p, S.cinfo.p, S.pair_count.p,
+                                                     S.counters.p, S.err_elem.p);
+      else
+        k_pairs<1><<<nblk((long long)n, kPairWarps), kPairThreads, 0, st>>>(
+            lo, hi, S.cand_off.p, 0, nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
+            S.counters.p, S.err_elem.p);
       scan64(S, S.pair_count.p + lo, true, n, S.pair_off.p + lo, st);
       k_pairs_compact<<<nblk((long long)n * 32, 256), 256, 0, st>>>(
           lo, hi, S.cand_off.p, 0, S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p, S.info.p);
