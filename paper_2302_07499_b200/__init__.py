@@ -309,10 +309,18 @@ class ElementTable:
         return self.coords.shape[0]
 
     def _structs(self):
+        # cached per set of array objects (repeated one-shot calls on one table)
+        arrs = (self.coords, self.verts, self.neighbor, self.center, self.radius, self.volume,
+                self.diam, self.region, self.inv_edges, self.dof_of_node)
+        key = tuple(id(a) for a in arrs) + (self.node_count, self.elem_count, self.unknowns)
+        cached = getattr(self, "_structs_cache", None)
+        if cached is not None and cached[0] == key:
+            return cached[1], cached[2]
         m = _Mesh(self.node_count, self.elem_count, _p(self.coords), _p(self.verts),
                   _p(self.neighbor), _p(self.center), _p(self.radius), _p(self.volume),
                   _p(self.diam), _p(self.region), _p(self.inv_edges))
         d = _Dofs(self.node_count, self.unknowns, _p(self.dof_of_node))
+        self._structs_cache = (key, m, d)
         return m, d
 
     def nbytes(self) -> int:
@@ -648,6 +656,25 @@ def _take_csr(csr) -> dict:
     }
 
 
+_PROBLEMS: dict = {}
+
+
+def _problem(delta: float, normalization: str, problem_terms):
+    """(kernel constant, normalised u terms, forcing terms), memoised for
+    repeated one-shot calls with the same problem."""
+    pt = None if problem_terms is None else np.asarray(problem_terms, np.float64)
+    key = (delta, normalization, None if pt is None else (pt.shape, pt.tobytes()))
+    hit = _PROBLEMS.get(key)
+    if hit is None:
+        Cn = kernel_constant(delta, normalization)
+        u = default_problem_terms() if pt is None else _check_terms(pt)
+        hit = (Cn, u, forcing_terms(delta, u, normalization))
+        if len(_PROBLEMS) > 64:
+            _PROBLEMS.clear()
+        _PROBLEMS[key] = hit
+    return hit
+
+
 def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
              normalization: str = "mass", problem_terms=None, seed: int = 0x5EED,
              mc_samples: int = 200, device: int = -1, f_terms=None,
@@ -660,9 +687,7 @@ def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
     if strategy not in STRATEGIES:
         raise NlfemError(8, f"BadConfig: unknown strategy '{strategy}'")
     L = lib()
-    Cn = kernel_constant(delta, normalization)
-    u = default_problem_terms() if problem_terms is None else _check_terms(problem_terms)
-    f = forcing_terms(delta, u, normalization)
+    Cn, u, f = _problem(float(delta), normalization, problem_terms)
     if f_terms is not None:
         f = np.asarray(f_terms, np.float64).reshape(-1, 4)
     if g_terms is not None:

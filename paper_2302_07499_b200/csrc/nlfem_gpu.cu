@@ -2445,8 +2445,25 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   double volsum = 0;
   S.h_interior.clear();
+  // std::pow (the reference's expression, kept for bit-identical floors) is
+  // memoised per distinct diameter: lattice meshes have a handful of shapes
+  struct PowMemo {
+    uint64_t key[256];
+    double val[256];
+  } memo;
+  std::memset(memo.key, 0xff, sizeof(memo.key));  // NaN pattern: never a diameter
   for (int t = 0; t < S.K; ++t) {
-    tau[t] = 1e-14 * std::pow(m->diam[t], 3);
+    {
+      const double dm = m->diam[t];
+      uint64_t b;
+      std::memcpy(&b, &dm, 8);
+      const unsigned h = (unsigned)((b * 0x9E3779B97F4A7C15ull) >> 56);
+      if (memo.key[h] != b) {
+        memo.key[h] = b;
+        memo.val[h] = 1e-14 * std::pow(dm, 3);
+      }
+      tau[t] = memo.val[h];
+    }
     rmax = std::max(rmax, m->radius[t]);
     dmax = std::max(dmax, m->diam[t]);
     volsum += m->volume[t];
