@@ -125,6 +125,8 @@ struct Dev {
   // fixed point
   const double* scale;
   const double* iscale;
+  const double4* escale;      // [K] fixed-point scales of the element's 4 nodes
+  const unsigned char* econ;  // [K] bit k: node k of the element is constrained
   Poly f, g;
   unsigned long long* flags;  // counter 7: approxcaps hull face-table overflow
 };
@@ -273,6 +275,17 @@ __global__ void k_scales(int J, const int* acnt, const unsigned long long* avmax
 
 
 // ---------------------------------------------------------------------------
+// per element: the scales and constrained flags of its four nodes, so the
+// combine reads them with the partner id (one gather level instead of two)
+__global__ void k_elem_scales(int K, const double* scale, double4* escale, unsigned char* econ) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K) return;
+  const int4 w = cD.verts[t];
+  escale[t] = make_double4(scale[w.x], scale[w.y], scale[w.z], scale[w.w]);
+  econ[t] = (unsigned char)((cD.dof[w.x] < 0) | ((cD.dof[w.y] < 0) << 1) |
+                            ((cD.dof[w.z] < 0) << 2) | ((cD.dof[w.w] < 0) << 3));
+}
+
 // K1: element pairs
 
 // Class codes (5 bits per quadrature point): 0 none, 1 whole element,
@@ -2010,8 +2023,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     if (!constr) {
       const int4 wP = cD.verts[Tp];
       const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
-      const bool conP[4] = {cD.dof[NP[0]] < 0, cD.dof[NP[1]] < 0, cD.dof[NP[2]] < 0,
-                            cD.dof[NP[3]] < 0};
+      const double4 esc = cD.escale[Tp];
+      const double scP[4] = {esc.x, esc.y, esc.z, esc.w};
+      const unsigned cm = cD.econ[Tp];
+      const bool conP[4] = {(cm & 1u) != 0, (cm & 2u) != 0, (cm & 4u) != 0, (cm & 8u) != 0};
       // T x T' cross block -C w X[a][b] at (N_a, M_b): shared-memory rows
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -2031,7 +2046,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
         for (int cc = b; cc < 4; ++cc) {
           const int k = s2i(b, cc);
-          red_fixed_sel(V, es[k], C * wq * S2[k], cD.scale[min(NP[b], NP[cc])],
+          red_fixed_sel(V, es[k], C * wq * S2[k], NP[b] <= NP[cc] ? scP[b] : scP[cc],
                         conP[b] || conP[cc]);
         }
     }
@@ -2270,6 +2285,8 @@ struct nlfem_gpu_session {
   DBuf<long long> cell_start64, ni_off64, scan_tmp, scan_tmp2;
   DBuf<int> cell_start, ni_off;
   DBuf<double> scale, iscale;
+  DBuf<double4> escale;
+  DBuf<unsigned char> econ;
   // pairs
   DBuf<int> pair_count, partner, err_elem, ovf, cand_count, cpartner;
   DBuf<long long> cand_off;
@@ -2614,6 +2631,10 @@ void run_prep(nlfem_gpu_session& S) {
   D.ni_el = S.ni_el.p;
   D.scale = S.scale.p;
   D.iscale = S.iscale.p;
+  S.escale.ensure(std::max(K, 1));
+  S.econ.ensure(std::max(K, 1));
+  D.escale = S.escale.p;
+  D.econ = S.econ.p;
   CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
   // fixed-point bound per row: every contribution to
   // row i is bounded by C |B(delta + 3 rmax)| times the volume of the elements
@@ -2621,7 +2642,8 @@ void run_prep(nlfem_gpu_session& S) {
   const double rr = D.delta + 3 * D.rmax;
   const double cbound = 6.0 * D.C * (4.0 / 3.0 * M_PI * rr * rr * rr);
   k_scales<<<nblk(J, 256), 256, 0, st>>>(J, S.ai_cnt.p, S.ai_vmax.p, cbound, S.scale.p, S.iscale.p);
-  ++S.launches;
+  if (K > 0) k_elem_scales<<<nblk(K, 256), 256, 0, st>>>(K, S.scale.p, S.escale.p, S.econ.p);
+  S.launches += 2;
 }
 
 void run_finalize(nlfem_gpu_session& S, int r0, int r1) {
