@@ -271,6 +271,12 @@ int nlfem_gpu_session_solve(nlfem_gpu_session* s, double tol, int32_t max_iter,
  * call with NULL buffers. */
 int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* outer_offsets,
                             int32_t* partner, uint32_t* info, char* err, size_t errlen);
+/* The same element-pair list in place in device memory (valid until the
+ * session's next run): outer offsets int64 [interior + 1], partner ids int32
+ * and class codes uint32 [npairs]. */
+int nlfem_gpu_session_pairs_device(nlfem_gpu_session* s, int64_t* npairs,
+                                   const int64_t** outer_offsets, const int32_t** partner,
+                                   const uint32_t** info);
 /* Kernel launches of the last run (for the bench's gpu_launches key). */
 int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s);
 void nlfem_gpu_session_destroy(nlfem_gpu_session* s);

@@ -165,6 +165,8 @@ def lib():
     L.nlfem_gpu_session_outputs.argtypes = [vp, P(vp), P(vp), P(vp), P(vp), P(i32), P(i64)]
     L.nlfem_gpu_session_pairs.restype = C.c_int
     L.nlfem_gpu_session_pairs.argtypes = [vp, P(i64), vp, vp, vp, C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_pairs_device.restype = C.c_int
+    L.nlfem_gpu_session_pairs_device.argtypes = [vp, P(i64), P(vp), P(vp), P(vp)]
     L.nlfem_gpu_session_launches.restype = i64
     L.nlfem_gpu_session_launches.argtypes = [vp]
     L.nlfem_gpu_session_destroy.argtypes = [vp]
@@ -189,6 +191,7 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
     "nlfem_gpu_session_run", "nlfem_gpu_session_reset", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
+    "nlfem_gpu_session_pairs_device",
     "nlfem_gpu_fp64_peak", "nlfem_gpu_session_run_shard", "nlfem_gpu_session_partials",
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
     "nlfem_gpu_session_outputs", "nlfem_gpu_session_pairs_shard",
@@ -594,6 +597,18 @@ class Session:
         _check(L.nlfem_gpu_session_pairs(self._h, C.byref(n), _p(off), _p(partner), _p(info),
                                          err, 512), err)
         return {"offsets": off, "partner": partner[:n.value], "info": info[:n.value],
+                "interior": np.nonzero(self.table.region == 0)[0].astype(np.int32)}
+
+    def pairs_device(self) -> dict:
+        """The element-pair list of the last run as device views (no copy):
+        offsets int64 [interior + 1], partner int32 and info uint32 [npairs]."""
+        n, o, pt, inf = C.c_int64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        lib().nlfem_gpu_session_pairs_device(self._h, C.byref(n), C.byref(o), C.byref(pt),
+                                             C.byref(inf))
+        ki = self.interior_count
+        return {"offsets": _CudaView(o.value or 0, ki + 1, "<i8"),
+                "partner": _CudaView(pt.value or 0, n.value, "<i4"),
+                "info": _CudaView(inf.value or 0, n.value, "<u4"),
                 "interior": np.nonzero(self.table.region == 0)[0].astype(np.int32)}
 
     def launches(self) -> int:

@@ -3648,6 +3648,16 @@ int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* e
   });
 }
 
+int nlfem_gpu_session_pairs_device(nlfem_gpu_session* s, int64_t* npairs,
+                                   const int64_t** outer_offsets, const int32_t** partner,
+                                   const uint32_t** info) {
+  *npairs = s->npairs;
+  *outer_offsets = reinterpret_cast<const int64_t*>(s->pair_off.p);
+  *partner = s->partner.p;
+  *info = s->info.p;
+  return 0;
+}
+
 int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* outer_offsets,
                             int32_t* partner, uint32_t* info, char* err, size_t errlen) {
   return guard(err, errlen, [&] {

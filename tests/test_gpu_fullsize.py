@@ -93,41 +93,53 @@ def test_full_size_constant_solution(full):
     s.close()
 
 
-def _sampled_gpu_sets(pairs, sample):
-    off, partner, info, interior = pairs["offsets"], pairs["partner"], pairs["info"], pairs["interior"]
-    pos = {int(T): ii for ii, T in enumerate(interior)}
+def _sampled_gpu_sets(s, sample):
+    """{(T, q): {(parent, kind)}} for the sampled outer elements, gathered from
+    the device pair list (no full download)."""
+    pd = s.pairs_device()
+    off = _dev(pd["offsets"])
+    pos = {int(T): ii for ii, T in enumerate(pd["interior"])}
+    part, info = _dev(pd["partner"]), _dev(pd["info"])
     out = {}
     for T in sample:
         ii = pos[int(T)]
-        for p in range(off[ii], off[ii + 1]):
+        a, b = int(off[ii]), int(off[ii + 1])
+        ps = part[a:b].cpu().numpy()
+        cs = info[a:b].cpu().numpy()
+        for tp, code in zip(ps, cs):
             for q in range(4):
-                c = (int(info[p]) >> (5 * q)) & 31
+                c = (int(code) >> (5 * q)) & 31
                 if c:
-                    out.setdefault((int(T), q), set()).add((int(partner[p]), "W" if c == 1 else "P"))
+                    out.setdefault((int(T), q), set()).add((int(tp), "W" if c == 1 else "P"))
     return out
 
 
-@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
-@pytest.mark.parametrize("res,strat", [(24, "nocaps"), (24, "fullcaps"), (24, "approxcaps")])
-def test_config3_sets_sample_against_reference_walk(res, strat):
-    # config-3 geometry (jittered, delta = 3h); sets of 64 seeded outer elements
-    delta = 3.0 / res
-    m = P.generate_mesh(3, res, delta, jitter_seed=7)
-    t = P.ElementTable(m["coords"], m["cells"], m["region"], device=0)
-    s = P.Session(t, delta, strat, "moment2", U2, seed=SEED, mc_samples=16, device=0)
-    s.run()
-    pairs = s.pairs()
-    s.close()
-    interior = pairs["interior"]
-    sample = np.random.default_rng(11).choice(interior, size=64, replace=False)
-    got = _sampled_gpu_sets(pairs, sample)
+def _reference_sets(m, sample, delta, strat):
     R = ref.Problem(m["coords"], m["cells"], m["region"])
     rows = []
     for T in sample:
         for q in range(4):
             par, kind = R.walk_pieces(int(T), q, delta, strat)
             rows += [(int(T), q, int(a), int(b)) for a, b in zip(par, kind)]
-    want = walk_sets(np.array(rows, np.int64))
+    return walk_sets(np.array(rows, np.int64))
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("res,strat,nsample", [(24, "nocaps", 64), (24, "fullcaps", 64),
+                                               (24, "approxcaps", 64), (48, "fullcaps", 128)])
+def test_config3_sets_sample_against_reference_walk(res, strat, nsample):
+    # config-3 geometry (jittered, delta = 3h; N=48 is C3 itself): the sets of
+    # seeded outer elements against the reference's walk_ball
+    delta = 3.0 / res
+    m = P.generate_mesh(3, res, delta, jitter_seed=7)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"], device=0)
+    s = P.Session(t, delta, strat, "moment2", U2, seed=SEED, mc_samples=16, device=0)
+    s.run()
+    interior = np.nonzero(t.region == 0)[0]
+    sample = np.random.default_rng(11).choice(interior, size=nsample, replace=False)
+    got = _sampled_gpu_sets(s, sample)
+    s.close()
+    want = _reference_sets(m, sample, delta, strat)
     assert len(want) > 0
     for key in set(want) | set(got):
         assert got.get(key, set()) == want.get(key, set()), (res, strat, key)
