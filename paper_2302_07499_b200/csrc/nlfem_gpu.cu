@@ -3341,8 +3341,8 @@ void session_solve(nlfem_gpu_session& S, double tol, int32_t max_iter, const nlf
   if (S.nnz_out < 0 || !S.values.p)
     throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: solve needs an assembled system (run first)"};
   CK(cudaSetDevice(S.device));
-  static bool rule_set = false;  // per process; the rule is a constant
-  if (!rule_set) {
+  static std::atomic<unsigned long long> rule_set{0};  // bit d: uploaded to device d
+  if (!(rule_set.load() >> (S.device & 63) & 1ull)) {
     const double a = 0.3108859192633005, wa = 0.1126879257180162;
     const double b = 0.0927352503108912, wb = 0.0734930431163619;
     const double c = 0.0455037041256497, d = 0.5 - c, wc = 0.0425460207770812;
@@ -3353,7 +3353,7 @@ void session_solve(nlfem_gpu_session& S, double tol, int32_t max_iter, const nlf
                                 {c, d, c, d, wc}, {c, d, d, c, wc}, {d, c, c, d, wc},
                                 {d, c, d, c, wc}, {d, d, c, c, wc}};
     CK(cudaMemcpyToSymbol(cL2Rule, rows, sizeof(rows)));
-    rule_set = true;
+    rule_set.fetch_or(1ull << (S.device & 63));
   }
   Poly ex, g;
   poly_to_dev(exact, ex);
