@@ -431,6 +431,9 @@ __device__ __noinline__ bool facet_too_close(const Vd* v, int4 nb, Vd xq) {
 // exact geometric evaluation (classify_deferred), so a warp can queue those and
 // work them with all lanes.
 constexpr unsigned kDefer = 0x80u;
+// STRAT: the strategy as a compile-time constant (k_pairs is instantiated per
+// strategy, so each instance carries only its own decision code)
+template <int STRAT>
 __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, const Vd v[4],
                                                    double cert2, double vol, double tau) {
   const double delta = cD.delta;
@@ -446,7 +449,7 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
     gap = sqrt(g2);
     if (gap >= rad + delta) return kNone;
   }
-  if (cD.strategy == NLFEM_STRATEGY_OVERLAP) {
+  if (STRAT == NLFEM_STRATEGY_OVERLAP) {
     // gap + rad < delta || distance_point_simplex(x_q, T') < delta
     const double t2 = delta - rad;
     if (t2 > 0) {
@@ -465,7 +468,7 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
       if (vnorm2(vsub(v[i], xq)) < c2) return kWhole;
     return kDefer;
   }
-  if (cD.strategy == NLFEM_STRATEGY_BARYCENTER) {
+  if (STRAT == NLFEM_STRATEGY_BARYCENTER) {
     if (g2 < delta * delta * (1.0 - 1e-12)) return kWhole;
     if (g2 >= delta * delta * (1.0 + 1e-12)) return kNone;
     if (gap < 0) gap = sqrt(g2);
@@ -493,15 +496,15 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
     }
   }
   if (mask == 15) return kWhole;
-  if (cD.strategy == NLFEM_STRATEGY_INSIDE) return kNone;  // straddlers dropped
+  if (STRAT == NLFEM_STRATEGY_INSIDE) return kNone;  // straddlers dropped
   if (mask == 0) {
-    if (cD.strategy != NLFEM_STRATEGY_FULLCAPS) return kNone;
+    if (STRAT != NLFEM_STRATEGY_FULLCAPS) return kNone;
     // the barycenter lies in T': gap < delta (with margin) certifies that the
     // computed distance_point_simplex is < delta; otherwise evaluate it
     if (g2 < delta * delta * (1.0 - 1e-11)) return kOutCap;
     return kDefer;
   }
-  if (cD.strategy == NLFEM_STRATEGY_NOCAPS || cD.strategy == NLFEM_STRATEGY_APPROXCAPS) {
+  if (STRAT == NLFEM_STRATEGY_NOCAPS || STRAT == NLFEM_STRATEGY_APPROXCAPS) {
     // (approxcaps: the hull contains the nocaps polytope, whose certified
     // volume > 64 tau exceeds its <= 16 fan pieces x tau)
 #pragma unroll
@@ -513,14 +516,15 @@ __device__ __forceinline__ unsigned classify_cheap(Vd xq, Vd cen, double rad, co
   return kDefer | mask;
 }
 
+template <int STRAT>
 __device__ __forceinline__ unsigned classify_deferred(Vd xq, const Vd v[4], int mask, double tau) {
   if (mask == 0)
     return outside_cap_hits(xq, v, cD.delta)
-               ? (cD.strategy == NLFEM_STRATEGY_OVERLAP ? kWhole : kOutCap)
+               ? (STRAT == NLFEM_STRATEGY_OVERLAP ? kWhole : kOutCap)
                : kNone;
-  if (cD.strategy == NLFEM_STRATEGY_NOCAPS)
+  if (STRAT == NLFEM_STRATEGY_NOCAPS)
     return inner_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
-  if (cD.strategy == NLFEM_STRATEGY_APPROXCAPS)
+  if (STRAT == NLFEM_STRATEGY_APPROXCAPS)
     return approx_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
   return any_pieces_exact(v, mask, xq, tau) ? (kStraddle | mask) : kNone;
 }
@@ -568,7 +572,7 @@ struct CandStage {
 //   WIDE: one outer element per CTA, its staged survivors split over the four
 //         warps in groups of 8 (small ranges, e.g. one rank's shard: four times
 //         the warps per element, a quarter of the per-CTA latency).
-template <int MODE, bool WIDE = false>
+template <int MODE, bool WIDE = false, int STRAT = NLFEM_STRATEGY_FULLCAPS>
 #ifndef NLFEM_PAIRS_MINBLOCKS
 #define NLFEM_PAIRS_MINBLOCKS 6
 #endif
@@ -644,7 +648,8 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
         const Vd cp = {a.x, a.y, a.z};
         const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
         const Vd xq = quad_point(o.v, q);
-        const unsigned c = classify_cheap(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]);
+        const unsigned c =
+            classify_cheap<STRAT>(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]);
         if (c & kDefer) ent = 16u | (c & 15u);
         else code = c << (5 * q);
         if (sg.bnd[k]) ent |= 32u;
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
       const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
       const Vd xq = quad_point(o.v, q);
       if (ent & 16u) {
-        const unsigned c = classify_deferred(xq, v, (int)(ent & 15u), sg.tau[k]);
+        const unsigned c = classify_deferred<STRAT>(xq, v, (int)(ent & 15u), sg.tau[k]);
         if (c) atomicOr(&wcode[wl][t], c << (5 * q));
       }
       if (ent & 32u) {
@@ -2779,6 +2784,30 @@ void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
 // pair_count[ii], cand_off[ii], pair_off[ii] are indexed absolutely, offsets are
 // relative to the range start (pair_off[lo] = 0); partner / info hold the
 // range's pairs in outer order.  Resets the counters and the BallExitsMesh flag.
+// K1 classification pass, instantiated per strategy (and WIDE)
+template <bool WIDE>
+void launch_pairs1(int strategy, unsigned grid, cudaStream_t st, int lo, int hi,
+                   const long long* cand_off, long long cand_base, int* cpartner, unsigned* cinfo,
+                   int* pair_count, unsigned long long* counters, int* err_elem) {
+#define NLFEM_K1_CASE(ST)                                                                     \
+  case ST:                                                                                    \
+    k_pairs<1, WIDE, ST><<<grid, kPairThreads, 0, st>>>(lo, hi, cand_off, cand_base, nullptr, \
+                                                        cpartner, cinfo, pair_count, counters, \
+                                                        err_elem);                            \
+    break;
+  switch (strategy) {
+    NLFEM_K1_CASE(NLFEM_STRATEGY_INSIDE)
+    NLFEM_K1_CASE(NLFEM_STRATEGY_OVERLAP)
+    NLFEM_K1_CASE(NLFEM_STRATEGY_BARYCENTER)
+    NLFEM_K1_CASE(NLFEM_STRATEGY_NOCAPS)
+    NLFEM_K1_CASE(NLFEM_STRATEGY_APPROXCAPS)
+    NLFEM_K1_CASE(NLFEM_STRATEGY_FULLCAPS)
+    default:
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown strategy"};
+  }
+#undef NLFEM_K1_CASE
+}
+
 // ranges of at most this many outer elements take the one-element-per-CTA K1
 // (NLFEM_PAIRS_WIDE_MAX overrides)
 int pairs_wide_max() {
@@ -2833,13 +2862,12 @@ void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
     S.cinfo.ensure(nc + 1);
     if (n > 0) {
       if (n <= pairs_wide_max())
-        k_pairs<1, true><<<n, kPairThreads, 0, st>>>(lo, hi, S.cand_off.p, 0, nullptr,
-                                                     S.cpartner.p, S.cinfo.p, S.pair_count.p,
-                                                     S.counters.p, S.err_elem.p);
+        launch_pairs1<true>(S.dev.strategy, (unsigned)n, st, lo, hi, S.cand_off.p, 0,
+                            S.cpartner.p, S.cinfo.p, S.pair_count.p, S.counters.p, S.err_elem.p);
       else
-        k_pairs<1><<<nblk((long long)n, kPairWarps), kPairThreads, 0, st>>>(
-            lo, hi, S.cand_off.p, 0, nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
-            S.counters.p, S.err_elem.p);
+        launch_pairs1<false>(S.dev.strategy, (unsigned)nblk((long long)n, kPairWarps), st, lo, hi,
+                             S.cand_off.p, 0, S.cpartner.p, S.cinfo.p, S.pair_count.p,
+                             S.counters.p, S.err_elem.p);
       scan64(S, S.pair_count.p + lo, true, n, S.pair_off.p + lo, st);
       k_pairs_compact<<<nblk((long long)n * 32, 256), 256, 0, st>>>(
           lo, hi, S.cand_off.p, 0, S.cpartner.p, S.cinfo.p, S.pair_off.p, S.partner.p, S.info.p);
@@ -2859,9 +2887,9 @@ void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
       const long long nc = coff(c1) - coff(c0);
       S.cpartner.ensure(nc + 1);
       S.cinfo.ensure(nc + 1);
-      k_pairs<1><<<nblk((long long)(c1 - c0), kPairWarps), kPairThreads, 0, st>>>(
-          c0, c1, S.cand_off.p, coff(c0), nullptr, S.cpartner.p, S.cinfo.p, S.pair_count.p,
-          S.counters.p, S.err_elem.p);
+      launch_pairs1<false>(S.dev.strategy, (unsigned)nblk((long long)(c1 - c0), kPairWarps), st,
+                           c0, c1, S.cand_off.p, coff(c0), S.cpartner.p, S.cinfo.p,
+                           S.pair_count.p, S.counters.p, S.err_elem.p);
       ++S.launches;
       // pair offsets of this chunk continue the running total
       scan64(S, S.pair_count.p + c0, true, c1 - c0, S.pair_off.p + c0, st);
