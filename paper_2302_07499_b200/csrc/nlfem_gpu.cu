@@ -2956,6 +2956,9 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     CK(cudaEventRecord(S.ev[1], st));
     build_pairs(S, 0, KI);
   } else {
+    // the device parameter block is per device, not per session: rebind this
+    // session's (another session may have run since its pairs were built)
+    CK(cudaMemcpyToSymbolAsync(cD, &D, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(S.ev[1], st));
     S.pairs_installed = false;  // one run per installation
   }
@@ -3614,6 +3617,7 @@ int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_l
       CK(cudaEventRecord(s->ev[7], user));
       CK(cudaStreamWaitEvent(s->stream, s->ev[7], 0));
     }
+    CK(cudaMemcpyToSymbolAsync(cD, &s->dev, sizeof(Dev), 0, cudaMemcpyHostToDevice, s->stream));
     run_finalize(*s, std::max(0, row_lo), std::min(row_hi, s->unknowns));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s->stream));

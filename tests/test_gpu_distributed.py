@@ -118,3 +118,31 @@ def test_sharded_pairs_sum_to_single_gpu_bitwise(strat, mc, nshard):
     got = s0.download_rows(0, s0.unknowns)
     for k in ("row_ptr", "col_idx", "values", "rhs"):
         assert np.array_equal(got[k], want[k]), (strat, k)
+
+
+def test_interleaved_sessions_on_one_device():
+    # the device parameter block is per device: a session whose pairs were
+    # built before another session ran must rebind its own state for
+    # run_shard / finalize (different meshes, so a stale binding would show)
+    import torch
+    mA = P.generate_mesh(3, 5, 0.34, jitter_seed=3)
+    tA = P.ElementTable(mA["coords"], mA["cells"], mA["region"])
+    mB = P.generate_mesh(3, 6, 0.3)
+    tB = P.ElementTable(mB["coords"], mB["cells"], mB["region"])
+    a = P.Session(tA, 0.34, "fullcaps", "moment2", U2, seed=SEED, mc_samples=8)
+    a.run()
+    want = a.download()
+    b = P.Session(tB, 0.3, "nocaps", "moment2", U2, seed=SEED)
+    KI = a.interior_count
+    n = a.pairs_shard(0, KI)
+    cv, pv = a.pairs_shard_out()
+    counts = torch.as_tensor(cv, device="cuda").clone()
+    partners = torch.as_tensor(pv, device="cuda").clone()
+    b.run()                      # another session binds its state in between
+    a.pairs_install(counts, partners, n)
+    a.run_shard(0, KI)
+    b.run()
+    a.finalize(0, a.unknowns)
+    got = a.download_rows(0, a.unknowns)
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(got[k], want[k]), k
