@@ -2096,6 +2096,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
   }
 }
 
+
 // ---------------------------------------------------------------------------
 // K6: fixed point -> CSR values, constraint folding
 
@@ -2303,10 +2304,14 @@ struct nlfem_gpu_session {
   DBuf<int> rlen, rcols, tcnt, tcols, slen, scols, olen, ocols;
   DBuf<long long> roff, toff, soff, mirror, eslot, ooff, omap;
   // Monte Carlo units (per chunk)
-  DBuf<int> ucount, pair_outer, upair, ulist, nlist;
-  DBuf<long long> uoff;
-  DBuf<unsigned char> uqs;
-  DBuf<double> mom;
+  // two sets, alternating by chunk: the combine of chunk c (on stream4) reads
+  // set c & 1 while the units of chunk c + 1 fill the other
+  struct UnitBufs {
+    DBuf<int> ucount, pair_outer, upair, ulist, nlist;
+    DBuf<long long> uoff;
+    DBuf<unsigned char> uqs;
+    DBuf<double> mom;
+  } ub[2];
   float mc_ms = 0;
   int g_deg = 0;  // total degree of g
   // values
@@ -2334,8 +2339,11 @@ struct nlfem_gpu_session {
   // Gauss units and the one-piece Monte Carlo lists run on stream3, beside the
   // three-piece Monte Carlo lists on `stream`
   cudaStream_t stream3 = nullptr;
+  // the combine runs on stream4, overlapping the next chunk's units
+  cudaStream_t stream4 = nullptr;
   std::vector<cudaEvent_t> ev;  // 0..7 phases on stream; 8, 9 pattern on stream2; 10, 11 fork/join;
-                                // 12, 13 solve
+                                // 12, 13 solve; 14..21 per unit-buffer set: units start / end,
+                                // combine ready, combine done (kEvUnits0 + 4 set + k)
   DBuf<double> solx, nodev, study_tmp;  // solve: x, node values, reduction scratch
 };
 
@@ -2449,7 +2457,8 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&S.stream2, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithFlags(&S.stream3, cudaStreamNonBlocking));
-    for (int i = 0; i < 14; ++i) {
+    CK(cudaStreamCreateWithFlags(&S.stream4, cudaStreamNonBlocking));
+    for (int i = 0; i < 24; ++i) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       S.ev.push_back(e);
@@ -2808,6 +2817,16 @@ void launch_pairs1(int strategy, unsigned grid, cudaStream_t st, int lo, int hi,
 #undef NLFEM_K1_CASE
 }
 
+// element pairs per units / combine chunk (bounds the unit buffers; two sets
+// are alive at a time).  NLFEM_PAIRS_PER_CHUNK overrides (tests use tiny chunks).
+long long pairs_per_chunk() {
+  static const long long v = [] {
+    const char* e = std::getenv("NLFEM_PAIRS_PER_CHUNK");
+    return e ? std::max(1LL, std::atoll(e)) : (8LL << 20);
+  }();
+  return v;
+}
+
 // ranges of at most this many outer elements take the one-element-per-CTA K1
 // (NLFEM_PAIRS_WIDE_MAX overrides)
 int pairs_wide_max() {
@@ -3039,7 +3058,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   // chunk needs no host round trip when its first pair and a bound on its
   // pairs are known on the host: a full run (pairs <= K1 survivors) or a
   // sharded run on installed pairs (offset and count from the install).
-  const long long kPairsPerChunk = need_units ? (8LL << 20) : (1LL << 40);
+  const long long kPairsPerChunk = need_units ? pairs_per_chunk() : (1LL << 40);
   const bool full_run = !installed && shard_lo == 0 && shard_hi == KI;
   const bool own_range = installed && shard_lo == S.pairs_lo && shard_hi == S.pairs_hi;
   const bool fast = (full_run && S.survivors <= kPairsPerChunk) ||
@@ -3058,8 +3077,21 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
                      std::to_string(err_elem_h)};
     S.npairs = poff[KI];
   }
+  // events of unit-buffer set k: units start / end, combine ready / done
+  auto evu = [&](int set, int k) { return S.ev[14 + 4 * set + k]; };
+  bool set_busy[2] = {false, false};   // a combine may still read the set
+  bool set_timed[2] = {false, false};  // units events not yet accumulated
+  auto collect = [&](int set) {        // Monte Carlo phase time of the set's last chunk
+    if (!set_timed[set]) return;
+    CK(cudaEventSynchronize(evu(set, 1)));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, evu(set, 0), evu(set, 1)));
+    mc_ms += ms;
+    set_timed[set] = false;
+  };
   if (shard_hi > shard_lo) {
     int ii0 = shard_lo;
+    int chunk = 0;
     while (ii0 < shard_hi) {
       int ii1;
       long long P0, np;
@@ -3074,30 +3106,36 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         P0 = poff[ii0];
         np = poff[ii1] - P0;
       }
+      const int set = chunk & 1;
+      auto& U = S.ub[set];
+      if (set_busy[set]) {  // the combine of chunk - 2 still reads this set
+        CK(cudaStreamWaitEvent(st, evu(set, 3), 0));
+        collect(set);
+      }
       const long long* pend = S.pair_off.p + ii1;  // the chunk's actual pair end
       long long nitems = 0;
       if (need_units) {
-        S.ucount.ensure(np + 1);
-        S.uoff.ensure(np + 1);
-        S.pair_outer.ensure(np + 1);
-        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, pend, S.info.p, S.ucount.p);
+        U.ucount.ensure(np + 1);
+        U.uoff.ensure(np + 1);
+        U.pair_outer.ensure(np + 1);
+        k_units_count<<<nblk(np, 256), 256, 0, st>>>(P0, np, pend, S.info.p, U.ucount.p);
         k_pair_outer<<<nblk(32LL * (ii1 - ii0), 256), 256, 0, st>>>(ii0, ii1, S.pair_off.p, P0,
-                                                                    S.pair_outer.p);
+                                                                    U.pair_outer.p);
         S.launches += 2;
-        S.nlist.ensure(16);  // 8 list lengths, 8 work cursors
-        CK(cudaMemsetAsync(S.nlist.p, 0, 16 * sizeof(int), st));
-        scan64(S, S.ucount.p, true, np, S.uoff.p, st);
+        U.nlist.ensure(16);  // 8 list lengths, 8 work cursors
+        CK(cudaMemsetAsync(U.nlist.p, 0, 16 * sizeof(int), st));
+        scan64(S, U.ucount.p, true, np, U.uoff.p, st);
         // buffers by the upper bound (4 items per pair): no count read-back
         nitems = 4 * np;
-        S.upair.ensure(nitems + 1);
-        S.uqs.ensure(nitems + 1);
-        S.mom.ensure(kMomStride * (size_t)(nitems + 1));
-        S.ulist.ensure(8 * (size_t)(nitems + 1));
+        U.upair.ensure(nitems + 1);
+        U.uqs.ensure(nitems + 1);
+        U.mom.ensure(kMomStride * (size_t)(nitems + 1));
+        U.ulist.ensure(8 * (size_t)(nitems + 1));
         k_units_fill<<<nblk(np, kFillThreads), kFillThreads, 0, st>>>(
-            P0, np, pend, S.info.p, S.uoff.p, S.upair.p, S.uqs.p, S.partner.p, S.ulist.p,
-            nitems + 1, S.nlist.p);
+            P0, np, pend, S.info.p, U.uoff.p, U.upair.p, U.uqs.p, S.partner.p, U.ulist.p,
+            nitems + 1, U.nlist.p);
         ++S.launches;
-        CK(cudaEventRecord(S.ev[6], st));
+        CK(cudaEventRecord(evu(set, 0), st));
         cudaStream_t s3 = S.stream3;
         CK(cudaEventRecord(S.ev[10], st));  // fork
         CK(cudaStreamWaitEvent(s3, S.ev[10], 0));
@@ -3114,14 +3152,14 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         // list lengths to the host (one round trip) for exactly sized grids, so
         // the CTAs retire as the lists drain and the pattern stream keeps SMs
         int nl[8];
-        CK(cudaMemcpyAsync(nl, S.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(nl, U.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
 #endif
         auto launch = [&](auto kern, int kind, cudaStream_t s) {
           if (nl[kind] <= 0) return;
-          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(P0, nitems, S.ulist.p + kind * ls, S.nlist.p + kind,
-                                             S.upair.p, S.uqs.p, S.pair_outer.p, S.partner.p,
-                                             S.info.p, S.mom.p, S.counters.p + 1);
+          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(P0, nitems, U.ulist.p + kind * ls, U.nlist.p + kind,
+                                             U.upair.p, U.uqs.p, U.pair_outer.p, S.partner.p,
+                                             S.info.p, U.mom.p, S.counters.p + 1);
           ++S.launches;
         };
         // lists 0..3: interior parents by cap case, 4..7: constraint parents;
@@ -3155,31 +3193,40 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         }
         CK(cudaEventRecord(S.ev[11], s3));  // join
         CK(cudaStreamWaitEvent(st, S.ev[11], 0));
-        CK(cudaEventRecord(S.ev[7], st));
+        CK(cudaEventRecord(evu(set, 1), st));
+        set_timed[set] = true;
       }
       setup_combine();
+      // the combine of this chunk on stream4, after its units (and the
+      // accumulator set-up) on `stream`; the next chunk's units proceed on
+      // `stream` meanwhile
+      cudaStream_t s4 = S.stream4;
+      CK(cudaEventRecord(evu(set, 2), st));
+      CK(cudaStreamWaitEvent(s4, evu(set, 2), 0));
       // block size from delta/h (pairs per outer element grow like (delta/h)^3):
       // a property of the mesh, the same for every shard and chunk -- the
       // per-warp partial sums, hence the last bits, must not depend on sharding
       if (S.delta_over_h < 2.5)
-        k_integrate<128><<<ii1 - ii0, 128, ismem, st>>>(
+        k_integrate<128><<<ii1 - ii0, 128, ismem, s4>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
-            S.rhsT.p, S.uoff.p, need_units ? S.mom.p : nullptr, P0, S.counters.p + 1, hcap,
+            S.rhsT.p, U.uoff.p, need_units ? U.mom.p : nullptr, P0, S.counters.p + 1, hcap,
             rowcap);
       else
-        k_integrate<256><<<ii1 - ii0, 256, ismem, st>>>(
+        k_integrate<256><<<ii1 - ii0, 256, ismem, s4>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
-            S.rhsT.p, S.uoff.p, need_units ? S.mom.p : nullptr, P0, S.counters.p + 1, hcap,
+            S.rhsT.p, U.uoff.p, need_units ? U.mom.p : nullptr, P0, S.counters.p + 1, hcap,
             rowcap);
       ++S.launches;
-      if (need_units) {
-        CK(cudaEventSynchronize(S.ev[7]));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, S.ev[6], S.ev[7]));
-        mc_ms += ms;
-      }
+      CK(cudaEventRecord(evu(set, 3), s4));
+      set_busy[set] = true;
       ii0 = ii1;
+      ++chunk;
     }
+  }
+  // everything after the chunks (finalize, read-backs) waits for the combines
+  for (int set = 0; set < 2; ++set) {
+    if (set_busy[set]) CK(cudaStreamWaitEvent(st, evu(set, 3), 0));
+    collect(set);
   }
   S.mc_ms = mc_ms;
   setup_combine();  // empty shard: the pattern is still needed by finalize
@@ -3713,6 +3760,7 @@ void nlfem_gpu_session_destroy(nlfem_gpu_session* s) {
   if (s->stream) cudaStreamDestroy(s->stream);
   if (s->stream2) cudaStreamDestroy(s->stream2);
   if (s->stream3) cudaStreamDestroy(s->stream3);
+  if (s->stream4) cudaStreamDestroy(s->stream4);
   delete s;
 }
 
