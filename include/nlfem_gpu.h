@@ -267,7 +267,8 @@ int nlfem_gpu_session_solve(nlfem_gpu_session* s, double tol, int32_t max_iter,
 
 /* Element-pair list of the last run, for set parity: for each interior outer
  * element (in ascending id order) its partner ids and per-quad-point class
- * codes (5 bits per point).  Arrays sized by *npairs after a
+ * codes (5 bits per point) -- per (T, q) the parents the
+ * reference's walk_ball emits pieces for (ball_approx.hpp:164-175).  Arrays sized by *npairs after a
  * call with NULL buffers. */
 int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* outer_offsets,
                             int32_t* partner, uint32_t* info, char* err, size_t errlen);
