@@ -59,6 +59,9 @@ CONFIGS = {
     "P3n": dict(res=24, delta=3 / 24, strategy="nocaps", mc=1, jitter=7),
     "P3f": dict(res=24, delta=3 / 24, strategy="fullcaps", mc=128, jitter=7),
 }
+# B200 FP64 (non-tensor) nominal: 148 SMs x 64 DFMA/clk x 2 FLOP x 1.965 GHz
+FP64_NOMINAL_TF = 148 * 64 * 2 * 1.965e9 / 1e12
+
 # dram__bytes_read.sum + dram__bytes_write.sum of the units kernels (all k_mc
 # launches of one step) from the committed ncu --set full capture; None where
 # no capture was taken for that workload
@@ -411,7 +414,10 @@ def main():
         "phase_ms": [round(x, 3) for x in st.phase_ms[:6]],
         "roofline": {"kernel": rl_kernel, "bound": "fp64", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": "nlfem_gpu_fp64_peak() DFMA microbenchmark, this run (burst)",
+                     "peak_source": "of measured: nlfem_gpu_fp64_peak() DFMA microbenchmark, "
+                                    "this run (burst); MEASURED_PEAKS.json has no FP64 figure",
+                     "peak_nominal": FP64_NOMINAL_TF,
+                     "frac_of_nominal": achieved / FP64_NOMINAL_TF,
                      "ledger_flops_per_launch": int(rl_flops), "launch_ms": rl_ms,
                      "traffic": TRAFFIC.get(args.config) if units else None,
                      "traffic_source": "profiles/r1_c1_kmc_ncu.txt (dram read+write summed over "
