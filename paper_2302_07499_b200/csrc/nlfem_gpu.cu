@@ -702,17 +702,51 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
   // batch's barrier orders this batch's staging writes before any reads.
   __shared__ int wcount[2][kPairWarps];
   int par = 0;
-  for (int z = z0; z <= z1; ++z) {
-    for (int y = y0; y <= y1; ++y) {
+  // the grid rows of the reach box (z-major, then y; each row a contiguous run
+  // of cells x0..x1, hence of cell_elems) are streamed as one flat candidate
+  // sequence, a group of rows at a time: batches span row boundaries, so all
+  // threads stage a candidate in every batch (same candidate order as a
+  // row-by-row walk)
+  constexpr int kRowGroup = 256;
+  __shared__ int rstart[kRowGroup], rpre[kRowGroup + 1];
+  const int ny = y1 - y0 + 1, nz = z1 - z0 + 1;
+  const int nrows = (ny > 0 && nz > 0 && x1 >= x0) ? ny * nz : 0;
+  for (int rg = 0; rg < nrows; rg += kRowGroup) {
+    const int nr = min(kRowGroup, nrows - rg);
+    __syncthreads();  // the previous group's row table is no longer read
+    for (int t = threadIdx.x; t < nr; t += kPairThreads) {
+      const int r = rg + t, z = z0 + r / ny, y = y0 + r % ny;
       const int row = (z * cD.gy + y) * cD.gx;
       const int e0 = cD.cell_start[row + x0], e1 = cD.cell_start[row + x1 + 1];
-      for (int base = e0; base < e1; base += kPairThreads) {
-        const int e = base + threadIdx.x;
+      rstart[t] = e0;
+      rpre[t + 1] = e1 - e0;
+    }
+    __syncthreads();
+    if (wl == 0) {  // inclusive scan of the row lengths
+      int carry = 0;
+      for (int t0 = 0; t0 < nr; t0 += 32) {
+        int v = (t0 + lane < nr) ? rpre[t0 + lane + 1] : 0;
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const int u = __shfl_up_sync(FULLMASK, v, sh);
+          if (lane >= sh) v += u;
+        }
+        if (t0 + lane < nr) rpre[t0 + lane + 1] = v + carry;
+        carry += __shfl_sync(FULLMASK, v, 31);
+      }
+      if (lane == 0) rpre[0] = 0;
+    }
+    __syncthreads();
+    const int total = rpre[nr];
+    int rr = 0;  // this thread's row (its candidate index only grows)
+    {
+      for (int base = 0; base < total; base += kPairThreads) {
+        const int g = base + threadIdx.x;
         unsigned pm = 0;
         int Tp = -1;
         double4 a;
-        if (e < e1) {
-          Tp = cD.cell_elems[e];
+        if (g < total) {
+          while (rpre[rr + 1] <= g) ++rr;
+          Tp = cD.cell_elems[rstart[rr] + (g - rpre[rr])];
           a = cD.erec[4 * Tp];
 #pragma unroll
           for (int w = 0; w < kPairWarps; ++w) {
