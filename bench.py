@@ -65,7 +65,7 @@ FP64_NOMINAL_TF = 148 * 64 * 2 * 1.965e9 / 1e12
 # dram__bytes_read.sum + dram__bytes_write.sum of the units kernels (all k_mc
 # launches of one step) from the committed ncu --set full capture; None where
 # no capture was taken for that workload
-TRAFFIC = {"C1": 434211584}
+TRAFFIC = {"C1": 432594432}
 
 
 def describe(name, cfg):
