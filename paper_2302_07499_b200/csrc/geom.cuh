@@ -357,23 +357,26 @@ __device__ __forceinline__ bool approx_pieces(const Vd v[4], int mask, Vd c, dou
     }
     if (!vis) continue;
     // horizon: directed edges of visible faces whose reverse lies in an
-    // invisible face, in (face, edge) order -> new faces (a, b, pi)
+    // invisible face, in (face, edge) order -> new faces (a, b, pi).  The
+    // directed edges of the invisible faces are marked in a 10 x 10 bit
+    // matrix (bit 10 x + y for edge x -> y), so each test is one bit probe.
+    unsigned long long em[2] = {0ull, 0ull};
+    for (int g = 0; g < nf; ++g) {
+      if (vis >> g & 1) continue;
+      const int x = F[g] & 255, y = (F[g] >> 8) & 255, z = F[g] >> 16;
+      const int k1 = 10 * x + y, k2 = 10 * y + z, k3 = 10 * z + x;
+      em[k1 >> 6] |= 1ull << (k1 & 63);
+      em[k2 >> 6] |= 1ull << (k2 & 63);
+      em[k3 >> 6] |= 1ull << (k3 & 63);
+    }
     int nh = 0;
     for (int f = 0; f < nf; ++f) {
       if (!(vis >> f & 1)) continue;
       const int e3[3] = {(int)(F[f] & 255), (int)((F[f] >> 8) & 255), (int)(F[f] >> 16)};
       for (int e = 0; e < 3; ++e) {
         const int a = e3[e], b = e3[e == 2 ? 0 : e + 1];
-        // reverse edge (b, a) as a directed edge of face g: one of its three
-        // rotations starts with b then a
-        const unsigned ba = (unsigned)b | ((unsigned)a << 8);
-        bool open = true;
-        for (int g = 0; g < nf && open; ++g) {
-          if (vis >> g & 1) continue;
-          const unsigned w = F[g];
-          const unsigned r1 = (w & 0xffffu), r2 = (w >> 8), r3 = (w >> 16) | ((w & 255u) << 8);
-          if (r1 == ba || r2 == ba || r3 == ba) open = false;
-        }
+        const int kb = 10 * b + a;  // the reverse edge b -> a
+        const bool open = !((em[kb >> 6] >> (kb & 63)) & 1ull);
         if (!open) {
           if (nf + nh >= kHullScratch) return false;
           F[nf + nh++] = outward(a, b, pi);

@@ -81,11 +81,24 @@ struct Poly {
 __device__ __forceinline__ double poly_eval(const Poly& P, Vd p) {
   // Polynomial::eval (reference polynomial.cpp:28-37)
   double acc = 0;
+  // the same multiplications in the same order, with short exponents unrolled
+  // (data-dependent loops cost more than the arithmetic)
+  auto powmul = [](double v, double x, int e) {
+    switch (e) {
+      case 0: return v;
+      case 1: return v * x;
+      case 2: return (v * x) * x;
+      case 3: return ((v * x) * x) * x;
+      default:
+        for (int i = 0; i < e; ++i) v *= x;
+        return v;
+    }
+  };
   for (int t = 0; t < P.n; ++t) {
     double v = P.c[t];
-    for (int i = 0; i < P.e[t][0]; ++i) v *= p.x;
-    for (int i = 0; i < P.e[t][1]; ++i) v *= p.y;
-    for (int i = 0; i < P.e[t][2]; ++i) v *= p.z;
+    v = powmul(v, p.x, P.e[t][0]);
+    v = powmul(v, p.y, P.e[t][1]);
+    v = powmul(v, p.z, P.e[t][2]);
     acc += v;
   }
   return acc;
