@@ -2321,6 +2321,7 @@ PinnedPool g_result_pool;
 
 struct nlfem_gpu_session {
   int device = 0;
+  int sms = 148;  // streaming multiprocessors of the device (grid sizing)
   Dev dev{};
   int K = 0, J = 0, KI = 0, unknowns = 0;
   std::vector<int> h_interior, h_dof_node;
@@ -2494,6 +2495,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     throw Fail{NLFEM_GPU_ENODEVICE, "no CUDA device available (the GPU path has no CPU fallback)"};
   if (cfg->device >= 0) CK(cudaSetDevice(cfg->device));
   CK(cudaGetDevice(&S.device));
+  CK(cudaDeviceGetAttribute(&S.sms, cudaDevAttrMultiProcessorCount, S.device));
   int major = 0;
   CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, S.device));
   if (major < 10)
@@ -2734,7 +2736,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
   S.rlen.ensure(J);
   S.roff.ensure(J + 1);
-  const unsigned rgrid = (unsigned)std::min<long long>(J, 148LL * 16);
+  const unsigned rgrid = (unsigned)std::min<long long>(J, (long long)S.sms * 16);
   k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
                                                nullptr, S.ovf.p);
   ++S.launches;
@@ -3187,21 +3189,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         CK(cudaEventRecord(S.ev[10], st));  // fork
         CK(cudaStreamWaitEvent(s3, S.ev[10], 0));
         const long long ls = nitems + 1;
-#ifndef NLFEM_MC_PERSIST
-#define NLFEM_MC_PERSIST 1
-#endif
-#if NLFEM_MC_PERSIST
         // list lengths stay on the device: launches of two waves of resident CTAs
         int nl[8];
         for (int k = 0; k < 8; ++k)
-          nl[k] = (int)std::min<long long>(nitems, 148LL * NLFEM_MC_MINBLOCKS * 2 * kMcThreads);
-#else
-        // list lengths to the host (one round trip) for exactly sized grids, so
-        // the CTAs retire as the lists drain and the pattern stream keeps SMs
-        int nl[8];
-        CK(cudaMemcpyAsync(nl, U.nlist.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-#endif
+          nl[k] = (int)std::min<long long>(nitems, (long long)S.sms * NLFEM_MC_MINBLOCKS * 2 * kMcThreads);
         auto launch = [&](auto kern, int kind, cudaStream_t s) {
           if (nl[kind] <= 0) return;
           kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(P0, nitems, U.ulist.p + kind * ls, U.nlist.p + kind,
