@@ -78,9 +78,23 @@ def allgather_csr(block: dict, group=None, device=None) -> dict:
                        for a, b, c, d in zip(rps, cis, vas, rhs)])
 
 
+def _comm_device(group=None):
+    """Where the collectives' buffers live: HBM for NCCL, host memory for gloo
+    (the CPU test backend; it also drives several ranks on one GPU)."""
+    import torch
+    import torch.distributed as dist
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else torch.device("cuda")
+
+
 def allreduce_partials(V, rhsT, group=None) -> None:
     """In-place integer sum of the fixed-point partials across ranks."""
     import torch.distributed as dist
+    if V.device.type == "cuda" and _comm_device(group).type == "cpu":
+        for t in (V, rhsT):
+            h = t.cpu()
+            dist.all_reduce(h, group=group)
+            t.copy_(h)
+        return
     dist.all_reduce(V, group=group)
     dist.all_reduce(rhsT, group=group)
 
@@ -96,13 +110,17 @@ def gather_pairs(session, lo: int, hi: int, group=None, device=None) -> int:
     npairs = session.pairs_shard(lo, hi)
     cview, pview = session.pairs_shard_out()
     dev = torch.device("cuda") if device is None else torch.device(device)
-    counts = (torch.as_tensor(cview, device=dev) if hi > lo
+    src = "cuda" if torch.cuda.is_available() else dev  # the session's arrays live in HBM
+    counts = (torch.as_tensor(cview, device=src).to(dev) if hi > lo
               else torch.zeros(0, dtype=torch.int32, device=dev))
-    partners = (torch.as_tensor(pview, device=dev) if npairs > 0
+    partners = (torch.as_tensor(pview, device=src).to(dev) if npairs > 0
                 else torch.zeros(0, dtype=torch.int32, device=dev))
     counts, partners = counts.to(torch.int32), partners.to(torch.int32)
-    stream = torch.cuda.current_stream().cuda_stream if dev.type == "cuda" else None
+    # the install reads device arrays, after torch's current stream
+    stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
     if world == 1:
+        if counts.device.type != "cuda" and torch.cuda.is_available():
+            counts, partners = counts.cuda(), partners.cuda()
         session.pairs_install(counts, partners, npairs, stream=stream)
         return npairs
     # flat outputs viewed as (world, n): accepted by NCCL and gloo alike
@@ -123,6 +141,8 @@ def gather_pairs(session, lo: int, hi: int, group=None, device=None) -> int:
     all_counts = torch.cat([gc[r, : int(m[r, 0])] for r in range(world)])
     all_partners = torch.cat([gp[r, : int(m[r, 1])] for r in range(world)])
     total = int(m[:, 1].sum())
+    if all_counts.device.type != "cuda" and torch.cuda.is_available():
+        all_counts, all_partners = all_counts.cuda(), all_partners.cuda()
     session.pairs_install(all_counts, all_partners, total, stream=stream)
     return total
 
@@ -148,15 +168,18 @@ def device_step(session, group=None, stream: int | None = None):
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    cdev = _comm_device(group)
     lo, hi = shard_range(session.interior_count, rank, world)
-    gather_pairs(session, lo, hi, group)
+    gather_pairs(session, lo, hi, group, device=cdev)
     st = session.run_shard(lo, hi, finalize=False, stream=stream)
     vv, rv = session.partials()
     V = torch.as_tensor(vv, device="cuda")
     R = torch.as_tensor(rv, device="cuda")
     allreduce_partials(V, R, group)
     r0, r1 = shard_range(session.unknowns, rank, world)
-    session.finalize(r0, r1)
+    # the reduced partials are ready on torch's current stream (NCCL enqueues
+    # there): the session's finalize waits on it
+    session.finalize(r0, r1, stream=torch.cuda.current_stream().cuda_stream)
     ro, ci, va, rh = (torch.as_tensor(x, device="cuda") for x in session.outputs())
     # row-block extents on every rank (row offsets are identical everywhere)
     bounds = [shard_range(session.unknowns, r, world) for r in range(world)]
@@ -169,9 +192,10 @@ def device_step(session, group=None, stream: int | None = None):
         ext = [((a, b) if per_row else (int(offs[a]), int(offs[b]))) for a, b in bounds]
         m = max(b - a for a, b in ext)
         a, b = ext[rank]
-        pad = torch.zeros(max(m, 1), dtype=arr.dtype, device="cuda")
-        pad[: b - a] = arr[a:b]
-        gathered = torch.empty((world, max(m, 1)), dtype=arr.dtype, device="cuda")
+        pad = torch.zeros(max(m, 1), dtype=arr.dtype, device=cdev)
+        pad[: b - a] = arr[a:b].to(cdev)
+        gathered = torch.empty(world * max(m, 1), dtype=arr.dtype, device=cdev)
         dist.all_gather_into_tensor(gathered, pad, group=group)
-        out.append(torch.cat([gathered[r, : e[1] - e[0]] for r, e in enumerate(ext)]))
+        gathered = gathered.view(world, max(m, 1))
+        out.append(torch.cat([gathered[r, : e[1] - e[0]] for r, e in enumerate(ext)]).to("cuda"))
     return out, st
