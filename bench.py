@@ -250,8 +250,11 @@ def run_reference_arm(args, cfg_name, cfg):
         "e2e": {"value": value, "unit": "element-pair integrals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_JSON_OUT, flush=True)
     return 0
+
+
+_JSON_OUT = sys.stdout
 
 
 def main():
@@ -268,6 +271,12 @@ def main():
                          "the N>1 code on a single GPU")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    # stdout carries exactly one JSON line: anything else written to file
+    # descriptor 1 (NCCL's version banner, library prints) goes to stderr
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         return run_reference_arm(args, args.config, cfg)
 
@@ -440,7 +449,7 @@ def main():
         except Exception as exc:  # report, never fail the bench line
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_JSON_OUT, flush=True)
     sess.close()
     if dist is not None:
         dist.destroy_process_group()
