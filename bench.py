@@ -284,6 +284,8 @@ def main():
     import paper_2302_07499_b200 as P
 
     rank, world, local = dist_env()
+    if os.environ.get("NLFEM_BENCH_BACKEND", "nccl") != "nccl":
+        local %= max(torch.cuda.device_count(), 1)  # test mode: ranks may share a GPU
     torch.cuda.set_device(local)
     dist = None
     use_dist = world > 1 or args.dist
@@ -293,7 +295,11 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29531")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("NLFEM_BENCH_BACKEND", "nccl")  # gloo: tests on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist is not None:
@@ -417,8 +423,10 @@ def main():
                    "element_pairs": pairs, "items": int(st.items),
                    "mc_samples": int(st.mc_samples), "mc_hits": int(st.mc_hits),
                    "l2": "flushed between steps (256 MiB write; inputs smaller than L2)",
-                   "parallelism": f"outer-element shards x{world} (NCCL int64 all-reduce + "
-                                  "row-block all-gather)" if use_dist else "single GPU"},
+                   "parallelism": (f"outer-element shards x{world} "
+                                   f"({os.environ.get('NLFEM_BENCH_BACKEND', 'nccl').upper()} "
+                                   "int64 all-reduce + row-block all-gather)")
+                                  if use_dist else "single GPU"},
         "fp64_gflops_ledger": st.ledger_flops / (t_total / args.steps * 1e-3) / 1e9,
         "phase_ms": [round(x, 3) for x in st.phase_ms[:6]],
         "roofline": {"kernel": rl_kernel, "bound": "fp64", "achieved": achieved,
