@@ -146,3 +146,30 @@ def test_interleaved_sessions_on_one_device():
     got = a.download_rows(0, a.unknowns)
     for k in ("row_ptr", "col_idx", "values", "rhs"):
         assert np.array_equal(got[k], want[k]), k
+
+
+def test_session_reset_equals_fresh_session():
+    # the workspace reuse behind repeated one-shot calls: a session reloaded
+    # with another mesh gives that mesh's system bit for bit
+    mA = P.generate_mesh(3, 5, 0.34, jitter_seed=3)
+    tA = P.ElementTable(mA["coords"], mA["cells"], mA["region"])
+    mB = P.generate_mesh(3, 6, 0.3)
+    tB = P.ElementTable(mB["coords"], mB["cells"], mB["region"])
+    s = P.Session(tA, 0.3, "fullcaps", "moment2", U2, seed=SEED, mc_samples=8)
+    s.run()
+    s.reset(tB)
+    s.run()
+    got = s.download()
+    f = P.Session(tB, 0.3, "fullcaps", "moment2", U2, seed=SEED, mc_samples=8)
+    f.run()
+    want = f.download()
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(got[k], want[k]), k
+    # the device pair list equals the host download
+    import torch
+    pd, ph = f.pairs_device(), f.pairs()
+    assert np.array_equal(torch.as_tensor(pd["offsets"], device="cuda").cpu().numpy(),
+                          ph["offsets"])
+    assert np.array_equal(torch.as_tensor(pd["partner"], device="cuda").cpu().numpy(),
+                          ph["partner"])
+    assert np.array_equal(torch.as_tensor(pd["info"], device="cuda").cpu().numpy(), ph["info"])
