@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """Benchmark: nonlocal stiffness assembly on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-One "step" = one full assembly (nlfem::assemble analogue: element pairs ->
+Default workload: C4 (BASELINE configs[4]: N=96, delta=3h, fullcaps M=128,
+7.0e9 element pairs), the largest configuration that fits one B200 and the
+one the multi-GPU scaling is quoted on.  One "step" = one full assembly (nlfem::assemble analogue: element pairs ->
 pattern -> FP64 integration -> CSR) of the named workload.  Prints ONE JSON
 line (rank 0).
 
@@ -14,11 +16,15 @@ line (rank 0).
   roofline   the integration kernel (k_integrate, FP64-pipe bound) against the
              FP64 DFMA peak measured live by nlfem_gpu_fp64_peak()
   cpu_baseline  the unmodified reference assemble() (oracle/_ref, all host
-             cores) on the same workload, when built; else the CPU port
+             cores) on a bounded sample of the workload (see sample_cfg)
 
---impl reference times the reference's own CPU assemble() on this box's host
-cores for the same config (rank 0 only) and prints the same line with
-"impl": "reference".
+--impl reference times the unmodified reference's assemble() (oracle/_ref,
+its own mesh generator and element table; nothing from paper_2302_07499_b200
+is imported) on this box's host cores, one reference assemble() of the
+sample mesh per step (rank 0 only), and prints the same line with
+"impl": "reference" and the same `config`.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run.
 
 Multi-GPU (torchrun, NCCL): the assembly is sharded -- each rank integrates a
 contiguous range of outer elements into exact fixed-point partial sums, an
@@ -59,13 +65,15 @@ CONFIGS = {
     "P3n": dict(res=24, delta=3 / 24, strategy="nocaps", mc=1, jitter=7),
     "P3f": dict(res=24, delta=3 / 24, strategy="fullcaps", mc=128, jitter=7),
 }
+METRIC = "element-pair integrals/s"
 # B200 FP64 (non-tensor) nominal: 148 SMs x 64 DFMA/clk x 2 FLOP x 1.965 GHz
 FP64_NOMINAL_TF = 148 * 64 * 2 * 1.965e9 / 1e12
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the units kernels (all k_mc
-# launches of one step) from the committed ncu --set full capture; None where
-# no capture was taken for that workload
-TRAFFIC = {"C1": 432594432}
+# launches of one step, or of one chunk scaled to the step) from the committed
+# ncu --set full captures; None where no capture was taken for that workload
+TRAFFIC = {"C1": (432594432, "profiles/r1_c1_kmc_ncu.txt (dram read+write summed over the "
+                             "step's k_mc launches)")}
 
 
 def describe(name, cfg):
@@ -173,103 +181,151 @@ class ClockSampler:
                 "samples": len(self.rows), "sampler": self.source}
 
 
-def cpu_baseline(cfg_name, cfg, steps=1):
-    """Reference assemble() on this host's cores; bounded sample of the workload."""
-    from oracle import ref, port
-    import paper_2302_07499_b200 as P
-    sample = dict(cfg)
-    note = "full workload"
-    if cfg["res"] > 12:
-        # same delta/h and M on a smaller mesh; pairs/s is per-outer-element work
-        ratio = cfg["delta"] * cfg["res"]
-        sample["res"] = 10 if cfg["strategy"] != "fullcaps" else 8
-        sample["delta"] = ratio / sample["res"]
-        note = (f"N={sample['res']} mesh at the same delta/h={ratio:g} and M; rate per element "
-                "pair is mesh-size independent at fixed delta/h")
-    m = P.generate_mesh(3, sample["res"], sample["delta"], jitter_seed=sample["jitter"])
+# The reference's per-element-pair rate at fixed delta/h and M does not depend
+# on the mesh size (same Monte Carlo draws per pair, 760.8 at delta = 3h,
+# M = 128, for every N; measured rates N = 8 / 12 / 16 / 24 in
+# profiles/r2_ref_rate_vs_n.txt), so the reference's CPU time is sampled on
+# the N = SAMPLE_RES mesh at the workload's delta/h and M: one step of the
+# reference arm is one full reference assemble() of that mesh (seconds of CPU
+# work), where the benchmarked C2-C4 workloads would take hours.
+SAMPLE_RES = 8
+
+
+def sample_cfg(cfg):
+    """The bounded CPU sample of a workload (same delta/h, strategy, M)."""
+    if cfg["res"] <= 12:
+        return dict(cfg), "full workload"
+    ratio = cfg["delta"] * cfg["res"]
+    s = dict(cfg, res=SAMPLE_RES, delta=ratio / SAMPLE_RES)
+    note = (f"[est.] N={SAMPLE_RES} mesh at the workload's delta/h={ratio:g} and M: the "
+            "per-element-pair rate is mesh-size independent at fixed delta/h "
+            "(profiles/r2_ref_rate_vs_n.txt)")
+    return s, note
+
+
+def reference_sample(cfg):
+    """The unmodified reference (oracle/_ref) on the sample mesh: its own
+    generate_mesh / build_cmap / build_element_table / build_dofmap, plus the
+    element pairs of the sample counted by the restated oracle on the
+    reference's own table.  Imports nothing from paper_2302_07499_b200."""
+    import types
+    from oracle import port, ref
+    s, note = sample_cfg(cfg)
+    coords, cells, region = ref.generate_mesh(s["res"], s["delta"], jitter_seed=s["jitter"])
+    R = ref.Problem(coords, cells, region)
+    t = types.SimpleNamespace(**R.table())
+    t.coords = np.ascontiguousarray(coords, np.float64)
+    t.elem_count, t.node_count, t.unknowns = R.elems, R.nodes, R.unknowns
+    Cc, f = ref.forcing(s["delta"], U2)
+    # the pair set does not depend on M (mode R: the reference's own stream)
+    o = port.assemble(t, s["delta"], s["strategy"], Cc, f, U2, seed=SEED, mc_samples=1,
+                      sampler="R", threads=os.cpu_count() or 1)
+    sample = (f"{s['strategy']} N={s['res']} delta={s['delta']:.6g} M={s['mc']}: {note}; "
+              f"unmodified reference assemble(), AssemblyStats.seconds")
+    return R, s, int(o["element_pairs"]), sample
+
+
+def reference_steps(R, s, steps, cores):
+    out = []
+    for _ in range(steps):
+        r = R.assemble(s["delta"], s["strategy"], U2, threads=cores, seed=SEED,
+                       mc_samples=s["mc"])
+        out.append(r["seconds"])
+    return out
+
+
+def cpu_baseline(cfg):
+    """One bounded reference run beside the GPU line (rank 0, N=1)."""
     cores = os.cpu_count() or 1
-    times, pairs = [], None
-    if ref.available():
-        R = ref.Problem(m["coords"], m["cells"], m["region"])
-        for _ in range(steps):
-            out = R.assemble(sample["delta"], sample["strategy"], U2, threads=cores, seed=SEED,
-                             mc_samples=sample["mc"])
-            times.append(out["seconds"])
-        kind = "reference"
-    else:
-        t = P.ElementTable(m["coords"], m["cells"], m["region"])
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            port.assemble(t, sample["delta"], sample["strategy"],
-                          P.kernel_constant(sample["delta"], "moment2"),
-                          P.forcing_terms(sample["delta"], U2, "moment2"), P.normalize_terms(U2),
-                          seed=SEED, mc_samples=sample["mc"], sampler="R", threads=cores)
-            times.append(time.perf_counter() - t0)
-        kind = "port"
-    # element pairs of the sample (count with the GPU pair kernel when available)
-    pairs = count_pairs(m, sample)
-    return dict(times=times, pairs=pairs, cores=cores, kind=kind, note=note,
-                sample=f"{sample['strategy']} N={sample['res']} delta={sample['delta']:.6g} "
-                       f"M={sample['mc']}: {note}")
-
-
-def count_pairs(m, cfg):
-    """Element pairs (T,T') with a piece for some quad point of T (the metric's
-    unit), counted by the restated CPU oracle outside any timed region, so the
-    reference arm never touches the GPU code."""
-    from oracle import port
-    import paper_2302_07499_b200 as P
-    t = P.ElementTable(m["coords"], m["cells"], m["region"])
-    mc = 1 if cfg["strategy"] != "fullcaps" else 1  # pair sets do not depend on M
-    o = port.assemble(t, cfg["delta"], cfg["strategy"], P.kernel_constant(cfg["delta"], "moment2"),
-                      P.forcing_terms(cfg["delta"], U2, "moment2"), P.normalize_terms(U2),
-                      seed=SEED, mc_samples=mc, sampler="P", threads=os.cpu_count() or 1)
-    return int(o["element_pairs"])
+    R, s, pairs, sample = reference_sample(cfg)
+    t = reference_steps(R, s, 1, cores)
+    return {"value": pairs / t[0], "unit": "element-pair integrals/s", "cores": cores,
+            "kind": "reference", "sample": sample}
 
 
 def run_reference_arm(args, cfg_name, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    for _ in range(args.warmup):
-        cpu_baseline(cfg_name, cfg, steps=1)
-    cb = cpu_baseline(cfg_name, cfg, steps=args.steps)
-    tot = sum(cb["times"])
-    value = cb["pairs"] * len(cb["times"]) / tot
+    cores = os.cpu_count() or 1
+    R, s, pairs, sample = reference_sample(cfg)
+    reference_steps(R, s, max(args.warmup, 0), cores)
+    times = reference_steps(R, s, args.steps, cores)
+    tot = sum(times)
+    value = pairs * len(times) / tot
     line = {
-        "impl": "reference", "metric": "element-pair integrals/s", "value": value,
-        "unit": "element-pair integrals/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(cb["times"]),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": describe(cfg_name, cfg)["text"], "name": cfg_name,
-                   "element_pairs": int(cb["pairs"]),
-                   "parallelism": f"reference assemble() on {cb['cores']} host threads (rank 0)"},
-        "cpu_baseline": {"value": value, "unit": "element-pair integrals/s", "cores": cb["cores"],
-                         "kind": cb["kind"], "sample": cb["sample"]},
-        "e2e": {"value": value, "unit": "element-pair integrals/s", "h2d_bytes_per_step": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": METRIC,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(cfg_name, cfg),
+        "parallelism": f"reference assemble() on {cores} host threads (rank 0)",
+        "sample_element_pairs": pairs,
+        "cpu_baseline": {"value": value, "unit": METRIC, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=_JSON_OUT, flush=True)
     return 0
 
 
+def bench_config(cfg_name, cfg):
+    """The `config` object: identical in both arms (the workload, nothing else)."""
+    return {"workload": describe(cfg_name, cfg)["text"], "name": cfg_name}
+
+
 _JSON_OUT = sys.stdout
+
+
+def self_launch(args) -> int | None:
+    """`--gpus N` without a torchrun environment: re-launch this command as N
+    ranks under torch.distributed.run (one process per GPU, 127.0.0.1
+    rendezvous); the rank-0 JSON line reaches this process's stdout."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return None
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(args.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def system_sha(sess, dist_out=None) -> str:
+    """SHA-256 of the assembled system (row offsets, columns, values, rhs as
+    raw bytes): the bitwise check of N-GPU runs against one GPU."""
+    import hashlib
+    import torch
+    ro, ci, va, rh = (torch.as_tensor(x, device="cuda") for x in sess.outputs())
+    if dist_out is not None:
+        va, ci, rh = dist_out
+    h = hashlib.sha256()
+    for t in (ro, ci, va, rh):
+        h.update(t.contiguous().cpu().numpy().tobytes())
+    return h.hexdigest()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--verify", action="store_true",
+                    help="add the SHA-256 of the assembled system to the line")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU (sharded, NCCL) path even on one rank: exercises "
                          "the N>1 code on a single GPU")
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
     cfg = CONFIGS[args.config]
     # stdout carries exactly one JSON line: anything else written to file
     # descriptor 1 (NCCL's version banner, library prints) goes to stderr
@@ -317,10 +373,10 @@ def main():
         from paper_2302_07499_b200 import distributed as D
 
         def step():
-            return D.device_step(sess, stream=stream.cuda_stream)[1]
+            return D.device_step(sess, stream=stream.cuda_stream)
     else:
         def step():
-            return sess.run(stream.cuda_stream)
+            return None, sess.run(stream.cuda_stream)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -332,13 +388,13 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     step_ms, k3_ms, mc_ms = [], [], []
-    st = None
+    st = out = None
     for _ in range(args.steps):
         flush.fill_(1.0)  # evict L2 between timed steps (inputs are smaller than L2)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        st = step()
+        out, st = step()
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -354,6 +410,14 @@ def main():
         t_total = float(t.item())
     pairs = int(st.element_pairs)  # all element pairs of the workload (every rank builds them)
     value = pairs * args.steps / (t_total * 1e-3)
+    sha = system_sha(sess, out) if args.verify else None
+    stats = {"items": int(st.items), "mc_samples": int(st.mc_samples),
+             "mc_hits": int(st.mc_hits)}
+    if dist is not None:  # this rank's shard only: sum over ranks
+        c = torch.tensor([stats["items"], stats["mc_samples"], stats["mc_hits"]],
+                         dtype=torch.int64, device="cuda")
+        dist.all_reduce(c)
+        stats = dict(zip(stats, (int(x) for x in c.cpu())))
 
     # end to end: one-shot C-ABI call with host arrays (upload + run + download).
     # The device-resident session is released first: at C4 its buffers alone
@@ -366,16 +430,17 @@ def main():
         h2d = table.nbytes() + 8 * 8 * (len(sess.fterms) + len(sess.uterms))
         e2e_t = []
         d2h = 0
-        out = None
-        nwarm = 2  # the first calls also set up the workspace and the pinned result pool
+        res = None
+        nwarm = 1  # the first call also sets up the workspace and the pinned result pool
+        nsteps = max(1, min(args.steps, 3))
         ws = None
-        for i in range(max(1, min(args.steps, 3)) + nwarm):
-            out = None  # release the previous result (its pinned block goes back to the pool)
+        for i in range(nsteps + nwarm):
+            res = None  # release the previous result (its pinned block goes back to the pool)
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
             if not use_dist:
-                out, _ = P.assemble(table, cfg["delta"], cfg["strategy"], "moment2", U2,
+                res, _ = P.assemble(table, cfg["delta"], cfg["strategy"], "moment2", U2,
                                     seed=SEED, mc_samples=cfg["mc"], device=local)
             else:  # upload into the rank's workspace session (reused, like the one-shot
                 # call's), sharded assembly, row blocks gathered to host on every rank
@@ -384,7 +449,7 @@ def main():
                                    seed=SEED, mc_samples=cfg["mc"], device=local)
                 else:
                     ws.reset(table)
-                out, _ = D.assemble_distributed(ws)
+                res, _ = D.assemble_distributed(ws)
             t1 = time.perf_counter()
             dt = t1 - t0
             if dist is not None:
@@ -393,12 +458,14 @@ def main():
                 dt = float(tt.item())
             if i >= nwarm:
                 e2e_t.append(dt)
-            d2h = sum(out[k].nbytes for k in ("row_ptr", "col_idx", "values", "rhs"))
+            d2h = sum(res[k].nbytes for k in ("row_ptr", "col_idx", "values", "rhs"))
         if ws is not None:
             ws.close()
-        e2e = {"value": pairs / float(np.mean(e2e_t)), "unit": "element-pair integrals/s",
+        e2e = {"value": pairs / float(np.mean(e2e_t)), "unit": METRIC,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * float(np.mean(e2e_t))}
+               "ms_per_step": 1e3 * float(np.mean(e2e_t)), "steps": len(e2e_t),
+               "path": "nlfem_gpu_assemble (one-shot C-ABI call, host arrays)" if not use_dist
+               else "assemble_distributed (sharded, host CSR on every rank)"}
 
     peak = P.fp64_peak_tflops(local)
     k3 = float(np.mean(k3_ms))
@@ -414,19 +481,18 @@ def main():
         achieved = st.ledger_flops / (k3 * 1e-3) / 1e12
         rl_kernel, rl_flops, rl_ms = "k_integrate (combine)", st.ledger_flops, k3
     integ = st.ledger_flops / (k3 * 1e-3) / 1e12
+    traffic = TRAFFIC.get(args.config) if units and world == 1 else None
     line = {
-        "metric": "element-pair integrals/s", "value": value, "unit": "element-pair integrals/s",
+        "metric": METRIC, "value": value, "unit": METRIC,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(args.config, cfg)["text"], "name": args.config,
-                   "element_pairs": pairs, "items": int(st.items),
-                   "mc_samples": int(st.mc_samples), "mc_hits": int(st.mc_hits),
-                   "l2": "flushed between steps (256 MiB write; inputs smaller than L2)",
-                   "parallelism": (f"outer-element shards x{world} "
-                                   f"({os.environ.get('NLFEM_BENCH_BACKEND', 'nccl').upper()} "
-                                   "int64 all-reduce + row-block all-gather)")
-                                  if use_dist else "single GPU"},
+        "config": bench_config(args.config, cfg),
+        "parallelism": (f"outer-element shards x{world} "
+                        f"({os.environ.get('NLFEM_BENCH_BACKEND', 'nccl').upper()} "
+                        "int64 all-reduce + row-block all-gather)") if use_dist else "single GPU",
+        "l2": "flushed between steps (256 MiB write; inputs smaller than L2)",
+        "element_pairs": pairs, **stats,
         "fp64_gflops_ledger": st.ledger_flops / (t_total / args.steps * 1e-3) / 1e9,
         "phase_ms": [round(x, 3) for x in st.phase_ms[:6]],
         "roofline": {"kernel": rl_kernel, "bound": "fp64", "achieved": achieved,
@@ -436,29 +502,25 @@ def main():
                      "peak_nominal": FP64_NOMINAL_TF,
                      "frac_of_nominal": achieved / FP64_NOMINAL_TF,
                      "ledger_flops_per_launch": int(rl_flops), "launch_ms": rl_ms,
-                     "traffic": TRAFFIC.get(args.config) if units else None,
-                     "traffic_source": "profiles/r1_c1_kmc_ncu.txt (dram read+write summed over "
-                                       "the step's k_mc launches)" if units else None,
+                     "traffic": traffic[0] if traffic else None,
+                     "traffic_source": traffic[1] if traffic else None,
                      "integration_phase": {"kernels": "k_mc + k_integrate", "ms": k3,
                                            "ledger_flops": int(st.ledger_flops),
                                            "achieved": integ, "frac": integ / peak}},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
+    if sha:
+        line["system_sha256"] = sha
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(args.config, cfg, steps=1)
-            v = cb["pairs"] / min(cb["times"])
-            line["cpu_baseline"] = {"value": v, "unit": "element-pair integrals/s",
-                                    "cores": cb["cores"], "kind": cb["kind"],
-                                    "sample": cb["sample"]}
+            line["cpu_baseline"] = cpu_baseline(cfg)
         except Exception as exc:  # report, never fail the bench line
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if rank == 0:
         print(json.dumps(line), file=_JSON_OUT, flush=True)
-    sess.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0

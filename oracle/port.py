@@ -38,7 +38,7 @@ def lib():
         L.oracle_assemble.restype = vp
         L.oracle_assemble.argtypes = [C.c_int, C.c_int] + [vp] * 10 + [C.c_int, dbl, dbl, vp, C.c_int,
                                       vp, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int,
-                                      C.POINTER(C.c_int), C.c_char_p, C.c_int]
+                                      vp, i64, C.POINTER(C.c_int), C.c_char_p, C.c_int]
         L.oracle_result_sizes.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
         L.oracle_result_copy.argtypes = [vp, vp, vp, vp, vp]
         L.oracle_result_stats.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32),
@@ -64,8 +64,11 @@ class OracleError(RuntimeError):
 
 
 def assemble(table, delta, strategy, C_kernel, fterms, gterms, *, seed=0x5EED,
-             mc_samples=200, sampler="P", threads=0) -> dict:
-    """Restated nlfem::assemble on a paper_2302_07499_b200.ElementTable-like object."""
+             mc_samples=200, sampler="P", threads=0, outer=None) -> dict:
+    """Restated nlfem::assemble on a paper_2302_07499_b200.ElementTable-like object.
+
+    outer: optional interior element ids -- integrate only these outer elements
+    (the partial system of a sample, for parity at full mesh sizes)."""
     L = lib()
     f = np.ascontiguousarray(fterms, np.float64)
     g = np.ascontiguousarray(gterms, np.float64)
@@ -73,11 +76,14 @@ def assemble(table, delta, strategy, C_kernel, fterms, gterms, *, seed=0x5EED,
     err = C.create_string_buffer(512)
     threads = threads or os.cpu_count() or 1
     t = table
+    ov = None if outer is None else np.ascontiguousarray(outer, np.int32)
     h = L.oracle_assemble(t.elem_count, t.node_count, _p(t.coords), _p(t.verts), _p(t.neighbor),
                           _p(t.center), _p(t.radius), _p(t.volume), _p(t.diam), _p(t.region),
                           _p(t.inv_edges), _p(t.dof_of_node), t.unknowns, C_kernel, delta,
                           _p(f), len(f), _p(g), len(g), STRATEGY[strategy], seed & (2**64 - 1),
-                          mc_samples, {"P": 0, "R": 1}[sampler], threads, C.byref(code), err, 512)
+                          mc_samples, {"P": 0, "R": 1}[sampler], threads,
+                          None if ov is None else _p(ov), 0 if ov is None else len(ov),
+                          C.byref(code), err, 512)
     if not h:
         raise OracleError(code.value, err.value.decode())
     rows, nnz = C.c_int64(), C.c_int64()

@@ -34,6 +34,8 @@ def lib():
         P = C.POINTER
         L.ref_mesh_generate.restype = vp
         L.ref_mesh_generate.argtypes = [C.c_int, dbl]
+        L.ref_mesh_generate_jittered.restype = vp
+        L.ref_mesh_generate_jittered.argtypes = [C.c_int, dbl, i64]
         L.ref_mesh_from_arrays.restype = vp
         L.ref_mesh_from_arrays.argtypes = [vp, i64, vp, vp, i64]
         L.ref_mesh_sizes.argtypes = [vp, P(i64), P(i64)]
@@ -66,10 +68,13 @@ def _p(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def generate_mesh(res: int, delta: float):
-    """Reference generate_mesh(3, res, delta) -> (coords, cells, region)."""
+def generate_mesh(res: int, delta: float, jitter_seed: int | None = None):
+    """Reference generate_mesh(3, res, delta) -> (coords, cells, region);
+    jitter_seed: the config-3 interior-vertex jitter drawn with the
+    reference's own nlfem::Rng (oracle/ref_driver.cpp)."""
     L = lib()
-    h = L.ref_mesh_generate(res, delta)
+    h = (L.ref_mesh_generate(res, delta) if jitter_seed is None
+         else L.ref_mesh_generate_jittered(res, delta, int(jitter_seed)))
     nn, nc = C.c_int64(), C.c_int64()
     L.ref_mesh_sizes(h, C.byref(nn), C.byref(nc))
     coords = np.empty((nn.value, 3), np.float64)

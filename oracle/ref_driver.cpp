@@ -87,6 +87,30 @@ void* ref_mesh_generate(int res, double delta) {
   }
 }
 
+// Config-3 jitter (builder-defined): the reference's own
+// nlfem::Rng (core.hpp:108-133) seeded with `seed`; for every node in id
+// order draw u0, u1, u2; a node strictly inside (0,1)^3 (lattice index
+// 0 < i < res per axis) moves by h (0.4 u - 0.2) per axis.
+void* ref_mesh_generate_jittered(int res, double delta, std::int64_t seed) {
+  try {
+    auto* md = new MeshData(generate_mesh(3, res, delta));
+    nlfem::Rng rng(static_cast<std::uint64_t>(seed));
+    const double h = 1.0 / res;
+    for (auto& p : md->coords) {
+      const double u0 = rng.uniform(), u1 = rng.uniform(), u2 = rng.uniform();
+      const long i = std::lround(p.x * res), j = std::lround(p.y * res), k = std::lround(p.z * res);
+      if (i > 0 && i < res && j > 0 && j < res && k > 0 && k < res) {
+        p.x = p.x + h * (0.4 * u0 - 0.2);
+        p.y = p.y + h * (0.4 * u1 - 0.2);
+        p.z = p.z + h * (0.4 * u2 - 0.2);
+      }
+    }
+    return md;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
 void* ref_mesh_from_arrays(const double* coords, std::int64_t nnodes,
                            const std::int32_t* cells, const std::uint8_t* region,
                            std::int64_t ncells) {

@@ -953,8 +953,11 @@ void* oracle_assemble(int K, int Jn, const double* node, const int32_t* verts,
                       const double* volume, const double* diam, const uint8_t* region,
                       const double* inv, const int32_t* dof_of_node, int unknowns, double C,
                       double delta, const double* fterms, int nf, const double* gterms, int ng,
-                      int strategy, uint64_t seed, int M, int sampler, int threads, int* code,
-                      char* err, int errlen) {
+                      int strategy, uint64_t seed, int M, int sampler, int threads,
+                      const int32_t* outer, int64_t n_outer, int* code, char* err, int errlen) {
+  // outer != NULL: integrate only these outer elements (interior ids, in the
+  // given order) -- a partial system for sampled parity at full mesh sizes;
+  // NULL: every interior element, as assembly.cpp:624-627
   using namespace orc;
   *code = 0;
   try {
@@ -967,8 +970,14 @@ void* oracle_assemble(int K, int Jn, const double* node, const int32_t* verts,
     J.tau.resize(K);
     for (int t = 0; t < K; ++t) {
       J.tau[t] = 1e-14 * std::pow(diam[t], 3);
-      if (!region[t]) J.interior.push_back(t);
+      if (!region[t] && !outer) J.interior.push_back(t);
     }
+    if (outer)
+      for (int64_t i = 0; i < n_outer; ++i) {
+        if (outer[i] < 0 || outer[i] >= K || region[outer[i]])
+          throw Err(8, "BadConfig: outer element is not interior");
+        J.interior.push_back(outer[i]);
+      }
     J.gnode.assign(Jn, 0.0);
     for (int v = 0; v < Jn; ++v)
       if (dof_of_node[v] < 0) J.gnode[v] = J.g.eval({node[3 * v], node[3 * v + 1], node[3 * v + 2]});

@@ -66,3 +66,42 @@ def walk_sets(rows):
     for key, d in tmp.items():
         out[key] = {(par, "W" if kinds == [0] else "P") for par, kinds in d.items()}
     return out
+
+
+def cluster_rows(t, res, nclusters, rng):
+    """Seeded clusters of unknowns of a lattice (or jittered lattice) mesh: a
+    node and its +x / +y lattice neighbours when they are unknowns; the first
+    cluster in the bulk (>= 0.3 from the boundary of [0,1]^3), the second next
+    to the boundary.  Returns (sorted unknown rows, their node ids)."""
+    dof = t.dof_of_node
+    xyz = t.coords
+    unk = np.nonzero(dof >= 0)[0]
+    h = 1.0 / res
+    dist = np.min(np.minimum(xyz[unk], 1.0 - xyz[unk]), axis=1)
+    picks = [rng.choice(unk[dist > 0.3])]
+    if nclusters > 1:
+        picks.append(rng.choice(unk[dist < 1.5 * h]))
+    nodes = []
+    for v in picks:
+        for off in ((0, 0, 0), (h, 0, 0), (0, h, 0)):
+            p = xyz[v] + np.array(off)
+            j = int(np.argmin(np.abs(xyz - p).sum(axis=1)))
+            if dof[j] >= 0 and np.abs(xyz[j] - p).max() < 0.45 * h:
+                nodes.append(j)
+    nodes = sorted(set(nodes))
+    return sorted({int(dof[j]) for j in nodes}), nodes
+
+
+def affecting_outer(t, delta, nodes):
+    """Every interior (outer) element whose element pairs can put an entry in
+    the rows of `nodes`: v in T gives |c_T - x_v| <= r_T; v in T' with T'
+    meeting B_delta(x_q), x_q in T, gives |c_T - x_v| <= delta + 2 r_T' + r_T.
+    So centre within delta + 3 r_max (a superset; extra elements only add to
+    other rows)."""
+    interior = np.nonzero(t.region == 0)[0]
+    reach = (delta + 3.0 * float(t.radius.max())) * (1 + 1e-6) + 1e-12
+    c = t.center[interior]
+    keep = np.zeros(len(interior), bool)
+    for v in nodes:
+        keep |= np.sum((c - t.coords[v]) ** 2, axis=1) <= reach * reach
+    return interior[keep].astype(np.int32)

@@ -13,7 +13,8 @@ DEMO = os.path.join(ROOT, "oracle", "_ref", "adapter_demo")
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(DEMO), reason="oracle/_ref/adapter_demo not built")
-@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "fullcaps"])
+@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "approxcaps",
+                                   "fullcaps"])
 def test_adapter_drop_in_matches_reference(strat):
     out = subprocess.run([DEMO, "6", "0.34", strat], capture_output=True, text=True, timeout=600)
     rec = json.loads(out.stdout.strip().splitlines()[-1])

@@ -23,6 +23,30 @@ def test_generate_mesh_matches_fixture(name, res, delta, jit):
     assert np.array_equal(m["region"], g["region"])
 
 
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("res,delta", [(4, 0.3), (5, 0.4), (6, 0.25), (7, 0.3), (8, 0.25),
+                                       (8, 0.375)])
+def test_generate_mesh_matches_reference(res, delta):
+    # the restated lattice generator against the reference's own
+    # generate_mesh (mesh.cpp:115-121) -- not against fixtures it produced
+    coords, cells, region = ref.generate_mesh(res, delta)
+    m = P.generate_mesh(3, res, delta)
+    assert np.array_equal(m["coords"], coords)
+    assert np.array_equal(m["cells"], cells)
+    assert np.array_equal(m["region"], region)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("res,delta", [(5, 0.4), (10, 0.3), (24, 0.125)])
+def test_jittered_mesh_matches_reference_rng(res, delta):
+    # the config-3 jitter, drawn with the reference's own nlfem::Rng
+    coords, cells, region = ref.generate_mesh(res, delta, jitter_seed=7)
+    m = P.generate_mesh(3, res, delta, jitter_seed=7)
+    assert np.array_equal(m["coords"], coords)
+    assert np.array_equal(m["cells"], cells)
+    assert np.array_equal(m["region"], region)
+
+
 def test_mesh_sizes():
     # K = 6 (N+2L)^3, nodes (N+2L+1)^3
     for N, d in ((8, 0.25), (32, 0.1)):

@@ -104,3 +104,43 @@ def test_bad_config():
     with pytest.raises(port.OracleError) as ei:
         _run(t, 0.3, "fullcaps", 0, "P")
     assert ei.value.code == 8
+
+
+def test_outer_subset_rows_are_complete():
+    # the sampled-row parity at full sizes (tests/test_gpu_fullsize_values.py)
+    # relies on affecting_outer() covering every outer element that touches a
+    # row: on a delta = 3h mesh the oracle's rows from that subset equal its
+    # rows of the whole system (pattern exact, values to rounding of the
+    # different block merge order)
+    import paper_2302_07499_b200 as P
+    from tests.helpers import affecting_outer, cluster_rows, U2
+    res, delta = 10, 0.3
+    m = P.generate_mesh(3, res, delta, jitter_seed=7)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    full = _run(t, delta, "nocaps", 1, "R")
+    rows, nodes = cluster_rows(t, res, 2, np.random.default_rng(5))
+    assert len(rows) >= 4
+    outer = affecting_outer(t, delta, nodes)
+    assert 0 < len(outer) < int((t.region == 0).sum())
+    sub = port.assemble(t, delta, "nocaps", P.kernel_constant(delta, "moment2"),
+                        P.forcing_terms(delta, U2, "moment2"), P.normalize_terms(U2),
+                        seed=1234, mc_samples=1, sampler="R", outer=outer)
+    for r in rows:
+        a, b = full["row_ptr"][r], full["row_ptr"][r + 1]
+        c, d = sub["row_ptr"][r], sub["row_ptr"][r + 1]
+        assert np.array_equal(full["col_idx"][a:b], sub["col_idx"][c:d]), r
+        rm = np.abs(full["values"][a:b]).max()
+        assert np.abs(full["values"][a:b] - sub["values"][c:d]).max() <= 1e-13 * rm, r
+        assert abs(full["rhs"][r] - sub["rhs"][r]) <= 1e-13 * np.abs(full["rhs"]).max(), r
+    # dropping the outer elements at one sampled node changes its row (the
+    # comparison has teeth)
+    v = nodes[0]
+    keep = outer[~np.any(t.verts[outer] == v, axis=1)]
+    assert len(keep) < len(outer)
+    sub2 = port.assemble(t, delta, "nocaps", P.kernel_constant(delta, "moment2"),
+                         P.forcing_terms(delta, U2, "moment2"), P.normalize_terms(U2),
+                         seed=1234, mc_samples=1, sampler="R", outer=keep)
+    r = int(t.dof_of_node[v])
+    a, b = full["row_ptr"][r], full["row_ptr"][r + 1]
+    c, d = sub2["row_ptr"][r], sub2["row_ptr"][r + 1]
+    assert (b - a != d - c) or np.abs(full["values"][a:b] - sub2["values"][c:d]).max() > 1e-8
