@@ -9,22 +9,29 @@
  *     the ball;
  *   - mc_samples draws per sub-simplex, weight vol(sub)/mc_samples per hit,
  *     accept iff |y - x_q|^2 < delta^2;
- *   - uniform points by sorted spacings (quadrature.cpp:94-108).
+ *   - uniform points by sorted spacings (quadrature.cpp:94-108):
+ *     y = u0 V0 + (u1-u0) V1 + (u2-u1) V2 + (1-u2) V3, u0 <= u1 <= u2.
  * What is ours (the reference uses xoshiro256++ keyed by a walk-order piece
  * index, assembly.cpp:386-387, which a parallel kernel cannot reproduce):
  *   - Philox4x32-10 (Salmon et al. 2011; Random123 constants), key =
  *     (seed & 0xffffffff, seed >> 32);
- *   - sample k of sub-simplex `sub` of item (outer elem T, quad pt q, inner
- *     elem T') uses block j = k / 4 of counters
- *         (T, T', q | sub << 2, 3j + c),  c = 0, 1, 2
- *     whose 12 output words W[0..11] give uniforms W[3i], W[3i+1], W[3i+2] to
- *     sample k = 4j + i;
- *   - u = (w + 0.5) * 2^-32, the three sorted as integers first;
- *   - the point relative to x_q, with sorted u0 <= u1 <= u2 and sub-simplex
- *     vertices V0..V3:  r = (V3 - x_q) + u0 (V0-V1) + u1 (V1-V2) + u2 (V2-V3),
- *     evaluated with the fused multiply-adds written below (this is the
- *     reference's  y = u0 V0 + (u1-u0) V1 + (u2-u1) V2 + (1-u2) V3  regrouped);
- *   - accept iff fma(rz, rz, fma(ry, ry, rx*rx)) < delta*delta.
+ *   - samples come in blocks of four: block j of sub-simplex `sub` of item
+ *     (outer elem T, quad pt q, inner elem T') is the 8 words W[0..7] of the
+ *     counters  (T, T', q | sub << 2, 2j + c),  c = 0, 1;  sample k = 4j + i;
+ *   - each sample takes three 21-bit fields (two samples per Philox output):
+ *     sample 2c   : W[4c] >> 11, W[4c+1] >> 11, W[4c+2] >> 11
+ *     sample 2c+1 : ((W[4c+t] & 0x7ff) << 10) | ((W[4c+3] >> (22 - 10 t)) & 0x3ff),
+ *                   t = 0, 1, 2;
+ *     sorted s0 <= s1 <= s2 as integers, u_t = (s_t + 1/2) 2^-21;
+ *   - with F_t = 2^-21 E_t (E0 = V0-V1, E1 = V1-V2, E2 = V2-V3, exact power-of-
+ *     two scaling) the point is y - x_q = a + s0 F0 + s1 F1 + s2 F2,
+ *     a = (V3 - x_q) + (F0 + F1 + F2)/2 (the spacings formula regrouped), and
+ *     the hit test evaluates |y - x_q|^2 as the quadratic form in s,
+ *         Q(s) = c + s.(b + A s),   c = |a|^2, b_t = 2 F_t.a, A_tu = F_t.F_u,
+ *     in the fused multiply-add order written below: accept iff Q < delta^2.
+ *     (No point is formed for the test; the GPU accumulates the exact integer
+ *     moments sum s, sum s s^T of the hits and maps them through a and F once
+ *     per sub-simplex.)
  */
 #ifndef NLFEM_MC_STREAM_H
 #define NLFEM_MC_STREAM_H
@@ -80,17 +87,29 @@ NLFEM_HD void nlfem_philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_
   out[3] = c3;
 }
 
-/* The 12 words of sample block j of sub-simplex `sub` of item (T, q, T'). */
+/* The 8 words of sample block j of sub-simplex `sub` of item (T, q, T'). */
 NLFEM_HD void nlfem_mc_block(uint64_t seed, uint32_t T, uint32_t Tp, uint32_t q,
-                             uint32_t sub, uint32_t j, uint32_t W[12]) {
+                             uint32_t sub, uint32_t j, uint32_t W[8]) {
   const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
-  for (uint32_t c = 0; c < 3; ++c) {
-    const uint32_t ctr[4] = {T, Tp, q | (sub << 2), 3u * j + c};
+  for (uint32_t c = 0; c < 2; ++c) {
+    const uint32_t ctr[4] = {T, Tp, q | (sub << 2), 2u * j + c};
     nlfem_philox4x32_10(ctr, k0, k1, W + 4 * c);
   }
 }
 
-NLFEM_HD double nlfem_u01(uint32_t w) { return ((double)w + 0.5) * 0x1.0p-32; }
+/* The three 21-bit fields of sample i (0..3) of a block. */
+NLFEM_HD void nlfem_mc_fields(const uint32_t W[8], int i, uint32_t f[3]) {
+  const uint32_t* w = W + 4 * (i >> 1);
+  if ((i & 1) == 0) {
+    f[0] = w[0] >> 11;
+    f[1] = w[1] >> 11;
+    f[2] = w[2] >> 11;
+  } else {
+    f[0] = ((w[0] & 0x7ffu) << 10) | ((w[3] >> 22) & 0x3ffu);
+    f[1] = ((w[1] & 0x7ffu) << 10) | ((w[3] >> 12) & 0x3ffu);
+    f[2] = ((w[2] & 0x7ffu) << 10) | ((w[3] >> 2) & 0x3ffu);
+  }
+}
 
 NLFEM_HD void nlfem_sort3u(uint32_t* a, uint32_t* b, uint32_t* c) {
   uint32_t x = *a, y = *b, z = *c, t;
@@ -102,31 +121,60 @@ NLFEM_HD void nlfem_sort3u(uint32_t* a, uint32_t* b, uint32_t* c) {
   *c = z;
 }
 
-/* Sub-simplex frame for sampling: E0 = V0-V1, E1 = V1-V2, E2 = V2-V3,
- * P = V3 - x_q (plain IEEE subtractions). */
+/* Per-sub-simplex constants: F_t = 2^-21 E_t (rows), a, and the quadratic
+ * form Q(s) = c + s.(b + A s) of |y - x_q|^2 (A2 = off-diagonals doubled). */
 typedef struct {
-  double e0[3], e1[3], e2[3], p[3];
-} nlfem_mc_frame;
+  double F[3][3], a[3];
+  double c, b[3], A[3], A2[3]; /* A: 00 11 22; A2: 2*01 2*02 2*12 */
+} nlfem_mc_quad;
 
-NLFEM_HD void nlfem_mc_make_frame(const double v0[3], const double v1[3], const double v2[3],
-                                  const double v3[3], const double xq[3], nlfem_mc_frame* f) {
-  for (int a = 0; a < 3; ++a) {
-    f->e0[a] = v0[a] - v1[a];
-    f->e1[a] = v1[a] - v2[a];
-    f->e2[a] = v2[a] - v3[a];
-    f->p[a] = v3[a] - xq[a];
-  }
+NLFEM_HD double nlfem_dot3(const double x[3], const double y[3]) {
+  return fma(x[2], y[2], fma(x[1], y[1], x[0] * y[0]));
 }
 
-/* One sample from three raw words: writes r = y - x_q, returns 1 on a hit. */
-NLFEM_HD int nlfem_mc_point(uint32_t w0, uint32_t w1, uint32_t w2, const nlfem_mc_frame* f,
-                            double dd, double r[3]) {
-  nlfem_sort3u(&w0, &w1, &w2);
-  const double u0 = nlfem_u01(w0), u1 = nlfem_u01(w1), u2 = nlfem_u01(w2);
-  for (int a = 0; a < 3; ++a)
-    r[a] = fma(u2, f->e2[a], fma(u1, f->e1[a], fma(u0, f->e0[a], f->p[a])));
-  const double d2 = fma(r[2], r[2], fma(r[1], r[1], r[0] * r[0]));
-  return d2 < dd;
+NLFEM_HD void nlfem_mc_make_quad(const double v0[3], const double v1[3], const double v2[3],
+                                 const double v3[3], const double xq[3], nlfem_mc_quad* Q) {
+  for (int t = 0; t < 3; ++t) {
+    Q->F[0][t] = (v0[t] - v1[t]) * 0x1p-21;
+    Q->F[1][t] = (v1[t] - v2[t]) * 0x1p-21;
+    Q->F[2][t] = (v2[t] - v3[t]) * 0x1p-21;
+  }
+  for (int t = 0; t < 3; ++t)
+    Q->a[t] = (v3[t] - xq[t]) + ((Q->F[0][t] + Q->F[1][t]) + Q->F[2][t]) * 0.5;
+  Q->c = nlfem_dot3(Q->a, Q->a);
+  for (int t = 0; t < 3; ++t) {
+    Q->b[t] = 2.0 * nlfem_dot3(Q->F[t], Q->a);
+    Q->A[t] = nlfem_dot3(Q->F[t], Q->F[t]);
+  }
+  Q->A2[0] = 2.0 * nlfem_dot3(Q->F[0], Q->F[1]);
+  Q->A2[1] = 2.0 * nlfem_dot3(Q->F[0], Q->F[2]);
+  Q->A2[2] = 2.0 * nlfem_dot3(Q->F[1], Q->F[2]);
+}
+
+/* Q(s) for the sorted fields as exact doubles d_t = s_t. */
+NLFEM_HD double nlfem_mc_q(const nlfem_mc_quad* Q, double d0, double d1, double d2) {
+  const double t0 = fma(Q->A[0], d0, fma(Q->A2[0], d1, fma(Q->A2[1], d2, Q->b[0])));
+  const double t1 = fma(Q->A[1], d1, fma(Q->A2[2], d2, Q->b[1]));
+  const double t2 = fma(Q->A[2], d2, Q->b[2]);
+  return fma(d0, t0, fma(d1, t1, fma(d2, t2, Q->c)));
+}
+
+/* The sample's offset r = y - x_q = a + F^T d (for per-hit evaluations). */
+NLFEM_HD void nlfem_mc_r(const nlfem_mc_quad* Q, double d0, double d1, double d2, double r[3]) {
+  for (int t = 0; t < 3; ++t)
+    r[t] = fma(d2, Q->F[2][t], fma(d1, Q->F[1][t], fma(d0, Q->F[0][t], Q->a[t])));
+}
+
+/* One sample i of a block: the sorted fields as doubles; returns 1 on a hit. */
+NLFEM_HD int nlfem_mc_sample(const uint32_t W[8], int i, const nlfem_mc_quad* Q, double dd,
+                             double d[3]) {
+  uint32_t f[3];
+  nlfem_mc_fields(W, i, f);
+  nlfem_sort3u(&f[0], &f[1], &f[2]);
+  d[0] = (double)f[0];
+  d[1] = (double)f[1];
+  d[2] = (double)f[2];
+  return nlfem_mc_q(Q, d[0], d[1], d[2]) < dd;
 }
 
 #endif /* NLFEM_MC_STREAM_H */

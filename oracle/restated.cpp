@@ -578,18 +578,18 @@ struct Acc {
       const double w = tvol(s.v[0], s.v[1], s.v[2], s.v[3]) / J.M;
       const double v0[3] = {s.v[0].x, s.v[0].y, s.v[0].z}, v1[3] = {s.v[1].x, s.v[1].y, s.v[1].z},
                    v2[3] = {s.v[2].x, s.v[2].y, s.v[2].z}, v3[3] = {s.v[3].x, s.v[3].y, s.v[3].z};
-      nlfem_mc_frame fr;
-      nlfem_mc_make_frame(v0, v1, v2, v3, xq, &fr);
-      uint32_t W[12];
+      nlfem_mc_quad Q;
+      nlfem_mc_make_quad(v0, v1, v2, v3, xq, &Q);
+      uint32_t W[8];
       for (int k = 0; k < J.M; ++k) {
         if (k % 4 == 0)
           nlfem_mc_block(J.seed, uint32_t(elemN), uint32_t(t), uint32_t(q), uint32_t(sb),
                          uint32_t(k / 4), W);
-        const int i = k % 4;
-        double r[3];
+        double d[3], r[3];
         ++mc_done;
-        if (!nlfem_mc_point(W[3 * i], W[3 * i + 1], W[3 * i + 2], &fr, r2, r)) continue;
+        if (!nlfem_mc_sample(W, k % 4, &Q, r2, d)) continue;
         ++mc_hit;
+        nlfem_mc_r(&Q, d[0], d[1], d[2], r);
         point({p.x + r[0], p.y + r[1], p.z + r[2]}, w);
       }
     }

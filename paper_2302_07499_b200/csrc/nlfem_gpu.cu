@@ -1328,76 +1328,123 @@ __global__ void k_pair_outer(int ii0, int ii1, const long long* pair_off, long l
 
 // Philox4x32-10 on three counters in lockstep (independent chains -> ILP 3);
 // same function as nlfem_philox4x32_10 applied to each counter.
-__device__ __forceinline__ void philox3(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t j3,
-                                        uint32_t A[4], uint32_t B[4], uint32_t Cw[4]) {
-  uint32_t a0 = c0, a1 = c1, a2 = c2, a3 = j3;
-  uint32_t b0 = c0, b1 = c1, b2 = c2, b3 = j3 + 1;
-  uint32_t d0 = c0, d1 = c1, d2 = c2, d3 = j3 + 2;
+__device__ __forceinline__ void philox2(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t j2,
+                                        uint32_t A[4], uint32_t B[4]) {
+  uint32_t a0 = c0, a1 = c1, a2 = c2, a3 = j2;
+  uint32_t b0 = c0, b1 = c1, b2 = c2, b3 = j2 + 1;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const unsigned long long pa0 = (unsigned long long)NLFEM_PHILOX_M0 * a0;
     const unsigned long long pa2 = (unsigned long long)NLFEM_PHILOX_M1 * a2;
     const unsigned long long pb0 = (unsigned long long)NLFEM_PHILOX_M0 * b0;
     const unsigned long long pb2 = (unsigned long long)NLFEM_PHILOX_M1 * b2;
-    const unsigned long long pd0 = (unsigned long long)NLFEM_PHILOX_M0 * d0;
-    const unsigned long long pd2 = (unsigned long long)NLFEM_PHILOX_M1 * d2;
     // round keys from constant memory: LOP3 reads them as c[][] operands
     const uint32_t kk0 = cD.rkey[2 * r], kk1 = cD.rkey[2 * r + 1];
     a0 = (uint32_t)(pa2 >> 32) ^ a1 ^ kk0; a1 = (uint32_t)pa2;
     a2 = (uint32_t)(pa0 >> 32) ^ a3 ^ kk1; a3 = (uint32_t)pa0;
     b0 = (uint32_t)(pb2 >> 32) ^ b1 ^ kk0; b1 = (uint32_t)pb2;
     b2 = (uint32_t)(pb0 >> 32) ^ b3 ^ kk1; b3 = (uint32_t)pb0;
-    d0 = (uint32_t)(pd2 >> 32) ^ d1 ^ kk0; d1 = (uint32_t)pd2;
-    d2 = (uint32_t)(pd0 >> 32) ^ d3 ^ kk1; d3 = (uint32_t)pd0;
   }
   A[0] = a0; A[1] = a1; A[2] = a2; A[3] = a3;
   B[0] = b0; B[1] = b1; B[2] = b2; B[3] = b3;
-  Cw[0] = d0; Cw[1] = d1; Cw[2] = d2; Cw[3] = d3;
 }
 
-// w + 0.5 as a double with one DADD: the bits 0x43300000:w are 2^52 + w
-__device__ __forceinline__ double u32_plus_half(uint32_t w) {
-  return __hiloint2double(0x43300000, (int)w) - 4503599627370495.5;  // 2^52 - 0.5
+#ifndef NLFEM_MC_I2F
+#define NLFEM_MC_I2F 0
+#endif
+// a 21-bit field as an exact double with one DADD: the bits 0x43300000:s are 2^52 + s
+__device__ __forceinline__ double u21_to_double(uint32_t s) {
+#if NLFEM_MC_I2F
+  return __uint2double_rn(s);  // I2F.F64.U32
+#else
+  return __hiloint2double(0x43300000, (int)s) - 4503599627370496.0;  // 2^52
+#endif
 }
 
-// nlfem_mc_point with the frame pre-scaled by 2^-32 (E' = 2^-32 E): since
-// u E = (w + 1/2) 2^-32 E = (w + 1/2) E' exactly, fma(u, E, p) == fma(w + 1/2, E', p)
-// bit for bit, so decisions and r equal include/nlfem_mc_stream.h's.
-__device__ __forceinline__ double mc_point_r2(uint32_t w0, uint32_t w1, uint32_t w2,
-                                               const nlfem_mc_frame& f, double& rx, double& ry,
-                                               double& rz) {
-  // sorted words: 3-input min/max (VIMNMX3) and the median from the sum, exact
-  // in u32 wrap-around arithmetic
-  const uint32_t s0 = min(min(w0, w1), w2), s2 = max(max(w0, w1), w2);
-  const uint32_t s1 = w0 + w1 + w2 - s0 - s2;
-  const double u0 = u32_plus_half(s0), u1 = u32_plus_half(s1), u2 = u32_plus_half(s2);
-  rx = fma(u2, f.e2[0], fma(u1, f.e1[0], fma(u0, f.e0[0], f.p[0])));
-  ry = fma(u2, f.e2[1], fma(u1, f.e1[1], fma(u0, f.e0[1], f.p[1])));
-  rz = fma(u2, f.e2[2], fma(u1, f.e1[2], fma(u0, f.e0[2], f.p[2])));
-  return fma(rz, rz, fma(ry, ry, rx * rx));
+// the sorted fields of the even / odd sample of a Philox output w[0..3]
+// (nlfem_mc_fields, include/nlfem_mc_stream.h): 3-input min / max (VIMNMX3)
+// and the median from the sum (exact: the fields are < 2^21)
+__device__ __forceinline__ void sorted3(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t& s0,
+                                        uint32_t& s1, uint32_t& s2) {
+  s0 = min(min(f0, f1), f2);
+  s2 = max(max(f0, f1), f2);
+  s1 = f0 + f1 + f2 - s0 - s2;
+}
+__device__ __forceinline__ void fields_even(const uint32_t w[4], uint32_t& s0, uint32_t& s1,
+                                            uint32_t& s2) {
+  sorted3(w[0] >> 11, w[1] >> 11, w[2] >> 11, s0, s1, s2);
+}
+__device__ __forceinline__ void fields_odd(const uint32_t w[4], uint32_t& s0, uint32_t& s1,
+                                           uint32_t& s2) {
+  // (w_t << 10) | bits of w3: a funnel shift and a mask each
+  sorted3(__funnelshift_l(w[3], w[0], 10) & 0x1fffffu,
+          __funnelshift_l(w[3] << 10, w[1], 10) & 0x1fffffu,
+          __funnelshift_l(w[3] << 20, w[2], 10) & 0x1fffffu, s0, s1, s2);
 }
 
-// hit test r2 < dd and, on a hit, n += 1, t1 += r, t2 += r r^T (upper, 6).
-// A plain branch: ptxas lowers predicated FP64 ops to FSEL pairs, which cost
-// more than the (almost always warp-uniform-taken) branch.
-struct HitMoments {
+// Hit test Q(s) < delta^2 (nlfem_mc_q) and, on a hit, the exact moments of
+// the sorted fields: n and sum s in u32 (< 2^21 per sample, <= 1024 samples
+// per segment), sum s s^T in FP64 -- the products of two fields are integers
+// < 2^42 and their sum over a segment < 2^52, so every DFMA is exact.  The
+// fields are masked (zero on a miss), not branched on: the warp issues no
+// divergent code.  The mix balances the pipes: Philox's IMAD.WIDE.U32s keep
+// the FMA-heavy pipe busy, so the six products go to the FP64 pipe (ncu at
+// P3f with them as IMAD.WIDEs: FMA-heavy 59% busy against 55% issue).
+struct IntMoments {
   unsigned n = 0;
-  double t1x = 0, t1y = 0, t1z = 0, t2[6] = {0, 0, 0, 0, 0, 0};
-  __device__ __forceinline__ void add(double r2, double dd, double rx, double ry, double rz) {
-    if (r2 < dd) {
-      ++n;
-      t1x += rx;
-      t1y += ry;
-      t1z += rz;
-      t2[0] = fma(rx, rx, t2[0]);
-      t2[1] = fma(rx, ry, t2[1]);
-      t2[2] = fma(rx, rz, t2[2]);
-      t2[3] = fma(ry, ry, t2[3]);
-      t2[4] = fma(ry, rz, t2[4]);
-      t2[5] = fma(rz, rz, t2[5]);
-    }
+  uint32_t s[3] = {0, 0, 0};
+  double ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
+  __device__ __forceinline__ void sample(const nlfem_mc_quad& Q, double dd, uint32_t s0,
+                                         uint32_t s1, uint32_t s2) {
+    const double d0 = u21_to_double(s0), d1 = u21_to_double(s1), d2 = u21_to_double(s2);
+    const bool hit = nlfem_mc_q(&Q, d0, d1, d2) < dd;
+    const uint32_t m = hit ? 0xffffffffu : 0u;
+    n -= m;  // += 1 on a hit
+    s[0] += s0 & m;
+    s[1] += s1 & m;
+    s[2] += s2 & m;
+    const double h = hit ? 1.0 : 0.0;
+    const double m0 = h * d0, m1 = h * d1, m2 = h * d2;
+    ss[0] = fma(m0, d0, ss[0]);
+    ss[1] = fma(m0, d1, ss[1]);
+    ss[2] = fma(m0, d2, ss[2]);
+    ss[3] = fma(m1, d1, ss[3]);
+    ss[4] = fma(m1, d2, ss[4]);
+    ss[5] = fma(m2, d2, ss[5]);
   }
 };
+
+// Moments of the hits about x_q from the integer sums: with r = a + F^T s,
+//   sum r = n a + g,  g = F^T sum s,
+//   sum r r^T = n a a^T + a g^T + g a^T + F^T (sum s s^T) F   (upper 6),
+// added to t1 / t2 (FP64); the integer sums are exact, so this is the sum of
+// the hits' r and r r^T up to the rounding of these few products.
+__device__ __forceinline__ void fold_moments(const nlfem_mc_quad& Q, const IntMoments& im,
+                                             double& nh, double t1[3], double t2[6]) {
+  const double n = (double)im.n;
+  const double S[3] = {(double)im.s[0], (double)im.s[1], (double)im.s[2]};
+  const double SS[3][3] = {{im.ss[0], im.ss[1], im.ss[2]},
+                           {im.ss[1], im.ss[3], im.ss[4]},
+                           {im.ss[2], im.ss[4], im.ss[5]}};
+  double g[3], H[3][3];  // g = F^T S; H[t][y] = sum_u SS[t][u] F[u][y]
+#pragma unroll
+  for (int y = 0; y < 3; ++y) {
+    g[y] = S[0] * Q.F[0][y] + S[1] * Q.F[1][y] + S[2] * Q.F[2][y];
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+      H[t][y] = SS[t][0] * Q.F[0][y] + SS[t][1] * Q.F[1][y] + SS[t][2] * Q.F[2][y];
+  }
+  nh += n;
+#pragma unroll
+  for (int x = 0; x < 3; ++x) t1[x] += n * Q.a[x] + g[x];
+  int k = 0;
+#pragma unroll
+  for (int x = 0; x < 3; ++x)
+#pragma unroll
+    for (int y = x; y < 3; ++y, ++k)
+      t2[k] += (n * Q.a[x] * Q.a[y] + Q.a[x] * g[y] + g[x] * Q.a[y]) +
+               (Q.F[0][x] * H[0][y] + Q.F[1][x] * H[1][y] + Q.F[2][x] * H[2][y]);
+}
 
 constexpr long long kMomStride = 10;   // doubles per MC item record (80 B)
 
@@ -1569,8 +1616,12 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
                                                       unsigned long long* mc_stats) {
   constexpr int NOUT = !OUTER ? 0 : ((CASE == 1 || CASE == 2) ? 3 : 1);  // outer pieces
   constexpr int NV = CONS ? 2 : 10;                       // record doubles
-  __shared__ double sP[NOUT == 3 ? 18 : 1][kMcThreads];  // outer prism points
-  __shared__ double sV[NOUT == 3 ? 3 : 1][kMcThreads];   // outer piece volumes
+  // per-thread item state parked in shared memory while the sample loop runs
+  // (it keeps only the quadratic form, the moments and the Philox state in
+  // registers): the outer pieces' points and volumes, x_q and x_q - v0(T')
+  __shared__ double sP[NOUT == 3 ? 18 : (NOUT == 1 ? 12 : 1)][kMcThreads];
+  __shared__ double sV[NOUT == 3 ? 3 : 1][kMcThreads];
+  __shared__ double sX[OUTER ? 6 : 1][kMcThreads];
   static_assert(OUTER || CASE != 0, "nocaps has no whole-element caps");
   __shared__ double sAcc[NV][kMcThreads];
   unsigned long long draws = 0, hits = 0, led = 0;
@@ -1688,121 +1739,163 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     }
 #pragma unroll
     for (int kk = 0; kk < NV; ++kk) sAcc[kk][threadIdx.x] = acc[kk];
+    if constexpr (OUTER) {
+      if constexpr (NOUT == 1) {  // park the single outer piece with the prism layout
+        const Vd P4[4] = {pa, pb, pc, pd};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sP[3 * k][threadIdx.x] = P4[k].x;
+          sP[3 * k + 1][threadIdx.x] = P4[k].y;
+          sP[3 * k + 2][threadIdx.x] = P4[k].z;
+        }
+        sV[0][threadIdx.x] = vol1;
+      }
+      sX[0][threadIdx.x] = xq.x;
+      sX[1][threadIdx.x] = xq.y;
+      sX[2][threadIdx.x] = xq.z;
+      sX[3][threadIdx.x] = xq.x - v0P.x;  // c0: moments about v0(T')
+      sX[4][threadIdx.x] = xq.y - v0P.y;
+      sX[5][threadIdx.x] = xq.z - v0P.z;
+    }
     const int M = cD.mc;
     const double dd = cD.dd;
     const double otau = CASE == 0 ? -1.0 : tau;
-    double g0 = 0, gr[3] = {0, 0, 0}, H[6] = {0, 0, 0, 0, 0, 0};
-    if (OUTER && CONS && G2) poly2_taylor(cD.g, xq, g0, gr, H);
     int kept = 0;
 #pragma unroll 1
     for (int k = 0; k < NOUT; ++k) {
-      double vol = vol1;
-      if (NOUT == 3) {  // prism piece k = points k .. k+3
+      // piece k = prism points k .. k+3 (the single piece: points 0 .. 3)
+      auto piece_quad = [&](nlfem_mc_quad& Qp) {
         const int r = 3 * k;
-        pa = {sP[r][threadIdx.x], sP[r + 1][threadIdx.x], sP[r + 2][threadIdx.x]};
-        pb = {sP[r + 3][threadIdx.x], sP[r + 4][threadIdx.x], sP[r + 5][threadIdx.x]};
-        pc = {sP[r + 6][threadIdx.x], sP[r + 7][threadIdx.x], sP[r + 8][threadIdx.x]};
-        pd = {sP[r + 9][threadIdx.x], sP[r + 10][threadIdx.x], sP[r + 11][threadIdx.x]};
-        vol = sV[k][threadIdx.x];
-      }
+        double v[4][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int t = 0; t < 3; ++t) v[i][t] = sP[r + 3 * i + t][threadIdx.x];
+        const double x[3] = {sX[0][threadIdx.x], sX[1][threadIdx.x], sX[2][threadIdx.x]};
+        nlfem_mc_make_quad(v[0], v[1], v[2], v[3], x, &Qp);
+      };
+      const double vol = sV[k][threadIdx.x];
       if (!(vol > otau)) continue;  // push_piece volume floor (ball_approx.cpp:141)
       const uint32_t c2 = (uint32_t)q | ((uint32_t)kept << 2);
       ++kept;
       const double w = cD.inv_mc > 0 ? vol * cD.inv_mc : vol / M;  // vol / M
-      nlfem_mc_frame fr;
-      {
-        const double a0[3] = {pa.x, pa.y, pa.z}, a1[3] = {pb.x, pb.y, pb.z},
-                     a2[3] = {pc.x, pc.y, pc.z}, a3[3] = {pd.x, pd.y, pd.z},
-                     x[3] = {xq.x, xq.y, xq.z};
-        nlfem_mc_make_frame(a0, a1, a2, a3, x, &fr);
-      }
-      nlfem_mc_frame fs = fr;  // frame pre-scaled by 2^-32 (exact)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        fs.e0[a] = fr.e0[a] * 0x1p-32;
-        fs.e1[a] = fr.e1[a] * 0x1p-32;
-        fs.e2[a] = fr.e2[a] * 0x1p-32;
-      }
-      // interior: sums of r and r r^T over hits, r = y - x_q; constraint: sum g(y)
-      HitMoments hm;
-      unsigned ngh = 0;
-      double ng = 0;
-      auto sample = [&](uint32_t a, uint32_t b, uint32_t cc, double ddv) {
-        double rx, ry, rz;
-        const double r2 = mc_point_r2(a, b, cc, fs, rx, ry, rz);
-        if (CONS && !G2) {
-          if (r2 < ddv) {
-            ++ngh;
-            ng += poly_eval(cD.g, {xq.x + rx, xq.y + ry, xq.z + rz});
-          }
+      unsigned nh = 0;
+      // the item record gains w x (the hits' S0 and moments about v0(T')) --
+      // linear in (n, sum r, sum r r^T), so it is added segment by segment
+      auto add_moments = [&](unsigned n_u, const double t1[3], const double t2[6]) {
+        const double n = (double)n_u;
+        nh += n_u;
+        double vals[NV];
+        vals[0] = w * n;
+        if constexpr (CONS) {
+          // sum over hits of g(x_q + r) = n g + grad g . sum r + 1/2 sum H_ab r_a r_b
+          double g0, gr[3], H[6];
+          poly2_taylor(cD.g, {sX[0][threadIdx.x], sX[1][threadIdx.x], sX[2][threadIdx.x]}, g0,
+                       gr, H);
+          const double quad = 0.5 * (H[0] * t2[0] + H[3] * t2[3] + H[5] * t2[5]) +
+                              H[1] * t2[1] + H[2] * t2[2] + H[4] * t2[4];
+          vals[1] = w * (n * g0 + gr[0] * t1[0] + gr[1] * t1[1] + gr[2] * t1[2] + quad);
         } else {
-          hm.add(r2, ddv, rx, ry, rz);
+          // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
+          const double c0x = sX[3][threadIdx.x], c0y = sX[4][threadIdx.x],
+                       c0z = sX[5][threadIdx.x];
+          vals[1] = w * (t1[0] + n * c0x);
+          vals[2 % NV] = w * (t1[1] + n * c0y);
+          vals[3 % NV] = w * (t1[2] + n * c0z);
+          vals[4 % NV] = w * (t2[0] + 2.0 * c0x * t1[0] + n * c0x * c0x);
+          vals[5 % NV] = w * (t2[1] + c0x * t1[1] + c0y * t1[0] + n * c0x * c0y);
+          vals[6 % NV] = w * (t2[2] + c0x * t1[2] + c0z * t1[0] + n * c0x * c0z);
+          vals[7 % NV] = w * (t2[3] + 2.0 * c0y * t1[1] + n * c0y * c0y);
+          vals[8 % NV] = w * (t2[4] + c0y * t1[2] + c0z * t1[1] + n * c0y * c0z);
+          vals[9 % NV] = w * (t2[5] + 2.0 * c0z * t1[2] + n * c0z * c0z);
         }
+        // item totals: inner pieces, then the kept outer pieces in piece order
+#pragma unroll
+        for (int kk = 0; kk < NV; ++kk) sAcc[kk][threadIdx.x] += vals[kk];
+      };
+      // the integer moments of a segment mapped through F and a, recomputed
+      // from the parked points (a compiler barrier first: F and a must not stay
+      // live in registers across the sample loop)
+      auto fold = [&](const IntMoments& im) {
+        asm volatile("" ::: "memory");
+        nlfem_mc_quad Qf;
+        piece_quad(Qf);
+        double n = 0, t1[3] = {0, 0, 0}, t2[6] = {0, 0, 0, 0, 0, 0};
+        fold_moments(Qf, im, n, t1, t2);
+        add_moments(im.n, t1, t2);
       };
       const int full = M >> 2;
-#pragma unroll kMcUnroll
-      for (int j = 0; j < full; ++j) {
-        // words W0..W11 of block j: sample i uses W[3i..3i+2] (include/nlfem_mc_stream.h)
-        uint32_t A[4], B[4], Cw[4];
-        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)j, A, B, Cw);
-        if (CONS && !G2) {
-          sample(A[0], A[1], A[2], dd);
-          sample(A[3], B[0], B[1], dd);
-          sample(B[2], B[3], Cw[0], dd);
-          sample(Cw[1], Cw[2], Cw[3], dd);
-        } else {
-          // the four points and |r|^2 first (four independent FP64 chains),
-          // then the hit updates
-          double rx[4], ry[4], rz[4], r2[4];
-          r2[0] = mc_point_r2(A[0], A[1], A[2], fs, rx[0], ry[0], rz[0]);
-          r2[1] = mc_point_r2(A[3], B[0], B[1], fs, rx[1], ry[1], rz[1]);
-          r2[2] = mc_point_r2(B[2], B[3], Cw[0], fs, rx[2], ry[2], rz[2]);
-          r2[3] = mc_point_r2(Cw[1], Cw[2], Cw[3], fs, rx[3], ry[3], rz[3]);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) hm.add(r2[i], dd, rx[i], ry[i], rz[i]);
+      if constexpr (CONS && !G2) {  // g of degree > 2: evaluated at every hit
+        nlfem_mc_quad Qd;
+        piece_quad(Qd);
+        const Vd xs = {sX[0][threadIdx.x], sX[1][threadIdx.x], sX[2][threadIdx.x]};
+        unsigned ngh = 0;
+        double ng = 0;
+        auto one = [&](uint32_t s0, uint32_t s1, uint32_t s2, double ddv) {
+          const double d0 = u21_to_double(s0), d1 = u21_to_double(s1), d2 = u21_to_double(s2);
+          if (nlfem_mc_q(&Qd, d0, d1, d2) < ddv) {
+            double r[3];
+            nlfem_mc_r(&Qd, d0, d1, d2, r);
+            ++ngh;
+            ng += poly_eval(cD.g, {xs.x + r[0], xs.y + r[1], xs.z + r[2]});
+          }
+        };
+        for (int j = 0; j <= full; ++j) {
+          const int rem = j < full ? 4 : (M & 3);
+          if (rem == 0) break;
+          uint32_t A[4], B[4], s0, s1, s2;
+          philox2((uint32_t)T, (uint32_t)Tp, c2, 2u * (uint32_t)j, A, B);
+          fields_even(A, s0, s1, s2);
+          one(s0, s1, s2, dd);
+          fields_odd(A, s0, s1, s2);
+          one(s0, s1, s2, rem > 1 ? dd : -1.0);
+          fields_even(B, s0, s1, s2);
+          one(s0, s1, s2, rem > 2 ? dd : -1.0);
+          fields_odd(B, s0, s1, s2);
+          one(s0, s1, s2, rem > 3 ? dd : -1.0);
         }
-      }
-      if (M & 3) {  // partial last block: samples past M are drawn but never hit
-        uint32_t A[4], B[4], Cw[4];
-        philox3((uint32_t)T, (uint32_t)Tp, c2, 3u * (uint32_t)full, A, B, Cw);
-        const int rem = M & 3;
-        sample(A[0], A[1], A[2], dd);
-        sample(A[3], B[0], B[1], rem > 1 ? dd : -1.0);
-        sample(B[2], B[3], Cw[0], rem > 2 ? dd : -1.0);
-      }
-      const unsigned nh = (CONS && !G2) ? ngh : hm.n;
-      const double t1x = hm.t1x, t1y = hm.t1y, t1z = hm.t1z;
-      const double* t2 = hm.t2;
-      double vals[NV];
-      vals[0] = w * nh;
-      if (CONS && G2) {
-        // sum over hits of g(x_q + r) = n g + grad g . sum r + 1/2 sum H_ab r_a r_b
-        const double n = (double)nh;
-        const double quad = 0.5 * (H[0] * t2[0] + H[3] * t2[3] + H[5] * t2[5]) +
-                            H[1] * t2[1] + H[2] * t2[2] + H[4] * t2[4];
-        vals[1] = w * (n * g0 + gr[0] * t1x + gr[1] * t1y + gr[2] * t1z + quad);
-      } else if (CONS) {
-        vals[1] = w * ng;
-      } else {
-        // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
-        const double c0x = xq.x - v0P.x, c0y = xq.y - v0P.y, c0z = xq.z - v0P.z;
-        const double n = (double)nh;
-        vals[1] = w * (t1x + n * c0x);
-        vals[2 % NV] = w * (t1y + n * c0y);
-        vals[3 % NV] = w * (t1z + n * c0z);
-        vals[4 % NV] = w * (t2[0] + 2.0 * c0x * t1x + n * c0x * c0x);
-        vals[5 % NV] = w * (t2[1] + c0x * t1y + c0y * t1x + n * c0x * c0y);
-        vals[6 % NV] = w * (t2[2] + c0x * t1z + c0z * t1x + n * c0x * c0z);
-        vals[7 % NV] = w * (t2[3] + 2.0 * c0y * t1y + n * c0y * c0y);
-        vals[8 % NV] = w * (t2[4] + c0y * t1z + c0z * t1y + n * c0y * c0z);
-        vals[9 % NV] = w * (t2[5] + 2.0 * c0z * t1z + n * c0z * c0z);
+        nh = ngh;
+        sAcc[0][threadIdx.x] += w * ngh;
+        sAcc[1][threadIdx.x] += w * ng;
+      } else if constexpr (OUTER) {
+        nlfem_mc_quad Qc;  // only the form's coefficients are read in the loop
+        piece_quad(Qc);
+        // segments of 256 blocks (1024 samples) keep the integer sums exact
+        for (int j0 = 0; j0 < full; j0 += 256) {
+          IntMoments im;
+          const int j1 = min(full, j0 + 256);
+#pragma unroll kMcUnroll
+          for (int j = j0; j < j1; ++j) {
+            uint32_t A[4], B[4], s0, s1, s2;
+            philox2((uint32_t)T, (uint32_t)Tp, c2, 2u * (uint32_t)j, A, B);
+            fields_even(A, s0, s1, s2);
+            im.sample(Qc, dd, s0, s1, s2);
+            fields_odd(A, s0, s1, s2);
+            im.sample(Qc, dd, s0, s1, s2);
+            fields_even(B, s0, s1, s2);
+            im.sample(Qc, dd, s0, s1, s2);
+            fields_odd(B, s0, s1, s2);
+            im.sample(Qc, dd, s0, s1, s2);
+          }
+          fold(im);
+        }
+        if (M & 3) {  // partial last block: samples past M are drawn but never hit
+          IntMoments im;
+          const int rem = M & 3;
+          uint32_t A[4], B[4], s0, s1, s2;
+          philox2((uint32_t)T, (uint32_t)Tp, c2, 2u * (uint32_t)full, A, B);
+          fields_even(A, s0, s1, s2);
+          im.sample(Qc, dd, s0, s1, s2);
+          fields_odd(A, s0, s1, s2);
+          im.sample(Qc, rem > 1 ? dd : -1.0, s0, s1, s2);
+          fields_even(B, s0, s1, s2);
+          im.sample(Qc, rem > 2 ? dd : -1.0, s0, s1, s2);
+          fold(im);
+        }
       }
       draws += (unsigned long long)M;
       hits += nh;
       led += 25ull + 35ull * (unsigned long long)M + (CONS ? 12ull : 62ull) * nh;
-      // item totals: inner pieces, then the kept outer pieces in piece order
-#pragma unroll
-      for (int kk = 0; kk < NV; ++kk) sAcc[kk][threadIdx.x] += vals[kk];
     }
     // one record per cap item: S0, then sum g (constraint parents) or sum r'
     // and sum r' r'^T (6) about v0(T') (interior parents), inner pieces included
@@ -3518,6 +3611,34 @@ void session_solve(nlfem_gpu_session& S, double tol, int32_t max_iter, const nlf
   out->device_ms = ms;
 }
 
+// Every entry point that touches a session runs under its device's lock and
+// with that device current (the caller's current device is restored on
+// return).  Sessions on one device share the per-device __constant__
+// parameter block cD, which each run / finalize rebinds, so two host threads
+// (ctypes releases the GIL) or two sessions driven alternately must not
+// interleave on a device.  Recursive: the one-shot call nests session calls.
+std::recursive_mutex& device_mutex(int dev) {
+  static std::recursive_mutex mu[64];
+  return mu[dev & 63];
+}
+struct DeviceScope {
+  int prev = -1;
+  std::unique_lock<std::recursive_mutex> lk;
+  explicit DeviceScope(int dev) : lk(device_mutex(dev < 0 ? 0 : dev)) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && prev != dev) cudaSetDevice(dev);  // a failure surfaces at the next CK
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+int config_device(const nlfem_gpu_config* cfg) {
+  int dev = cfg ? cfg->device : -1;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return dev;
+}
+
 extern "C" {
 
 int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen) {
@@ -3554,7 +3675,10 @@ int nlfem_gpu_session_create(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* d
                              nlfem_gpu_session** out, char* err, size_t errlen) {
   *out = nullptr;
   auto* S = new nlfem_gpu_session;
-  const int rc = guard(err, errlen, [&] { session_init(*S, mesh, dofs, kernel, f, g, cfg); });
+  const int rc = guard(err, errlen, [&] {
+    DeviceScope ds(config_device(cfg));
+    session_init(*S, mesh, dofs, kernel, f, g, cfg);
+  });
   if (rc) {
     nlfem_gpu_session_destroy(S);
     return rc;
@@ -3568,6 +3692,7 @@ int nlfem_gpu_session_reset(nlfem_gpu_session* s, const nlfem_gpu_mesh* mesh,
                             const nlfem_gpu_poly* f, const nlfem_gpu_poly* g,
                             const nlfem_gpu_config* cfg, char* err, size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(config_device(cfg));
     s->pairs_installed = false;
     session_init(*s, mesh, dofs, kernel, f, g, cfg);
   });
@@ -3575,14 +3700,17 @@ int nlfem_gpu_session_reset(nlfem_gpu_session* s, const nlfem_gpu_mesh* mesh,
 
 int nlfem_gpu_session_run(nlfem_gpu_session* s, void* stream, nlfem_gpu_stats* stats, char* err,
                           size_t errlen) {
-  return guard(err, errlen,
-               [&] { run_all(*s, static_cast<cudaStream_t>(stream), stats, 0, s->KI, true); });
+  return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
+    run_all(*s, static_cast<cudaStream_t>(stream), stats, 0, s->KI, true);
+  });
 }
 
 int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
                                 int32_t finalize, nlfem_gpu_stats* stats, char* err,
                                 size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     run_all(*s, static_cast<cudaStream_t>(stream), stats, lo, hi, finalize != 0);
   });
 }
@@ -3590,6 +3718,7 @@ int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, 
 int nlfem_gpu_session_pairs_shard(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
                                   int64_t* npairs, char* err, size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     nlfem_gpu_session& S = *s;
     cudaStream_t st = S.stream;
     if (stream) {
@@ -3629,6 +3758,7 @@ int nlfem_gpu_session_pairs_install(nlfem_gpu_session* s, void* stream, const vo
                                     const void* partners, int64_t npairs_total, char* err,
                                     size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     nlfem_gpu_session& S = *s;
     cudaStream_t st = S.stream;
     if (stream) {
@@ -3680,7 +3810,10 @@ int nlfem_gpu_session_partials(nlfem_gpu_session* s, void** V, int64_t* nwords, 
 int nlfem_gpu_session_solve(nlfem_gpu_session* s, double tol, int32_t max_iter,
                             const nlfem_gpu_poly* exact, double* u_node, nlfem_gpu_study* out,
                             char* err, size_t errlen) {
-  return guard(err, errlen, [&] { session_solve(*s, tol, max_iter, exact, u_node, out); });
+  return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
+    session_solve(*s, tol, max_iter, exact, u_node, out);
+  });
 }
 
 int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_idx,
@@ -3697,6 +3830,7 @@ int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_i
 int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_lo,
                                int32_t row_hi, char* err, size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     if (user) {
       CK(cudaEventRecord(s->ev[7], user));
@@ -3712,6 +3846,7 @@ int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_l
 int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,
                                     nlfem_gpu_csr* out, char* err, size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     const int r0 = std::max(0, row_lo), r1 = std::max(r0, std::min(row_hi, s->unknowns));
     const int n = r1 - r0;
     std::vector<long long> off(n + 1);
@@ -3737,6 +3872,7 @@ int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_
 int nlfem_gpu_session_download(nlfem_gpu_session* s, nlfem_gpu_csr* out, char* err,
                                size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     const int U = s->unknowns;
     const long long nnz = s->nnz_out;
     if (nnz > (long long)0x7fffffff)
@@ -3778,6 +3914,7 @@ int nlfem_gpu_session_pairs_device(nlfem_gpu_session* s, int64_t* npairs,
 int nlfem_gpu_session_pairs(nlfem_gpu_session* s, int64_t* npairs, int64_t* outer_offsets,
                             int32_t* partner, uint32_t* info, char* err, size_t errlen) {
   return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
     *npairs = s->npairs;
     if (!outer_offsets) return;
     std::vector<long long> off(s->KI + 1);
@@ -3794,30 +3931,40 @@ int64_t nlfem_gpu_session_launches(const nlfem_gpu_session* s) { return s ? s->l
 
 void nlfem_gpu_session_destroy(nlfem_gpu_session* s) {
   if (!s) return;
+  {
+  DeviceScope ds(s->device);
   for (auto e : s->ev) cudaEventDestroy(e);
   if (s->stream) cudaStreamDestroy(s->stream);
   if (s->stream2) cudaStreamDestroy(s->stream2);
   if (s->stream3) cudaStreamDestroy(s->stream3);
   if (s->stream4) cudaStreamDestroy(s->stream4);
+  }
   delete s;
 }
 
 // The one-shot entry keeps one workspace per device (stream, events, device
 // buffers; grow-only) across calls, so repeated assemblies do not pay for
-// cudaMalloc / cudaFree.  Like the reference's assemble, it is meant to be
-// called from one host thread at a time.
+// cudaMalloc / cudaFree.  Calls from several host threads are serialised per
+// device (the workspace and the device's parameter block are shared), so the
+// entry is reentrant like the reference's pure assemble().
 int nlfem_gpu_assemble(const nlfem_gpu_mesh* mesh, const nlfem_gpu_dofs* dofs,
                        const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
                        const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
                        nlfem_gpu_csr* out, nlfem_gpu_stats* stats, char* err, size_t errlen) {
   const auto t0 = std::chrono::steady_clock::now();
-  static std::vector<nlfem_gpu_session*> workspaces;
-  int dev = cfg ? cfg->device : -1;
-  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
-  if ((int)workspaces.size() <= dev) workspaces.resize(dev + 1, nullptr);
+  static nlfem_gpu_session* workspaces[64] = {};
+  const int dev = config_device(cfg);
+  if (dev < 0 || dev >= 64) {
+    std::snprintf(err, errlen, "BadConfig: device ordinal out of range");
+    return NLFEM_GPU_BAD_CONFIG;
+  }
+  std::unique_lock<std::recursive_mutex> lk(device_mutex(dev));  // held to the download
   if (!workspaces[dev]) workspaces[dev] = new nlfem_gpu_session;
   nlfem_gpu_session* s = workspaces[dev];
-  int rc = guard(err, errlen, [&] { session_init(*s, mesh, dofs, kernel, f, g, cfg); });
+  int rc = guard(err, errlen, [&] {
+    DeviceScope ds(dev);
+    session_init(*s, mesh, dofs, kernel, f, g, cfg);
+  });
   if (rc) return rc;
   const auto t1 = std::chrono::steady_clock::now();
   rc = nlfem_gpu_session_run(s, nullptr, stats, err, errlen);

@@ -313,3 +313,47 @@ def test_config1_solved_l2_against_unmodified_reference(strat, mc, tol):
     if strat == "fullcaps":
         # C1 L2 5.528e-3 (seed spread +-0.1%)
         assert abs(rsol["l2"] / 5.528e-3 - 1) < 0.005, rsol["l2"]
+
+
+def test_concurrent_one_shot_calls_and_interleaved_sessions():
+    # the one-shot call and sessions on one device share the
+    # device's workspace and parameter block; calls from several host threads
+    # (ctypes releases the GIL) are serialised per device, so every result
+    # equals the serial one bit for bit.
+    import threading
+    m = P.generate_mesh(3, 6, 0.34)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    cases = [("nocaps", 1), ("fullcaps", 16), ("barycenter", 1), ("fullcaps", 8)]
+    want = [P.assemble(t, 0.34, s_, "moment2", U2, seed=SEED, mc_samples=mc)[0]
+            for s_, mc in cases]
+    got = [None] * (3 * len(cases))
+    errs = []
+
+    def work(i):
+        try:
+            s_, mc = cases[i % len(cases)]
+            out, _ = P.assemble(t, 0.34, s_, "moment2", U2, seed=SEED, mc_samples=mc)
+            got[i] = {k: np.array(v) for k, v in out.items()}
+        except Exception as exc:  # pragma: no cover
+            errs.append(exc)
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(got))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    for i, g in enumerate(got):
+        w = want[i % len(cases)]
+        for k in ("row_ptr", "col_idx", "values", "rhs"):
+            assert np.array_equal(g[k], w[k]), (i, k)
+    # two sessions on one device, driven alternately
+    a = P.Session(t, 0.34, "fullcaps", "moment2", U2, seed=SEED, mc_samples=16)
+    b = P.Session(t, 0.34, "nocaps", "moment2", U2, seed=SEED)
+    for _ in range(2):
+        a.run()
+        b.run()
+        ra, rb = a.download(), b.download()
+        for k in ("values", "rhs"):
+            assert np.array_equal(ra[k], want[1][k]) and np.array_equal(rb[k], want[0][k])
+    a.close()
+    b.close()
