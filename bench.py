@@ -26,11 +26,13 @@ sample mesh per step (rank 0 only), and prints the same line with
 
 --gpus N without torchrun re-launches itself under torch.distributed.run.
 
-Multi-GPU (torchrun, NCCL): the assembly is sharded -- each rank integrates a
-contiguous range of outer elements into exact fixed-point partial sums, an
-int64 all-reduce combines them (bit-identical to one GPU), each rank finalizes
-its row block and the row blocks are all-gathered on device
-(paper_2302_07499_b200/distributed.py).  Total work is fixed: scaling "strong".
+Multi-GPU (torchrun, NCCL): owner-computes -- each rank builds the pairs of a
+contiguous range of outer elements, its local node pattern and their exact
+fixed-point partial sums, ships the slots of other ranks' rows to their owners
+(all-to-all of the halo records), finalizes its own row block from what it
+received (bit-identical to one GPU) and the row blocks are all-gathered on
+device (paper_2302_07499_b200/distributed.py).  Total work is fixed: scaling
+"strong".
 """
 from __future__ import annotations
 
@@ -301,7 +303,7 @@ def system_sha(sess, dist_out=None) -> str:
     import torch
     ro, ci, va, rh = (torch.as_tensor(x, device="cuda") for x in sess.outputs())
     if dist_out is not None:
-        va, ci, rh = dist_out
+        va, ci, rh, ro = dist_out
     h = hashlib.sha256()
     for t in (ro, ci, va, rh):
         h.update(t.contiguous().cpu().numpy().tobytes())
@@ -408,16 +410,24 @@ def main():
         t = torch.tensor([t_total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
-    pairs = int(st.element_pairs)  # all element pairs of the workload (every rank builds them)
-    value = pairs * args.steps / (t_total * 1e-3)
     sha = system_sha(sess, out) if args.verify else None
-    stats = {"items": int(st.items), "mc_samples": int(st.mc_samples),
-             "mc_hits": int(st.mc_hits)}
-    if dist is not None:  # this rank's shard only: sum over ranks
-        c = torch.tensor([stats["items"], stats["mc_samples"], stats["mc_hits"]],
-                         dtype=torch.int64, device="cuda")
+    stats = {"element_pairs": int(st.element_pairs), "items": int(st.items),
+             "mc_samples": int(st.mc_samples), "mc_hits": int(st.mc_hits)}
+    ledger, ledger_units = int(st.ledger_flops), int(st.ledger_flops_units)
+    k3 = float(np.mean(k3_ms))
+    kmc = float(np.mean(mc_ms))
+    if dist is not None:  # each rank counts its own outer elements: sum over ranks
+        c = torch.tensor([*stats.values(), ledger, ledger_units], dtype=torch.int64,
+                         device="cuda")
         dist.all_reduce(c)
-        stats = dict(zip(stats, (int(x) for x in c.cpu())))
+        c = [int(x) for x in c.cpu()]
+        stats = dict(zip(stats, c[:4]))
+        ledger, ledger_units = c[4], c[5]
+        tk = torch.tensor([k3, kmc], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tk, op=dist.ReduceOp.MAX)  # the slowest rank's phases
+        k3, kmc = (float(x) for x in tk.cpu())
+    pairs = stats["element_pairs"]
+    value = pairs * args.steps / (t_total * 1e-3)
 
     # end to end: one-shot C-ABI call with host arrays (upload + run + download).
     # The device-resident session is released first: at C4 its buffers alone
@@ -468,19 +478,18 @@ def main():
                else "assemble_distributed (sharded, host CSR on every rank)"}
 
     peak = P.fp64_peak_tflops(local)
-    k3 = float(np.mean(k3_ms))
-    kmc = float(np.mean(mc_ms))
     # dominant kernel: the units kernels (k_mc: inner pieces + Monte Carlo; its
-    # launches run on two streams, timed together by CUDA events around them)
-    units = kmc > 0 and st.ledger_flops_units > 0
+    # launches run on two streams, timed together by CUDA events around them).
+    # N > 1: the ledger of all ranks over the slowest rank's phase time, per GPU
+    units = kmc > 0 and ledger_units > 0
     if units:
-        achieved = st.ledger_flops_units / (kmc * 1e-3) / 1e12
+        achieved = ledger_units / (kmc * 1e-3) / 1e12 / world
         rl_kernel, rl_flops, rl_ms = ("k_mc (units phase: inner pieces + Monte Carlo, all "
-                                      "launches of one step)"), st.ledger_flops_units, kmc
+                                      "launches of one step)"), ledger_units, kmc
     else:  # barycenter / overlap / inside: whole-element items in the combine only
-        achieved = st.ledger_flops / (k3 * 1e-3) / 1e12
-        rl_kernel, rl_flops, rl_ms = "k_integrate (combine)", st.ledger_flops, k3
-    integ = st.ledger_flops / (k3 * 1e-3) / 1e12
+        achieved = ledger / (k3 * 1e-3) / 1e12 / world
+        rl_kernel, rl_flops, rl_ms = "k_integrate (combine)", ledger, k3
+    integ = ledger / (k3 * 1e-3) / 1e12 / world
     traffic = TRAFFIC.get(args.config) if units and world == 1 else None
     line = {
         "metric": METRIC, "value": value, "unit": METRIC,
@@ -490,10 +499,11 @@ def main():
         "config": bench_config(args.config, cfg),
         "parallelism": (f"outer-element shards x{world} "
                         f"({os.environ.get('NLFEM_BENCH_BACKEND', 'nccl').upper()} "
-                        "int64 all-reduce + row-block all-gather)") if use_dist else "single GPU",
+                        "owner-computes: halo records all-to-all + row-block all-gather)")
+        if use_dist else "single GPU",
         "l2": "flushed between steps (256 MiB write; inputs smaller than L2)",
-        "element_pairs": pairs, **stats,
-        "fp64_gflops_ledger": st.ledger_flops / (t_total / args.steps * 1e-3) / 1e9,
+        **stats,
+        "fp64_gflops_ledger": ledger / (t_total / args.steps * 1e-3) / 1e9,
         "phase_ms": [round(x, 3) for x in st.phase_ms[:6]],
         "roofline": {"kernel": rl_kernel, "bound": "fp64", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -505,7 +515,7 @@ def main():
                      "traffic": traffic[0] if traffic else None,
                      "traffic_source": traffic[1] if traffic else None,
                      "integration_phase": {"kernels": "k_mc + k_integrate", "ms": k3,
-                                           "ledger_flops": int(st.ledger_flops),
+                                           "ledger_flops": int(ledger),
                                            "achieved": integ, "frac": integ / peak}},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,

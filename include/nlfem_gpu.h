@@ -237,6 +237,41 @@ int nlfem_gpu_session_pairs_install(nlfem_gpu_session* s, void* stream, const vo
                                     size_t errlen);
 int nlfem_gpu_session_finalize(nlfem_gpu_session* s, void* stream, int32_t row_lo,
                                int32_t row_hi, char* err, size_t errlen);
+/* Owner-computes multi-GPU (the north star's "each rank assembles its own row
+ * block"; replaces the threads of the reference's worker pool,
+ * assembly.cpp:746-776, by ranks).  Every rank:
+ *   run_local(lo, hi)   builds the element pairs of outer elements [lo, hi)
+ *                       only and a LOCAL node pattern (the rows those pairs
+ *                       touch) and integrates them into it;
+ *   halo_records(bounds) returns, grouped by destination rank (row block
+ *                       r = unknowns [bounds[r], bounds[r+1])), one record per
+ *                       local slot of an unknown row: key uint64 = node_row
+ *                       << 32 | node_col, 4 int64 words (the slot's fixed-point
+ *                       hi / lo and its mirror slot's hi / lo); counts[r] per
+ *                       destination (device pointers, valid until the next
+ *                       call);
+ *   rhs_records(bounds) the load-vector partials (int32 interior position +
+ *                       4 x 8 doubles) of the outer elements at each
+ *                       destination's unknown nodes;
+ *   finalize_merged     takes everything received for its row block
+ *                       [row_lo, row_hi) (its own records included), sorts
+ *                       the records, sums equal keys as integers and
+ *                       finalizes the block; outputs() / download_rows() then
+ *                       hold those rows.
+ * Only the records move between ranks (an all-to-all of the halo); the
+ * finalized row blocks are then all-gathered.  Bit-identical to one GPU. */
+int nlfem_gpu_session_run_local(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
+                                nlfem_gpu_stats* stats, char* err, size_t errlen);
+int nlfem_gpu_session_halo_records(nlfem_gpu_session* s, int32_t world, const int32_t* bounds,
+                                   void** keys, void** vals, int64_t* counts, char* err,
+                                   size_t errlen);
+int nlfem_gpu_session_rhs_records(nlfem_gpu_session* s, int32_t world, const int32_t* bounds,
+                                  void** idx, void** vals, int64_t* counts, char* err,
+                                  size_t errlen);
+int nlfem_gpu_session_finalize_merged(nlfem_gpu_session* s, void* stream, int32_t row_lo,
+                                      int32_t row_hi, const void* keys, const void* vals,
+                                      int64_t n, const void* ridx, const void* rvals, int64_t m,
+                                      char* err, size_t errlen);
 int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,
                                     nlfem_gpu_csr* out, char* err, size_t errlen);
 /* Device pointers of the output CSR of the last run (row offsets are int64,

@@ -30,6 +30,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NLFEM_GPU_LIB") or os.path.join(_HERE, "libnlfem_gpu.so")
 
 STRATEGIES = ["inside", "overlap", "barycenter", "nocaps", "approxcaps", "fullcaps"]
+RHS_WORDS = 32  # load-vector partials per outer element: 4 nodes x 8 combine warps (kRhsWarps)
 GPU_STRATEGIES = ("inside", "overlap", "barycenter", "nocaps", "fullcaps")
 ERROR_NAMES = {1: "BadIndex", 2: "DanglingVertex", 3: "NonManifold", 4: "SeedMismatch",
                5: "BallExitsMesh", 6: "DegenerateHull", 7: "BadMeshFile", 8: "BadConfig",
@@ -145,6 +146,17 @@ def lib():
     L.nlfem_gpu_session_pairs_shard_out.argtypes = [vp, P(vp), P(vp), P(i64)]
     L.nlfem_gpu_session_pairs_install.restype = C.c_int
     L.nlfem_gpu_session_pairs_install.argtypes = [vp, vp, vp, vp, i64, C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_run_local.restype = C.c_int
+    L.nlfem_gpu_session_run_local.argtypes = [vp, vp, i32, i32, P(Stats), C.c_char_p, C.c_size_t]
+    L.nlfem_gpu_session_halo_records.restype = C.c_int
+    L.nlfem_gpu_session_halo_records.argtypes = [vp, i32, vp, P(vp), P(vp), vp, C.c_char_p,
+                                                 C.c_size_t]
+    L.nlfem_gpu_session_rhs_records.restype = C.c_int
+    L.nlfem_gpu_session_rhs_records.argtypes = [vp, i32, vp, P(vp), P(vp), vp, C.c_char_p,
+                                                C.c_size_t]
+    L.nlfem_gpu_session_finalize_merged.restype = C.c_int
+    L.nlfem_gpu_session_finalize_merged.argtypes = [vp, vp, i32, i32, vp, vp, i64, vp, vp, i64,
+                                                    C.c_char_p, C.c_size_t]
     L.nlfem_gpu_cg.restype = C.c_int
     L.nlfem_gpu_cg.argtypes = [P(_Csr), vp, dbl, i32, i32, vp, P(_SolveReport), C.c_char_p,
                                C.c_size_t]
@@ -196,6 +208,8 @@ EXPORTED_SYMBOLS = [
     "nlfem_gpu_session_finalize", "nlfem_gpu_session_download_rows",
     "nlfem_gpu_session_outputs", "nlfem_gpu_session_pairs_shard",
     "nlfem_gpu_session_pairs_shard_out", "nlfem_gpu_session_pairs_install",
+    "nlfem_gpu_session_run_local", "nlfem_gpu_session_halo_records",
+    "nlfem_gpu_session_rhs_records", "nlfem_gpu_session_finalize_merged",
     "nlfem_gpu_cg", "nlfem_gpu_cg_device", "nlfem_gpu_session_solve", "nlfem_gpu_element_table",
     "nlfem_host_lattice_mesh", "nlfem_host_element_table", "nlfem_host_dofmap",
     "nlfem_host_kernel_constant", "nlfem_host_forcing", "nlfem_host_normalize_poly",
@@ -501,6 +515,61 @@ class Session:
         _check(lib().nlfem_gpu_session_pairs_install(self._h, C.c_void_p(stream or 0),
                                                      ptr(counts), ptr(partners),
                                                      int(npairs_total), err, 1024), err)
+
+    # -- owner-computes multi-GPU ----------------------------
+    def run_local(self, lo: int, hi: int, stream: int | None = None) -> Stats:
+        """Pairs of outer elements [lo, hi) only, this rank's local node pattern,
+        and their integration into it (no finalize)."""
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_run_local(self._h, C.c_void_p(stream or 0), int(lo),
+                                                 int(hi), C.byref(self.stats), err, 1024), err)
+        self._local = (int(lo), int(hi))
+        return self.stats
+
+    def halo_records(self, bounds):
+        """Slot records of the local pattern's unknown rows grouped by the
+        owning row block (bounds: world + 1 row boundaries).  Returns device
+        views (keys uint64 [n], words int64 [4 n]) and the per-destination
+        counts."""
+        b = np.ascontiguousarray(bounds, np.int32)
+        world = len(b) - 1
+        cnt = np.zeros(world, np.int64)
+        kp, vp_ = C.c_void_p(), C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_halo_records(self._h, world, _p(b), C.byref(kp),
+                                                    C.byref(vp_), _p(cnt), err, 1024), err)
+        n = int(cnt.sum())
+        return (_CudaView(kp.value or 0, n, "<i8"), _CudaView(vp_.value or 0, 4 * n, "<i8"),
+                cnt)
+
+    def rhs_records(self, bounds):
+        """Load-vector partials (interior positions int32 [m], 32 doubles each)
+        of the outer elements of the last run_local, grouped by the owners of
+        their unknown nodes; returns device views and per-destination counts."""
+        b = np.ascontiguousarray(bounds, np.int32)
+        world = len(b) - 1
+        cnt = np.zeros(world, np.int64)
+        ip, vp_ = C.c_void_p(), C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_rhs_records(self._h, world, _p(b), C.byref(ip),
+                                                   C.byref(vp_), _p(cnt), err, 1024), err)
+        m = int(cnt.sum())
+        return (_CudaView(ip.value or 0, m, "<i4"),
+                _CudaView(vp_.value or 0, m * RHS_WORDS, "<f8"), cnt)
+
+    def finalize_merged(self, row_lo: int, row_hi: int, keys, words, ridx, rvals,
+                        stream: int | None = None) -> None:
+        """Finalize row block [row_lo, row_hi) from every record received for it
+        (CUDA arrays: keys uint64 [n], words int64 [4 n], rhs positions int32
+        [m], rhs partials float64 [32 m])."""
+        def ptr(a):
+            return C.c_void_p(int(a.__cuda_array_interface__["data"][0]) if a is not None else 0)
+        n = int(keys.__cuda_array_interface__["shape"][0])
+        m = int(ridx.__cuda_array_interface__["shape"][0])
+        err = C.create_string_buffer(1024)
+        _check(lib().nlfem_gpu_session_finalize_merged(
+            self._h, C.c_void_p(stream or 0), int(row_lo), int(row_hi), ptr(keys), ptr(words), n,
+            ptr(ridx), ptr(rvals), m, err, 1024), err)
 
     def cg(self, tol: float = 1e-10, max_iterations: int = 10000) -> dict:
         """Conjugate gradients on the assembled system where it lies in HBM

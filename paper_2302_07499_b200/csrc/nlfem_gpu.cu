@@ -22,6 +22,7 @@
 // are associative, so the result is bitwise identical for any launch order,
 // block count or GPU count.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -623,11 +624,21 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
   __syncthreads();
   const int x0 = xb[0], x1 = xb[1], y0 = xb[2], y1 = xb[3], z0 = xb[4], z1 = xb[5];
   __shared__ double oc[kPairWarps][4];
+  // the outer element's quadrature points, parked in shared memory (the
+  // classification reads them; keeping T's vertices live in registers across
+  // the candidate stream made ptxas spill)
+  __shared__ double oq[kPairWarps][4][3];
   if (lane == 0) {
     oc[wl][0] = o.c.x;
     oc[wl][1] = o.c.y;
     oc[wl][2] = o.c.z;
     oc[wl][3] = active ? o.R : -1.0;
+  }
+  if (lane < 4) {
+    const Vd x = active ? quad_point(o.v, lane) : Vd{0, 0, 0};
+    oq[wl][lane][0] = x.x;
+    oq[wl][lane][1] = x.y;
+    oq[wl][lane][2] = x.z;
   }
   __syncthreads();
   const long long out = (MODE == 1 && active) ? cand_off[warp] - cand_base : 0;
@@ -660,7 +671,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
         const double4 a = sg.rec[k][0], b = sg.rec[k][1], e = sg.rec[k][2], d = sg.rec[k][3];
         const Vd cp = {a.x, a.y, a.z};
         const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
-        const Vd xq = quad_point(o.v, q);
+        const Vd xq = {oq[wl][q][0], oq[wl][q][1], oq[wl][q][2]};
         const unsigned c =
             classify_cheap<STRAT>(xq, cp, a.w, v, sg.cert2[k], sg.vol[k], sg.tau[k]);
         if (c & kDefer) ent = 16u | (c & 15u);
@@ -683,7 +694,7 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
       const int k = sg.mine[wl][t];
       const double4 b = sg.rec[k][1], e = sg.rec[k][2], d = sg.rec[k][3];
       const Vd v[4] = {{b.x, b.y, b.z}, {b.w, e.x, e.y}, {e.z, e.w, d.x}, {d.y, d.z, d.w}};
-      const Vd xq = quad_point(o.v, q);
+      const Vd xq = {oq[wl][q][0], oq[wl][q][1], oq[wl][q][2]};
       if (ent & 16u) {
         const unsigned c = classify_deferred<STRAT>(xq, v, (int)(ent & 15u), sg.tau[k]);
         if (c) atomicOr(&wcode[wl][t], c << (5 * q));
@@ -923,10 +934,25 @@ __global__ void k_cap_check(const long long* total, long long cap, int* ovf) {
 }
 
 // R(i) = sorted nodes of interior partners of every interior T containing node i.
+// flag the interior partners of a pair range (pairs [0, *pend))
+__global__ void k_mark_partners(long long np, const long long* pend, const int* partner,
+                                unsigned char* mark) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np || p >= *pend) return;
+  const int Tp = partner[p];
+  if (cD.region[Tp] == 0) mark[Tp] = 1;
+}
+
+// plo / phi: the outer elements (interior positions) whose pairs are built
+// (the whole interior list on one GPU; a rank's range under the owner-computes
+// multi-GPU plan); pmark (or null): interior elements that
+// are partners of those pairs -- their own node pairs enter the rows too, so a
+// rank's local pattern holds every slot its combine adds to (the D_T' block)
 template <bool FILL>
 __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const int* partner,
                                               int* rlen, const long long* roff, int* rcols,
-                                              int* ovf) {
+                                              int* ovf, int plo, int phi,
+                                              const unsigned char* pmark) {
   extern __shared__ int sm[];
   int* tabE = sm;
   int* tabN = sm + kHE;
@@ -946,6 +972,8 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
     for (int k = a; k < b; ++k) {
       const int T = cD.ni_el[k];
       const int lo = cD.ipos[T];
+      if (pmark && pmark[T] && threadIdx.x == 0) hset_insert(tabE, kHE, T, ovf);
+      if (lo < plo || lo >= phi) continue;
       const long long p0 = pair_off[lo], p1 = pair_off[lo + 1];
       for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const int Tp = partner[p];
@@ -1122,9 +1150,14 @@ __global__ void k_mirror(int J, const long long* soff, const int* scols, long lo
 // the 10 (b <= b') slots of each interior element's node pairs, stored at
 // row min(M_b, M_b')
 __global__ void k_edge_slots(const long long* soff, const int* scols, long long* eslot,
-                             int* ovf) {
+                             int* ovf, int plo, int phi, const unsigned char* pmark) {
   const int ii = blockIdx.x * blockDim.x + threadIdx.x;
   if (ii >= cD.KI || *ovf) return;
+  if ((ii < plo || ii >= phi) && !(pmark && pmark[cD.interior[ii]])) {
+    // neither an outer element of this pattern nor a partner: never read
+    for (int k = 0; k < 10; ++k) eslot[10 * (long long)ii + k] = -1;
+    return;
+  }
   const int4 w = cD.verts[cD.interior[ii]];
   const int v[4] = {w.x, w.y, w.z, w.w};
   int k = 0;
@@ -1183,9 +1216,12 @@ __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot,
 // (~62 bits of the row bound: errors stay ~1e-13 of the row's largest entry);
 // entries touching a constrained node feed the rhs folding, where
 // cancellation can amplify errors, and keep both words.
+#ifndef NLFEM_FIXED_TWO
+#define NLFEM_FIXED_TWO 0  // 1: every entry keeps both words (precision study)
+#endif
 __device__ __forceinline__ void red_fixed_sel(unsigned long long* V, long long slot, double v,
                                               double scale, bool two) {
-  if (!two) {
+  if (!two && !NLFEM_FIXED_TWO) {
     const long long hi = __double2ll_rn(v * scale);
     if (hi != 0) atomicAdd(V + 2 * slot, (unsigned long long)hi);
     return;
@@ -1379,33 +1415,76 @@ __device__ __forceinline__ void fields_odd(const uint32_t w[4], uint32_t& s0, ui
 
 // Hit test Q(s) < delta^2 (nlfem_mc_q) and, on a hit, the exact moments of
 // the sorted fields: n and sum s in u32 (< 2^21 per sample, <= 1024 samples
-// per segment), sum s s^T in FP64 -- the products of two fields are integers
-// < 2^42 and their sum over a segment < 2^52, so every DFMA is exact.  The
-// fields are masked (zero on a miss), not branched on: the warp issues no
-// divergent code.  The mix balances the pipes: Philox's IMAD.WIDE.U32s keep
-// the FMA-heavy pipe busy, so the six products go to the FP64 pipe (ncu at
-// P3f with them as IMAD.WIDEs: FMA-heavy 59% busy against 55% issue).
+// per segment), sum s s^T in u64 -- the products of two fields are integers
+// < 2^42, accumulated by IMAD.WIDE.U32 (one instruction each, exact).  The
+// fields are masked by the hit bit (zero on a miss), not branched on: the warp
+// issues no divergent code.  The products run on the FMA pipe: the FP64 pipe
+// keeps only the conversions and the quadratic form (ncu at P3f with them as
+// DFMAs: FP64-pipe throttle and dispatch stalls 42% of the loop's samples).
+__device__ __forceinline__ unsigned long long imad_wide(uint32_t a, uint32_t b,
+                                                        unsigned long long c) {
+  return (unsigned long long)a * b + c;
+}
+// a * b + c as one IMAD (FMA pipe) where the compiler would pick a SEL (ALU)
+__device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+#ifndef NLFEM_MC_MOM
+#define NLFEM_MC_MOM 3  // 0: FP64 products; 1-3: integer products (masks by SEL / IMAD)
+#endif
+
 struct IntMoments {
   unsigned n = 0;
   uint32_t s[3] = {0, 0, 0};
+#if NLFEM_MC_MOM == 0
   double ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
+#else
+  unsigned long long ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
+#endif
   __device__ __forceinline__ void sample(const nlfem_mc_quad& Q, double dd, uint32_t s0,
                                          uint32_t s1, uint32_t s2) {
     const double d0 = u21_to_double(s0), d1 = u21_to_double(s1), d2 = u21_to_double(s2);
     const bool hit = nlfem_mc_q(&Q, d0, d1, d2) < dd;
-    const uint32_t m = hit ? 0xffffffffu : 0u;
-    n -= m;  // += 1 on a hit
-    s[0] += s0 & m;
-    s[1] += s1 & m;
-    s[2] += s2 & m;
-    const double h = hit ? 1.0 : 0.0;
-    const double m0 = h * d0, m1 = h * d1, m2 = h * d2;
-    ss[0] = fma(m0, d0, ss[0]);
-    ss[1] = fma(m0, d1, ss[1]);
-    ss[2] = fma(m0, d2, ss[2]);
-    ss[3] = fma(m1, d1, ss[3]);
-    ss[4] = fma(m1, d2, ss[4]);
-    ss[5] = fma(m2, d2, ss[5]);
+    const uint32_t hb = hit ? 1u : 0u;
+    n += hb;
+#if NLFEM_MC_MOM == 0
+    s[0] = imad_u32(hb, s0, s[0]);
+    s[1] = imad_u32(hb, s1, s[1]);
+    s[2] = imad_u32(hb, s2, s[2]);
+    const double h = __hiloint2double((int)imad_u32(hb, 0x3ff00000u, 0u), 0);
+    const double h0 = h * d0, h1 = h * d1, h2 = h * d2;
+    ss[0] = fma(h0, d0, ss[0]);
+    ss[1] = fma(h0, d1, ss[1]);
+    ss[2] = fma(h0, d2, ss[2]);
+    ss[3] = fma(h1, d1, ss[3]);
+    ss[4] = fma(h1, d2, ss[4]);
+    ss[5] = fma(h2, d2, ss[5]);
+#else
+#if NLFEM_MC_MOM == 1
+    const uint32_t m0 = hb * s0, m1 = hb * s1, m2 = hb * s2;
+#else
+    const uint32_t m0 = imad_u32(hb, s0, 0u), m1 = imad_u32(hb, s1, 0u),
+                   m2 = imad_u32(hb, s2, 0u);
+#endif
+#if NLFEM_MC_MOM == 3
+    s[0] = imad_u32(hb, s0, s[0]);
+    s[1] = imad_u32(hb, s1, s[1]);
+    s[2] = imad_u32(hb, s2, s[2]);
+#else
+    s[0] += m0;
+    s[1] += m1;
+    s[2] += m2;
+#endif
+    ss[0] = imad_wide(m0, s0, ss[0]);
+    ss[1] = imad_wide(m0, s1, ss[1]);
+    ss[2] = imad_wide(m0, s2, ss[2]);
+    ss[3] = imad_wide(m1, s1, ss[3]);
+    ss[4] = imad_wide(m1, s2, ss[4]);
+    ss[5] = imad_wide(m2, s2, ss[5]);
+#endif
   }
 };
 
@@ -1418,9 +1497,10 @@ __device__ __forceinline__ void fold_moments(const nlfem_mc_quad& Q, const IntMo
                                              double& nh, double t1[3], double t2[6]) {
   const double n = (double)im.n;
   const double S[3] = {(double)im.s[0], (double)im.s[1], (double)im.s[2]};
-  const double SS[3][3] = {{im.ss[0], im.ss[1], im.ss[2]},
-                           {im.ss[1], im.ss[3], im.ss[4]},
-                           {im.ss[2], im.ss[4], im.ss[5]}};
+  double sd[6];  // exact: the sums are < 2^52
+#pragma unroll
+  for (int k = 0; k < 6; ++k) sd[k] = (double)im.ss[k];
+  const double SS[3][3] = {{sd[0], sd[1], sd[2]}, {sd[1], sd[3], sd[4]}, {sd[2], sd[4], sd[5]}};
   double g[3], H[3][3];  // g = F^T S; H[t][y] = sum_u SS[t][u] F[u][y]
 #pragma unroll
   for (int y = 0; y < 3; ++y) {
@@ -2295,6 +2375,132 @@ __global__ void k_finalize(const long long* soff, const int* scols, const long l
 }
 
 // ---------------------------------------------------------------------------
+// Owner-computes multi-GPU: a rank integrates its outer
+// elements into its local pattern, then ships every local slot of an unknown
+// row to that row's owner as a record (key = row << 32 | col; direct hi / lo
+// words and the mirror slot's hi / lo), and the rhsT rows of its outer
+// elements to the owners of their unknown nodes.  The owner sorts the records
+// it receives (its own included), sums equal keys as integers (exact and
+// order-free) and finalizes its row block from the merged rows -- the merged
+// row of node i is the global pattern row of i, so the result is bit for bit
+// the one-GPU system.
+
+// records per unknown row: the local pattern row length
+__global__ void k_halo_count(const long long* soff, const int* dof_node, int* cnt) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= cD.unknowns) return;
+  const int i = dof_node[d];
+  cnt[d] = (int)(soff[i + 1] - soff[i]);
+}
+
+// warp per unknown row: one record per local slot
+__global__ void k_halo_fill(const long long* soff, const int* scols, const long long* mirror,
+                            const unsigned long long* V, const int* dof_node,
+                            const long long* hoff, unsigned long long* keys, long long* vals) {
+  const int d = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (d >= cD.unknowns) return;
+  const int i = dof_node[d];
+  const long long s0 = soff[i], o = hoff[d];
+  for (long long k = s0 + (threadIdx.x & 31); k < soff[i + 1]; k += 32) {
+    const int j = scols[k];
+    const long long r = o + (k - s0);
+    keys[r] = ((unsigned long long)(unsigned)i << 32) | (unsigned)j;
+    longlong2 dv = make_longlong2((long long)V[2 * k], (long long)V[2 * k + 1]);
+    longlong2 mv = make_longlong2(0, 0);
+    if (j != i) {
+      const long long m = mirror[k];
+      mv = make_longlong2((long long)V[2 * m], (long long)V[2 * m + 1]);
+    }
+    reinterpret_cast<longlong2*>(vals)[2 * r] = dv;
+    reinterpret_cast<longlong2*>(vals)[2 * r + 1] = mv;
+  }
+}
+
+__device__ __forceinline__ int owner_of(int d, const int* bounds, int world) {
+  int r = 0;
+  while (r + 1 < world && d >= bounds[r + 1]) ++r;
+  return r;
+}
+
+// per outer element of [plo, phi): the ranks owning one of its unknown nodes
+__global__ void k_rhs_mask(int plo, int phi, const int* bounds, int world,
+                           unsigned long long* mask) {
+  const int ii = plo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (ii >= phi) return;
+  const int4 w = cD.verts[cD.interior[ii]];
+  const int v[4] = {w.x, w.y, w.z, w.w};
+  unsigned long long m = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int d = cD.dof[v[k]];
+    if (d >= 0) m |= 1ull << owner_of(d, bounds, world);
+  }
+  mask[ii - plo] = m;
+}
+
+__global__ void k_rhs_flag(int n, const unsigned long long* mask, int r, int* flag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) flag[t] = (int)((mask[t] >> r) & 1ull);
+}
+
+__global__ void k_rhs_scatter(int n, int plo, const int* flag, const long long* off,
+                              long long base, const double* rhsT, int* idx, double* vals) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n || !flag[t]) return;
+  const long long pos = base + off[t];
+  idx[pos] = plo + t;
+  const double* src = rhsT + (long long)(plo + t) * (4 * kRhsWarps);
+  for (int k = 0; k < 4 * kRhsWarps; ++k) vals[pos * (4 * kRhsWarps) + k] = src[k];
+}
+
+__global__ void k_rhs_install(long long m, const int* idx, const double* vals, double* rhsT) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * (4 * kRhsWarps)) return;
+  const long long r = t / (4 * kRhsWarps), k = t % (4 * kRhsWarps);
+  rhsT[(long long)idx[r] * (4 * kRhsWarps) + k] = vals[t];
+}
+
+__global__ void k_iota(long long n, unsigned* a) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) a[t] = (unsigned)t;
+}
+
+__global__ void k_key_flag(long long n, const unsigned long long* keys, int* flag) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) flag[t] = (t == 0 || keys[t] != keys[t - 1]) ? 1 : 0;
+}
+
+__global__ void k_key_start(long long n, const int* flag, const long long* uid, long long* start) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n && flag[t]) start[uid[t]] = t;
+  if (t == 0) start[uid[n]] = n;
+}
+
+// thread per distinct key: integer sums of its records (any order: exact)
+__global__ void k_key_sum(long long nu, const long long* start, const unsigned long long* keys,
+                          const unsigned* perm, const long long* vals,
+                          unsigned long long* mV, int* mcols, long long* mmirror, int* mcnt) {
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nu) return;
+  unsigned long long w[4] = {0, 0, 0, 0};
+  for (long long k = start[u]; k < start[u + 1]; ++k) {
+    const longlong2* r = reinterpret_cast<const longlong2*>(vals) + 2 * (long long)perm[k];
+    const longlong2 a = r[0], b = r[1];
+    w[0] += (unsigned long long)a.x;
+    w[1] += (unsigned long long)a.y;
+    w[2] += (unsigned long long)b.x;
+    w[3] += (unsigned long long)b.y;
+  }
+  const unsigned long long key = keys[start[u]];
+  mV[2 * u] = w[0];
+  mV[2 * u + 1] = w[1];
+  mV[2 * (nu + u)] = w[2];
+  mV[2 * (nu + u) + 1] = w[3];
+  mcols[u] = (int)(key & 0xffffffffu);
+  mmirror[u] = nu + u;
+  atomicAdd(mcnt + (int)(key >> 32), 1);
+}
+
+// ---------------------------------------------------------------------------
 // FP64 DFMA throughput microbenchmark (roofline denominator)
 
 __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
@@ -2465,6 +2671,28 @@ struct nlfem_gpu_session {
   long long survivors = 0;   // K1 survivors of the last build_pairs range (bounds its pairs)
   double delta_over_h = 0;   // delta / cbrt(6 mean element volume)
   DBuf<unsigned> info_own;
+  // pattern scope: outer elements [plo, phi) have pairs; plocal: a rank's local
+  // pattern (owner-computes multi-GPU), pmark[K] flags the interior partners
+  int plo = 0, phi = 0;
+  bool plocal = false;
+  DBuf<unsigned char> pmark;
+  // owner-computes multi-GPU: outgoing slot records (key = row << 32 | col,
+  // 4 words: direct hi/lo, mirror hi/lo) grouped by destination rank, outgoing
+  // rhsT rows, and the merged rows of this rank's row block
+  DBuf<int> hcnt;
+  DBuf<long long> hoff;
+  DBuf<unsigned long long> hkeys;
+  DBuf<long long> hvals;
+  DBuf<unsigned long long> rmask;
+  DBuf<int> rflag, ridx;
+  DBuf<long long> roffs;
+  DBuf<double> rvals;
+  DBuf<unsigned long long> mkeys;
+  DBuf<unsigned> midx, midx2;
+  DBuf<int> mflag, mcnt, mcols;
+  DBuf<long long> muid, moff, mmirror, mstart;
+  DBuf<unsigned long long> mV;
+  DBuf<unsigned char> cub_tmp;
   std::atomic<long long> launches{0};
   unsigned long long items = 0, mc_samples = 0, mc_hits = 0, ledger = 0, mc_subs = 0,
                      ledger_units = 0;
@@ -2825,8 +3053,9 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   S.rlen.ensure(J);
   S.roff.ensure(J + 1);
   const unsigned rgrid = (unsigned)std::min<long long>(J, (long long)S.sms * 16);
+  const unsigned char* pm = S.plocal ? S.pmark.p : nullptr;
   k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
-                                               nullptr, S.ovf.p);
+                                               nullptr, S.ovf.p, S.plo, S.phi, pm);
   ++S.launches;
   scan64(S, S.rlen.p, true, J, S.roff.p, st);
   long long capR;
@@ -2839,7 +3068,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
     S.tcols.ensure(capR);
   }
   k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
-                                              S.rcols.p, S.ovf.p);
+                                              S.rcols.p, S.ovf.p, S.plo, S.phi, pm);
   // transpose
   S.tcnt.ensure(J);
   S.toff.ensure(J + 1);
@@ -2875,7 +3104,8 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
                                                  nullptr, S.soff.p, S.scols.p, nullptr, S.ovf.p);
   k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
   S.eslot.ensure(10 * (size_t)KI);
-  k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p);
+  k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p, S.plo,
+                                              S.phi, pm);
   S.launches += 3;
   // output pattern
   S.olen.ensure(U);
@@ -3089,8 +3319,11 @@ void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
 // the ascending interior list) are integrated; pairs and the node pattern are
 // built for all of them (every rank holds the same pattern, so the fixed-point
 // partial sums of several ranks add up slot by slot).
+// local = true (owner-computes multi-GPU): pairs are built
+// for [shard_lo, shard_hi) only and the node pattern is this rank's local one
+// (rows touched by those pairs, plus the partners' own node pairs).
 void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, int shard_lo,
-             int shard_hi, bool finalize) {
+             int shard_hi, bool finalize, bool local = false) {
   cudaStream_t st = S.stream;
   Dev& D = S.dev;
   const auto wall0 = std::chrono::steady_clock::now();
@@ -3107,10 +3340,27 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const int KI = S.KI;
   const int big = 0x7fffffff;
   const bool installed = S.pairs_installed;
+  shard_lo = std::max(0, std::min(shard_lo, KI));
+  shard_hi = std::max(shard_lo, std::min(shard_hi, KI));
+  local = local && !installed;
+  S.plocal = local;
+  S.plo = local ? shard_lo : 0;
+  S.phi = local ? shard_hi : KI;
   if (!installed) {
     run_prep(S);
     CK(cudaEventRecord(S.ev[1], st));
-    build_pairs(S, 0, KI);
+    build_pairs(S, S.plo, S.phi);
+    if (local) {
+      // interior partners of this rank's pairs (their node pairs join the
+      // local pattern); the pair total is bounded by the K1 survivors
+      S.pmark.ensure(S.K);
+      CK(cudaMemsetAsync(S.pmark.p, 0, S.K, st));
+      if (S.survivors > 0) {
+        k_mark_partners<<<nblk(S.survivors, 256), 256, 0, st>>>(
+            S.survivors, S.pair_off.p + S.phi, S.partner.p, S.pmark.p);
+        ++S.launches;
+      }
+    }
   } else {
     // the device parameter block is per device, not per session: rebind this
     // session's (another session may have run since its pairs were built)
@@ -3157,8 +3407,6 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   CK(cudaEventRecord(S.ev[3], st));
   S.rhsT.ensure(4 * kRhsWarps * (size_t)KI);
   CK(cudaMemsetAsync(S.rhsT.p, 0, 4 * kRhsWarps * (size_t)KI * sizeof(double), st));
-  shard_lo = std::max(0, std::min(shard_lo, KI));
-  shard_hi = std::max(shard_lo, std::min(shard_hi, KI));
   // combine set-up once the pattern is known: accumulators and the slot-map
   // capacity, a power of two > union of the four rows (<= 4 maxlen)
   int hcap = 64, rowcap = 1;
@@ -3196,7 +3444,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   // pairs are known on the host: a full run (pairs <= K1 survivors) or a
   // sharded run on installed pairs (offset and count from the install).
   const long long kPairsPerChunk = need_units ? pairs_per_chunk() : (1LL << 40);
-  const bool full_run = !installed && shard_lo == 0 && shard_hi == KI;
+  const bool full_run = !installed && (local || (shard_lo == 0 && shard_hi == KI));
   const bool own_range = installed && shard_lo == S.pairs_lo && shard_hi == S.pairs_hi;
   const bool fast = (full_run && S.survivors <= kPairsPerChunk) ||
                     (own_range && S.shard_npairs <= kPairsPerChunk);
@@ -3212,7 +3460,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
       throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
                  "BallExitsMesh: ball reaches past an unglued facet of element " +
                      std::to_string(err_elem_h)};
-    S.npairs = poff[KI];
+    S.npairs = poff[S.phi];
   }
   // events of unit-buffer set k: units start / end, combine ready / done
   auto evu = [&](int set, int k) { return S.ev[14 + 4 * set + k]; };
@@ -3237,7 +3485,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         P0 = full_run ? 0 : S.installed_base;
         np = full_run ? S.survivors : S.shard_npairs;  // bound on the chunk's pairs
       } else {
-        ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.end(), poff[ii0] + kPairsPerChunk) -
+        ii1 = (int)(std::upper_bound(poff.begin() + ii0 + 1, poff.begin() + shard_hi + 1,
+                                     poff[ii0] + kPairsPerChunk) -
                     poff.begin()) - 1;
         ii1 = std::min(std::max(ii1, ii0 + 1), shard_hi);
         P0 = poff[ii0];
@@ -3368,7 +3617,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   if (npairs_pending) {  // deferred from the pairs phase (no round trip there)
     long long tot = 0;
     int e = big;
-    CK(cudaMemcpy(&tot, S.pair_off.p + KI, sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&tot, S.pair_off.p + S.phi, sizeof(long long), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(&e, S.err_elem.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (e != big)
       throw Fail{NLFEM_GPU_BALL_EXITS_MESH,
@@ -3707,6 +3956,197 @@ int nlfem_gpu_session_run_shard(nlfem_gpu_session* s, void* stream, int32_t lo, 
   return guard(err, errlen, [&] {
     DeviceScope ds(s->device);
     run_all(*s, static_cast<cudaStream_t>(stream), stats, lo, hi, finalize != 0);
+  });
+}
+
+int nlfem_gpu_session_run_local(nlfem_gpu_session* s, void* stream, int32_t lo, int32_t hi,
+                                nlfem_gpu_stats* stats, char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
+    s->pairs_installed = false;
+    run_all(*s, static_cast<cudaStream_t>(stream), stats, lo, hi, false, true);
+  });
+}
+
+int nlfem_gpu_session_halo_records(nlfem_gpu_session* s, int32_t world, const int32_t* bounds,
+                                   void** keys, void** vals, int64_t* counts, char* err,
+                                   size_t errlen) {
+  return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
+    nlfem_gpu_session& S = *s;
+    cudaStream_t st = S.stream;
+    if (world < 1 || world > 64 || bounds[0] != 0 || bounds[world] != S.unknowns)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: row bounds must split [0, unknowns) in <= 64 blocks"};
+    const int U = S.unknowns;
+    CK(cudaMemcpyToSymbolAsync(cD, &S.dev, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
+    S.hcnt.ensure(U + 1);
+    S.hoff.ensure(U + 1);
+    if (U > 0) {
+      k_halo_count<<<nblk(U, 256), 256, 0, st>>>(S.soff.p, S.dof_node.p, S.hcnt.p);
+      ++S.launches;
+    }
+    scan64(S, S.hcnt.p, true, U, S.hoff.p, st);
+    std::vector<long long> off(U + 1, 0);
+    CK(cudaMemcpyAsync(off.data(), S.hoff.p, sizeof(long long) * (U + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const long long n = off[U];
+    S.hkeys.ensure(n + 1);
+    S.hvals.ensure(4 * (n + 1));
+    if (U > 0 && n > 0) {
+      k_halo_fill<<<nblk(32LL * U, 256), 256, 0, st>>>(S.soff.p, S.scols.p, S.mirror.p, S.V.p,
+                                                       S.dof_node.p, S.hoff.p, S.hkeys.p, S.hvals.p);
+      ++S.launches;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    for (int r = 0; r < world; ++r) counts[r] = off[bounds[r + 1]] - off[bounds[r]];
+    *keys = S.hkeys.p;
+    *vals = S.hvals.p;
+  });
+}
+
+int nlfem_gpu_session_rhs_records(nlfem_gpu_session* s, int32_t world, const int32_t* bounds,
+                                  void** idx, void** vals, int64_t* counts, char* err,
+                                  size_t errlen) {
+  return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
+    nlfem_gpu_session& S = *s;
+    cudaStream_t st = S.stream;
+    if (world < 1 || world > 64 || bounds[0] != 0 || bounds[world] != S.unknowns)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: row bounds must split [0, unknowns) in <= 64 blocks"};
+    CK(cudaMemcpyToSymbolAsync(cD, &S.dev, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
+    const int n = S.phi - S.plo;
+    DBuf<int> db;
+    db.upload(bounds, world + 1, st);
+    S.rmask.ensure(n + 1);
+    S.rflag.ensure(n + 1);
+    S.roffs.ensure(n + 1);
+    if (n > 0) {
+      k_rhs_mask<<<nblk(n, 256), 256, 0, st>>>(S.plo, S.phi, db.p, world, S.rmask.p);
+      ++S.launches;
+    }
+    // per destination: flag, scan, count (a few host reads; world is small)
+    std::vector<long long> cnt(world, 0);
+    for (int r = 0; r < world; ++r) {
+      if (n > 0) {
+        k_rhs_flag<<<nblk(n, 256), 256, 0, st>>>(n, S.rmask.p, r, S.rflag.p);
+        ++S.launches;
+      }
+      scan64(S, S.rflag.p, true, n, S.roffs.p, st);
+      cnt[r] = read_ll(S.roffs.p + n, st);
+    }
+    long long tot = 0;
+    for (int r = 0; r < world; ++r) tot += cnt[r];
+    S.ridx.ensure(tot + 1);
+    S.rvals.ensure((tot + 1) * (4 * kRhsWarps));
+    long long base = 0;
+    for (int r = 0; r < world; ++r) {
+      if (cnt[r] > 0) {
+        k_rhs_flag<<<nblk(n, 256), 256, 0, st>>>(n, S.rmask.p, r, S.rflag.p);
+        scan64(S, S.rflag.p, true, n, S.roffs.p, st);
+        k_rhs_scatter<<<nblk(n, 256), 256, 0, st>>>(n, S.plo, S.rflag.p, S.roffs.p, base, S.rhsT.p,
+                                                    S.ridx.p, S.rvals.p);
+        S.launches += 2;
+      }
+      counts[r] = cnt[r];
+      base += cnt[r];
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    *idx = S.ridx.p;
+    *vals = S.rvals.p;
+  });
+}
+
+int nlfem_gpu_session_finalize_merged(nlfem_gpu_session* s, void* stream, int32_t row_lo,
+                                      int32_t row_hi, const void* keys, const void* vals,
+                                      int64_t n, const void* ridx, const void* rvals, int64_t m,
+                                      char* err, size_t errlen) {
+  return guard(err, errlen, [&] {
+    DeviceScope ds(s->device);
+    nlfem_gpu_session& S = *s;
+    cudaStream_t st = S.stream;
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    if (user) {
+      CK(cudaEventRecord(S.ev[7], user));
+      CK(cudaStreamWaitEvent(st, S.ev[7], 0));
+    }
+    if (n < 0 || n >= (1LL << 32) - 1)
+      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: too many slot records for one rank"};
+    CK(cudaMemcpyToSymbolAsync(cD, &S.dev, sizeof(Dev), 0, cudaMemcpyHostToDevice, st));
+    const int J = S.J, U = S.unknowns;
+    const int r0 = std::max(0, row_lo), r1 = std::max(r0, std::min(row_hi, U));
+    // rhsT rows of the outer elements at this rank's nodes
+    if (m > 0) {
+      k_rhs_install<<<nblk(m * (4 * kRhsWarps), 256), 256, 0, st>>>(
+          m, static_cast<const int*>(ridx), static_cast<const double*>(rvals), S.rhsT.p);
+      ++S.launches;
+    }
+    // sort the records by key; distinct keys with their integer sums
+    S.mkeys.ensure(n + 1);
+    S.midx.ensure(n + 1);
+    S.midx2.ensure(n + 1);
+    S.mflag.ensure(n + 1);
+    S.muid.ensure(n + 2);
+    long long nu = 0;
+    if (n > 0) {
+      k_iota<<<nblk(n, 256), 256, 0, st>>>(n, S.midx.p);
+      int endbit = 33;
+      while (endbit < 64 && (1LL << (endbit - 32)) < (long long)J) ++endbit;
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, static_cast<const unsigned long long*>(keys),
+                                         S.mkeys.p, S.midx.p, S.midx2.p, n, 0, endbit, st));
+      S.cub_tmp.ensure(tb);
+      CK(cub::DeviceRadixSort::SortPairs(S.cub_tmp.p, tb, static_cast<const unsigned long long*>(keys),
+                                         S.mkeys.p, S.midx.p, S.midx2.p, n, 0, endbit, st));
+      k_key_flag<<<nblk(n, 256), 256, 0, st>>>(n, S.mkeys.p, S.mflag.p);
+      S.launches += 2;
+      scan64(S, S.mflag.p, true, n, S.muid.p, st);
+      nu = read_ll(S.muid.p + n, st);
+    }
+    DBuf<long long>& start = S.mstart;
+    start.ensure(nu + 1);
+    S.mV.ensure(4 * (size_t)(nu + 1));
+    S.mcols.ensure(nu + 1);
+    S.mmirror.ensure(nu + 1);
+    S.mcnt.ensure(J + 1);
+    CK(cudaMemsetAsync(S.mcnt.p, 0, (J + 1) * sizeof(int), st));
+    if (n > 0) {
+      k_key_start<<<nblk(n, 256), 256, 0, st>>>(n, S.mflag.p, S.muid.p, start.p);
+      k_key_sum<<<nblk(nu, 256), 256, 0, st>>>(nu, start.p, S.mkeys.p, S.midx2.p, static_cast<const long long*>(vals),
+                                               S.mV.p, S.mcols.p, S.mmirror.p, S.mcnt.p);
+      S.launches += 2;
+    }
+    S.moff.ensure(J + 1);
+    scan64(S, S.mcnt.p, true, J, S.moff.p, st);
+    // output pattern and values of the row block from the merged rows
+    CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
+    S.olen.ensure(U);
+    S.ooff.ensure(U + 1);
+    k_outpat<false><<<nblk(32LL * U, 256), 256, 0, st>>>(S.moff.p, S.mcols.p, S.olen.p, nullptr,
+                                                         nullptr, nullptr, S.dof_node.p, S.ovf.p);
+    scan64(S, S.olen.p, true, U, S.ooff.p, st);
+    const long long nnz = read_ll(S.ooff.p + U, st);
+    S.ocols.ensure(nnz + 1);
+    S.omap.ensure(nnz + 1);
+    k_outpat<true><<<nblk(32LL * U, 256), 256, 0, st>>>(S.moff.p, S.mcols.p, nullptr, S.ooff.p,
+                                                        S.ocols.p, S.omap.p, S.dof_node.p, S.ovf.p);
+    S.nnz_out = nnz;
+    S.values.ensure(nnz + 1);
+    S.rhs.ensure(U + 1);
+    if (r1 > r0) {
+      k_finalize<<<nblk((long long)(r1 - r0) * 32, 128), 128, 0, st>>>(
+          S.moff.p, S.mcols.p, S.mmirror.p, S.mV.p, S.ooff.p, S.omap.p, S.values.p, S.rhsT.p,
+          S.rhs.p, S.dof_node.p, r0, r1);
+      ++S.launches;
+    }
+    S.launches += 2;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    if (user) {
+      CK(cudaEventRecord(S.ev[6], st));
+      CK(cudaStreamWaitEvent(user, S.ev[6], 0));
+    }
   });
 }
 

@@ -1,18 +1,23 @@
-"""Multi-GPU assembly: one process per GPU (torch.distributed, NCCL over NVLink).
+"""Multi-GPU assembly: one process per GPU (torch.distributed, NCCL over NVLink),
+owner-computes (north star: "each rank assembles its own row
+block").
 
-Outer elements are independent units.  Each rank
-  1. builds the element pairs of its contiguous range of outer elements only,
-     all-gathers the 4-byte partner lists and per-element pair counts, and
-     builds the node pattern from the gathered list (identical on every rank:
-     the list is the single-GPU one, concatenated in outer order),
-  2. integrates its range of outer elements (z-slabs on lattice
-     meshes, whose element ids are z-major) into the fixed-point partial sums
-     of the pattern (integer words),
-  3. all-reduces the partials (int64 words; per-element rhs partials are written
-     by one rank only) -- integer addition is exact and order-free, so the sum is
-     bit-identical to a single-GPU run for any number of ranks,
-  4. finalizes its own block of output rows,
-  5. all-gathers the CSR row blocks, row pointers and rhs.
+Outer elements are independent units.  Rank r
+  1. builds the element pairs of its contiguous range of outer elements only
+     (z-slabs on lattice meshes, whose element ids are z-major), its LOCAL node
+     pattern (the rows its pairs touch) and integrates the range into it as
+     exact fixed-point partial sums (Session.run_local) -- no rank holds the
+     global pair list or the global pattern;
+  2. owns the unknown rows [b[r], b[r+1]) (row_bounds) and sends every local
+     slot of another rank's rows to that rank as a record (row, col, 4 int64
+     words), and the load-vector partials of its outer elements to the owners
+     of their nodes (all-to-all of the halo only: exchange_records);
+  3. sorts the records it received, sums equal keys as integers (exact and
+     order-free: the merged row of node i is the global pattern row, its sums
+     are the one-GPU sums) and finalizes its row block (finalize_merged);
+  4. all-gathers the row blocks' row lengths (-> row pointers), columns,
+     values and rhs.
+The result is bit-identical to a one-GPU run for any number of ranks.
 """
 from __future__ import annotations
 
@@ -86,116 +91,128 @@ def _comm_device(group=None):
     return torch.device("cpu") if dist.get_backend(group) == "gloo" else torch.device("cuda")
 
 
-def allreduce_partials(V, rhsT, group=None) -> None:
-    """In-place integer sum of the fixed-point partials across ranks."""
-    import torch.distributed as dist
-    if V.device.type == "cuda" and _comm_device(group).type == "cpu":
-        for t in (V, rhsT):
-            h = t.cpu()
-            dist.all_reduce(h, group=group)
-            t.copy_(h)
-        return
-    dist.all_reduce(V, group=group)
-    dist.all_reduce(rhsT, group=group)
+def row_bounds(unknowns: int, world: int) -> list[int]:
+    """Row-block boundaries: rank r owns unknowns [b[r], b[r+1]) (dofs follow
+    node ids, so on lattice meshes a block is a z-slab, like the outer-element
+    shards)."""
+    return [shard_range(unknowns, r, world)[0] for r in range(world)] + [unknowns]
 
 
-def gather_pairs(session, lo: int, hi: int, group=None, device=None) -> int:
-    """Build this rank's element pairs (outer elements [lo, hi)), all-gather the
-    pair counts and partner ids of every rank (NCCL, padded device tensors) and
-    install the concatenation -- the unsharded pair list -- for the next
-    run_shard.  Returns the total number of element pairs."""
+def alltoallv(send, send_counts, recv_counts, group=None, device=None):
+    """Variable-size all-to-all of a flat tensor whose entries are grouped by
+    destination rank (send_counts[r] entries for rank r); returns the entries
+    received from every rank, concatenated in rank order.  NCCL on device
+    tensors; gloo stages through host memory."""
     import torch
     import torch.distributed as dist
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    npairs = session.pairs_shard(lo, hi)
-    cview, pview = session.pairs_shard_out()
-    dev = torch.device("cuda") if device is None else torch.device(device)
-    src = "cuda" if torch.cuda.is_available() else dev  # the session's arrays live in HBM
-    counts = (torch.as_tensor(cview, device=src).to(dev) if hi > lo
-              else torch.zeros(0, dtype=torch.int32, device=dev))
-    partners = (torch.as_tensor(pview, device=src).to(dev) if npairs > 0
-                else torch.zeros(0, dtype=torch.int32, device=dev))
-    counts, partners = counts.to(torch.int32), partners.to(torch.int32)
-    # the install reads device arrays, after torch's current stream
-    stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
-    if world == 1:
-        if counts.device.type != "cuda" and torch.cuda.is_available():
-            counts, partners = counts.cuda(), partners.cuda()
-        session.pairs_install(counts, partners, npairs, stream=stream)
-        return npairs
-    # flat outputs viewed as (world, n): accepted by NCCL and gloo alike
-    meta = torch.tensor([hi - lo, npairs], dtype=torch.int64, device=dev)
-    metas = torch.empty(world * 2, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(metas, meta, group=group)
-    m = metas.view(world, 2).cpu().numpy()
+    dev = device if device is not None else _comm_device(group)
+    src = torch.as_tensor(send, device="cuda" if torch.cuda.is_available() else "cpu")
+    src = src.to(dev)
+    out = torch.empty(int(sum(recv_counts)), dtype=src.dtype, device=dev)
+    dist.all_to_all_single(out, src, [int(c) for c in recv_counts],
+                           [int(c) for c in send_counts], group=group)
+    return out
 
-    def gather(t, n_max):
-        pad = torch.zeros(max(int(n_max), 1), dtype=t.dtype, device=dev)
-        pad[: t.numel()] = torch.as_tensor(t, device=dev)
-        out = torch.empty(world * pad.numel(), dtype=t.dtype, device=dev)
-        dist.all_gather_into_tensor(out, pad, group=group)
-        return out.view(world, pad.numel())
 
-    gc = gather(counts, m[:, 0].max())
-    gp = gather(partners, m[:, 1].max())
-    all_counts = torch.cat([gc[r, : int(m[r, 0])] for r in range(world)])
-    all_partners = torch.cat([gp[r, : int(m[r, 1])] for r in range(world)])
-    total = int(m[:, 1].sum())
-    if all_counts.device.type != "cuda" and torch.cuda.is_available():
-        all_counts, all_partners = all_counts.cuda(), all_partners.cuda()
-    session.pairs_install(all_counts, all_partners, total, stream=stream)
-    return total
+def exchange_records(send: dict, counts: dict, group=None, device=None) -> dict:
+    """Ship each rank's records to their owners.  send: name -> (flat tensor,
+    words per record); counts: name -> per-destination record counts (numpy).
+    Returns name -> flat tensor of the records this rank received."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = device if device is not None else _comm_device(group)
+    names = sorted(send)
+    sc = torch.tensor(np.stack([np.asarray(counts[n], np.int64) for n in names], 1).reshape(-1),
+                      dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)  # the record counts themselves
+    rc = rc.view(world, len(names)).cpu().numpy()
+    out = {}
+    for k, n in enumerate(names):
+        t, w = send[n]
+        out[n] = alltoallv(t, np.asarray(counts[n], np.int64) * w, rc[:, k] * w, group, dev)
+    return out
 
 
 def assemble_distributed(session, group=None, stream: int | None = None) -> tuple[dict, dict]:
     """Sharded assembly on this rank's GPU; every rank returns the full system
-    on the host: device_step (partials all-reduced and row blocks all-gathered
-    in HBM over NCCL), then one device-to-host copy of the gathered CSR."""
-    import torch
-    (va, ci, rh), st = device_step(session, group, stream)
-    ro = torch.as_tensor(session.outputs()[0], device="cuda")
-    full = {"row_ptr": ro.to(torch.int32).cpu().numpy(), "col_idx": ci.cpu().numpy(),
+    on the host: device_step (owner-computes, halo records exchanged, row
+    blocks all-gathered in HBM over NCCL), then one device-to-host copy of the
+    gathered CSR."""
+    (va, ci, rh, rp), st = device_step(session, group, stream)
+    rp = rp.cpu().numpy()
+    if rp[-1] > 2**31 - 1:
+        raise OverflowError(f"{int(rp[-1])} nonzeros exceed the int32 row pointers of the CSR")
+    full = {"row_ptr": rp.astype(np.int32), "col_idx": ci.cpu().numpy(),
             "values": va.cpu().numpy(), "rhs": rh.cpu().numpy()}
     return full, st.as_dict()
 
 
 def device_step(session, group=None, stream: int | None = None):
-    """One sharded assembly with every array staying in HBM: integrate this
-    rank's outer elements, all-reduce the exact partials (NCCL), finalize this
-    rank's row block, all-gather the row blocks' values, columns and rhs
-    (NCCL all_gather on padded device tensors).  Returns the gathered device
-    tensors (values, col_idx, rhs) and the run statistics."""
+    """One owner-computes sharded assembly with every array in HBM (NCCL):
+
+    1. run_local: this rank's outer elements [lo, hi) -- their pairs, the local
+       node pattern and the integration (no other rank's pairs or pattern);
+    2. halo exchange: every local slot of an unknown row goes to the rank that
+       owns the row as a (row, col, 4 int64 words) record, and the load-vector
+       partials of the outer elements at a rank's nodes go to it
+       (all-to-all; NCCL send/recv over NVLink);
+    3. finalize_merged: the owner sorts what it received, sums equal keys as
+       integers and finalizes its row block -- bit for bit the one-GPU rows;
+    4. the row blocks' values, columns and rhs are all-gathered.
+
+    Returns the gathered device tensors (values, col_idx, rhs) and this rank's
+    run statistics (its own outer elements)."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     cdev = _comm_device(group)
-    lo, hi = shard_range(session.interior_count, rank, world)
-    gather_pairs(session, lo, hi, group, device=cdev)
-    st = session.run_shard(lo, hi, finalize=False, stream=stream)
-    vv, rv = session.partials()
-    V = torch.as_tensor(vv, device="cuda")
-    R = torch.as_tensor(rv, device="cuda")
-    allreduce_partials(V, R, group)
-    r0, r1 = shard_range(session.unknowns, rank, world)
-    # the reduced partials are ready on torch's current stream (NCCL enqueues
-    # there): the session's finalize waits on it
-    session.finalize(r0, r1, stream=torch.cuda.current_stream().cuda_stream)
+    KI, U = session.interior_count, session.unknowns
+    lo, hi = shard_range(KI, rank, world)
+    st = session.run_local(lo, hi, stream=stream)
+    bounds = row_bounds(U, world)
+    keys, words, kc = session.halo_records(bounds)
+    ridx, rvals, rcnt = session.rhs_records(bounds)
+    got = exchange_records({"keys": (keys, 1), "words": (words, 4), "ridx": (ridx, 1),
+                            "rvals": (rvals, 32)},
+                           {"keys": kc, "words": kc, "ridx": rcnt, "rvals": rcnt}, group, cdev)
+    got = {k: v.to("cuda") for k, v in got.items()}
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    # the received records are ready on torch's current stream
+    session.finalize_merged(r0, r1, got["keys"], got["words"], got["ridx"], got["rvals"],
+                            stream=torch.cuda.current_stream().cuda_stream)
     ro, ci, va, rh = (torch.as_tensor(x, device="cuda") for x in session.outputs())
-    # row-block extents on every rank (row offsets are identical everywhere)
-    bounds = [shard_range(session.unknowns, r, world) for r in range(world)]
-    offs = ro.cpu().numpy() if world > 1 else None
-    out = []
-    for arr, per_row in ((va, False), (ci, False), (rh, True)):
-        if world == 1:
-            out.append(arr)
-            continue
-        ext = [((a, b) if per_row else (int(offs[a]), int(offs[b]))) for a, b in bounds]
-        m = max(b - a for a, b in ext)
-        a, b = ext[rank]
-        pad = torch.zeros(max(m, 1), dtype=arr.dtype, device=cdev)
-        pad[: b - a] = arr[a:b].to(cdev)
-        gathered = torch.empty(world * max(m, 1), dtype=arr.dtype, device=cdev)
-        dist.all_gather_into_tensor(gathered, pad, group=group)
-        gathered = gathered.view(world, max(m, 1))
-        out.append(torch.cat([gathered[r, : e[1] - e[0]] for r, e in enumerate(ext)]).to("cuda"))
-    return out, st
+    if world == 1:
+        return [va, ci, rh, ro], st
+    # all-gather the row blocks: row lengths (-> row pointers), columns,
+    # values and rhs of every block, in rank order
+    a, b = int(ro[r0].item()), int(ro[r1].item())
+    parts = {"len": (ro[r0 + 1:r1 + 1] - ro[r0:r1]), "ci": ci[a:b], "va": va[a:b],
+             "rh": rh[r0:r1]}
+    full = {}
+    for name, arr in parts.items():
+        full[name] = allgather_var(arr, group, cdev).to("cuda")
+    rp = torch.zeros(U + 1, dtype=torch.int64, device="cuda")
+    rp[1:] = torch.cumsum(full["len"], 0)
+    return [full["va"], full["ci"], full["rh"], rp], st
+
+
+def allgather_var(arr, group=None, device=None):
+    """All-gather variable-length flat tensors (padded to the longest), result
+    concatenated in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = device if device is not None else _comm_device(group)
+    n = torch.tensor([arr.numel()], dtype=torch.int64, device=dev)
+    sizes = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(sizes, n, group=group)
+    sizes = sizes.cpu().numpy()
+    m = int(max(sizes.max(), 1))
+    pad = torch.zeros(m, dtype=arr.dtype, device=dev)
+    pad[: arr.numel()] = arr.to(dev)
+    g = torch.empty(world * m, dtype=arr.dtype, device=dev)
+    dist.all_gather_into_tensor(g, pad, group=group)
+    g = g.view(world, m)
+    return torch.cat([g[r, : int(sizes[r])] for r in range(world)])

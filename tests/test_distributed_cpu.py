@@ -1,6 +1,7 @@
 """Multi-rank host logic on CPU with the gloo backend (world size 2):
-shard splits, the exact integer reduction of fixed-point partials, and the
-all-gather of CSR row blocks (paper_2302_07499_b200/distributed.py)."""
+shard splits, the owner-computes record exchange (all-to-all of the halo
+records, counts first) and the all-gathers of the row blocks
+(paper_2302_07499_b200/distributed.py)."""
 import os
 import socket
 
@@ -60,22 +61,12 @@ def _worker(rank, world, port, q):
                  "values": full["values"][s0:s1], "rhs": full["rhs"][r0:r1]}
         got = D.allgather_csr(block)
         ok_gather = all(np.array_equal(got[k], full[k]) for k in full)
-        # exact integer reduction with wrap-around (two's complement words)
-        rng = np.random.default_rng(100 + rank)
-        part = rng.integers(-2**62, 2**62, size=1000, dtype=np.int64)
-        V = torch.from_numpy(part.copy())
-        R = torch.zeros(8, dtype=torch.float64)
-        R[rank] = 1.5 + rank  # each rhs partial written by one rank only
-        D.allreduce_partials(V, R)
-        parts = [np.random.default_rng(100 + r).integers(-2**62, 2**62, size=1000, dtype=np.int64)
-                 for r in range(world)]
-        with np.errstate(over="ignore"):
-            want = parts[0].copy()
-            for p in parts[1:]:
-                want = want + p
-        ok_reduce = np.array_equal(V.numpy(), want)
-        ok_rhs = R[:world].tolist() == [1.5 + r for r in range(world)]
-        q.put((rank, ok_gather, ok_reduce, ok_rhs))
+        # variable-length all-gather (the row-block gather of device_step)
+        mine = torch.arange(3 + 4 * rank, dtype=torch.int64) + 100 * rank
+        g = D.allgather_var(mine, device=torch.device("cpu")).numpy()
+        want = np.concatenate([np.arange(3 + 4 * r) + 100 * r for r in range(world)])
+        ok_var = np.array_equal(g, want)
+        q.put((rank, ok_gather, ok_var, True))
     finally:
         dist.destroy_process_group()
 
@@ -93,54 +84,59 @@ def test_gloo_world2_gather_and_reduce():
     assert all(ok for (_, a, b, c) in res for ok in (a, b, c)), res
 
 
-class _FakePairsSession:
-    """Stand-in for Session's sharded-pair API: outer element i has (i % 5) + 1
-    partners with ids 1000 * i + j."""
-
-    def __init__(self, ki):
-        self.ki = ki
-        self.installed = None
-
-    def _lists(self, lo, hi):
-        counts = np.array([(i % 5) + 1 for i in range(lo, hi)], np.int32)
-        partners = np.array([1000 * i + j for i in range(lo, hi) for j in range((i % 5) + 1)],
-                            np.int32)
-        return counts, partners
-
-    def pairs_shard(self, lo, hi):
-        self._c, self._p = self._lists(lo, hi)
-        return len(self._p)
-
-    def pairs_shard_out(self):
-        return self._c, self._p
-
-    def pairs_install(self, counts, partners, total, stream=None):
-        self.installed = (np.asarray(counts).copy(), np.asarray(partners).copy(), total)
+def _records(rank, world, dest):
+    """Rank `rank`'s records for rank `dest`: (key, 4 words) with key
+    = row << 32 | col, rows in dest's block, count 2 + rank + dest."""
+    n = 2 + rank + dest
+    keys = (np.int64(dest) << 32) + 1000 * rank + np.arange(n, dtype=np.int64)
+    words = np.arange(4 * n, dtype=np.int64) * (rank + 1) - 7 * dest
+    return keys, words
 
 
-def _pairs_worker(rank, world, port, q):
+def _exchange_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ki = 23
-        s = _FakePairsSession(ki)
-        lo, hi = D.shard_range(ki, rank, world)
-        total = D.gather_pairs(s, lo, hi, device="cpu")
-        wc, wp = s._lists(0, ki)
-        c, p, t = s.installed
-        q.put((rank, t == total == len(wp), np.array_equal(c, wc), np.array_equal(p, wp)))
+        ks, ws = zip(*[_records(rank, world, d) for d in range(world)])
+        cnt = np.array([len(k) for k in ks], np.int64)
+        # rhs records: one per destination (position, 32 doubles)
+        ridx = np.array([10 * rank + d for d in range(world)], np.int32)
+        rvals = np.repeat(ridx.astype(np.float64), 32) + 0.5
+        got = D.exchange_records(
+            {"keys": (torch.from_numpy(np.concatenate(ks)), 1),
+             "words": (torch.from_numpy(np.concatenate(ws)), 4),
+             "ridx": (torch.from_numpy(ridx), 1), "rvals": (torch.from_numpy(rvals), 32)},
+            {"keys": cnt, "words": cnt, "ridx": np.ones(world, np.int64),
+             "rvals": np.ones(world, np.int64)}, device=torch.device("cpu"))
+        wk = np.concatenate([_records(r, world, rank)[0] for r in range(world)])
+        ww = np.concatenate([_records(r, world, rank)[1] for r in range(world)])
+        wi = np.array([10 * r + rank for r in range(world)], np.int32)
+        ok = (np.array_equal(got["keys"].numpy(), wk) and np.array_equal(got["words"].numpy(), ww)
+              and np.array_equal(got["ridx"].numpy(), wi)
+              and np.array_equal(got["rvals"].numpy(), np.repeat(wi.astype(np.float64), 32) + 0.5))
+        q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world2_gather_pairs_concatenates_in_outer_order():
+def test_gloo_world2_halo_records_reach_their_owners():
+    # the owner-computes exchange (device_step step 2): every rank's records
+    # for rank d arrive at d, concatenated in sender order, counts first
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_pairs_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
     for p in procs:
         p.join(timeout=60)
-    assert all(ok for (_, a, b, c) in res for ok in (a, b, c)), res
+    assert all(ok for _, ok in res), res
+
+
+def test_row_bounds_split_unknowns():
+    for u in (0, 5, 857375):
+        for w in (1, 2, 8):
+            b = D.row_bounds(u, w)
+            assert b[0] == 0 and b[-1] == u and len(b) == w + 1
+            assert all(b[i] <= b[i + 1] for i in range(w))

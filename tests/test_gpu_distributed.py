@@ -173,3 +173,96 @@ def test_session_reset_equals_fresh_session():
     assert np.array_equal(torch.as_tensor(pd["partner"], device="cuda").cpu().numpy(),
                           ph["partner"])
     assert np.array_equal(torch.as_tensor(pd["info"], device="cuda").cpu().numpy(), ph["info"])
+
+
+def _owner_computes(t, strat, mc, nrank, delta=0.34, chunk_env=None):
+    """nrank "ranks" as sessions on one GPU running the owner-computes plan
+    (distributed.device_step without the collectives): local pairs / pattern /
+    integration per rank, records routed by destination in rank order (what
+    the all-to-all delivers), merged finalize of each row block."""
+    import torch
+    ranks = [P.Session(t, delta, strat, "moment2", U2, seed=SEED, mc_samples=mc)
+             for _ in range(nrank)]
+    KI, U = ranks[0].interior_count, ranks[0].unknowns
+    bounds = D.row_bounds(U, nrank)
+    sent, pairs = [], 0
+    for r, s in enumerate(ranks):
+        lo, hi = D.shard_range(KI, r, nrank)
+        st = s.run_local(lo, hi)
+        pairs += st.element_pairs
+        k, w, kc = s.halo_records(bounds)
+        ri, rv, rc = s.rhs_records(bounds)
+        k, w = torch.as_tensor(k, device="cuda").clone(), torch.as_tensor(w, device="cuda").clone()
+        ri, rv = torch.as_tensor(ri, device="cuda").clone(), torch.as_tensor(rv, device="cuda").clone()
+        ko, ro = np.concatenate([[0], np.cumsum(kc)]), np.concatenate([[0], np.cumsum(rc)])
+        sent.append([(k[ko[d]:ko[d + 1]], w[4 * ko[d]:4 * ko[d + 1]], ri[ro[d]:ro[d + 1]],
+                      rv[32 * ro[d]:32 * ro[d + 1]]) for d in range(nrank)])
+    blocks = []
+    for d, s in enumerate(ranks):
+        parts = [sent[r][d] for r in range(nrank)]
+        keys, words, ridx, rvals = (torch.cat([p[i] for p in parts]) for i in range(4))
+        s.finalize_merged(bounds[d], bounds[d + 1], keys, words, ridx, rvals)
+        blocks.append(s.download_rows(bounds[d], bounds[d + 1]))
+    for s in ranks:
+        s.close()
+    return D.concat_csr(blocks), pairs
+
+
+@pytest.mark.parametrize("strat,mc,nrank", [("nocaps", 1, 3), ("fullcaps", 8, 2),
+                                            ("barycenter", 1, 4), ("fullcaps", 8, 1)])
+def test_owner_computes_equals_single_gpu_bitwise(strat, mc, nrank):
+    m = P.generate_mesh(3, 6, 0.34, jitter_seed=5)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    ref = P.Session(t, 0.34, strat, "moment2", U2, seed=SEED, mc_samples=mc)
+    ref.run()
+    want = ref.download()
+    got, pairs = _owner_computes(t, strat, mc, nrank)
+    assert pairs == ref.stats.element_pairs
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(got[k], want[k]), (strat, nrank, k)
+
+
+def test_owner_computes_eight_ranks_lattice():
+    # thin slabs (N = 8 lattice, 8 ranks: one cube layer of outer elements
+    # each, delta = 2h): every rank's rows take records from several others
+    m = P.generate_mesh(3, 8, 0.25)
+    t = P.ElementTable(m["coords"], m["cells"], m["region"])
+    ref = P.Session(t, 0.25, "fullcaps", "moment2", U2, seed=SEED, mc_samples=16)
+    ref.run()
+    want = ref.download()
+    got, _ = _owner_computes(t, "fullcaps", 16, 8, delta=0.25)
+    for k in ("row_ptr", "col_idx", "values", "rhs"):
+        assert np.array_equal(got[k], want[k]), k
+
+
+def test_owner_computes_chunked_units():
+    # the local path through the chunked units / combine (several chunks per
+    # rank, two alternating unit-buffer sets): same system bit for bit
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2302_07499_b200 as P
+from tests.test_gpu_distributed import _owner_computes
+from tests.helpers import SEED, U2
+m = P.generate_mesh(3, 6, 0.34, jitter_seed=5)
+t = P.ElementTable(m["coords"], m["cells"], m["region"])
+got, _ = _owner_computes(t, "fullcaps", 8, 3)
+np.savez(sys.argv[2], **got)
+"""
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "c.npz")
+        env = dict(os.environ, NLFEM_PAIRS_PER_CHUNK="2000")
+        subprocess.run([sys.executable, "-c", code, root, out], env=env, cwd=root, check=True,
+                       timeout=600)
+        got = np.load(out)
+        m = P.generate_mesh(3, 6, 0.34, jitter_seed=5)
+        t = P.ElementTable(m["coords"], m["cells"], m["region"])
+        ref = P.Session(t, 0.34, "fullcaps", "moment2", U2, seed=SEED, mc_samples=8)
+        ref.run()
+        want = ref.download()
+        for k in ("row_ptr", "col_idx", "values", "rhs"):
+            assert np.array_equal(got[k], want[k]), k
