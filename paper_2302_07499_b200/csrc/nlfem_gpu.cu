@@ -133,6 +133,8 @@ struct Dev {
   int gx, gy, gz;
   const int* cell_start;
   const int* cell_elems;
+  const double4* cell_cen;  // [K] (center, radius) of cell_elems[k]: the K1 screen reads
+                            // it coalesced, beside the id instead of after it
   // node incidence (interior elements) sorted by element id
   const int* ni_off;
   const int* ni_el;
@@ -246,6 +248,11 @@ __global__ void k_fill_by_key(int n, const int* key, const long long* off, int* 
 
 // Sort each short segment ascending (insertion sort, one thread per segment);
 // makes the atomic fills deterministic.
+__global__ void k_cell_cen(int K, const int* cell_elems, const double4* erec, double4* cen) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < K) cen[k] = erec[4 * (long long)cell_elems[k]];
+}
+
 __global__ void k_sort_segments(int nseg, const long long* off, int* data) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nseg) return;
@@ -770,8 +777,9 @@ __global__ void __launch_bounds__(kPairThreads, NLFEM_PAIRS_MINBLOCKS) k_pairs(i
         double4 a;
         if (g < total) {
           while (rpre[rr + 1] <= g) ++rr;
-          Tp = cD.cell_elems[rstart[rr] + (g - rpre[rr])];
-          a = cD.erec[4 * Tp];
+          const int ci = rstart[rr] + (g - rpre[rr]);
+          Tp = cD.cell_elems[ci];
+          a = cD.cell_cen[ci];
 #pragma unroll
           for (int w = 0; w < kPairWarps; ++w) {
             const double thr = a.w + oc[w][3];
@@ -1212,12 +1220,15 @@ __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot,
   if (lo != 0) atomicAdd(V + 2 * slot + 1, (unsigned long long)lo);
 }
 
-// Entries whose row and column are both unknowns take the high word only
-// (~62 bits of the row bound: errors stay ~1e-13 of the row's largest entry);
-// entries touching a constrained node feed the rhs folding, where
-// cancellation can amplify errors, and keep both words.
+// Every entry keeps both words (~101 bits: the exact sum of its FP64
+// contributions up to one final rounding).  NLFEM_FIXED_TWO=0 restores the
+// round-1 choice -- unknown x unknown entries with the high word only (~62
+// bits of the row bound) -- measured at C4 as 3.8e-13 of a row's largest
+// entry at worst (mean 5e-15; scripts/fixed_point_precision.py,
+// profiles/r2_fixed_point_precision.txt), above the 1e-13 budget, for a 0.5%
+// (C2, P3f) to 3.5% (C3n) shorter step.
 #ifndef NLFEM_FIXED_TWO
-#define NLFEM_FIXED_TWO 0  // 1: every entry keeps both words (precision study)
+#define NLFEM_FIXED_TWO 1  // 0: unknown x unknown entries keep the high word only
 #endif
 __device__ __forceinline__ void red_fixed_sel(unsigned long long* V, long long slot, double v,
                                               double scale, bool two) {
@@ -1433,7 +1444,7 @@ __device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c)
 }
 
 #ifndef NLFEM_MC_MOM
-#define NLFEM_MC_MOM 3  // 0: FP64 products; 1-3: integer products (masks by SEL / IMAD)
+#define NLFEM_MC_MOM 0  // 0: FP64 products; 1-3: integer products (masks by SEL / IMAD)
 #endif
 
 struct IntMoments {
@@ -2134,13 +2145,6 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     const double volP = cD.vol[Tp];
     const double* invP = cD.inv + 9 * (long long)Tp;
     long long u = (mom != nullptr) ? uoff[p - pbase] : 0;  // first record of the pair
-    if (mom != nullptr && p + NTHR < p1) {
-      // next pair of this thread: pull its records (<= 4 x 80 B) into L2 now
-      const char* nr = reinterpret_cast<const char*>(mom + kMomStride * uoff[p + NTHR - pbase]);
-#pragma unroll
-      for (int l = 0; l < 3; ++l)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(nr + 128 * l));
-    }
 
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
@@ -2629,6 +2633,7 @@ struct nlfem_gpu_session {
   DBuf<unsigned char> bnd;
   // grid / incidence
   DBuf<int> cell_key, cell_cnt, cell_elems, cursor, ni_cnt, ni_el, ai_cnt;
+  DBuf<double4> cell_cen;
   DBuf<unsigned long long> ai_vmax;
   DBuf<long long> cell_start64, ni_off64, scan_tmp, scan_tmp2;
   DBuf<int> cell_start, ni_off;
@@ -2992,7 +2997,9 @@ void run_prep(nlfem_gpu_session& S) {
                                               S.cell_elems.p);
   k_sort_segments<<<nblk(ncell, 256), 256, 0, st>>>((int)ncell, S.cell_start64.p, S.cell_elems.p);
   k_ll_to_int<<<nblk(ncell + 1, 256), 256, 0, st>>>(ncell + 1, S.cell_start64.p, S.cell_start.p);
-  S.launches += 3;
+  S.cell_cen.ensure(K);
+  k_cell_cen<<<nblk(K, 256), 256, 0, st>>>(K, S.cell_elems.p, S.erec.p, S.cell_cen.p);
+  S.launches += 4;
   // node -> interior elements (ascending)
   scan64(S, S.ni_cnt.p, true, J, S.ni_off64.p, st);
   const long long nin = 4LL * S.KI;  // every interior element has 4 nodes: no read-back
@@ -3006,6 +3013,7 @@ void run_prep(nlfem_gpu_session& S) {
   S.iscale.ensure(J);
   D.cell_start = S.cell_start.p;
   D.cell_elems = S.cell_elems.p;
+  D.cell_cen = S.cell_cen.p;
   D.ni_off = S.ni_off.p;
   D.ni_el = S.ni_el.p;
   D.scale = S.scale.p;

@@ -20,5 +20,5 @@ print('$L $C', 'ms/step %.2f'%d['ms_per_step'], 'units ms %.2f'%r['launch_ms'], 
 done
 unset NLFEM_GPU_LIB
 [ -n "$PREC" ] && timeout 900 python scripts/fixed_point_precision.py $PREC > $O/precision.json 2> $O/precision.err
-[ -n "$EMU" ] && for C in $EMU; do timeout 1200 python scripts/owner_computes_emulate.py $C 2,4,8 > $O/emulate_$C.jsonl 2> $O/emulate_$C.err; done
+[ -n "$EMU" ] && for C in $EMU; do timeout 1500 python scripts/owner_computes_emulate.py ${C%:*} ${C#*:} > $O/emulate_${C%:*}.jsonl 2> $O/emulate_${C%:*}.err; done
 ls $O
