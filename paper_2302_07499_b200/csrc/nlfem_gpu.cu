@@ -882,9 +882,16 @@ __global__ void k_pairs_compact(int ii0, int ii1, const long long* cand_off, lon
 // ---------------------------------------------------------------------------
 // K5: pattern
 
-constexpr int kHE = 8192;   // element hash slots per node block
-constexpr int kHN = 4096;   // node hash slots
-constexpr int kRowMax = 4096;
+// Pattern tables per node block, in shared memory: element hash slots, node
+// hash slots and the longest row.  The small set covers delta/h <~ 5 (row
+// lengths ~(4/3) pi (delta/h + 2)^3 nodes); a pass that overflows it is rerun
+// with the large set (192 KB of shared memory per block: delta/h <~ 8.5, e.g.
+// the finest level of the reference's default convergence study).
+struct PatTabs {
+  int he, hn, rowmax;
+};
+constexpr PatTabs kPatSmall{8192, 4096, 4096};
+constexpr PatTabs kPatBig{32768, 8192, 8192};
 
 __device__ __forceinline__ unsigned hash32(unsigned x) {
   x ^= x >> 16;
@@ -960,8 +967,9 @@ template <bool FILL>
 __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const int* partner,
                                               int* rlen, const long long* roff, int* rcols,
                                               int* ovf, int plo, int phi,
-                                              const unsigned char* pmark) {
+                                              const unsigned char* pmark, PatTabs tb) {
   extern __shared__ int sm[];
+  const int kHE = tb.he, kHN = tb.hn, kRowMax = tb.rowmax;
   int* tabE = sm;
   int* tabN = sm + kHE;
   int* list = tabN + kHN;
@@ -1032,7 +1040,7 @@ __global__ void k_transpose_fill(int J, const long long* roff, const int* rcols,
 }
 
 __global__ void __launch_bounds__(256) k_sort_rows(int J, const long long* off, int* cols,
-                                                   int* ovf) {
+                                                   int* ovf, int kRowMax) {
   extern __shared__ int sm[];
   if (*ovf) return;
   for (int i = blockIdx.x; i < J; i += gridDim.x) {
@@ -1071,8 +1079,9 @@ __global__ void __launch_bounds__(kUnionThreads) k_union(int J, const long long*
                                                          const int* rcols, const long long* toff,
                                                          const int* tcols, int* slen,
                                                          const long long* soff, int* scols,
-                                                         int* maxlen, const int* ovf) {
-  __shared__ int pre[kRowMax + 1];
+                                                         int* maxlen, const int* ovf,
+                                                         int kRowMax) {
+  extern __shared__ int pre[];  // kRowMax + 1
   __shared__ int wtot[kUnionThreads / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   if (*ovf) return;
@@ -1211,8 +1220,16 @@ __global__ void k_outpat(const long long* soff, const int* scols, int* olen,
 // (exact: scale is a power of two) and lo = rint((v*scale - hi) * 2^40), so an
 // accumulated entry carries ~101 bits and equals the exact sum of the FP64
 // contributions up to one final rounding; integer adds make it order-free.
+#ifndef NLFEM_DIAG
+#define NLFEM_DIAG 0  // timing diagnostics of the combine (bit 1: no REDs; 2: no item
+                      // records; 4: no partner-element gathers) -- wrong results
+#endif
 __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot, double v,
                                           double scale) {
+  if (NLFEM_DIAG & 1) {
+    if (v == 1.2345e300) V[slot & 1] = 1;  // keeps the value live
+    return;
+  }
   const double x = v * scale;
   const long long hi = __double2ll_rn(x);
   const long long lo = __double2ll_rn((x - (double)hi) * 0x1p40);
@@ -1232,7 +1249,7 @@ __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot,
 #endif
 __device__ __forceinline__ void red_fixed_sel(unsigned long long* V, long long slot, double v,
                                               double scale, bool two) {
-  if (!two && !NLFEM_FIXED_TWO) {
+  if (!two && !NLFEM_FIXED_TWO && !(NLFEM_DIAG & 1)) {
     const long long hi = __double2ll_rn(v * scale);
     if (hi != 0) atomicAdd(V + 2 * slot, (unsigned long long)hi);
     return;
@@ -2058,10 +2075,15 @@ struct SlotMap {
   int* key;
   short4* val;  // slot offsets within row a (-1: absent); rows hold < 32768 entries
   int mask;
+  // slot of key k, or -1 if the table overflowed while it was built (the
+  // combine then flags the run; the host sizes the table up or fails cleanly)
   __device__ __forceinline__ int probe(int k) const {
     unsigned h = hash32((unsigned)k) & mask;
-    while (key[h] != k) h = (h + 1) & mask;
-    return (int)h;
+    for (int n = 0; n <= mask; ++n) {
+      if (key[h] == k) return (int)h;
+      h = (h + 1) & mask;
+    }
+    return -1;
   }
 };
 
@@ -2106,10 +2128,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     for (long long k = r0 + threadIdx.x; k < r1; k += blockDim.x) {
       const int col = scols[k];
       unsigned h = hash32((unsigned)col) & mp.mask;
-      while (true) {
+      int n = 0;
+      for (; n <= mp.mask; ++n) {
         const int prev = atomicCAS(mp.key + h, -1, col);
         if (prev == -1 || prev == col) break;
         h = (h + 1) & mp.mask;
+      }
+      if (n > mp.mask) {  // the four rows' union outgrew the table
+        atomicAdd(stats + 7, 1ull);
+        continue;
       }
       reinterpret_cast<short*>(mp.val + h)[a] = (short)(k - r0);
     }
@@ -2139,7 +2166,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
     for (int k = 0; k < 10; ++k) S2[k] = 0;
 
-    const int Tp = partner[p];
+    const int Tp = (NLFEM_DIAG & 4) ? T : partner[p];
     const unsigned code = info[p];
     const bool constr = cD.region[Tp] != 0;
     const double volP = cD.vol[Tp];
@@ -2173,7 +2200,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
       // Monte Carlo for fullcaps), Cartesian moments about v0(T')
       if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
         double g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
-        const double2* rec = reinterpret_cast<const double2*>(mom + kMomStride * u);
+        const double2* rec = reinterpret_cast<const double2*>(mom + kMomStride * ((NLFEM_DIAG & 2) ? 0 : u));
         const double2 r0 = rec[0];
         const double n0 = r0.x;
         if (constr) {
@@ -2254,7 +2281,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
       // T x T' cross block -C w X[a][b] at (N_a, M_b): shared-memory rows
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const short4 sl = mp.val[mp.probe(NP[b])];
+        const int hb = mp.probe(NP[b]);
+        if (hb < 0) continue;  // overflowed table (flagged above): the run fails
+        const short4 sl = mp.val[hb];
         const short sla[4] = {sl.x, sl.y, sl.z, sl.w};
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
@@ -2300,7 +2329,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
       int ra = 0;
       for (int r = 0; r < 4; ++r)
         if (NT[r] == lo) ra = r;
-      const short* v = reinterpret_cast<const short*>(mp.val + mp.probe(hi));
+      const int hh = mp.probe(hi);
+      const short* v = reinterpret_cast<const short*>(mp.val + (hh < 0 ? 0 : hh));
       red_fixed(V, rbase[ra] + v[ra], tot, sc[ra]);
     }
   } else if (lane < 14) {
@@ -2680,6 +2710,7 @@ struct nlfem_gpu_session {
   // pattern (owner-computes multi-GPU), pmark[K] flags the interior partners
   int plo = 0, phi = 0;
   bool plocal = false;
+  bool pattern_big = false;  // large pattern tables (delta/h >~ 5), kept once needed
   DBuf<unsigned char> pmark;
   // owner-computes multi-GPU: outgoing slot records (key = row << 32 | col,
   // 4 words: direct hi/lo, mirror hi/lo) grouped by destination rank, outgoing
@@ -2945,7 +2976,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   D.gbar = S.gbar.p;
   D.cert2 = S.cert2.p;
   D.bnd = S.bnd.p;
-  S.counters.ensure(8);
+  S.counters.ensure(9);
   D.flags = S.counters.p + 7;
   D.verts = S.verts.p;
   D.nbr = S.nbr.p;
@@ -3052,9 +3083,14 @@ void run_finalize(nlfem_gpu_session& S, int r0, int r1) {
 // allocates exactly.
 bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec) {
   const int KI = S.KI, J = S.J, U = S.unknowns;
-  const size_t rows_smem = (kHE + kHN + kRowMax) * sizeof(int);
+  const PatTabs tb = S.pattern_big ? kPatBig : kPatSmall;
+  const int kRowMax = tb.rowmax;
+  const size_t rows_smem = (size_t)(tb.he + tb.hn + tb.rowmax) * sizeof(int);
+  const size_t union_smem = (size_t)(kRowMax + 1) * sizeof(int);
   CK(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
   CK(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_union<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)union_smem));
+  CK(cudaFuncSetAttribute(k_union<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)union_smem));
   CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(kRowMax * sizeof(int))));
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
@@ -3063,7 +3099,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   const unsigned rgrid = (unsigned)std::min<long long>(J, (long long)S.sms * 16);
   const unsigned char* pm = S.plocal ? S.pmark.p : nullptr;
   k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
-                                               nullptr, S.ovf.p, S.plo, S.phi, pm);
+                                               nullptr, S.ovf.p, S.plo, S.phi, pm, tb);
   ++S.launches;
   scan64(S, S.rlen.p, true, J, S.roff.p, st);
   long long capR;
@@ -3076,7 +3112,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
     S.tcols.ensure(capR);
   }
   k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
-                                              S.rcols.p, S.ovf.p, S.plo, S.phi, pm);
+                                              S.rcols.p, S.ovf.p, S.plo, S.phi, pm, tb);
   // transpose
   S.tcnt.ensure(J);
   S.toff.ensure(J + 1);
@@ -3088,15 +3124,17 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
   k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p,
                                                         S.cursor.p, S.tcols.p, S.ovf.p);
-  k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p);
+  k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p,
+                                                          kRowMax);
   S.launches += 5;
   // union
   S.slen.ensure(J);
   S.soff.ensure(J + 1);
   CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
   int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
-  k_union<false><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
-                                                  S.slen.p, nullptr, nullptr, d_maxlen, S.ovf.p);
+  k_union<false><<<rgrid, kUnionThreads, union_smem, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+                                                  S.slen.p, nullptr, nullptr, d_maxlen, S.ovf.p,
+                                                  kRowMax);
   ++S.launches;
   scan64(S, S.slen.p, true, J, S.soff.p, st);
   long long capS;
@@ -3108,8 +3146,9 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
     S.scols.ensure(capS);
     S.mirror.ensure(capS);
   }
-  k_union<true><<<rgrid, kUnionThreads, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
-                                                 nullptr, S.soff.p, S.scols.p, nullptr, S.ovf.p);
+  k_union<true><<<rgrid, kUnionThreads, union_smem, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+                                                 nullptr, S.soff.p, S.scols.p, nullptr, S.ovf.p,
+                                                 kRowMax);
   k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
   S.eslot.ensure(10 * (size_t)KI);
   k_edge_slots<<<nblk(KI, 128), 128, 0, st>>>(S.soff.p, S.scols.p, S.eslot.p, S.ovf.p, S.plo,
@@ -3144,6 +3183,10 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   CK(cudaMemcpyAsync(&sz[2], S.ooff.p + U, sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (flags[0] == kCapRetry) return false;
+  if (flags[0] == 1 && !S.pattern_big) {  // a row or a node block outgrew the small tables
+    S.pattern_big = true;
+    return false;
+  }
   if (flags[0])
     throw Fail{NLFEM_GPU_BAD_CONFIG,
                "BadConfig: interaction neighbourhood too large for the pattern kernels (code " +
@@ -3161,7 +3204,8 @@ void run_pattern(nlfem_gpu_session& S, cudaStream_t st, int& maxlen) {
   const bool spec = S.rcols.n > 1 && S.tcols.n > 1 && S.scols.n > 1 && S.mirror.n > 1 &&
                     S.ocols.n > 1 && S.omap.n > 1;
   if (spec && pattern_pass(S, st, maxlen, true)) return;
-  pattern_pass(S, st, maxlen, false);
+  if (pattern_pass(S, st, maxlen, false)) return;
+  pattern_pass(S, st, maxlen, false);  // again with the large tables
 }
 
 // K1 over outer elements [lo, hi) (positions in the ascending interior list):
@@ -3219,11 +3263,11 @@ void build_pairs(nlfem_gpu_session& S, int lo, int hi) {
   S.pair_off.ensure(KI + 1);
   S.err_elem.ensure(1);
   S.ovf.ensure(1);
-  S.counters.ensure(8);
+  S.counters.ensure(9);
   const int big = 0x7fffffff;
   CK(cudaMemcpyAsync(S.err_elem.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(S.ovf.p, 0, sizeof(int), st));
-  CK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(S.counters.p, 0, 9 * sizeof(unsigned long long), st));
   // pass 0: survivors per outer element (cheap superset count)
   S.cand_count.ensure(KI + 1);
   S.cand_off.ensure(KI + 1);
@@ -3426,13 +3470,15 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
     wait_pattern();
     S.V.ensure(2 * (size_t)S.nnz_s);
     CK(cudaMemsetAsync(S.V.p, 0, 2 * S.nnz_s * sizeof(unsigned long long), st));
+    // the four rows of an outer element share most columns: their union is
+    // far below 4 maxlen (a table overflow is detected and fails the run)
     while (hcap <= 4 * std::max(maxlen, 1)) hcap <<= 1;
-    if (maxlen >= 32768)
+    const size_t kSlot = sizeof(int) + sizeof(short4);
+    while (hcap * kSlot > 220 * 1024 && hcap > 2 * std::max(maxlen, 1)) hcap >>= 1;
+    if (maxlen >= 32768 || hcap * kSlot > 220 * 1024 || hcap <= std::max(maxlen, 1))
       throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
     rowcap = std::max(maxlen, 1);
-    ismem = (size_t)hcap * (sizeof(int) + sizeof(short4));
-    if (ismem > 220 * 1024)
-      throw Fail{NLFEM_GPU_BAD_CONFIG, "BadConfig: pattern rows too long for the integration kernel"};
+    ismem = (size_t)hcap * kSlot;
     CK(cudaFuncSetAttribute(k_integrate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
     CK(cudaFuncSetAttribute(k_integrate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem));
   };
@@ -3620,7 +3666,7 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   CK(cudaEventRecord(S.ev[5], st));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
-  unsigned long long cnt[8];
+  unsigned long long cnt[9];
   CK(cudaMemcpy(cnt, S.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
   if (npairs_pending) {  // deferred from the pairs phase (no round trip there)
     long long tot = 0;
@@ -3638,6 +3684,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   S.ledger = cnt[3] + cnt[5];
   S.ledger_units = cnt[3];
   S.mc_subs = cnt[4];
+  if (cnt[8])
+    throw Fail{NLFEM_GPU_BAD_CONFIG,
+               "BadConfig: the rows of an outer element's nodes outgrew the integration "
+               "kernel's slot table (interaction neighbourhood too large)"};
   if (cnt[7])
     throw Fail{NLFEM_GPU_DEGENERATE_HULL,
                "DegenerateHull: approxcaps hull face table overflow (more than 32 faces)"};

@@ -4,14 +4,14 @@
 # owner-computes emulation.   scripts/r2_ab.sh TAG
 O=gpurun_out/${1:-ab}
 mkdir -p $O
-timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize_values.py \
-  tests/test_gpu_distributed.py -x -q -s -p no:cacheprovider > $O/tests.log 2>&1
+[ -z "$NOTEST" ] && timeout 1800 python -m pytest ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_fullsize_values.py tests/test_gpu_distributed.py} \
+  -x -q -s -p no:cacheprovider > $O/tests.log 2>&1
 echo "tests_rc=$?" >> $O/tests.log
 tail -2 $O/tests.log
 for L in ${LIBS:-default m0 m1 m2}; do
   for C in ${CONFIGS:-C1 P3f C2}; do
     if [ $L = default ]; then unset NLFEM_GPU_LIB; else export NLFEM_GPU_LIB=$PWD/paper_2302_07499_b200/libnlfem_gpu_$L.so; fi
-    timeout 900 python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu-baseline \
+    timeout 900 python bench.py --config $C --steps ${STEPS:-3} --warmup ${WARM:-3} --no-e2e --no-cpu-baseline \
       > $O/${L}_$C.json 2> $O/${L}_$C.err
     python -c "
 import json; d=json.load(open('$O/${L}_$C.json')); r=d['roofline']

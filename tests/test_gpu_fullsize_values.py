@@ -44,6 +44,11 @@ FULL = {
     "C3n": (48, 3 / 48, "nocaps", 1, 7, 2, 1024),
     "C3f": (48, 3 / 48, "fullcaps", 128, 7, 2, 512),
     "C4": (96, 3 / 96, "fullcaps", 128, None, 2, 512),
+    # delta/h = 7 (beyond the small pattern tables -- the node
+    # blocks' element sets overflow them and the pass reruns with the large
+    # ones; the combine's slot table sized down to fit): not a BASELINE config
+    "D7n": (8, 7 / 8, "nocaps", 1, None, 1, 64),
+    "D7f": (8, 7 / 8, "fullcaps", 8, None, 1, 32),
 }
 
 
