@@ -2858,7 +2858,13 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&S.stream2, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithFlags(&S.stream3, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&S.stream4, cudaStreamNonBlocking));
+#ifndef NLFEM_COMB_PRIO
+#define NLFEM_COMB_PRIO 0  // 1: the combine's stream at high priority
+#endif
+    if (NLFEM_COMB_PRIO)
+      CK(cudaStreamCreateWithPriority(&S.stream4, cudaStreamNonBlocking, hi));
+    else
+      CK(cudaStreamCreateWithFlags(&S.stream4, cudaStreamNonBlocking));
     for (int i = 0; i < 24; ++i) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -3635,7 +3641,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
       // block size from delta/h (pairs per outer element grow like (delta/h)^3):
       // a property of the mesh, the same for every shard and chunk -- the
       // per-warp partial sums, hence the last bits, must not depend on sharding
-      if (S.delta_over_h < 2.5)
+#ifndef NLFEM_COMB_THREADS
+#define NLFEM_COMB_THREADS 0  // 0: by delta/h; 128 / 256: forced
+#endif
+      if (NLFEM_COMB_THREADS == 128 || (NLFEM_COMB_THREADS == 0 && S.delta_over_h < 2.5))
         k_integrate<128><<<ii1 - ii0, 128, ismem, s4>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
             S.rhsT.p, U.uoff.p, need_units ? U.mom.p : nullptr, P0, S.counters.p + 1, hcap,
