@@ -77,6 +77,24 @@ typedef struct {
   const double* inv_edges;  /* [elem_count*9]  ElementTable::inv_edges       */
 } nlfem_gpu_mesh;
 
+/* ElementTable of a TWO-dimensional mesh (reference ball_approx.hpp:38-58 with
+ * n == 2: P1 triangles, ball_approx.cpp:51-80): node coordinates keep the
+ * reference's Vec layout (x, y, 0); three vertices / neighbours per element;
+ * inv_edges holds the four 2x2 entries the reference fills for n == 2. */
+typedef struct {
+  int32_t node_count;
+  int32_t elem_count;
+  const double* node_xyz;   /* [node_count*3]  (z = 0)                         */
+  const int32_t* verts;     /* [elem_count*3]                                  */
+  const int32_t* neighbor;  /* [elem_count*3]  -1 = unglued facet              */
+  const double* center;     /* [elem_count*3]                                  */
+  const double* radius;     /* [elem_count]                                    */
+  const double* volume;     /* [elem_count]    triangle area                   */
+  const double* diam;       /* [elem_count]                                    */
+  const uint8_t* region;    /* [elem_count]                                    */
+  const double* inv_edges;  /* [elem_count*4]                                  */
+} nlfem_gpu_mesh2d;
+
 /* DofMap (reference assembly.hpp:19-26): dof_of_node[v] = -1 when constrained. */
 typedef struct {
   int32_t node_count;
@@ -274,6 +292,18 @@ int nlfem_gpu_session_finalize_merged(nlfem_gpu_session* s, void* stream, int32_
                                       char* err, size_t errlen);
 int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,
                                     nlfem_gpu_csr* out, char* err, size_t errlen);
+/* The reference's 2D path: nlfem::assemble with et.n == 2 (P1 triangles, disk
+ * kernel; assembly.cpp:617-843) for the inside, overlap, barycenter, nocaps and
+ * fullcaps strategies (approxcaps returns BadConfig).  Same contract, errors
+ * and outputs as nlfem_gpu_assemble; fullcaps draws from the two-dimensional
+ * Philox stream of include/nlfem_mc_stream.h.  The entries are reduced by a
+ * stable key sort and in-order sums (deterministic, no atomics on values). */
+int nlfem_gpu_assemble_2d(const nlfem_gpu_mesh2d* mesh, const nlfem_gpu_dofs* dofs,
+                          const nlfem_gpu_kernel* kernel, const nlfem_gpu_poly* f,
+                          const nlfem_gpu_poly* g, const nlfem_gpu_config* cfg,
+                          nlfem_gpu_csr* out, nlfem_gpu_stats* stats, char* err,
+                          size_t errlen);
+
 /* Device pointers of the output CSR of the last run (row offsets are int64,
  * columns int32, values and rhs double), for device-side collectives. */
 int nlfem_gpu_session_outputs(nlfem_gpu_session* s, void** row_off, void** col_idx,

@@ -177,4 +177,28 @@ NLFEM_HD int nlfem_mc_sample(const uint32_t W[8], int i, const nlfem_mc_quad* Q,
   return nlfem_mc_q(Q, d[0], d[1], d[2]) < dd;
 }
 
+/* ---- the two-dimensional stream (triangles, the reference's n == 2 path) ----
+ * Sample k (0 <= k < M) of Monte Carlo sub-triangle `sub` of item (T, q, T'):
+ * W = Philox4x32-10 of the counter (T, T', q | sub << 2, k >> 1), key as above;
+ * its two uniforms are u_t = (W[2c + t] + 1/2) 2^-32, c = k & 1, t = 0, 1;
+ * sorted u0 <= u1 (reference sample_simplex, quadrature.cpp:98-102) the point
+ * is y = u0 V0 + (u1 - u0) V1 + (1 - u1) V2, summed left to right. */
+NLFEM_HD void nlfem_mc2_block(uint32_t k0, uint32_t k1, uint32_t T, uint32_t Tp, uint32_t q,
+                              uint32_t sub, uint32_t j, uint32_t W[4]) {
+  const uint32_t ctr[4] = {T, Tp, q | (sub << 2), j};
+  nlfem_philox4x32_10(ctr, k0, k1, W);
+}
+
+NLFEM_HD void nlfem_mc2_sample(const uint32_t W[4], int c, const double v0[3],
+                               const double v1[3], const double v2[3], double y[3]) {
+  double u0 = ((double)W[2 * c] + 0.5) * 0x1p-32, u1 = ((double)W[2 * c + 1] + 0.5) * 0x1p-32;
+  if (u0 > u1) {
+    const double t = u0;
+    u0 = u1;
+    u1 = t;
+  }
+  const double l0 = u0, l1 = u1 - u0, l2 = 1.0 - u1;
+  for (int a = 0; a < 3; ++a) y[a] = (l0 * v0[a] + l1 * v1[a]) + l2 * v2[a];
+}
+
 #endif /* NLFEM_MC_STREAM_H */

@@ -34,6 +34,12 @@ def lib():
         P = C.POINTER
         L.ref_mesh_generate.restype = vp
         L.ref_mesh_generate.argtypes = [C.c_int, dbl]
+        L.ref_mesh_generate_n.restype = vp
+        L.ref_mesh_generate_n.argtypes = [C.c_int, C.c_int, dbl]
+        L.ref_mesh_dim.restype = C.c_int
+        L.ref_mesh_dim.argtypes = [vp]
+        L.ref_forcing_n.restype = C.c_int
+        L.ref_forcing_n.argtypes = [C.c_int, dbl, C.c_int, vp, C.c_int, P(dbl), vp, C.c_int]
         L.ref_mesh_generate_jittered.restype = vp
         L.ref_mesh_generate_jittered.argtypes = [C.c_int, dbl, i64]
         L.ref_mesh_from_arrays.restype = vp
@@ -86,14 +92,20 @@ def generate_mesh(res: int, delta: float, jitter_seed: int | None = None):
 
 
 class Problem:
-    """Reference ElementTable + DofMap built from mesh arrays."""
+    """Reference ElementTable + DofMap built from mesh arrays (3D), or from the
+    reference's own generate_mesh in dimension n (Problem.generated)."""
 
-    def __init__(self, coords, cells, region):
+    def __init__(self, coords, cells, region, _mesh_handle=None):
         L = lib()
-        coords = np.ascontiguousarray(coords, np.float64)
-        cells = np.ascontiguousarray(cells, np.int32)
-        region = np.ascontiguousarray(region, np.uint8)
-        mh = L.ref_mesh_from_arrays(_p(coords), len(coords), _p(cells), _p(region), len(cells))
+        if _mesh_handle is None:
+            coords = np.ascontiguousarray(coords, np.float64)
+            cells = np.ascontiguousarray(cells, np.int32)
+            region = np.ascontiguousarray(region, np.uint8)
+            mh = L.ref_mesh_from_arrays(_p(coords), len(coords), _p(cells), _p(region),
+                                        len(cells))
+        else:
+            mh = _mesh_handle
+        self.n = L.ref_mesh_dim(mh)
         err = C.create_string_buffer(512)
         self.h = L.ref_problem_build(mh, err, 512)
         L.ref_mesh_free(mh)
@@ -102,6 +114,22 @@ class Problem:
         n, k, u = C.c_int64(), C.c_int64(), C.c_int64()
         L.ref_problem_sizes(self.h, C.byref(n), C.byref(k), C.byref(u))
         self.nodes, self.elems, self.unknowns = n.value, k.value, u.value
+
+    @classmethod
+    def generated(cls, n: int, res: int, delta: float):
+        """The reference's generate_mesh(n, res, delta) -> cmap -> element table
+        -> dof map (n = 2: the triangle path); also keeps the mesh arrays."""
+        L = lib()
+        mh = L.ref_mesh_generate_n(n, res, delta)
+        nn, nc = C.c_int64(), C.c_int64()
+        L.ref_mesh_sizes(mh, C.byref(nn), C.byref(nc))
+        coords = np.empty((nn.value, 3), np.float64)
+        cells = np.empty((nc.value, 4), np.int32)
+        region = np.empty(nc.value, np.uint8)
+        L.ref_mesh_copy(mh, _p(coords), _p(cells), _p(region))
+        self = cls(None, None, None, _mesh_handle=mh)
+        self.coords, self.cells, self.region = coords, cells[:, :n + 1].copy(), region
+        return self
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -163,10 +191,10 @@ class Problem:
         return dict(l2=l2.value, max_nodal=mx.value, iterations=it.value, converged=rc == 0)
 
 
-def forcing(delta, uterms, moment2=True):
+def forcing(delta, uterms, moment2=True, dim=3):
     """Reference make_kernel + make_problem_from -> (C, f terms)."""
     ut = np.ascontiguousarray(uterms, np.float64)
     Cc = C.c_double()
     f = np.empty((64, 4))
-    n = lib().ref_forcing(delta, int(moment2), _p(ut), len(ut), C.byref(Cc), _p(f), 64)
+    n = lib().ref_forcing_n(dim, delta, int(moment2), _p(ut), len(ut), C.byref(Cc), _p(f), 64)
     return Cc.value, f[:n].copy()

@@ -66,6 +66,7 @@ Polynomial poly_of(const double* terms, int nterms) {
 struct Problem {
   ElementTable et;
   DofMap dofs;
+  int n = 3;
 };
 
 struct Result {
@@ -86,6 +87,17 @@ void* ref_mesh_generate(int res, double delta) {
     return nullptr;
   }
 }
+
+// generate_mesh in dimension n (2: triangles, the reference's 2D path)
+void* ref_mesh_generate_n(int n, int res, double delta) {
+  try {
+    return new MeshData(generate_mesh(n, res, delta));
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int ref_mesh_dim(void* h) { return static_cast<MeshData*>(h)->n; }
 
 // Config-3 jitter (builder-defined): the reference's own
 // nlfem::Rng (core.hpp:108-133) seeded with `seed`; for every node in id
@@ -157,6 +169,7 @@ void* ref_problem_build(void* mesh, char* err, int errlen) {
     auto* p = new Problem;
     p->et = build_element_table(build_cmap(md->n, md->coords, md->cells, md->region));
     p->dofs = build_dofmap(p->et);
+    p->n = md->n;
     return p;
   } catch (const std::exception& e) {
     set_err(err, errlen, e.what());
@@ -207,10 +220,10 @@ void ref_problem_free(void* h) { delete static_cast<Problem*>(h); }
 // ---- kernel constant and manufactured forcing --------------------------------
 
 // Writes C and the forcing polynomial f = -L u (at most maxterms terms).
-int ref_forcing(double delta, int moment2, const double* uterms, int nu, double* C,
-                double* fterms, int maxterms) {
-  const Kernel k = make_kernel(3, delta, moment2 ? Normalization::SecondMoment
-                                                 : Normalization::Mass);
+int ref_forcing_n(int dim, double delta, int moment2, const double* uterms, int nu, double* C,
+                  double* fterms, int maxterms) {
+  const Kernel k = make_kernel(dim, delta, moment2 ? Normalization::SecondMoment
+                                                   : Normalization::Mass);
   const ManufacturedProblem mp = make_problem_from(poly_of(uterms, nu), k);
   *C = k.C;
   int n = 0;
@@ -223,6 +236,11 @@ int ref_forcing(double delta, int moment2, const double* uterms, int nu, double*
   return n;
 }
 
+int ref_forcing(double delta, int moment2, const double* uterms, int nu, double* C,
+                double* fterms, int maxterms) {
+  return ref_forcing_n(3, delta, moment2, uterms, nu, C, fterms, maxterms);
+}
+
 // ---- the hot path: unmodified nlfem::assemble ---------------------------------
 
 void* ref_assemble(void* problem, double delta, int strategy, int moment2,
@@ -230,8 +248,8 @@ void* ref_assemble(void* problem, double delta, int strategy, int moment2,
                    int mc_samples, char* err, int errlen) {
   try {
     auto* p = static_cast<Problem*>(problem);
-    const Kernel k = make_kernel(3, delta, moment2 ? Normalization::SecondMoment
-                                                   : Normalization::Mass);
+    const Kernel k = make_kernel(p->n, delta, moment2 ? Normalization::SecondMoment
+                                                      : Normalization::Mass);
     const ManufacturedProblem mp = make_problem_from(poly_of(uterms, nu), k);
     const Polynomial f = mp.f, u = mp.u;
     AssemblyConfig cfg;
@@ -288,9 +306,9 @@ int ref_walk_pieces(void* problem, std::int32_t t, int k, double delta, int stra
                     std::int32_t* parent, std::int32_t* kind, int maxout) {
   auto* p = static_cast<Problem*>(problem);
   const ElementTable& et = p->et;
-  const QuadratureRule& rule = gauss_rule(3, 2);
+  const QuadratureRule& rule = gauss_rule(et.n, 2);
   Vec x = rule.bary[k][0] * et.simplex[t].v[0];
-  for (int i = 1; i <= 3; ++i) x = x + rule.bary[k][i] * et.simplex[t].v[i];
+  for (int i = 1; i <= et.n; ++i) x = x + rule.bary[k][i] * et.simplex[t].v[i];
   struct Rec {
     std::int32_t* parent;
     std::int32_t* kind;

@@ -55,6 +55,13 @@ class _Mesh(C.Structure):
                 ("diam", C.c_void_p), ("region", C.c_void_p), ("inv_edges", C.c_void_p)]
 
 
+class _Mesh2D(C.Structure):
+    _fields_ = [("node_count", C.c_int32), ("elem_count", C.c_int32),
+                ("node_xyz", C.c_void_p), ("verts", C.c_void_p), ("neighbor", C.c_void_p),
+                ("center", C.c_void_p), ("radius", C.c_void_p), ("volume", C.c_void_p),
+                ("diam", C.c_void_p), ("region", C.c_void_p), ("inv_edges", C.c_void_p)]
+
+
 class _Dofs(C.Structure):
     _fields_ = [("node_count", C.c_int32), ("unknowns", C.c_int32),
                 ("dof_of_node", C.c_void_p)]
@@ -126,6 +133,9 @@ def lib():
     L.nlfem_gpu_assemble.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
                                      P(_Config), P(_Csr), P(Stats), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_free_csr.argtypes = [P(_Csr)]
+    L.nlfem_gpu_assemble_2d.restype = C.c_int
+    L.nlfem_gpu_assemble_2d.argtypes = [P(_Mesh2D), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
+                                        P(_Config), P(_Csr), P(Stats), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_session_create.restype = C.c_int
     L.nlfem_gpu_session_create.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
                                            P(_Config), P(vp), C.c_char_p, C.c_size_t]
@@ -201,6 +211,7 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
+    "nlfem_gpu_assemble_2d",
     "nlfem_gpu_session_run", "nlfem_gpu_session_reset", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
     "nlfem_gpu_session_pairs_device",
@@ -786,6 +797,72 @@ def assemble(table: ElementTable, delta: float, strategy: str = "nocaps",
     rc = L.nlfem_gpu_assemble(C.byref(m), C.byref(d), C.byref(_Kernel(Cn, float(delta))),
                               C.byref(fp), C.byref(gp), C.byref(cfg), C.byref(csr), C.byref(st),
                               err, 1024)
+    _check(rc, err)
+    return _take_csr(csr), st.as_dict()
+
+
+class ElementTable2D:
+    """The reference's ElementTable of a two-dimensional mesh (n == 2, P1
+    triangles; ball_approx.hpp:38-58, built by the reference's own
+    build_element_table upstream -- ball_approx.cpp:33-98) plus its DofMap, as
+    the flat arrays nlfem_gpu_assemble_2d borrows: node_xyz [J, 3] (z = 0),
+    verts / neighbor [K, 3], center [K, 3], radius / volume / diam [K], region
+    [K], inv_edges [K, 4], dof_of_node [J]."""
+
+    def __init__(self, node_xyz, verts, neighbor, center, radius, volume, diam, region,
+                 inv_edges, dof_of_node):
+        f64 = lambda a, shp: np.ascontiguousarray(np.asarray(a, np.float64).reshape(shp))
+        i32 = lambda a, shp: np.ascontiguousarray(np.asarray(a, np.int32).reshape(shp))
+        self.node_xyz = f64(node_xyz, (-1, 3))
+        K = len(np.asarray(radius))
+        self.verts = i32(np.asarray(verts)[:, :3], (K, 3))
+        self.neighbor = i32(np.asarray(neighbor)[:, :3], (K, 3))
+        self.center = f64(center, (K, 3))
+        self.radius = f64(radius, (K,))
+        self.volume = f64(volume, (K,))
+        self.diam = f64(diam, (K,))
+        self.region = np.ascontiguousarray(np.asarray(region, np.uint8).reshape(K))
+        self.inv_edges = f64(np.asarray(inv_edges)[:, :4], (K, 4))
+        self.dof_of_node = i32(dof_of_node, (-1,))
+        self.unknowns = int((self.dof_of_node >= 0).sum())
+
+    @property
+    def elem_count(self) -> int:
+        return len(self.radius)
+
+    @property
+    def node_count(self) -> int:
+        return len(self.node_xyz)
+
+    def _structs(self):
+        m = _Mesh2D(self.node_count, self.elem_count, *[_p(a) for a in (
+            self.node_xyz, self.verts, self.neighbor, self.center, self.radius, self.volume,
+            self.diam, self.region, self.inv_edges)])
+        d = _Dofs(self.node_count, self.unknowns, _p(self.dof_of_node))
+        return m, d
+
+
+def assemble_2d(table: ElementTable2D, delta: float, strategy: str, C_kernel: float,
+                f_terms, g_terms, seed: int = 0x5EED, mc_samples: int = 200,
+                device: int = -1) -> tuple[dict, dict]:
+    """The reference's 2D path on the GPU (nlfem_gpu_assemble_2d): nlfem::assemble
+    with et.n == 2 for kernel constant C_kernel, forcing f and constraint data g
+    (polynomial rows c, e0, e1, e2).  Returns the host CSR and the statistics."""
+    if strategy not in STRATEGIES:
+        raise NlfemError(8, f"BadConfig: unknown strategy '{strategy}'")
+    f = np.asarray(f_terms, np.float64).reshape(-1, 4)
+    g = np.asarray(g_terms, np.float64).reshape(-1, 4)
+    m, d = table._structs()
+    fp, fk = _poly_struct(f)
+    gp, gk = _poly_struct(g)
+    cfg = _Config(STRATEGIES.index(strategy), int(mc_samples), int(seed) & (2**64 - 1), 0,
+                  int(device))
+    csr, st = _Csr(), Stats()
+    err = C.create_string_buffer(1024)
+    rc = lib().nlfem_gpu_assemble_2d(C.byref(m), C.byref(d),
+                                     C.byref(_Kernel(float(C_kernel), float(delta))),
+                                     C.byref(fp), C.byref(gp), C.byref(cfg), C.byref(csr),
+                                     C.byref(st), err, 1024)
     _check(rc, err)
     return _take_csr(csr), st.as_dict()
 

@@ -19,7 +19,7 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libnlfem_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["nlfem_gpu.cu", "nlfem_cg.cu", "nlfem_setup.cu"]
+CU_SOURCES = ["nlfem_gpu.cu", "nlfem_cg.cu", "nlfem_setup.cu", "nlfem_gpu2d.cu"]
 CPP_SOURCES = ["host_setup.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
