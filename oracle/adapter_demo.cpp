@@ -20,12 +20,13 @@ int main(int argc, char** argv) {
   const int res = argc > 1 ? std::atoi(argv[1]) : 6;
   const double delta = argc > 2 ? std::atof(argv[2]) : 0.34;
   const std::string strat = argc > 3 ? argv[3] : "nocaps";
-  const MeshData md = generate_mesh(3, res, delta);
-  const ElementTable et = build_element_table(build_cmap(3, md.coords, md.cells, md.region));
+  const int dim = argc > 4 ? std::atoi(argv[4]) : 3;
+  const MeshData md = generate_mesh(dim, res, delta);
+  const ElementTable et = build_element_table(build_cmap(dim, md.coords, md.cells, md.region));
   const DofMap dofs = build_dofmap(et);
-  const Kernel k = make_kernel(3, delta, Normalization::SecondMoment);
-  Polynomial u = Polynomial::monomial({2, 0, 0}, 1.0) + Polynomial::monomial({0, 2, 0}, 1.0) +
-                 Polynomial::monomial({0, 0, 2}, 1.0);
+  const Kernel k = make_kernel(dim, delta, Normalization::SecondMoment);
+  Polynomial u = Polynomial::monomial({2, 0, 0}, 1.0) + Polynomial::monomial({0, 2, 0}, 1.0);
+  if (dim == 3) u = u + Polynomial::monomial({0, 0, 2}, 1.0);
   const ManufacturedProblem mp = make_problem_from(u, k);
   AssemblyConfig cfg;
   cfg.strategy = parse_strategy(strat);
