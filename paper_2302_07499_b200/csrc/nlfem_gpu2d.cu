@@ -125,6 +125,7 @@ struct Dev2 {
   const double* gnode;   // [J] g at constrained nodes
   double gox, goy, ginv, rmax;
   int gx, gy;
+  int kshift;             // entry keys: row << kshift | col, col = U for the rhs
   const int* cell_start;  // [gx*gy + 1]
   const int* cell_elems;  // [K]
   Poly2 f, g;
@@ -171,42 +172,55 @@ __device__ double dist_point_tri(Vd p, const Vd v[3]) {
 
 enum : unsigned { k2None = 0, k2Whole = 1, k2OutCap = 2, k2Straddle = 16 };
 
-// crossing_points (geometry.cpp:39-50) of a straddling triangle: inside slots
-// ascending, outside slots ascending, crossing k = i (3 - m) + o
-__device__ __forceinline__ int crossings2(const Vd v[3], unsigned mask, Vd xq, int ins[3],
-                                          int outs[3], Vd X[2]) {
-  int m = 0, mo = 0;
-  for (int i = 0; i < 3; ++i) {
-    if (mask >> i & 1u) ins[m++] = i;
-    else outs[mo++] = i;
+__device__ __forceinline__ Vd pick3(const Vd v[3], int i) {
+  return i == 0 ? v[0] : (i == 1 ? v[1] : v[2]);
+}
+
+// A straddling triangle in the reference's slot order (crossing_points,
+// geometry.cpp:39-50: inside slots ascending, outside slots ascending,
+// crossing k = i (3 - m) + o): m = 1 -> I0 | O0 O1, X0 = (I0,O0), X1 = (I0,O1);
+// m = 2 -> I0 I1 | O0, X0 = (I0,O0), X1 = (I1,O0).  Vertices are picked by
+// selects, so nothing is indexed at run time (all in registers).
+struct Strad2 {
+  int m;
+  Vd I0, I1, O0, O1, X0, X1;
+};
+__device__ __forceinline__ Strad2 straddle2(const Vd v[3], unsigned mask, Vd xq) {
+  Strad2 S;
+  const unsigned om = ~mask & 7u;
+  S.m = __popc(mask);
+  const int i0 = __ffs(mask) - 1, o0 = __ffs(om) - 1, last = 3 - i0 - o0;
+  S.I0 = pick3(v, i0);
+  S.O0 = pick3(v, o0);
+  if (S.m == 1) {
+    S.O1 = pick3(v, last);
+    S.I1 = S.I0;
+  } else {
+    S.I1 = pick3(v, last);
+    S.O1 = S.O0;
   }
-  int nx = 0;
-  for (int i = 0; i < m; ++i)
-    for (int o = 0; o < mo; ++o) {
-      const Vd a = v[ins[i]], b = v[outs[o]];
-      const double t = edge_crossing(a, b, xq, c2.delta);
-      X[nx++] = vadd(a, vscale(t, vsub(b, a)));
-    }
-  return m;
+  const Vd a1 = S.m == 1 ? S.I0 : S.I1, b1 = S.m == 1 ? S.O1 : S.O0;
+  const double t0 = edge_crossing(S.I0, S.O0, xq, c2.delta);
+  S.X0 = vadd(S.I0, vscale(t0, vsub(S.O0, S.I0)));
+  const double t1 = edge_crossing(a1, b1, xq, c2.delta);
+  S.X1 = vadd(a1, vscale(t1, vsub(b1, a1)));
+  return S;
 }
 
 // does the straddler emit a piece (push_piece's volume floor, ball_approx.cpp:
 // 141; straddle_inner / straddle_outer n == 2, 232-240 / 273-281)?  An item
 // without pieces never reaches the sink: no flush, no pattern keys.
 __device__ bool straddle_kept2(const Vd v[3], unsigned mask, Vd xq, double tau, bool outer) {
-  int ins[3], outs[3];
-  Vd X[2];
-  const int m = crossings2(v, mask, xq, ins, outs, X);
-  if (m == 1) {
-    if (tri_area(v[ins[0]], X[0], X[1]) > tau) return true;
+  const Strad2 S = straddle2(v, mask, xq);
+  if (S.m == 1) {
+    if (tri_area(S.I0, S.X0, S.X1) > tau) return true;
   } else {
-    if (tri_area(v[ins[0]], v[ins[1]], X[1]) > tau) return true;
-    if (tri_area(v[ins[0]], X[1], X[0]) > tau) return true;
+    if (tri_area(S.I0, S.I1, S.X1) > tau) return true;
+    if (tri_area(S.I0, S.X1, S.X0) > tau) return true;
   }
   if (!outer) return false;
-  if (m == 1)
-    return tri_area(v[outs[0]], v[outs[1]], X[1]) > tau || tri_area(v[outs[0]], X[1], X[0]) > tau;
-  return tri_area(v[outs[0]], X[0], X[1]) > tau;
+  if (S.m == 1) return tri_area(S.O0, S.O1, S.X1) > tau || tri_area(S.O0, S.X1, S.X0) > tau;
+  return tri_area(S.O0, S.X0, S.X1) > tau;
 }
 
 // The reference's per-(T, q, T') decision (assembly.cpp:722-760), n == 2.
@@ -374,13 +388,13 @@ __device__ __forceinline__ void acc_point2(Acc2& A, int t, bool cons, Vd y, doub
 }
 
 // sub (assembly.cpp:372-381): the degree-2 rule on a sub-triangle
-__device__ void sub2(Acc2& A, int t, bool cons, const Vd s[3], Vd v0) {
+__device__ __forceinline__ void sub2(Acc2& A, int t, bool cons, const Vd s[3], Vd v0) {
   const double vol = tri_area(s[0], s[1], s[2]);
   for (int k = 0; k < 3; ++k) acc_point2(A, t, cons, qpoint2(s, k), vol * kW2, v0);
 }
 
 // cap (assembly.cpp:383-399) with the 2D Philox stream (include/nlfem_mc_stream.h)
-__device__ void cap2(Acc2& A, int t, bool cons, const Vd s[3], Vd v0, Vd xq, uint32_t T,
+__device__ __forceinline__ void cap2(Acc2& A, int t, bool cons, const Vd s[3], Vd v0, Vd xq, uint32_t T,
                      uint32_t q, uint32_t sub, unsigned long long& draws,
                      unsigned long long& hits) {
   const int M = c2.mc;
@@ -402,6 +416,16 @@ __device__ void cap2(Acc2& A, int t, bool cons, const Vd s[3], Vd v0, Vd xq, uin
 
 constexpr int kEnt = 21;  // entries per pair: the upper triangle of <= 6 union nodes
 
+// Entry keys, the reference's (row, col) order in as few bits as the system
+// needs (the radix sort only sorts those): row << kshift | col with col = U
+// standing for the reference's rhs column 0xFFFFFFFF; the sentinel of an
+// unused slot, row = U, sorts after every real key.
+__device__ __forceinline__ unsigned long long kmat(unsigned r, unsigned c) {
+  return ((unsigned long long)r << c2.kshift) | c;
+}
+__device__ __forceinline__ unsigned long long krhs(unsigned r) { return kmat(r, (unsigned)c2.U); }
+__device__ __forceinline__ unsigned long long ksent() { return kmat((unsigned)c2.U, (unsigned)c2.U); }
+
 __device__ __forceinline__ void put2(unsigned long long* keys, double* vals, long long base,
                                      int& ne, unsigned long long key, double v) {
   keys[base + ne] = key;
@@ -415,12 +439,12 @@ __device__ __forceinline__ void add_pair2(unsigned long long* keys, double* vals
                                           double v) {
   if (dof_a >= 0 && dof_b >= 0) {
     const unsigned long long lo = (unsigned)min(dof_a, dof_b), hi = (unsigned)max(dof_a, dof_b);
-    put2(keys, vals, base, ne, (lo << 32) | hi, v);
+    put2(keys, vals, base, ne, kmat((unsigned)lo, (unsigned)hi), v);
   } else if (dof_a >= 0) {
-    put2(keys, vals, base, ne, ((unsigned long long)(unsigned)dof_a << 32) | 0xffffffffull,
+    put2(keys, vals, base, ne, krhs((unsigned)dof_a),
          -v * c2.gnode[node_b]);
   } else if (dof_b >= 0) {
-    put2(keys, vals, base, ne, ((unsigned long long)(unsigned)dof_b << 32) | 0xffffffffull,
+    put2(keys, vals, base, ne, krhs((unsigned)dof_b),
          -v * c2.gnode[node_a]);
   }
 }
@@ -455,33 +479,35 @@ __global__ void k2_integrate(long long npairs, const long long* off, const int* 
       dT[a] = c2.dof[nT[a]];
       nP[a] = c2.verts[3 * (long long)Tp + a];
     }
-    // union U = nodes(T) then the partner's unshared nodes (flush's order)
+    // union U (flush, assembly.cpp:430-450) in fixed slots: 0-2 the outer
+    // element's nodes, 3-5 the partner's nodes, active when not shared (the
+    // order of a pair's entries does not matter: each key occurs once per pair)
     int un[6], ud[6], ms[6];
-    int cnt = 0;
+    bool act[6];
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       int m = -1;
-      for (int j = 0; j < 3; ++j)
-        if (nP[j] == nT[a]) {
-          m = j;
-          break;
-        }
-      un[cnt] = nT[a];
-      ud[cnt] = dT[a];
-      ms[cnt] = m;
-      ++cnt;
+#pragma unroll
+      for (int j = 2; j >= 0; --j) m = nP[j] == nT[a] ? j : m;
+      un[a] = nT[a];
+      ud[a] = dT[a];
+      ms[a] = m;
+      act[a] = true;
     }
+#pragma unroll
     for (int j = 0; j < 3; ++j) {
       bool shared = false;
+#pragma unroll
       for (int a = 0; a < 3; ++a) shared |= nT[a] == nP[j];
-      if (!shared) {
-        un[cnt] = nP[j];
-        ud[cnt] = c2.dof[nP[j]];
-        ms[cnt] = j;
-        ++cnt;
-      }
+      un[3 + j] = nP[j];
+      ud[3 + j] = c2.dof[nP[j]];
+      ms[3 + j] = j;
+      act[3 + j] = !shared;
     }
     double V[6][6];
+#pragma unroll
     for (int x = 0; x < 6; ++x)
+#pragma unroll
       for (int y = 0; y < 6; ++y) V[x][y] = 0;
     double rhsT[3] = {0, 0, 0};
     const double tauP = c2.tau[Tp];
@@ -512,46 +538,29 @@ __global__ void k2_integrate(long long npairs, const long long* off, const int* 
         // the whole element as one Monte Carlo region (assembly.cpp:754-759)
         cap2(A, Tp, cons, vP, vP[0], xq, (uint32_t)T, (uint32_t)q, 0u, draws, hits);
       } else {
-        const unsigned mask = c & 7u;
-        int ins[3], outs[3];
-        Vd X[2];
-        const int m = crossings2(vP, mask, xq, ins, outs, X);
+        const Strad2 Sd = straddle2(vP, c & 7u, xq);
         // straddle_inner, n == 2 (ball_approx.cpp:232-240)
-        if (m == 1) {
-          const Vd s[3] = {vP[ins[0]], X[0], X[1]};
+        if (Sd.m == 1) {
+          const Vd s[3] = {Sd.I0, Sd.X0, Sd.X1};
           if (tri_area(s[0], s[1], s[2]) > tauP) sub2(A, Tp, cons, s, vP[0]);
         } else {
-          const Vd s1[3] = {vP[ins[0]], vP[ins[1]], X[1]};
+          const Vd s1[3] = {Sd.I0, Sd.I1, Sd.X1};
           if (tri_area(s1[0], s1[1], s1[2]) > tauP) sub2(A, Tp, cons, s1, vP[0]);
-          const Vd s2[3] = {vP[ins[0]], X[1], X[0]};
+          const Vd s2[3] = {Sd.I0, Sd.X1, Sd.X0};
           if (tri_area(s2[0], s2[1], s2[2]) > tauP) sub2(A, Tp, cons, s2, vP[0]);
         }
         if (c2.strategy == NLFEM_STRATEGY_FULLCAPS) {
-          // straddle_outer, n == 2 (ball_approx.cpp:273-281), then one cap over
-          // the kept pieces
-          Vd pc[2][3];
-          int np = 0;
-          if (m == 1) {
-            const Vd s1[3] = {vP[outs[0]], vP[outs[1]], X[1]};
-            const Vd s2[3] = {vP[outs[0]], X[1], X[0]};
-            if (tri_area(s1[0], s1[1], s1[2]) > tauP) {
-              for (int i = 0; i < 3; ++i) pc[np][i] = s1[i];
-              ++np;
-            }
-            if (tri_area(s2[0], s2[1], s2[2]) > tauP) {
-              for (int i = 0; i < 3; ++i) pc[np][i] = s2[i];
-              ++np;
-            }
-          } else {
-            const Vd s1[3] = {vP[outs[0]], X[0], X[1]};
-            if (tri_area(s1[0], s1[1], s1[2]) > tauP) {
-              for (int i = 0; i < 3; ++i) pc[np][i] = s1[i];
-              ++np;
-            }
+          // straddle_outer, n == 2 (ball_approx.cpp:273-281): the kept pieces
+          // in order, each a Monte Carlo region (sub index = kept order)
+          uint32_t kept = 0;
+          const Vd s1[3] = {Sd.O0, Sd.m == 1 ? Sd.O1 : Sd.X0, Sd.X1};
+          if (tri_area(s1[0], s1[1], s1[2]) > tauP)
+            cap2(A, Tp, cons, s1, vP[0], xq, (uint32_t)T, (uint32_t)q, kept++, draws, hits);
+          if (Sd.m == 1) {
+            const Vd s2[3] = {Sd.O0, Sd.X1, Sd.X0};
+            if (tri_area(s2[0], s2[1], s2[2]) > tauP)
+              cap2(A, Tp, cons, s2, vP[0], xq, (uint32_t)T, (uint32_t)q, kept++, draws, hits);
           }
-          for (int k = 0; k < np; ++k)
-            cap2(A, Tp, cons, pc[k], vP[0], xq, (uint32_t)T, (uint32_t)q, (uint32_t)k, draws,
-                 hits);
         }
       }
       // flush (assembly.cpp:413-473) into the per-pair sums
@@ -563,15 +572,28 @@ __global__ void k2_integrate(long long npairs, const long long* off, const int* 
           for (int b = a; b < 3; ++b) V[a][b] += base * A.S0 * rb2(q, a) * rb2(q, b);
         }
       } else {
+        // the moments by union slot through selects (static indices: the
+        // accumulators stay in registers)
+        double s1u[6];
+#pragma unroll
+        for (int x = 0; x < 6; ++x) {
+          s1u[x] = 0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) s1u[x] = ms[x] == i ? A.S1[i] : s1u[x];
+        }
         const double scale = C * wN;
-        for (int x = 0; x < cnt; ++x) {
+#pragma unroll
+        for (int x = 0; x < 6; ++x) {
           const double cx = x < 3 ? rb2(q, x) : 0.0;
-          const double s1x = ms[x] >= 0 ? A.S1[ms[x]] : 0.0;
-          for (int y = x; y < cnt; ++y) {
+#pragma unroll
+          for (int y = x; y < 6; ++y) {
             const double cy = y < 3 ? rb2(q, y) : 0.0;
-            const double s1y = ms[y] >= 0 ? A.S1[ms[y]] : 0.0;
-            const double s2 = (ms[x] >= 0 && ms[y] >= 0) ? A.S2[ms[x]][ms[y]] : 0.0;
-            V[x][y] += scale * (s2 - cx * s1y - cy * s1x + cx * cy * A.S0);
+            double s2 = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+              for (int j = 0; j < 3; ++j) s2 = (ms[x] == i && ms[y] == j) ? A.S2[i][j] : s2;
+            V[x][y] += scale * (s2 - cx * s1u[y] - cy * s1u[x] + cx * cy * A.S0);
           }
         }
       }
@@ -582,16 +604,19 @@ __global__ void k2_integrate(long long npairs, const long long* off, const int* 
     if (cons) {
       for (int a = 0; a < 3; ++a) {
         if (dT[a] >= 0)
-          put2(keys, vals, base, ne, ((unsigned long long)(unsigned)dT[a] << 32) | 0xffffffffull,
+          put2(keys, vals, base, ne, krhs((unsigned)dT[a]),
                rhsT[a]);
         for (int b = a; b < 3; ++b) add_pair2(keys, vals, base, ne, dT[a], nT[a], dT[b], nT[b], V[a][b]);
       }
     } else {
-      for (int x = 0; x < cnt; ++x)
-        for (int y = x; y < cnt; ++y) add_pair2(keys, vals, base, ne, ud[x], un[x], ud[y], un[y], V[x][y]);
+#pragma unroll
+      for (int x = 0; x < 6; ++x)
+#pragma unroll
+        for (int y = x; y < 6; ++y)
+          if (act[x] && act[y]) add_pair2(keys, vals, base, ne, ud[x], un[x], ud[y], un[y], V[x][y]);
     }
     for (; ne < kEnt; ++ne) {
-      keys[base + ne] = ~0ull;
+      keys[base + ne] = ksent();
       vals[base + ne] = 0;
     }
   }
@@ -626,7 +651,7 @@ __global__ void k2_fterm(long long base0, unsigned long long* keys, double* vals
   for (int a = 0; a < 3; ++a) {
     const int d = c2.dof[c2.verts[3 * (long long)T + a]];
     const long long o = base0 + 3LL * ii + a;
-    keys[o] = d >= 0 ? (((unsigned long long)(unsigned)d << 32) | 0xffffffffull) : ~0ull;
+    keys[o] = d >= 0 ? krhs((unsigned)d) : ksent();
     vals[o] = r[a];
   }
 }
@@ -635,7 +660,7 @@ __global__ void k2_fterm(long long base0, unsigned long long* keys, double* vals
 
 __global__ void k2_flag(long long n, const unsigned long long* k, int* flag) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) flag[i] = (k[i] != ~0ull && (i == 0 || k[i] != k[i - 1])) ? 1 : 0;
+  if (i < n) flag[i] = (k[i] != ksent() && (i == 0 || k[i] != k[i - 1])) ? 1 : 0;
 }
 
 // thread per distinct key: its entries summed in sorted (stable) order
@@ -657,22 +682,23 @@ __global__ void k2_mirror(long long nu, const unsigned long long* uk, const doub
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nu) return;
   const unsigned long long key = uk[i];
-  const unsigned r = (unsigned)(key >> 32), c = (unsigned)(key & 0xffffffffu);
-  if (c == 0xffffffffu) {
+  const unsigned r = (unsigned)(key >> c2.kshift),
+                 c = (unsigned)(key & ((1ull << c2.kshift) - 1));
+  if (c == (unsigned)c2.U) {
     rhs[r] = uv[i];
     fflag[2 * i] = fflag[2 * i + 1] = 0;
-    fk[2 * i] = fk[2 * i + 1] = ~0ull;
+    fk[2 * i] = fk[2 * i + 1] = ksent();
     return;
   }
   fk[2 * i] = key;
   fv[2 * i] = uv[i];
   fflag[2 * i] = 1;
   if (r != c) {
-    fk[2 * i + 1] = ((unsigned long long)c << 32) | r;
+    fk[2 * i + 1] = kmat(c, r);
     fv[2 * i + 1] = uv[i];
     fflag[2 * i + 1] = 1;
   } else {
-    fk[2 * i + 1] = ~0ull;
+    fk[2 * i + 1] = ksent();
     fflag[2 * i + 1] = 0;
   }
 }
@@ -682,9 +708,9 @@ __global__ void k2_csr(long long n, const unsigned long long* fk, const double* 
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const unsigned long long key = fk[i];
-  col[i] = (int)(key & 0xffffffffu);
+  col[i] = (int)(key & ((1ull << c2.kshift) - 1));
   val[i] = fv[i];
-  atomicAdd(rowcnt + (int)(key >> 32), 1);
+  atomicAdd(rowcnt + (int)(key >> c2.kshift), 1);
 }
 
 unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -766,9 +792,10 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
     cudaStream_t s;
     ~StreamGuard() { cudaStreamDestroy(s); }
   } sg{st};
-  cudaEvent_t e0, e1;
+  cudaEvent_t e0, e1, ep[3];
   CK2(cudaEventCreate(&e0));
   CK2(cudaEventCreate(&e1));
+  for (auto& e : ep) CK2(cudaEventCreate(&e));
 
   const int K = m->elem_count, J = m->node_count;
   Dev2 D{};
@@ -793,6 +820,10 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
     if (!m->region[t]) interior.push_back(t);
   D.KI = (int)interior.size();
   D.U = dofs->unknowns;
+  int kbits = 1;
+  while ((1LL << kbits) <= (long long)D.U) ++kbits;  // col in [0, U]
+  D.kshift = kbits;
+  const int key_bits = 2 * kbits;                      // row in [0, U] too
   std::vector<double> gnode(J, 0.0), tau(K);
   for (int v = 0; v < J; ++v)
     if (dofs->dof_of_node[v] < 0) gnode[v] = poly2_host(D.g, m->node_xyz + 3 * (size_t)v);
@@ -887,6 +918,7 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   partner.ensure(npairs + 1);
   code.ensure(npairs + 1);
   if (KI > 0) k2_pairs<1><<<KI, kP2Threads, 0, st>>>(poff.p, nullptr, partner.p, code.p, err.p);
+  CK2(cudaEventRecord(ep[0], st));
   // integration: keyed entries
   const long long nent = npairs * kEnt + 3LL * KI;
   Buf<unsigned long long> keys, skeys, ukeys;
@@ -900,16 +932,17 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
     k2_integrate<<<nb(npairs, 128), 128, 0, st>>>(npairs, poff.p, partner.p, code.p, keys.p,
                                                    vals.p, cnt.p);
   if (KI > 0) k2_fterm<<<nb(KI, 128), 128, 0, st>>>(npairs * kEnt, keys.p, vals.p);
+  CK2(cudaEventRecord(ep[1], st));
   // deterministic segmented reduction: stable radix sort, in-order sums
   skeys.ensure(nent + 1);
   svals.ensure(nent + 1);
   if (nent > 0) {
     size_t bytes = 0;
     CK2(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, skeys.p, vals.p, svals.p, nent, 0,
-                                        64, st));
+                                        key_bits, st));
     tmp.ensure(bytes);
     CK2(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, skeys.p, vals.p, svals.p, nent, 0,
-                                        64, st));
+                                        key_bits, st));
   }
   Buf<int> flag;
   Buf<long long> uid;
@@ -923,6 +956,7 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   if (nent > 0)
     k2_segsum<<<nb(nent, 256), 256, 0, st>>>(nent, skeys.p, svals.p, flag.p, uid.p, ukeys.p,
                                              uvals.p);
+  CK2(cudaEventRecord(ep[2], st));
   // CSR: mirror the upper triangle, sort by (row, col), count rows
   const int U = D.U;
   Buf<double> rhs, fv, fv2;
@@ -938,9 +972,11 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   fv2.ensure(2 * nu + 1);
   if (nu > 0) {
     size_t bytes = 0;
-    CK2(cub::DeviceRadixSort::SortPairs(nullptr, bytes, fk.p, fk2.p, fv.p, fv2.p, 2 * nu, 0, 64, st));
+    CK2(cub::DeviceRadixSort::SortPairs(nullptr, bytes, fk.p, fk2.p, fv.p, fv2.p, 2 * nu, 0,
+                                        key_bits, st));
     tmp.ensure(bytes);
-    CK2(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, fk.p, fk2.p, fv.p, fv2.p, 2 * nu, 0, 64, st));
+    CK2(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, fk.p, fk2.p, fv.p, fv2.p, 2 * nu, 0,
+                                        key_bits, st));
   }
   Buf<long long> nnzc;
   nnzc.ensure(2 * nu + 2);
@@ -983,6 +1019,12 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
     float ms = 0;
     CK2(cudaEventElapsedTime(&ms, e0, e1));
     stats->device_ms = ms;
+    // phases: grid + pairs, integration (entries), sort + segmented sums, CSR
+    cudaEvent_t seq[5] = {e0, ep[0], ep[1], ep[2], e1};
+    for (int i = 0; i < 4; ++i) {
+      CK2(cudaEventElapsedTime(&ms, seq[i], seq[i + 1]));
+      stats->phase_ms[i] = ms;
+    }
     stats->threads = 1;
     stats->blocks = (KI + 31) / 32;
     stats->mc_samples = c[0];
@@ -995,6 +1037,7 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  for (auto& e : ep) cudaEventDestroy(e);
 }
 
 }  // namespace

@@ -31,7 +31,7 @@ for res in [int(a) for a in sys.argv[1:]] or [128, 256]:
         pairs = st["element_pairs"]
         print(json.dumps({"res": res, "strategy": strat, "mc": mc, "elements": t.elem_count,
                           "element_pairs": pairs, "nnz": int(len(out["values"])),
-                          "gpu_device_ms": st["device_ms"], "gpu_e2e_ms": 1e3 * min(ts),
+                          "gpu_device_ms": st["device_ms"], "gpu_phase_ms": [round(x, 2) for x in st["phase_ms"][:4]], "mc_samples": st["mc_samples"], "gpu_e2e_ms": 1e3 * min(ts),
                           "gpu_pairs_per_s_e2e": pairs / min(ts),
                           "ref_s": r["seconds"], "ref_threads": r["threads"],
                           "ref_pairs_per_s": pairs / r["seconds"],
