@@ -3635,7 +3635,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
       // the combine of this chunk on stream4, after its units (and the
       // accumulator set-up) on `stream`; the next chunk's units proceed on
       // `stream` meanwhile
-      cudaStream_t s4 = S.stream4;
+#ifndef NLFEM_COMB_SERIAL
+#define NLFEM_COMB_SERIAL 0  // 1: the combine on `stream`, after its chunk's units
+#endif
+      cudaStream_t s4 = NLFEM_COMB_SERIAL ? st : S.stream4;
       CK(cudaEventRecord(evu(set, 2), st));
       CK(cudaStreamWaitEvent(s4, evu(set, 2), 0));
       // block size from delta/h (pairs per outer element grow like (delta/h)^3):

@@ -10,4 +10,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=fals
   -Xcompiler -fPIC -Xcompiler -ffp-contract=off -I include -I $D/csrc "$@" \
   -c $D/csrc/nlfem_gpu.cu -o $B/nlfem_gpu_$T.o
 nvcc -shared -gencode arch=compute_100a,code=sm_100a -o $D/libnlfem_gpu_$T.so $B/nlfem_gpu_$T.o \
-  $B/nlfem_cg.cu.o $B/nlfem_setup.cu.o $B/host_setup.cpp.o -lcudart_static -lrt -ldl -lpthread
+  $(ls $B/*.o | grep -v -e "/nlfem_gpu.cu.o" -e "/nlfem_gpu_") -lcudart_static -lrt -ldl -lpthread
