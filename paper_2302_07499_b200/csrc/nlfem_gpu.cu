@@ -1324,12 +1324,16 @@ __global__ void k_units_count(long long p0, long long np, const long long* pend,
 // per field), one warp scan, then a block prefix and one global atomic per
 // list and block.
 constexpr int kFillThreads = 256;
+// Each list entry is the item's whole descriptor -- (record slot u, outer
+// element T, inner element T', q | class code << 8) -- so the units kernels
+// reach the element records after one dependent load instead of five
+// (list -> pair -> outer position -> interior id / partner / class).
 __global__ void __launch_bounds__(kFillThreads) k_units_fill(long long p0, long long np,
                                                              const long long* pend,
                                                              const unsigned* info,
-                                                             const long long* uoff, int* upair,
-                                                             unsigned char* uqs,
-                                                             const int* partner, int* lists,
+                                                             const long long* uoff,
+                                                             const int* pair_outer,
+                                                             const int* partner, int4* lists,
                                                              long long lstride, int* nlist) {
   constexpr int W = kFillThreads / 32;
   __shared__ unsigned long long wtot[W];
@@ -1367,6 +1371,8 @@ __global__ void __launch_bounds__(kFillThreads) k_units_fill(long long p0, long 
   if (!act) return;
   unsigned long long excl = incl - packed;  // bumped per item: same-list items are consecutive
   long long u = uoff[i];
+  const int T = cD.interior[pair_outer[i]];
+  const int Tp = partner[p0 + i];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const unsigned c = (code >> (5 * q)) & 31;
@@ -1374,9 +1380,7 @@ __global__ void __launch_bounds__(kFillThreads) k_units_fill(long long p0, long 
     const int k = kind0 + cap_case(c);
     const int slot = bbase[k][wl] + (int)((excl >> (8 * k)) & 0xff);
     excl += 1ull << (8 * k);
-    lists[k * lstride + slot] = (int)u;
-    upair[u] = (int)i;
-    uqs[u] = (unsigned char)q;
+    lists[k * lstride + slot] = make_int4((int)u, T, Tp, (int)(q | (c << 8)));
     ++u;
   }
 }
@@ -1712,11 +1716,8 @@ __device__ __forceinline__ void inner_piece(Vd a, Vd b, Vd c, Vd d, double vol, 
 // OUTER = false (nocaps): the inner pieces only, no Monte Carlo.
 template <bool CONS, bool G2, int CASE, bool OUTER = true>
 __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long p0, long long nitems,
-                                                      const int* list, const int* nlistp,
-                                                      const int* upair, const unsigned char* uqs,
-                                                      const int* pair_outer, const int* partner,
-                                                      const unsigned* info, double* mom,
-                                                      unsigned long long* mc_stats) {
+                                                      const int4* list, const int* nlistp,
+                                                      double* mom, unsigned long long* mc_stats) {
   constexpr int NOUT = !OUTER ? 0 : ((CASE == 1 || CASE == 2) ? 3 : 1);  // outer pieces
   constexpr int NV = CONS ? 2 : 10;                       // record doubles
   // per-thread item state parked in shared memory while the sample loop runs
@@ -1741,13 +1742,11 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
     if (base >= nlist) break;
     const int li = base + lane;
     if (li >= nlist) continue;
-    const long long u = list[li];
-    const int pi = upair[u];
-    const int q = uqs[u];
-    const long long p = p0 + pi;
-    const int T = cD.interior[pair_outer[pi]];
-    const int Tp = partner[p];
-    const unsigned c = (info[p] >> (5 * q)) & 31;
+    const int4 dsc = list[li];  // (record slot, T, T', q | code << 8)
+    const long long u = dsc.x;
+    const int T = dsc.y, Tp = dsc.z;
+    const int q = dsc.w & 255;
+    const unsigned c = (unsigned)dsc.w >> 8;
     Vd vT[4];
     load_verts(T, vT);
     const Vd xq = quad_point(vT, q);
@@ -2027,22 +2026,17 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
 // ball_approx.cpp:210-229, assembly.cpp:372-381).
 template <bool CONS>
 __global__ void __launch_bounds__(kMcThreads) k_approx(long long p0, long long nitems,
-                                                       const int* list, const int* nlistp,
-                                                       const int* upair, const unsigned char* uqs,
-                                                       const int* pair_outer, const int* partner,
-                                                       const unsigned* info, double* mom,
-                                                       unsigned long long* mc_stats) {
+                                                       const int4* list, const int* nlistp,
+                                                       double* mom, unsigned long long* mc_stats) {
   constexpr int NV = CONS ? 2 : 10;
   unsigned long long led = 0;
   const int nlist = nlistp[0];
   for (int li = blockIdx.x * blockDim.x + threadIdx.x; li < nlist; li += gridDim.x * blockDim.x) {
-    const long long u = list[li];
-    const int pi = upair[u];
-    const int q = uqs[u];
-    const long long p = p0 + pi;
-    const int T = cD.interior[pair_outer[pi]];
-    const int Tp = partner[p];
-    const int mask = (int)((info[p] >> (5 * q)) & 15u);
+    const int4 dsc = list[li];  // (record slot, T, T', q | code << 8)
+    const long long u = dsc.x;
+    const int T = dsc.y, Tp = dsc.z;
+    const int q = dsc.w & 255;
+    const int mask = (int)(((unsigned)dsc.w >> 8) & 15u);
     Vd vT[4], w[4];
     load_verts(T, vT);
     const Vd xq = quad_point(vT, q);
@@ -2684,9 +2678,9 @@ struct nlfem_gpu_session {
   // two sets, alternating by chunk: the combine of chunk c (on stream4) reads
   // set c & 1 while the units of chunk c + 1 fill the other
   struct UnitBufs {
-    DBuf<int> ucount, pair_outer, upair, ulist, nlist;
+    DBuf<int> ucount, pair_outer, nlist;
+    DBuf<int4> ulist;  // item descriptors, 8 lists
     DBuf<long long> uoff;
-    DBuf<unsigned char> uqs;
     DBuf<double> mom;
   } ub[2];
   float mc_ms = 0;
@@ -3573,12 +3567,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         scan64(S, U.ucount.p, true, np, U.uoff.p, st);
         // buffers by the upper bound (4 items per pair): no count read-back
         nitems = 4 * np;
-        U.upair.ensure(nitems + 1);
-        U.uqs.ensure(nitems + 1);
         U.mom.ensure(kMomStride * (size_t)(nitems + 1));
         U.ulist.ensure(8 * (size_t)(nitems + 1));
         k_units_fill<<<nblk(np, kFillThreads), kFillThreads, 0, st>>>(
-            P0, np, pend, S.info.p, U.uoff.p, U.upair.p, U.uqs.p, S.partner.p, U.ulist.p,
+            P0, np, pend, S.info.p, U.uoff.p, U.pair_outer.p, S.partner.p, U.ulist.p,
             nitems + 1, U.nlist.p);
         ++S.launches;
         CK(cudaEventRecord(evu(set, 0), st));
@@ -3592,9 +3584,8 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
           nl[k] = (int)std::min<long long>(nitems, (long long)S.sms * NLFEM_MC_MINBLOCKS * 2 * kMcThreads);
         auto launch = [&](auto kern, int kind, cudaStream_t s) {
           if (nl[kind] <= 0) return;
-          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(P0, nitems, U.ulist.p + kind * ls, U.nlist.p + kind,
-                                             U.upair.p, U.uqs.p, U.pair_outer.p, S.partner.p,
-                                             S.info.p, U.mom.p, S.counters.p + 1);
+          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(
+              P0, nitems, U.ulist.p + kind * ls, U.nlist.p + kind, U.mom.p, S.counters.p + 1);
           ++S.launches;
         };
         // lists 0..3: interior parents by cap case, 4..7: constraint parents;
