@@ -977,7 +977,14 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
   if (FILL && *ovf) return;
   for (int i = blockIdx.x; i < cD.J; i += gridDim.x) {
     const int a = cD.ni_off[i], b = cD.ni_off[i + 1];
-    if (a == b) {
+    // a node none of whose incident elements has pairs here or is a partner
+    // (a rank's local pattern: most nodes) has an empty row: skip the tables
+    bool any = false;
+    for (int k = a; k < b && !any; ++k) {
+      const int T = cD.ni_el[k], lo = cD.ipos[T];
+      any = (lo >= plo && lo < phi) || (pmark && pmark[T]);
+    }
+    if (!any) {
       if (!FILL && threadIdx.x == 0) rlen[i] = 0;
       continue;
     }

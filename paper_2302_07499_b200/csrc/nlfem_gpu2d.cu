@@ -37,6 +37,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -776,6 +778,15 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Fail2{NLFEM_GPU_ENODEVICE, "no CUDA device"};
+  // one 2D call per device at a time: the parameter block c2 is per device
+  static std::mutex locks_mu;
+  static std::map<int, std::mutex> locks;
+  std::mutex* dmu;
+  {
+    std::lock_guard<std::mutex> g(locks_mu);
+    dmu = &locks[dev];
+  }
+  std::lock_guard<std::mutex> dev_lock(*dmu);
   int prev = 0;
   CK2(cudaGetDevice(&prev));
   CK2(cudaSetDevice(dev));
@@ -796,6 +807,14 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   CK2(cudaEventCreate(&e0));
   CK2(cudaEventCreate(&e1));
   for (auto& e : ep) CK2(cudaEventCreate(&e));
+  struct EventGuard {  // released on every exit path (exceptions included)
+    cudaEvent_t* e;
+    ~EventGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t evs[5] = {e0, e1, ep[0], ep[1], ep[2]};
+  EventGuard eguard{evs};
 
   const int K = m->elem_count, J = m->node_count;
   Dev2 D{};
@@ -1035,9 +1054,6 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
     stats->nnz_ext = nnz;
     stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  for (auto& e : ep) cudaEventDestroy(e);
 }
 
 }  // namespace
