@@ -293,8 +293,8 @@ int nlfem_gpu_session_finalize_merged(nlfem_gpu_session* s, void* stream, int32_
 int nlfem_gpu_session_download_rows(nlfem_gpu_session* s, int32_t row_lo, int32_t row_hi,
                                     nlfem_gpu_csr* out, char* err, size_t errlen);
 /* The reference's 2D path: nlfem::assemble with et.n == 2 (P1 triangles, disk
- * kernel; assembly.cpp:617-843) for the inside, overlap, barycenter, nocaps and
- * fullcaps strategies (approxcaps returns BadConfig).  Same contract, errors
+ * kernel; assembly.cpp:617-843) for all six strategies (approxcaps: the
+ * reference's 2D sphere-point hull).  Same contract, errors
  * and outputs as nlfem_gpu_assemble; fullcaps draws from the two-dimensional
  * Philox stream of include/nlfem_mc_stream.h.  The entries are reduced by a
  * stable key sort and in-order sums (deterministic, no atomics on values). */

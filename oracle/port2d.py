@@ -125,6 +125,48 @@ def edge_crossing(a, b, c, r):
     return min(max(t, 0.0), 1.0)
 
 
+def hull2d_pieces(pts, tau):
+    """straddle_inner(sphere_points) for n == 2 (ball_approx.cpp:210-229):
+    the reference's monotone-chain hull2d (geometry.cpp:161-196) and fan
+    triangulation from the centroid of the hull vertices summed in index order
+    (triangulate_polytope, geometry.cpp:307-329); pieces above tau."""
+    idx = sorted(range(len(pts)), key=lambda i: (pts[i][0], pts[i][1]))
+    uniq = []
+    for i in idx:
+        if uniq and pts[uniq[-1]][0] == pts[i][0] and pts[uniq[-1]][1] == pts[i][1]:
+            continue
+        uniq.append(i)
+
+    def cr(o, a, b):
+        return ((pts[a][0] - pts[o][0]) * (pts[b][1] - pts[o][1]) -
+                (pts[a][1] - pts[o][1]) * (pts[b][0] - pts[o][0]))
+    ring = []
+    for i in uniq:
+        while len(ring) >= 2 and cr(ring[-2], ring[-1], i) <= 0:
+            ring.pop()
+        ring.append(i)
+    t = len(ring) + 1
+    for i in reversed(uniq[:-1]):
+        while len(ring) >= t and cr(ring[-2], ring[-1], i) <= 0:
+            ring.pop()
+        ring.append(i)
+    if len(ring) < 4:
+        return []  # DegenerateHull: caught by hull_pieces, no pieces
+    ring = ring[:-1]
+    facets = [(ring[i], ring[(i + 1) % len(ring)]) for i in range(len(ring))]
+    vs = sorted(set(v for f in facets for v in f))
+    c = (0.0, 0.0, 0.0)
+    for v in vs:
+        c = add(c, pts[v])
+    c = scale(1.0 / float(len(vs)), c)
+    out = []
+    for f in facets:
+        s = (c, pts[f[0]], pts[f[1]])
+        if area(*s) > tau:
+            out.append(s)
+    return out
+
+
 def poly_eval(terms, x):
     acc = 0.0
     for c, e0, e1, e2 in terms:
@@ -270,13 +312,29 @@ def assemble(t2, delta, strategy, C, f_terms, g_terms, seed=1234, mc_samples=16)
                                 for o in outs:
                                     tt = edge_crossing(vP[i], vP[o], xq, delta)
                                     X.append(add(vP[i], scale(tt, sub(vP[o], vP[i]))))
-                            if len(ins) == 1:
-                                inner = [(vP[ins[0]], X[0], X[1])]
-                            else:
-                                inner = [(vP[ins[0]], vP[ins[1]], X[1]), (vP[ins[0]], X[1], X[0])]
-                            for s in inner:
-                                if area(*s) > tau[tp]:
+                            if S == "approxcaps":
+                                pts = [vP[i] for i in ins] + X
+                                cr_i = [(i, o) for i in ins for o in outs]
+                                for a in range(len(X)):
+                                    for b in range(a + 1, len(X)):
+                                        if cr_i[a][0] != cr_i[b][0] and cr_i[a][1] != cr_i[b][1]:
+                                            continue
+                                        mid = sub(scale(0.5, add(X[a], X[b])), xq)
+                                        ln = math.sqrt(dot(mid, mid))
+                                        if ln <= 0:
+                                            continue
+                                        pts.append(add(xq, scale(delta / ln, mid)))
+                                for s in hull2d_pieces(pts, tau[tp]):
                                     subp(s)
+                            else:
+                                if len(ins) == 1:
+                                    inner = [(vP[ins[0]], X[0], X[1])]
+                                else:
+                                    inner = [(vP[ins[0]], vP[ins[1]], X[1]),
+                                             (vP[ins[0]], X[1], X[0])]
+                                for s in inner:
+                                    if area(*s) > tau[tp]:
+                                        subp(s)
                             if S == "fullcaps":
                                 if len(ins) == 1:
                                     outer = [(vP[outs[0]], vP[outs[1]], X[1]),

@@ -209,6 +209,79 @@ __device__ __forceinline__ Strad2 straddle2(const Vd v[3], unsigned mask, Vd xq)
   return S;
 }
 
+// approxcaps, n == 2 (straddle_inner with sphere points, ball_approx.cpp:
+// 210-229): the inside vertices, the two crossings and the sphere point of the
+// crossing pair (it shares an inside or an outside vertex), then the
+// reference's monotone-chain hull (hull2d, geometry.cpp:161-196: points sorted
+// by (x, y), duplicates dropped, lower and upper chains with cross <= 0
+// popped) and the fan from the centroid of the hull vertices summed in index
+// order (triangulate_polytope, geometry.cpp:307-329).  Calls fn(a, b, c) for
+// every fan piece above tau; returns the number of them (a degenerate hull
+// has none: hull_pieces swallows DegenerateHull).
+template <class Fn>
+__device__ int approx_pieces2(const Strad2& S, Vd xq, double tau, Fn fn) {
+  Vd P[5];
+  int n = 0;
+  P[n++] = S.I0;
+  if (S.m == 2) P[n++] = S.I1;
+  P[n++] = S.X0;
+  P[n++] = S.X1;
+  {
+    const Vd mid = vsub(vscale(0.5, vadd(S.X0, S.X1)), xq);
+    const double len = sqrt(vnorm2(mid));
+    if (len > 0) P[n++] = vadd(xq, vscale(c2.delta / len, mid));
+  }
+  int idx[5];
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  for (int i = 1; i < n; ++i) {  // insertion sort by (x, y), stable
+    const int v = idx[i];
+    int j = i - 1;
+    while (j >= 0 && (P[idx[j]].x > P[v].x || (P[idx[j]].x == P[v].x && P[idx[j]].y > P[v].y))) {
+      idx[j + 1] = idx[j];
+      --j;
+    }
+    idx[j + 1] = v;
+  }
+  int u = 0;
+  for (int i = 0; i < n; ++i)
+    if (u == 0 || !(P[idx[u - 1]].x == P[idx[i]].x && P[idx[u - 1]].y == P[idx[i]].y))
+      idx[u++] = idx[i];
+  auto cr = [&](int o, int a, int b) {
+    return (P[a].x - P[o].x) * (P[b].y - P[o].y) - (P[a].y - P[o].y) * (P[b].x - P[o].x);
+  };
+  int ring[10], k = 0;
+  for (int i = 0; i < u; ++i) {
+    while (k >= 2 && cr(ring[k - 2], ring[k - 1], idx[i]) <= 0) --k;
+    ring[k++] = idx[i];
+  }
+  for (int i = u - 1, t = k + 1; i-- > 0;) {
+    while (k >= t && cr(ring[k - 2], ring[k - 1], idx[i]) <= 0) --k;
+    ring[k++] = idx[i];
+  }
+  if (k < 4) return 0;
+  const int nr = k - 1;
+  // centroid of the hull vertices, summed in ascending point index
+  unsigned used = 0;
+  for (int i = 0; i < nr; ++i) used |= 1u << ring[i];
+  Vd c = {0, 0, 0};
+  int nv = 0;
+  for (int i = 0; i < n; ++i)
+    if (used >> i & 1u) {
+      c = vadd(c, P[i]);
+      ++nv;
+    }
+  c = vscale(1.0 / double(nv), c);
+  int kept = 0;
+  for (int i = 0; i < nr; ++i) {
+    const Vd a = P[ring[i]], b = P[ring[(i + 1) % nr]];
+    if (tri_area(c, a, b) > tau) {
+      fn(c, a, b);
+      ++kept;
+    }
+  }
+  return kept;
+}
+
 // does the straddler emit a piece (push_piece's volume floor, ball_approx.cpp:
 // 141; straddle_inner / straddle_outer n == 2, 232-240 / 273-281)?  An item
 // without pieces never reaches the sink: no flush, no pattern keys.
@@ -248,6 +321,11 @@ __device__ unsigned decide2(Vd xq, int t) {
   if (mask == 7u) return k2Whole;
   if (mask != 0) {
     if (S == NLFEM_STRATEGY_INSIDE) return k2None;
+    if (S == NLFEM_STRATEGY_APPROXCAPS) {
+      const Strad2 Sd = straddle2(v, mask, xq);
+      return approx_pieces2(Sd, xq, c2.tau[t], [](Vd, Vd, Vd) {}) > 0 ? (k2Straddle | mask)
+                                                                       : k2None;
+    }
     return straddle_kept2(v, mask, xq, c2.tau[t], S == NLFEM_STRATEGY_FULLCAPS)
                ? (k2Straddle | mask)
                : k2None;
@@ -541,8 +619,12 @@ __global__ void k2_integrate(long long npairs, const long long* off, const int* 
         cap2(A, Tp, cons, vP, vP[0], xq, (uint32_t)T, (uint32_t)q, 0u, draws, hits);
       } else {
         const Strad2 Sd = straddle2(vP, c & 7u, xq);
-        // straddle_inner, n == 2 (ball_approx.cpp:232-240)
-        if (Sd.m == 1) {
+        if (c2.strategy == NLFEM_STRATEGY_APPROXCAPS) {
+          approx_pieces2(Sd, xq, tauP, [&](Vd a, Vd b, Vd cc) {
+            const Vd s[3] = {a, b, cc};
+            sub2(A, Tp, cons, s, vP[0]);
+          });
+        } else if (Sd.m == 1) {  // straddle_inner, n == 2 (ball_approx.cpp:232-240)
           const Vd s[3] = {Sd.I0, Sd.X0, Sd.X1};
           if (tri_area(s[0], s[1], s[2]) > tauP) sub2(A, Tp, cons, s, vP[0]);
         } else {
@@ -769,8 +851,6 @@ void assemble2d(const nlfem_gpu_mesh2d* m, const nlfem_gpu_dofs* dofs,
   const auto wall0 = std::chrono::steady_clock::now();
   if (!(k->delta > 0)) throw Fail2{NLFEM_GPU_BAD_CONFIG, "BadConfig: delta must be positive"};
   if (cfg->mc_samples <= 0) throw Fail2{NLFEM_GPU_BAD_CONFIG, "BadConfig: mc_samples must be positive"};
-  if (cfg->strategy == NLFEM_STRATEGY_APPROXCAPS)
-    throw Fail2{NLFEM_GPU_BAD_CONFIG, "BadConfig: approxcaps is not built for the 2D path"};
   if (cfg->strategy < 0 || cfg->strategy > NLFEM_STRATEGY_FULLCAPS)
     throw Fail2{NLFEM_GPU_BAD_CONFIG, "BadConfig: unknown strategy"};
   int dev = cfg->device;

@@ -18,7 +18,7 @@ pytestmark = [pytest.mark.gpu,
 SEED = 1234
 
 
-@pytest.mark.parametrize("strat", ["barycenter", "nocaps", "inside", "overlap"])
+@pytest.mark.parametrize("strat", ["barycenter", "nocaps", "inside", "overlap", "approxcaps"])
 @pytest.mark.parametrize("res,delta", [(4, 0.5), (8, 0.25), (16, 3 / 16)])
 def test_2d_matches_reference(strat, res, delta):
     R, t, Cc, f, g = problem2d(res, delta)
@@ -65,7 +65,7 @@ def test_2d_deterministic_and_bad_config():
     for k in ("row_ptr", "col_idx", "values", "rhs"):
         assert np.array_equal(a[k], b[k]), k
     with pytest.raises(P.NlfemError) as e:
-        P.assemble_2d(t, 0.25, "approxcaps", Cc, f, g, device=0)
+        P.assemble_2d(t, 0.25, "fullcaps", Cc, f, g, mc_samples=0, device=0)
     assert e.value.code == 8
     # a ball wider than the interaction layer reaches past the mesh boundary
     with pytest.raises(P.NlfemError) as e:

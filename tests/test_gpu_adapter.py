@@ -29,7 +29,8 @@ def test_adapter_drop_in_matches_reference(strat):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(DEMO), reason="oracle/_ref/adapter_demo not built")
-@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "fullcaps"])
+@pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "approxcaps",
+                                   "fullcaps"])
 def test_adapter_drop_in_2d_matches_reference(strat):
     # a 2D ElementTable (et.n == 2) through the same nlfem::gpu::assemble call
     out = subprocess.run([DEMO, "16", str(3 / 16), strat, "2"], capture_output=True, text=True,

@@ -49,7 +49,7 @@ def test_philox_known_answers_python():
                                 0x299f31d0) == (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1)
 
 
-@pytest.mark.parametrize("strat", ["barycenter", "nocaps", "inside", "overlap"])
+@pytest.mark.parametrize("strat", ["barycenter", "nocaps", "inside", "overlap", "approxcaps"])
 @pytest.mark.parametrize("res,delta", [(4, 0.5), (6, 0.34)])
 def test_port2d_equals_reference(strat, res, delta):
     R, t, Cc, f, g = problem2d(res, delta)
