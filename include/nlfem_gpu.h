@@ -352,6 +352,12 @@ void nlfem_gpu_session_destroy(nlfem_gpu_session* s);
  * (MEASURED_PEAKS.json has no FP64 figure). */
 int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen);
 
+/* Checked builds (-DNLFEM_CHECKED=1) surround every device buffer with
+ * canaries verified at the end of each run (an out-of-bounds write fails the
+ * call).  This self-test writes one element past (past = 1) or at the end of
+ * (past = 0) a fresh buffer: 1 = caught, 0 = not, -1 = default build, -2 = CUDA error. */
+int nlfem_gpu_debug_guard_selftest(int32_t past);
+
 /* Build / version string (e.g. "nlfem_gpu sm_100a ..."). */
 const char* nlfem_gpu_version(void);
 

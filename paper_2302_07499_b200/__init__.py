@@ -133,6 +133,8 @@ def lib():
     L.nlfem_gpu_assemble.argtypes = [P(_Mesh), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
                                      P(_Config), P(_Csr), P(Stats), C.c_char_p, C.c_size_t]
     L.nlfem_gpu_free_csr.argtypes = [P(_Csr)]
+    L.nlfem_gpu_debug_guard_selftest.restype = C.c_int
+    L.nlfem_gpu_debug_guard_selftest.argtypes = [i32]
     L.nlfem_gpu_assemble_2d.restype = C.c_int
     L.nlfem_gpu_assemble_2d.argtypes = [P(_Mesh2D), P(_Dofs), P(_Kernel), P(_Poly), P(_Poly),
                                         P(_Config), P(_Csr), P(Stats), C.c_char_p, C.c_size_t]
@@ -211,7 +213,7 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "nlfem_gpu_assemble", "nlfem_gpu_free_csr", "nlfem_gpu_session_create",
-    "nlfem_gpu_assemble_2d",
+    "nlfem_gpu_assemble_2d", "nlfem_gpu_debug_guard_selftest",
     "nlfem_gpu_session_run", "nlfem_gpu_session_reset", "nlfem_gpu_session_download", "nlfem_gpu_session_pairs",
     "nlfem_gpu_session_launches", "nlfem_gpu_session_destroy", "nlfem_gpu_version",
     "nlfem_gpu_session_pairs_device",

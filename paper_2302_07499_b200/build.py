@@ -73,5 +73,31 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out=None) 
     return lib
 
 
+CHECKED_LIB = os.path.join(HERE, "libnlfem_gpu_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """libnlfem_gpu_checked.so: the main translation unit with -DNLFEM_CHECKED=1
+    (canaries around every device buffer, verified after each run: the memory
+    checking substitute while compute-sanitizer is closed on the GPU pool),
+    linked with the default build's other objects.  Used only by
+    tests/test_gpu_checked.py through NLFEM_GPU_LIB."""
+    build()
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(INC, f) for f in os.listdir(INC)] + [__file__]
+    if not force and not _stale(CHECKED_LIB, deps):
+        return CHECKED_LIB
+    objdir = os.path.join(HERE, "_build")
+    obj = os.path.join(objdir, "nlfem_gpu_checked.o")
+    others = [os.path.join(objdir, f + ".o") for f in CU_SOURCES + CPP_SOURCES
+              if f != "nlfem_gpu.cu"]
+    with open(os.path.join(objdir, "build_checked.log"), "w") as log:
+        _run([NVCC, *NVCC_FLAGS, "-DNLFEM_CHECKED=1", "-I", INC, "-I", CSRC, "-c",
+              os.path.join(CSRC, "nlfem_gpu.cu"), "-o", obj], log)
+        _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", CHECKED_LIB,
+              obj, *others, "-lcudart_static", "-lrt", "-ldl", "-lpthread"], log)
+    return CHECKED_LIB
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)

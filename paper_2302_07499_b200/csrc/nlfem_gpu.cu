@@ -34,6 +34,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -2552,25 +2553,84 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, doubl
 // ---------------------------------------------------------------------------
 // host side
 
+// Checked build (-DNLFEM_CHECKED=1; compute-sanitizer is closed on this GPU
+// pool): every device buffer gets 4-KiB canaries on both sides, and each run
+// ends by verifying every live buffer's canaries -- an out-of-bounds write by
+// any kernel fails the run with the buffer's size (a bounded substitute for
+// memcheck's write checking).  Zero cost in the default build.
+#ifndef NLFEM_CHECKED
+#define NLFEM_CHECKED 0
+#endif
+constexpr size_t kGuardBytes = NLFEM_CHECKED ? 4096 : 0;
+constexpr unsigned char kGuardByte = 0xA5;
+struct GuardEntry {
+  char** p;
+  size_t* n;
+  size_t esz;
+};
+std::mutex g_guard_mu;
+std::map<const void*, GuardEntry> g_guards;
+void guard_register(const void* obj, char** p, size_t* n, size_t esz) {
+  std::lock_guard<std::mutex> g(g_guard_mu);
+  g_guards[obj] = GuardEntry{p, n, esz};
+}
+void guard_unregister(const void* obj) {
+  std::lock_guard<std::mutex> g(g_guard_mu);
+  g_guards.erase(obj);
+}
+// returns a description of the first buffer whose canaries changed, or ""
+std::string guard_check() {
+  if (!kGuardBytes) return "";
+  std::lock_guard<std::mutex> g(g_guard_mu);
+  std::vector<unsigned char> h(2 * kGuardBytes);
+  for (const auto& kv : g_guards) {
+    const GuardEntry& e = kv.second;
+    if (!*e.p) continue;
+    const size_t bytes = *e.n * e.esz;
+    if (cudaMemcpy(h.data(), *e.p - kGuardBytes, kGuardBytes, cudaMemcpyDeviceToHost) !=
+            cudaSuccess ||
+        cudaMemcpy(h.data() + kGuardBytes, *e.p + bytes, kGuardBytes, cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+      return "canary read failed";
+    for (size_t i = 0; i < h.size(); ++i)
+      if (h[i] != kGuardByte)
+        return "buffer of " + std::to_string(*e.n) + " x " + std::to_string(e.esz) +
+               " B: canary byte " + std::to_string(i) + (i < kGuardBytes ? " before" : " after") +
+               " the buffer overwritten";
+  }
+  return "";
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   void ensure(size_t m) {
     if (m <= n && p) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
+    release();
     const size_t bytes = std::max<size_t>(m, 1) * sizeof(T);
-    CK(cudaMalloc(&p, bytes));
+    char* base = nullptr;
+    CK(cudaMalloc(&base, bytes + 2 * kGuardBytes));
+    if (kGuardBytes) {  // checked build: canaries on both sides
+      CK(cudaMemset(base, kGuardByte, kGuardBytes));
+      CK(cudaMemset(base + kGuardBytes + bytes, kGuardByte, kGuardBytes));
+      guard_register(this, reinterpret_cast<char**>(&p), &n, sizeof(T));
+    }
+    p = reinterpret_cast<T*>(base + kGuardBytes);
     n = std::max<size_t>(m, 1);
   }
   void upload(const T* h, size_t m, cudaStream_t s) {
     ensure(m);
     if (m) CK(cudaMemcpyAsync(p, h, m * sizeof(T), cudaMemcpyHostToDevice, s));
   }
+  void release() {
+    if (p) cudaFree(reinterpret_cast<char*>(p) - kGuardBytes);
+    p = nullptr;
+    n = 0;
+  }
   ~DBuf() {
-    if (p) cudaFree(p);
+    release();
+    if (kGuardBytes) guard_unregister(this);
   }
 };
 
@@ -3688,6 +3748,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
                  "BallExitsMesh: ball reaches past an unglued facet of element " + std::to_string(e)};
     S.npairs = tot;
   }
+  if (NLFEM_CHECKED) {
+    const std::string g = guard_check();
+    if (!g.empty()) throw Fail{NLFEM_GPU_ENODEVICE, "checked build: " + g};
+  }
   S.items = cnt[0];
   S.mc_samples = cnt[1];
   S.mc_hits = cnt[2];
@@ -3951,7 +4015,26 @@ int config_device(const nlfem_gpu_config* cfg) {
   return dev;
 }
 
+__global__ void k_guard_poke(int* a, long long i) { a[i] = 7; }
+
 extern "C" {
+
+// Checked builds only: proves the canaries catch an out-of-bounds write (a
+// kernel writes one element past a fresh buffer).  Returns 1 if caught, 0 if
+// not, -1 in the default build.
+int nlfem_gpu_debug_guard_selftest(int32_t past) {
+  if (!NLFEM_CHECKED) return -1;
+  try {
+    DBuf<int> b;
+    b.ensure(1000);
+    k_guard_poke<<<1, 1>>>(b.p, past ? 1000 : 999);
+    CK(cudaDeviceSynchronize());
+    const std::string g = guard_check();
+    return g.empty() ? 0 : 1;
+  } catch (...) {
+    return -2;
+  }
+}
 
 int nlfem_gpu_fp64_peak(int32_t device, double* tflops, char* err, size_t errlen) {
   return guard(err, errlen, [&] {
@@ -4211,6 +4294,10 @@ int nlfem_gpu_session_finalize_merged(nlfem_gpu_session* s, void* stream, int32_
     S.launches += 2;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
+    if (NLFEM_CHECKED) {
+      const std::string g = guard_check();
+      if (!g.empty()) throw Fail{NLFEM_GPU_ENODEVICE, "checked build: " + g};
+    }
     if (user) {
       CK(cudaEventRecord(S.ev[6], st));
       CK(cudaStreamWaitEvent(user, S.ev[6], 0));
