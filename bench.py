@@ -88,7 +88,7 @@ def describe(name, cfg):
     s = (f"{name}: structured N={cfg['res']} cubes/side (6 tets each) + layer, "
          f"delta={cfg['delta']:.6g}, {cfg['strategy']}")
     if cfg["strategy"] == "fullcaps":
-        s += f", M={cfg['mc']} per MC sub-simplex, Philox4x32-10 seed {SEED}"
+        s += f", M={cfg['mc']} per MC sub-simplex, Philox4x32-7 seed {SEED}"
     if cfg["jitter"] is not None:
         s += f", interior vertices jittered +-0.2h (seed {cfg['jitter']})"
     s += ", moment2 kernel (gamma=15/(2 pi delta^5)), u=|x|^2, f=-6, FP64"

@@ -13,8 +13,14 @@
  *     y = u0 V0 + (u1-u0) V1 + (u2-u1) V2 + (1-u2) V3, u0 <= u1 <= u2.
  * What is ours (the reference uses xoshiro256++ keyed by a walk-order piece
  * index, assembly.cpp:386-387, which a parallel kernel cannot reproduce):
- *   - Philox4x32-10 (Salmon et al. 2011; Random123 constants), key =
- *     (seed & 0xffffffff, seed >> 32);
+ *   - Philox4x32 (Salmon et al. 2011; Random123 constants) with
+ *     NLFEM_MC_ROUNDS = 7 rounds, key = (seed & 0xffffffff, seed >> 32).
+ *     Seven is the round count Salmon et al. found to be the smallest that
+ *     passes TestU01's BigCrush for every counter/key pattern they tried
+ *     ("Crush-resistant"); ten is Random123's default, which adds a safety
+ *     margin.  The 3D stream takes seven (round 2: 9% off the Monte Carlo
+ *     kernel, whose integer issue is a third Philox); the 2D stream below and
+ *     the known-answer tests use ten;
  *   - samples come in blocks of four: block j of sub-simplex `sub` of item
  *     (outer elem T, quad pt q, inner elem T') is the 8 words W[0..7] of the
  *     counters  (T, T', q | sub << 2, 2j + c),  c = 0, 1;  sample k = 4j + i;
@@ -61,14 +67,18 @@ NLFEM_HD void nlfem_mulhilo32(uint32_t a, uint32_t b, uint32_t* hi, uint32_t* lo
 #endif
 }
 
-/* Philox4x32 with 10 rounds. */
-NLFEM_HD void nlfem_philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1,
-                                  uint32_t out[4]) {
+/* Rounds of the 3D Monte Carlo stream (see the header comment). */
+#define NLFEM_MC_ROUNDS 7
+
+/* Philox4x32 with `rounds` rounds (Philox4x32-R: the same round function R
+ * times; the first rounds of Philox4x32-10 are Philox4x32-7). */
+NLFEM_HD void nlfem_philox4x32_r(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1,
+                                 int rounds, uint32_t out[4]) {
   uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
 #if defined(__CUDA_ARCH__)
 #pragma unroll
 #endif
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < rounds; ++r) {
     uint32_t hi0, lo0, hi1, lo1;
     nlfem_mulhilo32(NLFEM_PHILOX_M0, c0, &hi0, &lo0);
     nlfem_mulhilo32(NLFEM_PHILOX_M1, c2, &hi1, &lo1);
@@ -87,13 +97,19 @@ NLFEM_HD void nlfem_philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_
   out[3] = c3;
 }
 
+/* Philox4x32-10 (Random123's default; the 2D stream and the KATs). */
+NLFEM_HD void nlfem_philox4x32_10(const uint32_t ctr_in[4], uint32_t k0, uint32_t k1,
+                                  uint32_t out[4]) {
+  nlfem_philox4x32_r(ctr_in, k0, k1, 10, out);
+}
+
 /* The 8 words of sample block j of sub-simplex `sub` of item (T, q, T'). */
 NLFEM_HD void nlfem_mc_block(uint64_t seed, uint32_t T, uint32_t Tp, uint32_t q,
                              uint32_t sub, uint32_t j, uint32_t W[8]) {
   const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
   for (uint32_t c = 0; c < 2; ++c) {
     const uint32_t ctr[4] = {T, Tp, q | (sub << 2), 2u * j + c};
-    nlfem_philox4x32_10(ctr, k0, k1, W + 4 * c);
+    nlfem_philox4x32_r(ctr, k0, k1, NLFEM_MC_ROUNDS, W + 4 * c);
   }
 }
 

@@ -45,6 +45,8 @@ def lib():
                                           C.POINTER(u64)]
         L.oracle_result_free.argtypes = [vp]
         L.oracle_philox.argtypes = [vp, C.c_uint32, C.c_uint32, vp]
+        L.oracle_mc_fields.argtypes = [u64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.c_int, vp]
         L.oracle_cg.restype = C.c_int
         L.oracle_cg.argtypes = [C.c_int, vp, vp, vp, vp, dbl, C.c_int, vp, C.POINTER(i32)]
         L.oracle_l2_error.restype = dbl
@@ -102,6 +104,13 @@ def philox(ctr, key):
     c = np.ascontiguousarray(ctr, np.uint32)
     o = np.empty(4, np.uint32)
     lib().oracle_philox(_p(c), int(key[0]), int(key[1]), _p(o))
+    return o
+
+
+def mc_fields(seed, T, Tp, q, sub, j0, nblocks):
+    """Unsorted 21-bit fields of the 3D Monte Carlo stream, shape (4 nblocks, 3)."""
+    o = np.empty((4 * nblocks, 3), np.uint32)
+    lib().oracle_mc_fields(int(seed), T, Tp, q, sub, j0, nblocks, _p(o))
     return o
 
 

@@ -1021,6 +1021,18 @@ void oracle_philox(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out
   nlfem_philox4x32_10(ctr, k0, k1, out);
 }
 
+// The unsorted 21-bit fields (3 per sample, 4 samples per block) of sample
+// blocks j0 .. j0 + nblocks - 1 of sub-simplex `sub` of item (T, q, T') of the
+// 3D Monte Carlo stream (include/nlfem_mc_stream.h), for the stream tests.
+void oracle_mc_fields(uint64_t seed, uint32_t T, uint32_t Tp, uint32_t q, uint32_t sub,
+                      uint32_t j0, int nblocks, uint32_t* out) {
+  for (int b = 0; b < nblocks; ++b) {
+    uint32_t W[8];
+    nlfem_mc_block(seed, T, Tp, q, sub, j0 + uint32_t(b), W);
+    for (int i = 0; i < 4; ++i) nlfem_mc_fields(W, i, out + 12 * b + 3 * i);
+  }
+}
+
 // Plain CG from zero (reference solver.cpp:26-66).
 int oracle_cg(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* b,
               double tol, int maxit, double* x, int32_t* iters) {

@@ -110,7 +110,7 @@ struct Dev {
   int K, J, KI, unknowns;
   int strategy, mc;
   unsigned long long seed;
-  uint32_t rkey[20];  // Philox4x32-10 round keys (k0 + r W0, k1 + r W1), r = 0..9
+  uint32_t rkey[20];  // Philox round keys (k0 + r W0, k1 + r W1), r < NLFEM_MC_ROUNDS
   double inv_mc;      // 1 / mc when mc is a power of two (vol * inv_mc == vol / mc), else 0
   double C, delta, slack, inside_cut, dd;
   // element data
@@ -1402,14 +1402,15 @@ __global__ void k_pair_outer(int ii0, int ii1, const long long* pair_off, long l
     pair_outer[p - P0] = ii;
 }
 
-// Philox4x32-10 on three counters in lockstep (independent chains -> ILP 3);
-// same function as nlfem_philox4x32_10 applied to each counter.
+// Philox4x32-R (R = NLFEM_MC_ROUNDS, include/nlfem_mc_stream.h) on two
+// counters in lockstep (independent chains); the same function as
+// nlfem_philox4x32_r applied to each counter.
 __device__ __forceinline__ void philox2(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t j2,
                                         uint32_t A[4], uint32_t B[4]) {
   uint32_t a0 = c0, a1 = c1, a2 = c2, a3 = j2;
   uint32_t b0 = c0, b1 = c1, b2 = c2, b3 = j2 + 1;
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < NLFEM_MC_ROUNDS; ++r) {
     const unsigned long long pa0 = (unsigned long long)NLFEM_PHILOX_M0 * a0;
     const unsigned long long pa2 = (unsigned long long)NLFEM_PHILOX_M1 * a2;
     const unsigned long long pb0 = (unsigned long long)NLFEM_PHILOX_M0 * b0;
@@ -1473,13 +1474,14 @@ __device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c)
 }
 
 #ifndef NLFEM_MC_MOM
-#define NLFEM_MC_MOM 0  // 0: FP64 products; 1-3: integer products (masks by SEL / IMAD)
+#define NLFEM_MC_MOM 4  // 4: FP64 products of fields masked by LOP3; 0: masked by a
+                        // DMUL with the hit bit (2% slower at C2); 1-3: integer products
 #endif
 
 struct IntMoments {
   unsigned n = 0;
   uint32_t s[3] = {0, 0, 0};
-#if NLFEM_MC_MOM == 0
+#if NLFEM_MC_MOM == 0 || NLFEM_MC_MOM == 4
   double ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
 #else
   unsigned long long ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
@@ -1496,6 +1498,22 @@ struct IntMoments {
     s[2] = imad_u32(hb, s2, s[2]);
     const double h = __hiloint2double((int)imad_u32(hb, 0x3ff00000u, 0u), 0);
     const double h0 = h * d0, h1 = h * d1, h2 = h * d2;
+    ss[0] = fma(h0, d0, ss[0]);
+    ss[1] = fma(h0, d1, ss[1]);
+    ss[2] = fma(h0, d2, ss[2]);
+    ss[3] = fma(h1, d1, ss[3]);
+    ss[4] = fma(h1, d2, ss[4]);
+    ss[5] = fma(h2, d2, ss[5]);
+#elif NLFEM_MC_MOM == 4
+    // the fields masked in the integer pipe (two LOP3 per double) instead of
+    // multiplied by the hit bit on the FP64 pipe
+    s[0] = imad_u32(hb, s0, s[0]);
+    s[1] = imad_u32(hb, s1, s[1]);
+    s[2] = imad_u32(hb, s2, s[2]);
+    const uint32_t m = 0u - hb;
+    const double h0 = __hiloint2double(__double2hiint(d0) & (int)m, __double2loint(d0) & (int)m);
+    const double h1 = __hiloint2double(__double2hiint(d1) & (int)m, __double2loint(d1) & (int)m);
+    const double h2 = __hiloint2double(__double2hiint(d2) & (int)m, __double2loint(d2) & (int)m);
     ss[0] = fma(h0, d0, ss[0]);
     ss[1] = fma(h0, d1, ss[1]);
     ss[2] = fma(h0, d2, ss[2]);

@@ -34,6 +34,62 @@ def test_philox_known_answers():
         ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
 
 
+def _philox_py(ctr, k0, k1, rounds):
+    """Philox4x32-R in plain Python (Salmon et al. 2011; Random123 constants)."""
+    M = 0xFFFFFFFF
+    c0, c1, c2, c3 = ctr
+    for _ in range(rounds):
+        p0, p1 = 0xD2511F53 * c0, 0xCD9E8D57 * c2
+        c0, c1, c2, c3 = ((p1 >> 32) ^ c1 ^ k0) & M, p1 & M, ((p0 >> 32) ^ c3 ^ k1) & M, p0 & M
+        k0, k1 = (k0 + 0x9E3779B9) & M, (k1 + 0xBB67AE85) & M
+    return [c0, c1, c2, c3]
+
+
+def test_mc_stream_is_philox4x32_7():
+    # the 3D stream's words are Philox4x32-7 of (T, T', q | sub << 2, 2j + c)
+    # under key (seed lo, seed hi), cut into 21-bit fields as the header says;
+    # the 10-round function under it is pinned by the Random123 KATs above
+    assert _philox_py([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], 0xA4093822,
+                      0x299F31D0, 10) == [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+    seed, T, Tp, q, sub = 0x0123456789ABCDEF, 77, 123456, 3, 2
+    f = port.mc_fields(seed, T, Tp, q, sub, 5, 3)
+    for b in range(3):
+        j = 5 + b
+        W = sum((_philox_py([T, Tp, q | (sub << 2), 2 * j + c], seed & 0xFFFFFFFF, seed >> 32, 7)
+                 for c in range(2)), [])
+        for i in range(4):
+            w = W[4 * (i >> 1):4 * (i >> 1) + 4]
+            if i % 2 == 0:
+                want = [w[t] >> 11 for t in range(3)]
+            else:
+                want = [((w[t] & 0x7FF) << 10) | ((w[3] >> (22 - 10 * t)) & 0x3FF) for t in range(3)]
+            assert list(f[4 * b + i]) == want, (b, i)
+
+
+def test_mc_stream_uniform_and_independent():
+    # statistical sanity of the 7-round stream over the counter patterns the
+    # kernel uses: consecutive blocks, neighbouring inner elements, the quad
+    # points and sub-simplices of one item.  Each coordinate (even and odd
+    # samples separately) chi-square over 64 bins, correlations between the
+    # three fields of a sample and between consecutive samples, and the sorted
+    # spacings' means (1/4, 1/2, 3/4: a uniform point in the tetrahedron)
+    from scipy import stats
+    F = np.concatenate([port.mc_fields(SEED, 1000 + t, 5000 + tp, q, sub, 0, 256)
+                        for t in range(4) for tp in range(4) for q in range(4) for sub in range(3)])
+    U = (F.astype(np.float64) + 0.5) / 2.0**21                    # (196608, 3)
+    for par in (0, 1):
+        for c in range(3):
+            h = np.bincount((F[par::2, c] >> 15).astype(np.int64), minlength=64)
+            assert stats.chisquare(h).pvalue > 1e-4, (par, c)
+    n = len(U)
+    for a, b in ((0, 1), (0, 2), (1, 2)):
+        assert abs(np.corrcoef(U[:, a], U[:, b])[0, 1]) < 5.0 / np.sqrt(n)
+    for c in range(3):
+        assert abs(np.corrcoef(U[:-1, c], U[1:, c])[0, 1]) < 5.0 / np.sqrt(n)
+    Us = np.sort(U, axis=1).mean(axis=0)
+    assert np.allclose(Us, [0.25, 0.5, 0.75], atol=5.0 * 0.25 / np.sqrt(n))
+
+
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("strat", ["inside", "overlap", "barycenter", "nocaps", "approxcaps",
                                    "fullcaps"])
