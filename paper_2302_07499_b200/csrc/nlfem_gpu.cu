@@ -964,11 +964,18 @@ __global__ void k_mark_partners(long long np, const long long* pend, const int* 
 // multi-GPU plan); pmark (or null): interior elements that
 // are partners of those pairs -- their own node pairs enter the rows too, so a
 // rank's local pattern holds every slot its combine adds to (the D_T' block)
-template <bool FILL>
+// MODE 0: row lengths; 1: rows written at roff (from the scanned lengths);
+// 2: one pass -- each row takes its place in rcols from a global cursor (rows in
+// arrival order: roff[i] = its start, rlen[i] = its length, roff[J] = the total;
+// the row contents, hence everything derived from them, do not depend on the
+// order), nothing written once the cursor passes cap (ovf = kCapRetry).
+template <int MODE>
 __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const int* partner,
-                                              int* rlen, const long long* roff, int* rcols,
+                                              int* rlen, long long* roff, int* rcols,
                                               int* ovf, int plo, int phi,
-                                              const unsigned char* pmark, PatTabs tb) {
+                                              const unsigned char* pmark, PatTabs tb,
+                                              unsigned long long* cursor, long long cap) {
+  constexpr bool FILL = MODE != 0;
   extern __shared__ int sm[];
   const int kHE = tb.he, kHN = tb.hn, kRowMax = tb.rowmax;
   int* tabE = sm;
@@ -986,7 +993,8 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
       any = (lo >= plo && lo < phi) || (pmark && pmark[T]);
     }
     if (!any) {
-      if (!FILL && threadIdx.x == 0) rlen[i] = 0;
+      if (MODE != 1 && threadIdx.x == 0) rlen[i] = 0;
+      if (MODE == 2 && threadIdx.x == 0) roff[i] = 0;
       continue;
     }
     for (int s = threadIdx.x; s < kHE; s += blockDim.x) tabE[s] = -1;
@@ -1019,15 +1027,34 @@ __global__ void __launch_bounds__(256) k_rows(const long long* pair_off, const i
     }
     __syncthreads();
     const int n = nlist < kRowMax ? nlist : kRowMax;
-    if (!FILL) {
+    if (MODE == 0) {
       if (threadIdx.x == 0) rlen[i] = n;
-    } else {
+    } else if (MODE == 1) {
       block_sort(list, n);
       const long long o = roff[i];
       for (int s = threadIdx.x; s < n; s += blockDim.x) rcols[o + s] = list[s];
+    } else {
+      __shared__ long long srow;
+      if (threadIdx.x == 0) {
+        srow = (long long)atomicAdd(cursor, (unsigned long long)n);
+        roff[i] = srow;
+        rlen[i] = n;
+      }
+      block_sort(list, n);
+      __syncthreads();
+      const long long o = srow;
+      if (o + n <= cap)
+        for (int s = threadIdx.x; s < n; s += blockDim.x) rcols[o + s] = list[s];
+      else if (threadIdx.x == 0)
+        atomicCAS(ovf, 0, kCapRetry);
     }
     __syncthreads();
   }
+}
+
+// single-pass rows: the total (the cursor) becomes roff[J]
+__global__ void k_rows_total(const unsigned long long* cursor, long long* total) {
+  *total = (long long)*cursor;
 }
 
 __global__ void k_col_count(const long long* total, const int* cols, int* cnt, const int* ovf) {
@@ -1037,11 +1064,12 @@ __global__ void k_col_count(const long long* total, const int* cols, int* cnt, c
 }
 
 // warp per row: lanes scatter the row's entries into the transposed rows
-__global__ void k_transpose_fill(int J, const long long* roff, const int* rcols,
+__global__ void k_transpose_fill(int J, const long long* roff, const int* rlen, const int* rcols,
                                  const long long* toff, int* cursor, int* tcols, const int* ovf) {
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= J || *ovf) return;
-  for (long long k = roff[i] + (threadIdx.x & 31); k < roff[i + 1]; k += 32) {
+  const long long rend = rlen ? roff[i] + rlen[i] : roff[i + 1];  // (rows in arrival order)
+  for (long long k = roff[i] + (threadIdx.x & 31); k < rend; k += 32) {
     const int j = rcols[k];
     tcols[toff[j] + atomicAdd(cursor + j, 1)] = i;
   }
@@ -1084,6 +1112,7 @@ __device__ __forceinline__ int lower_bound_int(const int* a, int n, int x) {
 constexpr int kUnionThreads = 128;
 template <bool FILL>
 __global__ void __launch_bounds__(kUnionThreads) k_union(int J, const long long* roff,
+                                                         const int* rlen,
                                                          const int* rcols, const long long* toff,
                                                          const int* tcols, int* slen,
                                                          const long long* soff, int* scols,
@@ -1095,7 +1124,7 @@ __global__ void __launch_bounds__(kUnionThreads) k_union(int J, const long long*
   if (*ovf) return;
   for (int i = blockIdx.x; i < J; i += gridDim.x) {
     const long long a0 = roff[i], b0 = toff[i];
-    const int na = (int)(roff[i + 1] - a0), nb = (int)(toff[i + 1] - b0);
+    const int na = rlen ? rlen[i] : (int)(roff[i + 1] - a0), nb = (int)(toff[i + 1] - b0);
     if (nb > kRowMax) continue;  // flagged by k_sort_rows
     const int* R = rcols + a0;
     const int* RT = tcols + b0;
@@ -1224,14 +1253,25 @@ __global__ void k_outpat(const long long* soff, const int* scols, int* olen,
 // ---------------------------------------------------------------------------
 // K3/K4: integration + scatter
 
-// Two-word fixed point: v*scale = hi + lo * 2^-40 with hi = rint(v*scale)
-// (exact: scale is a power of two) and lo = rint((v*scale - hi) * 2^40), so an
-// accumulated entry carries ~101 bits and equals the exact sum of the FP64
-// contributions up to one final rounding; integer adds make it order-free.
+// Two-word fixed point: x = v*scale (exact: scale is a power of two, |x| < 2^62)
+// is split as x = hi + lo * 2^-10 + e with hi = 2^32 rint(x 2^-32) (a multiple
+// of 2^32), lo = rint((x - hi) 2^10) (|lo| <= 2^41) and |e| <= 2^-11: an
+// accumulated entry resolves 2^-72 of its row bound, and integer adds make the
+// sum order-free.  (A single word, rint(x), measured 3.8e-13 of a row's largest
+// entry at C4 -- profiles/r2_fixed_point_precision.txt: contributions far below
+// one unit vanish systematically; the second word divides that by 2^10.)
+//
+// Both roundings use the 1.5 * 2^52 magic constant on the FP64 pipe: the
+// double <-> int64 conversion instructions (F2I.S64.F64 / I2F.F64.S64) issue on
+// the XU pipe at about one lane per clock per SM on sm_100 and held the combine
+// at 90% of that pipe (profiles/r2e_combine_ncu.txt) when every contribution
+// took three of them.
 #ifndef NLFEM_DIAG
 #define NLFEM_DIAG 0  // timing diagnostics of the combine (bit 1: no REDs; 2: no item
                       // records; 4: no partner-element gathers) -- wrong results
 #endif
+constexpr double kFixMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kFixLoScale = 0x1p10, kFixLoInv = 0x1p-10;
 __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot, double v,
                                           double scale) {
   if (NLFEM_DIAG & 1) {
@@ -1239,36 +1279,19 @@ __device__ __forceinline__ void red_fixed(unsigned long long* V, long long slot,
     return;
   }
   const double x = v * scale;
-  const long long hi = __double2ll_rn(x);
-  const long long lo = __double2ll_rn((x - (double)hi) * 0x1p40);
-  if (hi != 0) atomicAdd(V + 2 * slot, (unsigned long long)hi);
+  const double m1 = fma(x, 0x1p-32, kFixMagic);  // low mantissa word = rint(x 2^-32)
+  const int h1 = __double2loint(m1);
+  const double r = fma(m1 - kFixMagic, -0x1p32, x);  // exact, |r| <= 2^31
+  const double m3 = fma(r, kFixLoScale, kFixMagic);
+  const long long lo = __double_as_longlong(m3) - __double_as_longlong(kFixMagic);
+  if (h1 != 0) atomicAdd(V + 2 * slot, (unsigned long long)((long long)h1 << 32));
   if (lo != 0) atomicAdd(V + 2 * slot + 1, (unsigned long long)lo);
-}
-
-// Every entry keeps both words (~101 bits: the exact sum of its FP64
-// contributions up to one final rounding).  NLFEM_FIXED_TWO=0 restores the
-// round-1 choice -- unknown x unknown entries with the high word only (~62
-// bits of the row bound) -- measured at C4 as 3.8e-13 of a row's largest
-// entry at worst (mean 5e-15; scripts/fixed_point_precision.py,
-// profiles/r2_fixed_point_precision.txt), above the 1e-13 budget, for a 0.5%
-// (C2, P3f) to 3.5% (C3n) shorter step.
-#ifndef NLFEM_FIXED_TWO
-#define NLFEM_FIXED_TWO 1  // 0: unknown x unknown entries keep the high word only
-#endif
-__device__ __forceinline__ void red_fixed_sel(unsigned long long* V, long long slot, double v,
-                                              double scale, bool two) {
-  if (!two && !NLFEM_FIXED_TWO && !(NLFEM_DIAG & 1)) {
-    const long long hi = __double2ll_rn(v * scale);
-    if (hi != 0) atomicAdd(V + 2 * slot, (unsigned long long)hi);
-    return;
-  }
-  red_fixed(V, slot, v, scale);
 }
 
 __device__ __forceinline__ double fixed_value(const unsigned long long* V, long long slot,
                                               double iscale) {
   const long long hi = (long long)V[2 * slot], lo = (long long)V[2 * slot + 1];
-  return ((double)hi + (double)lo * 0x1p-40) * iscale;
+  return ((double)hi + (double)lo * kFixLoInv) * iscale;
 }
 
 // error-free transformation for compensated sums (Knuth TwoSum)
@@ -2116,6 +2139,13 @@ struct SlotMap {
 #define NLFEM_INT_MINBLOCKS 2
 #endif
 
+#ifndef NLFEM_COMB_PREFETCH
+#define NLFEM_COMB_PREFETCH 0
+#endif
+__device__ __forceinline__ void pf_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <int NTHR>
 __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 * NLFEM_INT_MINBLOCKS)) k_integrate(
     int ii0, const long long* pair_off, const int* partner, const unsigned* info,
@@ -2163,142 +2193,165 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
   }
   __syncthreads();
 
-  Vd vT[4];
-  load_verts(T, vT);
   const double wq = 0.25 * cD.vol[T];  // rule.w[k] * vol (reference assembly.cpp:702)
   const double C = cD.C;
-  const double sc[4] = {cD.scale[NT[0]], cD.scale[NT[1]], cD.scale[NT[2]], cD.scale[NT[3]]};
-  const bool conT[4] = {cD.dof[NT[0]] < 0, cD.dof[NT[1]] < 0, cD.dof[NT[2]] < 0,
-                        cD.dof[NT[3]] < 0};
+  // per-row constants of T, parked in shared memory (broadcast reads; they
+  // would otherwise stay live in registers across the pair loop)
+  __shared__ double sc[4];
+  __shared__ int sNT[4];
+  if (threadIdx.x < 4) {
+    sc[threadIdx.x] = cD.scale[NT[threadIdx.x]];
+    sNT[threadIdx.x] = NT[threadIdx.x];
+  }
+  __syncthreads();
   // per outer element: sum over pairs of S0_q (constraint parents weigh 2,
   // reference assembly.cpp:419) and of sum_q c_{q,a} Sg_q
   double s0w[4] = {0, 0, 0, 0}, sgc[4] = {0, 0, 0, 0};
   unsigned long long led = 0;
 
   const long long p0 = pair_off[ii], p1 = pair_off[ii + 1];
-  for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    // per pair: X[a][b] = sum_q c_{q,a} S1_q[b], S2 = sum_q S2_q
-    double X[4][4], S2[10];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) X[a][b] = 0;
-#pragma unroll
-    for (int k = 0; k < 10; ++k) S2[k] = 0;
-
-    const int Tp = (NLFEM_DIAG & 4) ? T : partner[p];
-    const unsigned code = info[p];
+  // software pipeline: the next pair's partner, codes and first record are
+  // loaded one iteration ahead, so a pair's dependent gathers start at once
+  long long p = p0 + threadIdx.x;
+  int TpN = 0;
+  unsigned codeN = 0;
+  long long uN = 0;
+  if (p < p1) {
+    TpN = (NLFEM_DIAG & 4) ? T : partner[p];
+    codeN = info[p];
+    uN = (mom != nullptr) ? uoff[p - pbase] : 0;
+  }
+  for (; p < p1; p += blockDim.x) {
+    const int Tp = TpN;
+    const unsigned code = codeN;
+    long long u = uN;  // first record of the pair
+    {
+      const long long pn = p + blockDim.x;
+      if (pn < p1) {
+        TpN = (NLFEM_DIAG & 4) ? T : partner[pn];
+        codeN = info[pn];
+        uN = (mom != nullptr) ? uoff[pn - pbase] : 0;
+      }
+    }
     const bool constr = cD.region[Tp] != 0;
     const double volP = cD.vol[Tp];
-    const double* invP = cD.inv + 9 * (long long)Tp;
-    long long u = (mom != nullptr) ? uoff[p - pbase] : 0;  // first record of the pair
 
-#pragma unroll 1
+    if (constr) {
+      // constraint parent: measure and g integral per point (reference
+      // assembly.cpp:350-359, 416-427); no matrix block
+      const double gb = cD.gbar[Tp];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned c = (code >> (5 * q)) & 31;
+        if (c == 0) continue;
+        double S0 = 0, Sg = 0;
+        if (c == kWhole) {
+          led += 133;
+          S0 = volP;
+          Sg = gb;
+        } else if (mom != nullptr) {
+          const double2 r0 =
+              *reinterpret_cast<const double2*>(mom + kMomStride * ((NLFEM_DIAG & 2) ? 0 : u));
+          ++u;
+          S0 = r0.x;
+          Sg = r0.y;
+        }
+        s0w[q] += 2.0 * S0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) sgc[a] += Sg * qbary(q, a);
+      }
+      continue;
+    }
+
+    // interior parent.  The basis moments of an item are an affine image of
+    // its Cartesian moments about v0(T') (lambda(y) = e_0 + J (y - v0)), and
+    // the pair's blocks are linear in them: X[a][b] = sum_q c_{q,a} S1_q[b],
+    // S2 = sum_q S2_q.  So the records are summed over the points first --
+    // n0_q and m1_q per point (the point weights c_{q,a} differ), the second
+    // moments altogether -- and mapped through J once per pair.
+    double n0q[4] = {0, 0, 0, 0}, m1q[4][3], Ms[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m1q[q][0] = m1q[q][1] = m1q[q][2] = 0;
+    double nw = 0;         // whole-element points (a double: no conversion later)
+    unsigned wmask = 0;    // ... and which
+#pragma unroll
     for (int q = 0; q < 4; ++q) {
       const unsigned c = (code >> (5 * q)) & 31;
       if (c == 0) continue;
-      double S0 = 0, S1[4] = {0, 0, 0, 0}, Sg = 0;
+      double S0 = 0;
       if (c == kWhole) {
-        led += constr ? 133 : 39;
+        led += 39;
         S0 = volP;
-        if (constr) {
-          // constraint parent: measure and g average (reference assembly.cpp:350-359),
-          // per element from prep (same expression)
-          Sg = cD.gbar[Tp];
-        } else {
-          // exact basis moments of a whole element (reference assembly.cpp:361-369)
-          const double s1 = volP / 4, off = volP / 20.0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            S1[b] = s1;
-#pragma unroll
-            for (int cc = b; cc < 4; ++cc) S2[s2i(b, cc)] += off * (b == cc ? 2.0 : 1.0);
-          }
-        }
-      }
-      // straddling / cap item: its record (k_mc: inner pieces, + outer pieces by
-      // Monte Carlo for fullcaps), Cartesian moments about v0(T')
-      if (mom != nullptr && (c == kOutCap || (c & kStraddle))) {
-        double g0 = 0, m1[3] = {0, 0, 0}, m2[6] = {0, 0, 0, 0, 0, 0};
-        const double2* rec = reinterpret_cast<const double2*>(mom + kMomStride * ((NLFEM_DIAG & 2) ? 0 : u));
-        const double2 r0 = rec[0];
-        const double n0 = r0.x;
-        if (constr) {
-          g0 = r0.y;
-        } else {
-          const double2 r1 = rec[1], r2 = rec[2], r3 = rec[3], r4 = rec[4];
-          m1[0] = r0.y;
-          m1[1] = r1.x;
-          m1[2] = r1.y;
-          m2[0] = r2.x;
-          m2[1] = r2.y;
-          m2[2] = r3.x;
-          m2[3] = r3.y;
-          m2[4] = r4.x;
-          m2[5] = r4.y;
-        }
+        nw += 1.0;
+        wmask |= 1u << q;
+      } else if (mom != nullptr) {
+        // straddling / cap item: its record (k_mc: inner pieces, + outer pieces
+        // by Monte Carlo for fullcaps)
+        const double2* rec =
+            reinterpret_cast<const double2*>(mom + kMomStride * ((NLFEM_DIAG & 2) ? 0 : u));
         ++u;
-        S0 += n0;
-        if (constr) {
-          Sg += g0;
-        } else {
-          // lambda(y) = e_0 + J (y - v0): J rows from inv_edges, J0 = -(J1+J2+J3)
-          double J[4][3];
-#pragma unroll
-          for (int r = 1; r < 4; ++r)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) J[r][a] = invP[3 * (r - 1) + a];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) J[0][a] = -(J[1][a] + J[2][a] + J[3][a]);
-          const double M[3][3] = {{m2[0], m2[1], m2[2]}, {m2[1], m2[3], m2[4]},
-                                  {m2[2], m2[4], m2[5]}};
-          double jm[4];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) jm[b] = J[b][0] * m1[0] + J[b][1] * m1[1] + J[b][2] * m1[2];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            double JM[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) JM[a] = J[b][0] * M[0][a] + J[b][1] * M[1][a] + J[b][2] * M[2][a];
-            S1[b] += (b == 0 ? n0 : 0.0) + jm[b];
-#pragma unroll
-            for (int cc = b; cc < 4; ++cc) {
-              double s2 = JM[0] * J[cc][0] + JM[1] * J[cc][1] + JM[2] * J[cc][2];
-              if (b == 0) s2 += jm[cc];
-              if (cc == 0) s2 += jm[b];
-              if (b == 0 && cc == 0) s2 += n0;
-              S2[s2i(b, cc)] += s2;
-            }
-          }
-        }
+        const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3], r4 = rec[4];
+        S0 = r0.x;
+        n0q[q] = r0.x;
+        m1q[q][0] = r0.y;
+        m1q[q][1] = r1.x;
+        m1q[q][2] = r1.y;
+        Ms[0] += r2.x;
+        Ms[1] += r2.y;
+        Ms[2] += r3.x;
+        Ms[3] += r3.y;
+        Ms[4] += r4.x;
+        Ms[5] += r4.y;
       }
-      // fold the item into the pair / outer-element accumulators
-      const double f = constr ? 2.0 * S0 : S0;
-      s0w[0] += q == 0 ? f : 0.0;
-      s0w[1] += q == 1 ? f : 0.0;
-      s0w[2] += q == 2 ? f : 0.0;
-      s0w[3] += q == 3 ? f : 0.0;
-      if (constr) {
-#pragma unroll
-        for (int a = 0; a < 4; ++a) sgc[a] += Sg * qbary(q, a);
-      } else {
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const double ca = qbary(q, a);
-#pragma unroll
-          for (int b = 0; b < 4; ++b) X[a][b] = fma(ca, S1[b], X[a][b]);
-        }
-      }
+      s0w[q] += S0;
     }
 
-    if (!constr) {
-      const int4 wP = cD.verts[Tp];
-      const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
-      const double4 esc = cD.escale[Tp];
-      const double scP[4] = {esc.x, esc.y, esc.z, esc.w};
-      const unsigned cm = cD.econ[Tp];
-      const bool conP[4] = {(cm & 1u) != 0, (cm & 2u) != 0, (cm & 4u) != 0, (cm & 8u) != 0};
-      // T x T' cross block -C w X[a][b] at (N_a, M_b): shared-memory rows
+#if NLFEM_COMB_PREFETCH
+    if (p + blockDim.x < p1) {
+      // the next pair's element fields and records towards L1 while this
+      // pair's blocks are formed
+      pf_l1(cD.vol + TpN);
+      pf_l1(cD.inv + 9 * (long long)TpN);
+      pf_l1(cD.inv + 9 * (long long)TpN + 8);
+      pf_l1(cD.verts + TpN);
+      pf_l1(cD.escale + TpN);
+      if (mom != nullptr) {
+        pf_l1(mom + kMomStride * uN);
+        pf_l1(mom + kMomStride * uN + 16);
+        pf_l1(mom + kMomStride * uN + 32);
+      }
+    }
+#endif
+    const int4 wP = cD.verts[Tp];
+    const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
+    const double4 esc = cD.escale[Tp];
+    const double scP[4] = {esc.x, esc.y, esc.z, esc.w};
+    const long long* es = eslot + 10 * (long long)interior_pos(Tp);
+
+    // J rows from inv_edges, J0 = -(J1+J2+J3)
+    const double* invP = cD.inv + 9 * (long long)Tp;
+    double J[4][3];
+#pragma unroll
+    for (int r = 1; r < 4; ++r)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) J[r][a] = invP[3 * (r - 1) + a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) J[0][a] = -(J[1][a] + J[2][a] + J[3][a]);
+
+    const double n0s = (n0q[0] + n0q[1]) + (n0q[2] + n0q[3]);
+    double m1s[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) m1s[k] = (m1q[0][k] + m1q[1][k]) + (m1q[2][k] + m1q[3][k]);
+    // whole elements: exact basis moments (reference assembly.cpp:361-369)
+    const double s1w = volP / 4, offw = nw * (volP / 20.0);
+    const double cw = -C * wq;
+
+    // T x T' cross block -C w X[a][b] at (N_a, M_b): shared-memory rows
+    {
+      double jms[4];  // J_b . sum_q m1_q
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        jms[b] = fma(J[b][2], m1s[2], fma(J[b][1], m1s[1], J[b][0] * m1s[0]));
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int hb = mp.probe(NP[b]);
@@ -2307,21 +2360,36 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
         const short sla[4] = {sl.x, sl.y, sl.z, sl.w};
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          const double x = -C * wq * X[a][b];
-          red_fixed_sel(V, rbase[a] + sla[a], NT[a] == NP[b] ? 2.0 * x : x, sc[a],
-                        conT[a] || conP[b]);
+          // sum_q c_{q,a} S1_q[b], c_{q,a} = QB + (QA - QB) [q == a]
+          const double wa = NLFEM_QB * nw + (((wmask >> a) & 1u) ? (NLFEM_QA - NLFEM_QB) : 0.0);
+          const double jma = fma(J[b][2], m1q[a][2], fma(J[b][1], m1q[a][1], J[b][0] * m1q[a][0]));
+          double xa = fma(NLFEM_QA - NLFEM_QB, jma, NLFEM_QB * jms[b]);
+          if (b == 0) xa += fma(NLFEM_QA - NLFEM_QB, n0q[a], NLFEM_QB * n0s);
+          const double x = cw * fma(wa, s1w, xa);
+          red_fixed(V, rbase[a] + sla[a], sNT[a] == NP[b] ? 2.0 * x : x, sc[a]);
         }
       }
       // T' x T' block C w sum_q S2_q at (M_b, M_c), row min(M_b, M_c)
-      const long long* es = eslot + 10 * (long long)interior_pos(Tp);
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < 4; ++b) {
+        double JM[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double m0 = a == 0 ? Ms[0] : (a == 1 ? Ms[1] : Ms[2]);
+          const double m1 = a == 0 ? Ms[1] : (a == 1 ? Ms[3] : Ms[4]);
+          const double m2 = a == 0 ? Ms[2] : (a == 1 ? Ms[4] : Ms[5]);
+          JM[a] = fma(J[b][2], m2, fma(J[b][1], m1, J[b][0] * m0));
+        }
 #pragma unroll
         for (int cc = b; cc < 4; ++cc) {
-          const int k = s2i(b, cc);
-          red_fixed_sel(V, es[k], C * wq * S2[k], NP[b] <= NP[cc] ? scP[b] : scP[cc],
-                        conP[b] || conP[cc]);
+          double s2 = fma(JM[2], J[cc][2], fma(JM[1], J[cc][1], JM[0] * J[cc][0]));
+          if (b == 0) s2 += jms[cc];
+          if (cc == 0) s2 += jms[b];
+          if (b == 0 && cc == 0) s2 += n0s;
+          s2 += offw * (b == cc ? 2.0 : 1.0);
+          red_fixed(V, es[s2i(b, cc)], -cw * s2, NP[b] <= NP[cc] ? scP[b] : scP[cc]);
         }
+      }
     }
   }
 
@@ -2345,10 +2413,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
     for (int q = 0; q < 4; ++q) tot += C * wq * s0w[q] * qbary(q, a) * qbary(q, b);
     if (tot != 0.0) {
-      const int lo = min(NT[a], NT[b]), hi = max(NT[a], NT[b]);
+      const int lo = min(sNT[a], sNT[b]), hi = max(sNT[a], sNT[b]);
       int ra = 0;
       for (int r = 0; r < 4; ++r)
-        if (NT[r] == lo) ra = r;
+        if (sNT[r] == lo) ra = r;
       const int hh = mp.probe(hi);
       const short* v = reinterpret_cast<const short*>(mp.val + (hh < 0 ? 0 : hh));
       red_fixed(V, rbase[ra] + v[ra], tot, sc[ra]);
@@ -2358,8 +2426,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     // assembly.cpp:703-709, warp 0 only) + this warp's constraint terms
     const int a = lane - 10;
     double r = 0;
-    if (wid == 0)
+    if (wid == 0) {
+      Vd vT[4];
+      load_verts(T, vT);
       for (int q = 0; q < 4; ++q) r += wq * qbary(q, a) * poly_eval(cD.f, quad_point(vT, q));
+    }
     const double ca = a == 0 ? sgc[0] : (a == 1 ? sgc[1] : (a == 2 ? sgc[2] : sgc[3]));
     rhsT[((long long)ii * kRhsWarps + wid) * 4 + a] = r + 2.0 * C * wq * ca;
   }
@@ -3172,8 +3243,9 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   const int kRowMax = tb.rowmax;
   const size_t rows_smem = (size_t)(tb.he + tb.hn + tb.rowmax) * sizeof(int);
   const size_t union_smem = (size_t)(kRowMax + 1) * sizeof(int);
-  CK(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
-  CK(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_rows<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
+  CK(cudaFuncSetAttribute(k_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem));
   CK(cudaFuncSetAttribute(k_union<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)union_smem));
   CK(cudaFuncSetAttribute(k_union<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)union_smem));
   CK(cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3183,21 +3255,30 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   S.roff.ensure(J + 1);
   const unsigned rgrid = (unsigned)std::min<long long>(J, (long long)S.sms * 16);
   const unsigned char* pm = S.plocal ? S.pmark.p : nullptr;
-  k_rows<false><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
-                                               nullptr, S.ovf.p, S.plo, S.phi, pm, tb);
-  ++S.launches;
-  scan64(S, S.rlen.p, true, J, S.roff.p, st);
   long long capR;
+  const int* rlenp = nullptr;  // non-null: rows in arrival order (roff[i], rlen[i])
   if (spec) {
+    // one pass: the rows take their places in the earlier run's buffer from a
+    // cursor (no counting pass; the row sets are built once)
     capR = (long long)std::min(S.rcols.n, S.tcols.n);
-    k_cap_check<<<1, 32, 0, st>>>(S.roff.p + J, capR, S.ovf.p);
+    unsigned long long* cur = S.counters.p + 6;  // (the longest-row slot, reset below)
+    CK(cudaMemsetAsync(cur, 0, sizeof(unsigned long long), st));
+    k_rows<2><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, S.roff.p,
+                                             S.rcols.p, S.ovf.p, S.plo, S.phi, pm, tb, cur, capR);
+    k_rows_total<<<1, 1, 0, st>>>(cur, S.roff.p + J);
+    S.launches += 2;
+    rlenp = S.rlen.p;
   } else {
+    k_rows<0><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, S.rlen.p, nullptr,
+                                             nullptr, S.ovf.p, S.plo, S.phi, pm, tb, nullptr, 0);
+    ++S.launches;
+    scan64(S, S.rlen.p, true, J, S.roff.p, st);
     capR = read_ll(S.roff.p + J, st);
     S.rcols.ensure(capR);
     S.tcols.ensure(capR);
+    k_rows<1><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
+                                             S.rcols.p, S.ovf.p, S.plo, S.phi, pm, tb, nullptr, 0);
   }
-  k_rows<true><<<rgrid, 256, rows_smem, st>>>(S.pair_off.p, S.partner.p, nullptr, S.roff.p,
-                                              S.rcols.p, S.ovf.p, S.plo, S.phi, pm, tb);
   // transpose
   S.tcnt.ensure(J);
   S.toff.ensure(J + 1);
@@ -3207,7 +3288,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   scan64(S, S.tcnt.p, true, J, S.toff.p, st);
   S.cursor.ensure(J);
   CK(cudaMemsetAsync(S.cursor.p, 0, J * sizeof(int), st));
-  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, S.rcols.p, S.toff.p,
+  k_transpose_fill<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.roff.p, rlenp, S.rcols.p, S.toff.p,
                                                         S.cursor.p, S.tcols.p, S.ovf.p);
   k_sort_rows<<<rgrid, 256, kRowMax * sizeof(int), st>>>(J, S.toff.p, S.tcols.p, S.ovf.p,
                                                           kRowMax);
@@ -3217,7 +3298,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
   S.soff.ensure(J + 1);
   CK(cudaMemsetAsync(S.counters.p + 6, 0, sizeof(unsigned long long), st));
   int* d_maxlen = reinterpret_cast<int*>(S.counters.p + 6);
-  k_union<false><<<rgrid, kUnionThreads, union_smem, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+  k_union<false><<<rgrid, kUnionThreads, union_smem, st>>>(J, S.roff.p, rlenp, S.rcols.p, S.toff.p, S.tcols.p,
                                                   S.slen.p, nullptr, nullptr, d_maxlen, S.ovf.p,
                                                   kRowMax);
   ++S.launches;
@@ -3231,7 +3312,7 @@ bool pattern_pass(nlfem_gpu_session& S, cudaStream_t st, int& maxlen, bool spec)
     S.scols.ensure(capS);
     S.mirror.ensure(capS);
   }
-  k_union<true><<<rgrid, kUnionThreads, union_smem, st>>>(J, S.roff.p, S.rcols.p, S.toff.p, S.tcols.p,
+  k_union<true><<<rgrid, kUnionThreads, union_smem, st>>>(J, S.roff.p, rlenp, S.rcols.p, S.toff.p, S.tcols.p,
                                                  nullptr, S.soff.p, S.scols.p, nullptr, S.ovf.p,
                                                  kRowMax);
   k_mirror<<<nblk(32LL * J, 256), 256, 0, st>>>(J, S.soff.p, S.scols.p, S.mirror.p, S.ovf.p);
