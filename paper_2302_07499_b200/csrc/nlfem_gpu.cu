@@ -1497,21 +1497,28 @@ __device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c)
 }
 
 #ifndef NLFEM_MC_MOM
-#define NLFEM_MC_MOM 4  // 4: FP64 products of fields masked by LOP3; 0: masked by a
-                        // DMUL with the hit bit (2% slower at C2); 1-3: integer products
+#define NLFEM_MC_MOM 6  // 6: fields masked by one SEL on the high word (-4.8% at C3f);
+                        // 4: masked by two LOP3 per field; 0: masked by a DMUL with
+                        // the hit bit (2% slower at C2); 1-3: integer products
+#endif
+#ifndef NLFEM_MC_I2F
+#define NLFEM_MC_I2F 2  // bit t: field t converted by I2F.F64.U32 instead of the DADD
 #endif
 
 struct IntMoments {
   unsigned n = 0;
   uint32_t s[3] = {0, 0, 0};
-#if NLFEM_MC_MOM == 0 || NLFEM_MC_MOM == 4
+#if NLFEM_MC_MOM == 0 || NLFEM_MC_MOM >= 4
   double ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
 #else
   unsigned long long ss[6] = {0, 0, 0, 0, 0, 0};  // 00 01 02 11 12 22
 #endif
   __device__ __forceinline__ void sample(const nlfem_mc_quad& Q, double dd, uint32_t s0,
                                          uint32_t s1, uint32_t s2) {
-    const double d0 = u21_to_double(s0), d1 = u21_to_double(s1), d2 = u21_to_double(s2);
+    // field 1 by I2F.F64.U32 (XU pipe, otherwise idle), the others by the DADD
+    const double d0 = (NLFEM_MC_I2F & 1) ? __uint2double_rn(s0) : u21_to_double(s0);
+    const double d1 = (NLFEM_MC_I2F & 2) ? __uint2double_rn(s1) : u21_to_double(s1);
+    const double d2 = (NLFEM_MC_I2F & 4) ? __uint2double_rn(s2) : u21_to_double(s2);
     const bool hit = nlfem_mc_q(&Q, d0, d1, d2) < dd;
     const uint32_t hb = hit ? 1u : 0u;
     n += hb;
@@ -1527,6 +1534,22 @@ struct IntMoments {
     ss[3] = fma(h1, d1, ss[3]);
     ss[4] = fma(h1, d2, ss[4]);
     ss[5] = fma(h2, d2, ss[5]);
+#elif NLFEM_MC_MOM == 6
+    // a field < 2^21 as a double has a zero low word, so masking the high word
+    // alone zeroes it: one SEL per field, in place, both factors masked
+    // (ptxas turns hit-predicated DFMAs into DFMA + 2 FSEL, which is slower)
+    s[0] = imad_u32(hb, s0, s[0]);
+    s[1] = imad_u32(hb, s1, s[1]);
+    s[2] = imad_u32(hb, s2, s[2]);
+    const double h0 = __hiloint2double(hit ? __double2hiint(d0) : 0, __double2loint(d0));
+    const double h1 = __hiloint2double(hit ? __double2hiint(d1) : 0, __double2loint(d1));
+    const double h2 = __hiloint2double(hit ? __double2hiint(d2) : 0, __double2loint(d2));
+    ss[0] = fma(h0, h0, ss[0]);
+    ss[1] = fma(h0, h1, ss[1]);
+    ss[2] = fma(h0, h2, ss[2]);
+    ss[3] = fma(h1, h1, ss[3]);
+    ss[4] = fma(h1, h2, ss[4]);
+    ss[5] = fma(h2, h2, ss[5]);
 #elif NLFEM_MC_MOM == 4
     // the fields masked in the integer pipe (two LOP3 per double) instead of
     // multiplied by the hit bit on the FP64 pipe
@@ -1584,22 +1607,28 @@ __device__ __forceinline__ void fold_moments(const nlfem_mc_quad& Q, const IntMo
   const double SS[3][3] = {{sd[0], sd[1], sd[2]}, {sd[1], sd[3], sd[4]}, {sd[2], sd[4], sd[5]}};
   double g[3], H[3][3];  // g = F^T S; H[t][y] = sum_u SS[t][u] F[u][y]
 #pragma unroll
+  // (explicit fma: the translation unit is compiled with -fmad=false for the
+  // geometric predicates; this per-piece fold is arithmetic of ours)
   for (int y = 0; y < 3; ++y) {
-    g[y] = S[0] * Q.F[0][y] + S[1] * Q.F[1][y] + S[2] * Q.F[2][y];
+    g[y] = fma(S[2], Q.F[2][y], fma(S[1], Q.F[1][y], S[0] * Q.F[0][y]));
 #pragma unroll
     for (int t = 0; t < 3; ++t)
-      H[t][y] = SS[t][0] * Q.F[0][y] + SS[t][1] * Q.F[1][y] + SS[t][2] * Q.F[2][y];
+      H[t][y] = fma(SS[t][2], Q.F[2][y], fma(SS[t][1], Q.F[1][y], SS[t][0] * Q.F[0][y]));
   }
   nh += n;
+  double na[3];
 #pragma unroll
-  for (int x = 0; x < 3; ++x) t1[x] += n * Q.a[x] + g[x];
+  for (int x = 0; x < 3; ++x) {
+    na[x] = n * Q.a[x];
+    t1[x] += na[x] + g[x];
+  }
   int k = 0;
 #pragma unroll
   for (int x = 0; x < 3; ++x)
 #pragma unroll
     for (int y = x; y < 3; ++y, ++k)
-      t2[k] += (n * Q.a[x] * Q.a[y] + Q.a[x] * g[y] + g[x] * Q.a[y]) +
-               (Q.F[0][x] * H[0][y] + Q.F[1][x] * H[1][y] + Q.F[2][x] * H[2][y]);
+      t2[k] += fma(g[x], Q.a[y], fma(Q.a[x], g[y], na[x] * Q.a[y])) +
+               fma(Q.F[2][x], H[2][y], fma(Q.F[1][x], H[1][y], Q.F[0][x] * H[0][y]));
 }
 
 constexpr long long kMomStride = 10;   // doubles per MC item record (80 B)
@@ -1950,15 +1979,16 @@ __global__ void __launch_bounds__(kMcThreads, NLFEM_MC_MINBLOCKS) k_mc(long long
           // shift to moments about v0(T'): r' = r + c0, c0 = x_q - v0
           const double c0x = sX[3][threadIdx.x], c0y = sX[4][threadIdx.x],
                        c0z = sX[5][threadIdx.x];
-          vals[1] = w * (t1[0] + n * c0x);
-          vals[2 % NV] = w * (t1[1] + n * c0y);
-          vals[3 % NV] = w * (t1[2] + n * c0z);
-          vals[4 % NV] = w * (t2[0] + 2.0 * c0x * t1[0] + n * c0x * c0x);
-          vals[5 % NV] = w * (t2[1] + c0x * t1[1] + c0y * t1[0] + n * c0x * c0y);
-          vals[6 % NV] = w * (t2[2] + c0x * t1[2] + c0z * t1[0] + n * c0x * c0z);
-          vals[7 % NV] = w * (t2[3] + 2.0 * c0y * t1[1] + n * c0y * c0y);
-          vals[8 % NV] = w * (t2[4] + c0y * t1[2] + c0z * t1[1] + n * c0y * c0z);
-          vals[9 % NV] = w * (t2[5] + 2.0 * c0z * t1[2] + n * c0z * c0z);
+          const double ncx = n * c0x, ncy = n * c0y, ncz = n * c0z;
+          vals[1] = w * (t1[0] + ncx);
+          vals[2 % NV] = w * (t1[1] + ncy);
+          vals[3 % NV] = w * (t1[2] + ncz);
+          vals[4 % NV] = w * fma(c0x, 2.0 * t1[0] + ncx, t2[0]);
+          vals[5 % NV] = w * fma(c0y, t1[0] + ncx, fma(c0x, t1[1], t2[1]));
+          vals[6 % NV] = w * fma(c0z, t1[0] + ncx, fma(c0x, t1[2], t2[2]));
+          vals[7 % NV] = w * fma(c0y, 2.0 * t1[1] + ncy, t2[3]);
+          vals[8 % NV] = w * fma(c0z, t1[1] + ncy, fma(c0y, t1[2], t2[4]));
+          vals[9 % NV] = w * fma(c0z, 2.0 * t1[2] + ncz, t2[5]);
         }
         // item totals: inner pieces, then the kept outer pieces in piece order
 #pragma unroll
