@@ -2169,19 +2169,30 @@ struct SlotMap {
 #define NLFEM_INT_MINBLOCKS 2
 #endif
 
-#ifndef NLFEM_COMB_PREFETCH
-#define NLFEM_COMB_PREFETCH 0
-#endif
-__device__ __forceinline__ void pf_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+// 16 bytes of an item record through the read-only path, or zeros when the
+// item is absent: a predicated load, not a branch, so the loads of a pair's
+// up to four records are independent of one another and of the code tests and
+// can all be in flight together (the combine is bound by load latency)
+__device__ __forceinline__ double2 rec_word(const double* rec, int k, unsigned has) {
+  double2 r;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\t"
+      "mov.f64 %0, 0d0000000000000000;\n\t"
+      "mov.f64 %1, 0d0000000000000000;\n\t"
+      "@p ld.global.nc.v2.f64 {%0, %1}, [%3];\n\t}"
+      : "=d"(r.x), "=d"(r.y)
+      : "r"(has), "l"(rec + 2 * k));
+  return r;
 }
 
 template <int NTHR>
 __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 * NLFEM_INT_MINBLOCKS)) k_integrate(
-    int ii0, const long long* pair_off, const int* partner, const unsigned* info,
-    const long long* soff, const int* scols, const long long* eslot, unsigned long long* V,
-    double* rhsT, const long long* uoff, const double* mom, long long pbase,
-    unsigned long long* stats, int hcap, int rowcap) {
+    int ii0, const long long* __restrict__ pair_off, const int* __restrict__ partner,
+    const unsigned* __restrict__ info, const long long* __restrict__ soff,
+    const int* __restrict__ scols, const long long* __restrict__ eslot,
+    unsigned long long* __restrict__ V, double* __restrict__ rhsT,
+    const long long* __restrict__ uoff, const double* __restrict__ mom, long long pbase,
+    unsigned long long* __restrict__ stats, int hcap, int rowcap) {
   static_assert(NTHR / 32 <= kRhsWarps, "one rhsT slot per combine warp");
   extern __shared__ unsigned long long sml[];
   SlotMap mp;
@@ -2263,13 +2274,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
         uN = (mom != nullptr) ? uoff[pn - pbase] : 0;
       }
     }
-    const bool constr = cD.region[Tp] != 0;
-    const double volP = cD.vol[Tp];
+    // partner fields through the read-only path (ld.global.nc): the compiler may
+    // then move these loads across the fixed-point REDs (no aliasing with V)
+    const bool constr = __ldg(cD.region + Tp) != 0;
+    const double volP = __ldg(cD.vol + Tp);
 
     if (constr) {
       // constraint parent: measure and g integral per point (reference
       // assembly.cpp:350-359, 416-427); no matrix block
-      const double gb = cD.gbar[Tp];
+      const double gb = __ldg(cD.gbar + Tp);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const unsigned c = (code >> (5 * q)) & 31;
@@ -2307,56 +2320,51 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const unsigned c = (code >> (5 * q)) & 31;
-      if (c == 0) continue;
-      double S0 = 0;
-      if (c == kWhole) {
+      const bool whole = c == kWhole;
+      // straddling / cap item: its record (k_mc: inner pieces, + outer pieces
+      // by Monte Carlo for fullcaps); absent items read as zeros
+      const unsigned has = (c != 0 && !whole && mom != nullptr) ? 1u : 0u;
+      const double* rec = mom + kMomStride * ((NLFEM_DIAG & 2) ? 0 : u);
+      u += has;
+      const double2 r0 = rec_word(rec, 0, has), r1 = rec_word(rec, 1, has),
+                    r2 = rec_word(rec, 2, has), r3 = rec_word(rec, 3, has),
+                    r4 = rec_word(rec, 4, has);
+      if (whole) {
         led += 39;
-        S0 = volP;
         nw += 1.0;
         wmask |= 1u << q;
-      } else if (mom != nullptr) {
-        // straddling / cap item: its record (k_mc: inner pieces, + outer pieces
-        // by Monte Carlo for fullcaps)
-        const double2* rec =
-            reinterpret_cast<const double2*>(mom + kMomStride * ((NLFEM_DIAG & 2) ? 0 : u));
-        ++u;
-        const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3], r4 = rec[4];
-        S0 = r0.x;
-        n0q[q] = r0.x;
-        m1q[q][0] = r0.y;
-        m1q[q][1] = r1.x;
-        m1q[q][2] = r1.y;
-        Ms[0] += r2.x;
-        Ms[1] += r2.y;
-        Ms[2] += r3.x;
-        Ms[3] += r3.y;
-        Ms[4] += r4.x;
-        Ms[5] += r4.y;
       }
-      s0w[q] += S0;
+      n0q[q] = r0.x;
+      m1q[q][0] = r0.y;
+      m1q[q][1] = r1.x;
+      m1q[q][2] = r1.y;
+      Ms[0] += r2.x;
+      Ms[1] += r2.y;
+      Ms[2] += r3.x;
+      Ms[3] += r3.y;
+      Ms[4] += r4.x;
+      Ms[5] += r4.y;
+      s0w[q] += whole ? volP : r0.x;
     }
 
-#if NLFEM_COMB_PREFETCH
-    if (p + blockDim.x < p1) {
-      // the next pair's element fields and records towards L1 while this
-      // pair's blocks are formed
-      pf_l1(cD.vol + TpN);
-      pf_l1(cD.inv + 9 * (long long)TpN);
-      pf_l1(cD.inv + 9 * (long long)TpN + 8);
-      pf_l1(cD.verts + TpN);
-      pf_l1(cD.escale + TpN);
-      if (mom != nullptr) {
-        pf_l1(mom + kMomStride * uN);
-        pf_l1(mom + kMomStride * uN + 16);
-        pf_l1(mom + kMomStride * uN + 32);
+    const int4 wP = __ldg(cD.verts + Tp);
+    const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
+    const double2 esc01 = __ldg(reinterpret_cast<const double2*>(cD.escale + Tp));
+    const double2 esc23 = __ldg(reinterpret_cast<const double2*>(cD.escale + Tp) + 1);
+    const double scP[4] = {esc01.x, esc01.y, esc23.x, esc23.y};
+    // the ten T' x T' slots, all loaded here (five 16-byte words): issued
+    // together instead of one by one between the REDs
+    long long es[10];
+    {
+      const longlong2* ep =
+          reinterpret_cast<const longlong2*>(eslot + 10 * (long long)__ldg(cD.ipos + Tp));
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const longlong2 e2 = __ldg(ep + k);
+        es[2 * k] = e2.x;
+        es[2 * k + 1] = e2.y;
       }
     }
-#endif
-    const int4 wP = cD.verts[Tp];
-    const int NP[4] = {wP.x, wP.y, wP.z, wP.w};
-    const double4 esc = cD.escale[Tp];
-    const double scP[4] = {esc.x, esc.y, esc.z, esc.w};
-    const long long* es = eslot + 10 * (long long)interior_pos(Tp);
 
     // J rows from inv_edges, J0 = -(J1+J2+J3)
     const double* invP = cD.inv + 9 * (long long)Tp;
@@ -2364,7 +2372,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
 #pragma unroll
     for (int r = 1; r < 4; ++r)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) J[r][a] = invP[3 * (r - 1) + a];
+      for (int a = 0; a < 3; ++a) J[r][a] = __ldg(invP + 3 * (r - 1) + a);
 #pragma unroll
     for (int a = 0; a < 3; ++a) J[0][a] = -(J[1][a] + J[2][a] + J[3][a]);
 
