@@ -2192,7 +2192,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     const int* __restrict__ scols, const long long* __restrict__ eslot,
     unsigned long long* __restrict__ V, double* __restrict__ rhsT,
     const long long* __restrict__ uoff, const double* __restrict__ mom, long long pbase,
-    unsigned long long* __restrict__ stats, int hcap, int rowcap) {
+    unsigned long long* __restrict__ stats, int hcap, int rowcap, int nelem, int* spread) {
   static_assert(NTHR / 32 <= kRhsWarps, "one rhsT slot per combine warp");
   extern __shared__ unsigned long long sml[];
   SlotMap mp;
@@ -2200,9 +2200,27 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
   mp.val = reinterpret_cast<short4*>(mp.key + hcap);
   mp.mask = hcap - 1;
   __shared__ long long rbase[4];
-
-  const int ii = ii0 + blockIdx.x;
+  __shared__ double sc[4];
+  __shared__ int sNT[4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+  // One outer element per CTA (spread == nullptr, grid = nelem); or -- overlap
+  // mode, the combine beside the next chunk's units -- exactly one CTA per SM
+  // walking the chunk's elements from a shared cursor.  The block scheduler
+  // packs CTAs onto SMs, so the grid holds several candidates per SM and every
+  // CTA but the first to arrive on its SM leaves at once (spread[1 + smid]
+  // counts arrivals, spread[0] is the element cursor; both zeroed per launch).
+  __shared__ int s_el;
+  if (spread != nullptr) {
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      s_el = atomicAdd(spread + 1 + smid, 1) == 0 ? atomicAdd(spread, 1) : nelem;
+    }
+    __syncthreads();
+  }
+  for (int el = spread ? s_el : (int)blockIdx.x; el < nelem;) {
+  const int ii = ii0 + el;
   const int T = cD.interior[ii];
   const int4 wT = cD.verts[T];
   const int NT[4] = {wT.x, wT.y, wT.z, wT.w};
@@ -2238,8 +2256,6 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
   const double C = cD.C;
   // per-row constants of T, parked in shared memory (broadcast reads; they
   // would otherwise stay live in registers across the pair loop)
-  __shared__ double sc[4];
-  __shared__ int sNT[4];
   if (threadIdx.x < 4) {
     sc[threadIdx.x] = cD.scale[NT[threadIdx.x]];
     sNT[threadIdx.x] = NT[threadIdx.x];
@@ -2472,6 +2488,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR == 256 ? NLFEM_INT_MINBLOCKS : 2 *
     const double ca = a == 0 ? sgc[0] : (a == 1 ? sgc[1] : (a == 2 ? sgc[2] : sgc[3]));
     rhsT[((long long)ii * kRhsWarps + wid) * 4 + a] = r + 2.0 * C * wq * ca;
   }
+  if (spread == nullptr) break;
+  __syncthreads();  // every warp is done with this element's map (and has read s_el)
+  if (threadIdx.x == 0) s_el = atomicAdd(spread, 1);
+  __syncthreads();
+  el = s_el;
+  }  // elements of this CTA
 }
 
 
@@ -2838,6 +2860,7 @@ PinnedPool g_result_pool;
 struct nlfem_gpu_session {
   int device = 0;
   int sms = 148;  // streaming multiprocessors of the device (grid sizing)
+  int smem_per_sm = 233472;  // shared memory per SM (overlap-mode residency)
   Dev dev{};
   int K = 0, J = 0, KI = 0, unknowns = 0;
   std::vector<int> h_interior, h_dof_node;
@@ -2859,7 +2882,7 @@ struct nlfem_gpu_session {
   DBuf<double4> escale;
   DBuf<unsigned char> econ;
   // pairs
-  DBuf<int> pair_count, partner, err_elem, ovf, cand_count, cpartner;
+  DBuf<int> pair_count, partner, err_elem, ovf, cand_count, cpartner, spread;
   DBuf<long long> cand_off;
   DBuf<unsigned> cinfo;
   DBuf<unsigned> info;
@@ -3036,6 +3059,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
   if (cfg->device >= 0) CK(cudaSetDevice(cfg->device));
   CK(cudaGetDevice(&S.device));
   CK(cudaDeviceGetAttribute(&S.sms, cudaDevAttrMultiProcessorCount, S.device));
+  CK(cudaDeviceGetAttribute(&S.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, S.device));
   int major = 0;
   CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, S.device));
   if (major < 10)
@@ -3053,7 +3077,7 @@ void session_init(nlfem_gpu_session& S, const nlfem_gpu_mesh* m, const nlfem_gpu
       CK(cudaStreamCreateWithPriority(&S.stream4, cudaStreamNonBlocking, hi));
     else
       CK(cudaStreamCreateWithFlags(&S.stream4, cudaStreamNonBlocking));
-    for (int i = 0; i < 24; ++i) {
+    for (int i = 0; i < 27; ++i) {  // 24..26: overlap-mode probe windows
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       S.ev.push_back(e);
@@ -3706,6 +3730,35 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   const bool own_range = installed && shard_lo == S.pairs_lo && shard_hi == S.pairs_hi;
   const bool fast = (full_run && S.survivors <= kPairsPerChunk) ||
                     (own_range && S.shard_npairs <= kPairsPerChunk);
+  // Overlap mode (Monte Carlo runs of more than two chunks): the combine of a
+  // chunk runs beside the units of the next one.  The units kernels use no
+  // memory pipe and the combine little else, but unit launches at four CTAs per
+  // SM hold every register; capped at three (shared-memory padding, -1.7% of
+  // their rate at C3f) they leave room for one 128-thread combine CTA per SM.
+  constexpr int kMcPadBytes = 57 * 1024;
+  // Whether that pays depends on the problem (B200: -5.7% of the step at C3f,
+  // -3% at C2, but +12% at C4, where the units slow down by more than the
+  // combine they hide), so a run of many chunks measures it: six chunks with
+  // the overlap, six without, timed on the units' stream, and the faster mode
+  // for the rest.  The results do not depend on the mode (the same per-element
+  // sums; integer accumulation).  NLFEM_COMB_OVERLAP: unset = measure, 0 = off,
+  // 1 = resident combine only, 2 = padding only, 3 = both, always.
+  const char* ov_s = std::getenv("NLFEM_COMB_OVERLAP");
+  const int overlap_env = ov_s ? atoi(ov_s) : -1;
+  const long long shard_pairs_bound =
+      full_run ? S.survivors : (own_range ? S.shard_npairs : (1LL << 62));
+  const bool overlap_able = need_mc && !fast && shard_pairs_bound > 2 * kPairsPerChunk;
+  constexpr int kProbe0 = 2, kProbeLen = 6;  // windows [2, 8) with, [8, 14) without
+  const bool probing = overlap_able && overlap_env < 0 &&
+                       shard_pairs_bound > (kProbe0 + 2 * kProbeLen + 6) * kPairsPerChunk;
+  int ov_bits = overlap_env > 0 ? (overlap_env & 3) : 0;  // this chunk's mode
+  bool overlap = overlap_able && ov_bits != 0;
+  auto fits_pad = [&]() {
+    return 3 * (kMcPadBytes + 1024) + (int)ismem + 2048 <= S.smem_per_sm;
+  };
+  auto fits_nopad = [&]() {  // 37,888 B: the largest static shared memory of a units kernel
+    return 3 * (37888 + 1024) + (int)ismem + 2048 <= S.smem_per_sm;
+  };
   bool npairs_pending = false;
   if (fast) {
     npairs_pending = full_run;  // read at the end with the BallExitsMesh flag
@@ -3750,6 +3803,23 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         P0 = poff[ii0];
         np = poff[ii1] - P0;
       }
+      if (probing) {  // overlap mode by measurement (see above)
+        if (chunk == kProbe0 || chunk == kProbe0 + kProbeLen || chunk == kProbe0 + 2 * kProbeLen)
+          CK(cudaEventRecord(S.ev[24 + (chunk - kProbe0) / kProbeLen], st));
+        if (chunk == kProbe0) ov_bits = 3;
+        if (chunk == kProbe0 + kProbeLen) ov_bits = 0;
+        if (chunk == kProbe0 + 2 * kProbeLen + 2) {
+          float with = 0, without = 0;
+          CK(cudaEventSynchronize(S.ev[26]));
+          CK(cudaEventElapsedTime(&with, S.ev[24], S.ev[25]));
+          CK(cudaEventElapsedTime(&without, S.ev[25], S.ev[26]));
+          ov_bits = with < 0.99f * without ? 3 : 0;
+          if (std::getenv("NLFEM_GPU_TRACE"))
+            fprintf(stderr, "[nlfem] overlap probe: %d chunks with %.2f ms, without %.2f ms -> %s\n",
+                    kProbeLen, with, without, ov_bits ? "on" : "off");
+        }
+        overlap = ov_bits != 0;
+      }
       const int set = chunk & 1;
       auto& U = S.ub[set];
       if (set_busy[set]) {  // the combine of chunk - 2 still reads this set
@@ -3786,9 +3856,25 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
         int nl[8];
         for (int k = 0; k < 8; ++k)
           nl[k] = (int)std::min<long long>(nitems, (long long)S.sms * NLFEM_MC_MINBLOCKS * 2 * kMcThreads);
+        // overlap mode: every units launch's shared memory is padded up to
+        // kMcPadBytes in total, which caps the launch at three resident CTAs per
+        // SM (48K registers) and leaves a quarter of the registers and ~54 KB of
+        // shared memory for the co-resident combine CTA of the previous chunk
+        // (once the combine's slot-map size is known, and only if its CTA then
+        // fits beside three padded ones; otherwise the resident combine CTAs,
+        // launched first, hold their registers and the units fit three beside
+        // them anyway)
+        const int mc_pad = (overlap && (ov_bits & 2) && combine_ready && fits_pad()) ? kMcPadBytes : 0;
         auto launch = [&](auto kern, int kind, cudaStream_t s) {
           if (nl[kind] <= 0) return;
-          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, 0, s>>>(
+          int dyn = 0;
+          if (mc_pad > 0) {  // pad the launch's shared memory up to mc_pad bytes in total
+            cudaFuncAttributes fa;
+            CK(cudaFuncGetAttributes(&fa, kern));
+            dyn = std::max(0, mc_pad - (int)fa.sharedSizeBytes);
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+          }
+          kern<<<nblk(nl[kind], kMcThreads), kMcThreads, dyn, s>>>(
               P0, nitems, U.ulist.p + kind * ls, U.nlist.p + kind, U.mom.p, S.counters.p + 1);
           ++S.launches;
         };
@@ -3842,16 +3928,36 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
 #ifndef NLFEM_COMB_THREADS
 #define NLFEM_COMB_THREADS 0  // 0: by delta/h; 128 / 256: forced
 #endif
-      if (NLFEM_COMB_THREADS == 128 || (NLFEM_COMB_THREADS == 0 && S.delta_over_h < 2.5))
-        k_integrate<128><<<ii1 - ii0, 128, ismem, s4>>>(
+      // (Monte Carlo runs take 128 threads as well: their combine runs beside
+      // the next chunk's units, below.)  Grid: one CTA per outer element, or --
+      // overlap mode, every chunk but the last -- one resident CTA per SM
+      // walking the chunk's elements while the next chunk's units, capped at
+      // three CTAs per SM, use the rest of the SM
+      const int nelem = ii1 - ii0;
+      // (only if that CTA fits beside three units CTAs, padded or not)
+      const bool resident = overlap && (ov_bits & 1) && (fits_pad() || fits_nopad()) && ii1 < shard_hi;
+      if (chunk == 1 && std::getenv("NLFEM_GPU_TRACE"))
+        fprintf(stderr, "[nlfem] combine: maxlen %d hcap %d ismem %zu overlap %d fits_pad %d "
+                        "fits_nopad %d resident %d nelem %d\n", maxlen, hcap, ismem, (int)overlap,
+                (int)fits_pad(), (int)fits_nopad(), (int)resident, ii1 - ii0);
+      const int cgrid = resident ? 4 * S.sms : nelem;
+      int* spread = nullptr;
+      if (resident) {
+        S.spread.ensure(1 + 1024);
+        CK(cudaMemsetAsync(S.spread.p, 0, (1 + 1024) * sizeof(int), s4));
+        spread = S.spread.p;
+      }
+      if (NLFEM_COMB_THREADS == 128 ||
+          (NLFEM_COMB_THREADS == 0 && (need_mc || S.delta_over_h < 2.5)))
+        k_integrate<128><<<cgrid, 128, ismem, s4>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
             S.rhsT.p, U.uoff.p, need_units ? U.mom.p : nullptr, P0, S.counters.p + 1, hcap,
-            rowcap);
+            rowcap, nelem, spread);
       else
-        k_integrate<256><<<ii1 - ii0, 256, ismem, s4>>>(
+        k_integrate<256><<<cgrid, 256, ismem, s4>>>(
             ii0, S.pair_off.p, S.partner.p, S.info.p, S.soff.p, S.scols.p, S.eslot.p, S.V.p,
             S.rhsT.p, U.uoff.p, need_units ? U.mom.p : nullptr, P0, S.counters.p + 1, hcap,
-            rowcap);
+            rowcap, nelem, spread);
       ++S.launches;
       CK(cudaEventRecord(evu(set, 3), s4));
       set_busy[set] = true;

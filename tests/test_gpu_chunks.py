@@ -31,12 +31,15 @@ np.savez(sys.argv[2], **out)
 """
 
 
-def _run(tmp_path, name, chunk):
+def _run(tmp_path, name, chunk, overlap=None):
     env = dict(os.environ)
     if chunk:
         env["NLFEM_PAIRS_PER_CHUNK"] = str(chunk)
     else:
         env.pop("NLFEM_PAIRS_PER_CHUNK", None)
+    env.pop("NLFEM_COMB_OVERLAP", None)
+    if overlap is not None:
+        env["NLFEM_COMB_OVERLAP"] = str(overlap)
     f = tmp_path / f"{name}.npz"
     subprocess.run([sys.executable, "-c", CHILD, ROOT, str(f)], check=True, env=env, cwd=ROOT)
     return np.load(f)
@@ -47,3 +50,18 @@ def test_many_chunks_bitwise_equal_one_chunk(tmp_path):
     many = _run(tmp_path, "many", 3000)   # ~10-20 chunks on this mesh
     for k in one.files:
         assert np.array_equal(one[k], many[k]), k
+
+
+def test_overlap_modes_bitwise_equal(tmp_path):
+    # Overlap mode of Monte Carlo runs (the combine of a chunk as one resident
+    # CTA per SM beside the next chunk's units, their launches padded to three
+    # CTAs per SM): forced on, forced off and chosen by the run's own
+    # measurement (many small chunks) all give the same bits as one chunk.
+    one = _run(tmp_path, "one", None)
+    on = _run(tmp_path, "on", 3000, overlap=3)
+    off = _run(tmp_path, "off", 3000, overlap=0)
+    probe = _run(tmp_path, "probe", 700)   # > 20 chunks: the measured choice
+    for k in one.files:
+        assert np.array_equal(one[k], on[k]), k
+        assert np.array_equal(one[k], off[k]), k
+        assert np.array_equal(one[k], probe[k]), k

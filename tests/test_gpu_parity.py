@@ -240,10 +240,12 @@ def test_fullcaps_custom_g_against_oracle(gterms):
     assert (st["mc_samples"], st["mc_hits"]) == (o["mc_samples"], o["mc_hits"])
 
 
-@pytest.mark.parametrize("mc", [5, 7, 10, 64])
+@pytest.mark.parametrize("mc", [5, 7, 10, 64, 1102])
 def test_fullcaps_partial_blocks_and_weights_against_oracle(mc):
     # M % 4 != 0 exercises the partial last Philox block; M not a power of two
-    # takes the vol / M division, M = 64 the exact vol * 2^-6 multiply.
+    # takes the vol / M division, M = 64 the exact vol * 2^-6 multiply;
+    # M = 1102 spans two 1024-sample segments of the exact moment sums plus a
+    # partial block.
     m = P.generate_mesh(3, 4, 0.3)
     t = P.ElementTable(m["coords"], m["cells"], m["region"])
     out, st = P.assemble(t, 0.3, "fullcaps", "moment2", U2, seed=SEED, mc_samples=mc)
