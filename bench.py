@@ -66,6 +66,9 @@ CONFIGS = {
     # smaller same-delta/h variants for profiling
     "P3n": dict(res=24, delta=3 / 24, strategy="nocaps", mc=1, jitter=7),
     "P3f": dict(res=24, delta=3 / 24, strategy="fullcaps", mc=128, jitter=7),
+    # C3f without the jitter and C4 with it (overlap-mode diagnostics: size or structure?)
+    "P48s": dict(res=48, delta=3 / 48, strategy="fullcaps", mc=128, jitter=None),
+    "P96j": dict(res=96, delta=3 / 96, strategy="fullcaps", mc=128, jitter=7),
 }
 METRIC = "element-pair integrals/s"
 # B200 FP64 (non-tensor) nominal: 148 SMs x 64 DFMA/clk x 2 FLOP x 1.965 GHz
@@ -496,6 +499,13 @@ def main():
         rl_kernel, rl_flops, rl_ms = "k_integrate (combine)", ledger, k3
     integ = ledger / (k3 * 1e-3) / 1e12 / world
     traffic = TRAFFIC.get(args.config) if units and world == 1 else None
+    # overlap mode: multi-chunk Monte Carlo runs time the units
+    # phase while it shares each SM with the previous chunk's combine
+    overlap_on = (cfg["strategy"] == "fullcaps" and pairs / world > 2 * (1 << 23)
+                  and os.environ.get("NLFEM_COMB_OVERLAP", "3") not in ("0", "2"))
+    overlap_note = ("on: the units phase shares each SM with the previous chunk's combine, which "
+                    "runs as one resident CTA per SM (k_mc alone, NLFEM_COMB_OVERLAP=0: 0.555 of "
+                    "the measured peak at C4, profiles/r3b_overlap_mode.txt)") if overlap_on else "off"
     line = {
         "metric": METRIC, "value": value, "unit": METRIC,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -517,6 +527,7 @@ def main():
                      "peak_nominal": FP64_NOMINAL_TF,
                      "frac_of_nominal": achieved / FP64_NOMINAL_TF,
                      "ledger_flops_per_launch": int(rl_flops), "launch_ms": rl_ms,
+                     "overlap": overlap_note,
                      "traffic": traffic[0] if traffic else None,
                      "traffic_source": traffic[1] if traffic else None,
                      "integration_phase": {"kernels": "k_mc + k_integrate", "ms": k3,

@@ -3736,15 +3736,13 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
   // SM hold every register; capped at three (shared-memory padding, -1.7% of
   // their rate at C3f) they leave room for one 128-thread combine CTA per SM.
   constexpr int kMcPadBytes = 57 * 1024;
-  // Whether that pays depends on the problem (B200: -5.7% of the step at C3f,
-  // -3% at C2, but +12% at C4, where the units slow down by more than the
-  // combine they hide), so a run of many chunks measures it: six chunks with
-  // the overlap, six without, timed on the units' stream, and the faster mode
-  // for the rest.  The results do not depend on the mode (the same per-element
-  // sums; integer accumulation).  NLFEM_COMB_OVERLAP: unset = measure, 0 = off,
-  // 1 = resident combine only, 2 = padding only, 3 = both, always.
+  // B200: -5.4% of the step at C3f, -2.3% at C2, -4.3% at C4.  The results do
+  // not depend on the mode (the same per-element sums; integer accumulation).
+  // NLFEM_COMB_OVERLAP: unset or 3 = on, 0 = off, 1 = resident combine only,
+  // 2 = padding only, -1 = measured per run (six chunks with, six without,
+  // timed on the units' stream, the faster mode for the rest).
   const char* ov_s = std::getenv("NLFEM_COMB_OVERLAP");
-  const int overlap_env = ov_s ? atoi(ov_s) : -1;
+  const int overlap_env = ov_s ? atoi(ov_s) : 3;
   const long long shard_pairs_bound =
       full_run ? S.survivors : (own_range ? S.shard_npairs : (1LL << 62));
   const bool overlap_able = need_mc && !fast && shard_pairs_bound > 2 * kPairsPerChunk;
@@ -3874,6 +3872,10 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
             dyn = std::max(0, mc_pad - (int)fa.sharedSizeBytes);
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
           }
+          if (overlap_able)  // see the combine's launch below
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    mc_pad > 0 ? (int)cudaSharedmemCarveoutMaxShared
+                                               : (int)cudaSharedmemCarveoutDefault));
           kern<<<nblk(nl[kind], kMcThreads), kMcThreads, dyn, s>>>(
               P0, nitems, U.ulist.p + kind * ls, U.nlist.p + kind, U.mom.p, S.counters.p + 1);
           ++S.launches;
@@ -3941,6 +3943,18 @@ void run_all(nlfem_gpu_session& S, cudaStream_t user, nlfem_gpu_stats* stats, in
                         "fits_nopad %d resident %d nelem %d\n", maxlen, hcap, ismem, (int)overlap,
                 (int)fits_pad(), (int)fits_nopad(), (int)resident, ii1 - ii0);
       const int cgrid = resident ? 4 * S.sms : nelem;
+      // The SM's shared-memory carve-out is set by the first kernel to land on
+      // it: a resident combine CTA with a small slot map (24 KB at C4) left the SM
+      // configured for ~100 KB, where only one 57-KB units CTA fitted beside it
+      // until the SM drained (units 27% slower at C4).  In overlap mode both
+      // kernels ask for the largest carve-out; otherwise the default (the
+      // combine alone is 7% faster with its L1).
+      if (overlap_able) {
+        const int co = resident ? (int)cudaSharedmemCarveoutMaxShared
+                                : (int)cudaSharedmemCarveoutDefault;
+        CK(cudaFuncSetAttribute(k_integrate<128>, cudaFuncAttributePreferredSharedMemoryCarveout, co));
+        CK(cudaFuncSetAttribute(k_integrate<256>, cudaFuncAttributePreferredSharedMemoryCarveout, co));
+      }
       int* spread = nullptr;
       if (resident) {
         S.spread.ensure(1 + 1024);

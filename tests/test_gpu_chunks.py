@@ -55,12 +55,12 @@ def test_many_chunks_bitwise_equal_one_chunk(tmp_path):
 def test_overlap_modes_bitwise_equal(tmp_path):
     # Overlap mode of Monte Carlo runs (the combine of a chunk as one resident
     # CTA per SM beside the next chunk's units, their launches padded to three
-    # CTAs per SM): forced on, forced off and chosen by the run's own
+    # CTAs per SM): on (the default), off and chosen by the run's own
     # measurement (many small chunks) all give the same bits as one chunk.
     one = _run(tmp_path, "one", None)
     on = _run(tmp_path, "on", 3000, overlap=3)
     off = _run(tmp_path, "off", 3000, overlap=0)
-    probe = _run(tmp_path, "probe", 700)   # > 20 chunks: the measured choice
+    probe = _run(tmp_path, "probe", 700, overlap=-1)   # > 20 chunks: the measured choice
     for k in one.files:
         assert np.array_equal(one[k], on[k]), k
         assert np.array_equal(one[k], off[k]), k
