@@ -79,10 +79,10 @@ FP64_NOMINAL_TF = 148 * 64 * 2 * 1.965e9 / 1e12
 # ncu --set full captures; None where no capture was taken for that workload
 TRAFFIC = {"C1": (432594432, "profiles/r1_c1_kmc_ncu.txt (dram read+write summed over the "
                              "step's k_mc launches)"),
-           # one units chunk's 8 k_mc launches: 2,210,805,504 B for 8,388,608 element
+           # one units chunk's 8 k_mc launches: 2,208,101,632 B for 8,388,608 element
            # pairs (~264 B per pair, mostly the 80-B item records), times the step's
            # 7,012,417,536 pairs
-           "C4": (1848e9, "profiles/r2m_c4_kmc_ncu.txt (dram read+write of one chunk's k_mc "
+           "C4": (1846e9, "profiles/r3d_c4_kmc_ncu.txt (dram read+write of one chunk's k_mc "
                           "launches, ncu --set full, scaled by element pairs to the step)")}
 
 
